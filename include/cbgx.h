@@ -1,0 +1,306 @@
+/*
+ * cbgx.h -- C-ABI of the B200-native FRSZ2 / compressed-basis GMRES path.
+ *
+ * This is the drop-in boundary for the reference's hot path
+ * (/root/reference/proj/include/cbg/{frsz2,basis,sparse,gmres}.hpp). Plain C
+ * types, caller-owned buffers, no exceptions across the boundary:
+ * every entry point returns a status (CBGX_OK = 0) and cbgx_last_error()
+ * gives the message of the calling thread's last failure. The C++ wrappers in
+ * include/cbg/*.hpp (libcbg_b200.so) turn statuses back into the
+ * reference's exception types and messages.
+ *
+ * Pointers prefixed d_ are device pointers (cudaMalloc / torch tensors);
+ * `stream` is a cudaStream_t (NULL = legacy default stream). Device-pointer
+ * entry points are stream-ordered and asynchronous unless noted.
+ *
+ * Build: paper_2409_15468_b200/libcbgx.so (nvcc, sm_100a only). There is no
+ * CPU fallback: on a machine without an sm_100a device every compute entry
+ * point returns CBGX_ECUDA.
+ */
+#ifndef CBGX_H
+#define CBGX_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+/* ------------------------------------------------------------- status */
+enum {
+    CBGX_OK = 0,
+    CBGX_EINVAL = 1,      /* std::invalid_argument in the reference */
+    CBGX_ENONFINITE = 2,  /* "frsz2: non-finite value at index N" (frsz2.cpp:28-31) */
+    CBGX_ERANGE = 3,      /* std::out_of_range */
+    CBGX_EBREAKDOWN = 4,  /* cbg::SolverBreakdown (gmres.hpp:48-53) */
+    CBGX_ECUDA = 5,       /* CUDA runtime failure / no device */
+    CBGX_ENOMEM = 6,
+    CBGX_ECOMM = 7,       /* NCCL / communicator failure */
+    CBGX_EINTERNAL = 8
+};
+
+const char* cbgx_last_error(void);
+/* index (non-finite value) or iteration (breakdown) attached to the last error */
+uint64_t cbgx_last_error_index(void);
+int cbgx_version(void);
+/* device ordinal, SM count and L2 bytes of the current device */
+int cbgx_device_info(int* device, int* sm_count, int64_t* l2_bytes);
+
+/* ------------------------------------------------------ FRSZ2 codec
+ * Reference: frsz2.hpp:16-87, frsz2.cpp:130-277. Block size bs >= 1,
+ * bit length 2 <= l <= 64. bs == 32 with l in {16, 21, 32} runs the
+ * warp-per-block register codec (warp max-exponent reduction, shuffle
+ * packing); every other (bs, l) runs the generic thread-per-block codec.
+ * Both are bit-exact with the reference. */
+uint64_t cbgx_frsz2_num_blocks(uint64_t n, uint32_t bs);
+uint64_t cbgx_frsz2_words_per_block(uint32_t bs, uint32_t l);   /* Frsz2Params::words_per_block */
+uint64_t cbgx_frsz2_storage_bytes(uint64_t n, uint32_t bs, uint32_t l); /* storage_bytes, frsz2.cpp:268-272 */
+double cbgx_frsz2_max_abs_error_bound(uint32_t e_max, uint32_t l);       /* frsz2.cpp:274-277 */
+
+/* compress (frsz2.hpp:70-71): d_exp gets num_blocks words, d_payload
+ * num_blocks*words_per_block words. Synchronises `stream` to report a
+ * non-finite input as CBGX_ENONFINITE with the lowest offending index. */
+int cbgx_frsz2_compress(const double* d_in, uint64_t n, uint32_t bs, uint32_t l,
+                        uint32_t* d_exp, uint32_t* d_payload, void* stream);
+/* Asynchronous form: *d_bad_index must be preset to UINT64_MAX by the caller
+ * and receives the lowest non-finite index (atomicMin) if any. */
+int cbgx_frsz2_compress_async(const double* d_in, uint64_t n, uint32_t bs, uint32_t l,
+                              uint32_t* d_exp, uint32_t* d_payload,
+                              uint64_t* d_bad_index, void* stream);
+/* decompress (frsz2.hpp:79-80) of the whole vector */
+int cbgx_frsz2_decompress(const uint32_t* d_exp, const uint32_t* d_payload, uint64_t n,
+                          uint32_t bs, uint32_t l, double* d_out, void* stream);
+/* decode stream positions [first, first+count) (may run past n into the
+ * last block's padding, as decompress_block does, frsz2.cpp:221-246);
+ * covers decompress_value (count 1) and decompress_block (count bs). */
+int cbgx_frsz2_decompress_range(const uint32_t* d_exp, const uint32_t* d_payload,
+                                uint64_t n, uint32_t bs, uint32_t l, uint64_t first,
+                                uint64_t count, double* d_out, void* stream);
+/* compress_block (frsz2.hpp:64-65): one block of `count` values ->
+ * *d_emax and count u64 codes. Synchronises for the non-finite check. */
+int cbgx_frsz2_encode_block(const double* d_values, uint32_t count, uint32_t l,
+                            uint32_t* d_emax, uint64_t* d_codes, void* stream);
+
+/* ------------------------------------------------ Krylov basis panel
+ * Reference: basis.hpp:23-83. Column-major panel, one contiguous region per
+ * column. Rows are padded to `n_pad` (a multiple of 8192) so the fused CGS
+ * kernels stream whole tiles; padding rows hold zeros. Layout per kind:
+ *   F64/F32/F16: d_data + j*col_stride_bytes holds n_pad values;
+ *   FRSZ2 (bs 32, l in {16,21,32}): d_exp + j*exp_col_stride holds n_pad/32
+ *   exponent words, d_data + j*col_stride_bytes holds n_pad/32*l payload
+ *   words -- i.e. each column is exactly the reference CompressedVector
+ *   (frsz2.hpp:29-48) plus zero padding blocks. */
+enum { CBGX_F64 = 0, CBGX_F32 = 1, CBGX_F16 = 2, CBGX_FRSZ2 = 3 };
+
+typedef struct {
+    uint32_t kind;        /* CBGX_F64 / F32 / F16 / FRSZ2 */
+    uint32_t bit_length;  /* FRSZ2: 16, 21 or 32 */
+    uint64_t n;           /* rows (StorageFormat length) */
+    uint64_t n_pad;       /* padded rows */
+    uint64_t capacity;    /* columns */
+    void* d_data;
+    uint32_t* d_exp;      /* FRSZ2 only */
+    uint64_t col_stride_bytes;
+    uint64_t exp_col_stride;  /* in u32 words */
+} cbgx_basis;
+
+/* Fill the layout for (kind, l, n, capacity); returns the byte sizes the
+ * caller must allocate for d_data and d_exp (0 for non-FRSZ2). */
+int cbgx_basis_layout(uint32_t kind, uint32_t bit_length, uint64_t n, uint64_t capacity,
+                      cbgx_basis* out, uint64_t* data_bytes, uint64_t* exp_bytes);
+
+typedef struct cbgx_workspace cbgx_workspace;  /* reduction partials + counters */
+int cbgx_workspace_create(cbgx_workspace** ws);
+int cbgx_workspace_destroy(cbgx_workspace* ws);
+
+/* write_vector (basis.cpp:85-115) with an optional fused scale:
+ * column j <- format(s * x[0..n)) where s = 1 if d_scale_src is NULL,
+ * s = *d_scale_src if scale_mode == 0, s = 1/sqrt(*d_scale_src) if
+ * scale_mode == 1 (the reference's scale(1.0/h_next, w), gmres.cpp:231,
+ * with h_next = sqrt(||w||^2): IEEE sqrt and division, so bit-identical).
+ * If d_v_out is non-NULL it also receives s*x (the fp64 SpMV input v).
+ * *d_bad_index (may be NULL) receives the lowest non-finite index. */
+int cbgx_basis_write(const cbgx_basis* V, uint64_t j, const double* d_x,
+                     const double* d_scale_src, int scale_mode, double* d_v_out,
+                     uint64_t* d_bad_index, void* stream);
+/* read_block / read_element (basis.cpp:117-166): rows [first, first+count) */
+int cbgx_basis_read(const cbgx_basis* V, uint64_t j, uint64_t first, uint64_t count,
+                    double* d_out, void* stream);
+
+/* Reduction order. TREE: fixed-shape, deterministic two-stage tree (CTA
+ * partials combined in CTA order) -- the fast path. REFERENCE: the exact
+ * sequential order of the reference (basis.cpp:168-187 per-block-then-
+ * running-total for basis dots, sparse.cpp:58-67 for dot/norm2), on one
+ * thread per column -- a parity/debug mode for small n that reproduces the
+ * reference bit for bit. */
+enum { CBGX_REDUCE_TREE = 0, CBGX_REDUCE_REFERENCE = 1 };
+
+/* Classical Gram-Schmidt projection, fused with decompression:
+ * d_h[i] = <V_{first+i}, w> for i < cols (KrylovBasis::dot, basis.cpp:168-187,
+ * called cols times by arnoldi_orthogonalize, gmres.cpp:44-46); if
+ * with_wnorm, d_h[cols] = <w, w> (the omega of gmres.cpp:43). One pass over
+ * w and the cols compressed columns. */
+int cbgx_cgs_dot(const cbgx_basis* V, uint64_t first, uint32_t cols, const double* d_w,
+                 int with_wnorm, int reduction, double* d_h, cbgx_workspace* ws, void* stream);
+/* w -= sum_i d_h[i] V_{first+i}, columns in order, every element
+ * w = w - (h_i * v_i) with two roundings (subtract_scaled, basis.cpp:189-205)
+ * -- bit-identical to the reference. If d_wnorm2 is non-NULL it receives
+ * <w_new, w_new> (h_next^2 of gmres.cpp:50) from the same pass.
+ * h_sign = -1 applies w += sum y_i V_i instead (accumulate_solution,
+ * gmres.cpp:134-139: subtract_scaled with -y_i). */
+int cbgx_cgs_update(const cbgx_basis* V, uint64_t first, uint32_t cols, const double* d_h,
+                    int h_sign, double* d_w, double* d_wnorm2, int reduction,
+                    cbgx_workspace* ws, void* stream);
+
+/* ------------------------------------------------ CSR SpMV and BLAS-1
+ * Reference: sparse.hpp:17-26, sparse.cpp:43-84. Per-row left-to-right
+ * accumulation from +0.0 with separate multiply and add roundings, so SpMV
+ * is bit-identical to the reference. row_ptr is int32 or int64
+ * (row_ptr_bits 32/64); col_idx is int32 (local column index). */
+typedef struct {
+    uint64_t n_rows;
+    uint64_t n_cols;
+    uint64_t nnz;
+    const void* d_row_ptr;
+    uint32_t row_ptr_bits;
+    const int32_t* d_col_idx;
+    const double* d_values;
+} cbgx_csr;
+
+/* y = A x; if d_ynorm2, also <y, y> (fused epilogue). */
+int cbgx_csr_spmv(const cbgx_csr* A, const double* d_x, double* d_y, double* d_ynorm2,
+                  int reduction, cbgx_workspace* ws, void* stream);
+/* r = b - A x (gmres.cpp:181-184); if d_rnorm2, also <r, r>. */
+int cbgx_csr_residual(const cbgx_csr* A, const double* d_x, const double* d_b, double* d_r,
+                      double* d_rnorm2, int reduction, cbgx_workspace* ws, void* stream);
+/* deterministic <x, y> (sparse.cpp:58-67) */
+int cbgx_dot(const double* d_x, const double* d_y, uint64_t n, int reduction, double* d_out,
+             cbgx_workspace* ws, void* stream);
+/* x *= alpha (sparse.cpp:80-84) and y += alpha x (:71-78) */
+int cbgx_scale(double alpha, double* d_x, uint64_t n, void* stream);
+int cbgx_axpy(double alpha, const double* d_x, double* d_y, uint64_t n, void* stream);
+
+/* Device-side generators (no host CSR round trip for the big configs).
+ * kind 0: 7-pt Poisson (centre 6, neighbours -1); 1: 7-pt upwind
+ * convection-diffusion (centre 6+3pe, x-1/y-1/z-1 -(1+pe), upper -1);
+ * 2: 27-pt (centre 26, neighbours -1). Row (iz*ny+iy)*nx+ix, Dirichlet
+ * truncation, columns ascending -- the 3-D analogue of gen_convdiff
+ * (sparse.cpp:249-291). Rows [row_begin, row_end) only; columns are global
+ * indices minus col_offset (row partitions with ghost remap pass
+ * col_offset = 0 and remap later). */
+uint64_t cbgx_stencil_nnz(int kind, uint64_t nx, uint64_t ny, uint64_t nz,
+                          uint64_t row_begin, uint64_t row_end);
+int cbgx_stencil_generate(int kind, uint64_t nx, uint64_t ny, uint64_t nz, double pe,
+                          uint64_t row_begin, uint64_t row_end, int64_t col_offset,
+                          void* d_row_ptr, uint32_t row_ptr_bits, int32_t* d_col_idx,
+                          double* d_values, void* stream);
+
+/* ------------------------------------------------------------- solver
+ * Reference: gmres.hpp:17-115, gmres.cpp:141-252. Restarted GMRES with the
+ * Krylov basis in `format`, CGS + at most one re-orthogonalisation pass,
+ * host-side incremental Givens least squares, explicit residual at every
+ * restart; convergence only on the explicit residual. */
+typedef struct {
+    uint64_t restart;               /* m (default 100) */
+    double target_rrn;              /* default 1e-10 */
+    uint64_t max_total_iterations;  /* default 20000 */
+    double eta;                     /* default 0.70710678118654752 */
+    uint32_t format_kind;           /* CBGX_F64 / F32 / F16 / FRSZ2 */
+    uint32_t bit_length;            /* FRSZ2: 16 / 21 / 32 */
+    uint32_t reduction;             /* CBGX_REDUCE_TREE / REFERENCE */
+    uint32_t flags;                 /* CBGX_SOLVER_* */
+} cbgx_gmres_config;
+
+enum {
+    CBGX_SOLVER_PHASE_TIMING = 1   /* record CUDA events around every phase */
+};
+
+typedef struct {
+    uint64_t* iteration;   /* caller arrays of `capacity` entries (may be NULL) */
+    double* rrn;
+    uint8_t* is_explicit;
+    uint64_t capacity;
+    uint64_t length;       /* out: records produced (may exceed capacity) */
+} cbgx_history;
+
+enum { CBGX_PHASE_SPMV = 0, CBGX_PHASE_DOT, CBGX_PHASE_UPDATE, CBGX_PHASE_WRITE,
+       CBGX_PHASE_RESIDUAL, CBGX_PHASE_SOLUTION, CBGX_PHASE_COMM, CBGX_PHASE_HOST,
+       CBGX_NUM_PHASES };
+
+typedef struct {
+    int converged;
+    uint64_t total_iterations;
+    uint64_t restarts;
+    double final_rrn;
+    double wall_seconds;               /* host clock around the solve (gmres.cpp:153-159) */
+    uint64_t reorth_passes;
+    double phase_ms[CBGX_NUM_PHASES];      /* device time per phase (PHASE_TIMING) */
+    double phase_bytes[CBGX_NUM_PHASES];   /* algorithmic HBM bytes per phase */
+    uint64_t phase_launches[CBGX_NUM_PHASES];
+    uint64_t kernel_launches;          /* kernels this solve launched */
+} cbgx_solve_stats;
+
+typedef struct cbgx_comm cbgx_comm;
+typedef struct cbgx_solver cbgx_solver;
+
+/* Device-resident solver for one (local) matrix. A is borrowed (must
+ * outlive the solver). comm may be NULL (single GPU). */
+int cbgx_solver_create(const cbgx_csr* A, const cbgx_gmres_config* cfg, cbgx_comm* comm,
+                       cbgx_solver** out);
+int cbgx_solver_destroy(cbgx_solver* s);
+/* gmres_solve on device vectors (local rows). d_x receives the solution. */
+int cbgx_solver_solve(cbgx_solver* s, const double* d_b, const double* d_x0, double* d_x,
+                      cbgx_history* hist, cbgx_solve_stats* stats, void* stream);
+
+/* Host-buffer drop-in for gmres_solve(const CsrMatrix&, span b, span x0,
+ * cfg) (gmres.hpp:113-115): size_t CSR as in CsrMatrix, uploads, solves on
+ * the current device, downloads the solution. */
+int cbgx_gmres_solve_host(uint64_t n, const uint64_t* row_ptrs, const uint64_t* col_idx,
+                          const double* values, const double* b, const double* x0,
+                          const cbgx_gmres_config* cfg, double* x_out, cbgx_history* hist,
+                          cbgx_solve_stats* stats);
+
+/* ---------------------------------------------- multi-GPU row partition
+ * One process per GPU; each rank owns rows [row_begin, row_end) (multiples
+ * of 32 so every FRSZ2 block is rank-local). Reductions: every rank's
+ * partial vector is all-gathered and summed in rank order (deterministic,
+ * identical on all ranks); SpMV ghosts move by a halo exchange. */
+int cbgx_nccl_unique_id(uint8_t out[128]);
+int cbgx_comm_create_nccl(const uint8_t unique_id[128], int nranks, int rank,
+                          cbgx_comm** out);
+int cbgx_comm_destroy(cbgx_comm* c);
+int cbgx_comm_rank(const cbgx_comm* c, int* rank, int* nranks);
+
+/* Halo plan for a row block whose CSR uses GLOBAL column indices (host
+ * arrays, int64 columns): computes the ghost set, exchanges request lists
+ * with the owners and remaps the block's columns to local indices
+ * (own rows first, then ghosts ordered by owner rank and global index,
+ * keeping each row's nonzero order). Collective over the communicator. */
+typedef struct cbgx_halo cbgx_halo;
+int cbgx_halo_create(cbgx_comm* c, uint64_t row_begin, uint64_t row_end, uint64_t n_global,
+                     const int64_t* d_global_cols, uint64_t nnz, int32_t* d_local_cols_out,
+                     cbgx_halo** out);
+int cbgx_halo_destroy(cbgx_halo* h);
+uint64_t cbgx_halo_ghosts(const cbgx_halo* h);
+
+/* Distributed solve: A_local has n_rows = local rows and columns already
+ * remapped by cbgx_halo_create; vectors are local (own rows). */
+int cbgx_solver_create_dist(const cbgx_csr* A_local, cbgx_halo* halo,
+                            const cbgx_gmres_config* cfg, cbgx_comm* comm,
+                            cbgx_solver** out);
+
+/* Single-GPU test harness for the partitioned solver: splits A into P row
+ * blocks (32-aligned), runs P ranks as P host threads on the current
+ * device with an in-process communicator, and returns rank 0's view. */
+int cbgx_gmres_solve_partitioned_local(uint64_t n, const uint64_t* row_ptrs,
+                                       const uint64_t* col_idx, const double* values,
+                                       const double* b, const double* x0,
+                                       const cbgx_gmres_config* cfg, int parts,
+                                       double* x_out, cbgx_history* hist,
+                                       cbgx_solve_stats* stats);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* CBGX_H */

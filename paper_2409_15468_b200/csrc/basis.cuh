@@ -1,0 +1,372 @@
+// basis.cuh -- Krylov basis panel access: per-format loaders/decoders shared
+// by the fused CGS kernels, the basis write/read kernels and the
+// reference-order (serial) kernels.
+//
+// Reference: basis.hpp:23-83, basis.cpp:85-205; codec kernels.hpp:18-58.
+#pragma once
+
+#include <cuda_fp16.h>
+
+#include "cbgx.h"
+#include "common.cuh"
+
+namespace cbgx {
+
+// Storage format tags (compile-time).
+enum Fmt : int { kF64 = 0, kF32 = 1, kF16 = 2, kZ16 = 3, kZ21 = 4, kZ32 = 5 };
+
+template <int F> struct FmtInfo;
+template <> struct FmtInfo<kF64> { static constexpr int L = 0;  static constexpr bool frsz = false; };
+template <> struct FmtInfo<kF32> { static constexpr int L = 0;  static constexpr bool frsz = false; };
+template <> struct FmtInfo<kF16> { static constexpr int L = 0;  static constexpr bool frsz = false; };
+template <> struct FmtInfo<kZ16> { static constexpr int L = 16; static constexpr bool frsz = true; };
+template <> struct FmtInfo<kZ21> { static constexpr int L = 21; static constexpr bool frsz = true; };
+template <> struct FmtInfo<kZ32> { static constexpr int L = 32; static constexpr bool frsz = true; };
+
+inline int fmt_of(const cbgx_basis& B) {
+    switch (B.kind) {
+    case CBGX_F64: return kF64;
+    case CBGX_F32: return kF32;
+    case CBGX_F16: return kF16;
+    case CBGX_FRSZ2:
+        if (B.bit_length == 16) return kZ16;
+        if (B.bit_length == 21) return kZ21;
+        if (B.bit_length == 32) return kZ32;
+        break;
+    }
+    throw Error(CBGX_EINVAL, "storage format: frsz2 bit length must be 16, 21 or 32");
+}
+
+// Plain-old-data view passed to kernels.
+struct BasisView {
+    const unsigned char* data;
+    const uint32_t* exp;
+    uint64_t col_stride_bytes;
+    uint64_t exp_col_stride;
+    uint64_t n;
+    uint64_t n_pad;
+};
+
+inline BasisView view_of(const cbgx_basis& B) {
+    return BasisView{static_cast<const unsigned char*>(B.d_data), B.d_exp, B.col_stride_bytes,
+                     B.exp_col_stride, B.n, B.n_pad};
+}
+
+// ---------------------------------------------------- binary16 (half.cpp)
+// half_to_double, half.cpp:62-81 (exact widening).
+__device__ __forceinline__ double half_bits_to_double(uint32_t h) {
+    const uint32_t e = (h >> 10) & 31u, f = h & 1023u;
+    const unsigned long long s = static_cast<unsigned long long>(h >> 15) << 63;
+    if (e == 0) {
+        const double mag = static_cast<double>(f) * 0x1p-24;
+        return (h & 0x8000u) ? -mag : mag;
+    }
+    if (e == 31) {
+        return __longlong_as_double(static_cast<long long>(s | (0x7FFull << 52) | (f ? static_cast<unsigned long long>(f) << 42 : 0ull)));
+    }
+    return __longlong_as_double(static_cast<long long>(s | (static_cast<unsigned long long>(e - 15 + 1023) << 52) |
+                                                       (static_cast<unsigned long long>(f) << 42)));
+}
+
+// half_from_double, half.cpp:9-60 (RNE, saturating to +-65504).
+__device__ __forceinline__ uint16_t double_to_half_bits(double x) {
+    const unsigned long long b = static_cast<unsigned long long>(__double_as_longlong(x));
+    const uint32_t s = static_cast<uint32_t>((b >> 48) & 0x8000u);
+    const int e = static_cast<int>((b >> 52) & 0x7FF);
+    const unsigned long long f = b & ((1ull << 52) - 1);
+    if (e == 0x7FF) return static_cast<uint16_t>(s | (f ? 0x7E00u : 0x7BFFu));
+    if (e == 0) return static_cast<uint16_t>(s);
+    const int ue = e - 1023;
+    if (ue >= 16) return static_cast<uint16_t>(s | 0x7BFFu);
+    unsigned long long sig;
+    int drop;
+    if (ue >= -14) {
+        sig = f;
+        drop = 42;
+    } else {
+        sig = f | (1ull << 52);
+        drop = 28 - ue;
+        if (drop >= 54) return static_cast<uint16_t>(s);
+    }
+    unsigned long long keep = sig >> drop;
+    const unsigned long long rest = sig & ((1ull << drop) - 1);
+    const unsigned long long halfp = 1ull << (drop - 1);
+    if (rest > halfp || (rest == halfp && (keep & 1))) ++keep;
+    if (ue >= -14) {
+        uint32_t he = static_cast<uint32_t>(ue + 15);
+        if (keep == 1024) {
+            keep = 0;
+            ++he;
+        }
+        if (he >= 31) return static_cast<uint16_t>(s | 0x7BFFu);
+        return static_cast<uint16_t>(s | (he << 10) | static_cast<uint32_t>(keep));
+    }
+    return static_cast<uint16_t>(s | static_cast<uint32_t>(keep));
+}
+
+// ------------------------------------------------ single-element decode
+template <int F>
+__device__ __forceinline__ double basis_value(const BasisView& B, uint64_t col, uint64_t row) {
+    const unsigned char* base = B.data + col * B.col_stride_bytes;
+    if constexpr (F == kF64) {
+        return reinterpret_cast<const double*>(base)[row];
+    } else if constexpr (F == kF32) {
+        return static_cast<double>(reinterpret_cast<const float*>(base)[row]);
+    } else if constexpr (F == kF16) {
+        return half_bits_to_double(reinterpret_cast<const uint16_t*>(base)[row]);
+    } else {
+        constexpr int L = FmtInfo<F>::L;
+        const uint32_t* w = reinterpret_cast<const uint32_t*>(base);
+        const uint32_t e = B.exp[col * B.exp_col_stride + row / 32];
+        uint32_t code;
+        if constexpr (L == 32) {
+            code = w[row];
+        } else if constexpr (L == 16) {
+            code = reinterpret_cast<const uint16_t*>(w)[row];
+        } else {
+            const uint64_t bit = (row / 32) * 672 + (row % 32) * 21;
+            const uint64_t q = bit >> 5;
+            const unsigned long long win = (static_cast<unsigned long long>(w[q + 1]) << 32) | w[q];
+            code = static_cast<uint32_t>(win >> (bit & 31)) & 0x1FFFFFu;
+        }
+        return BlockDecoder<L>(e)(code);
+    }
+}
+
+// --------------------------------------- vectorised 4-row step (fast CGS)
+// A thread's step covers 4 consecutive rows r..r+3 (r % 4 == 0), all in the
+// same 32-block, of one column. The fused kernels call
+//   dot(w)        -> sum_k v_k * w_k        (TREE order: any order is allowed)
+//   update(h, w)  -> w_k = w_k - h * v_k    (two roundings: bit-identical)
+//
+// FRSZ2 fast path. With scale = 2^(e_max-1023-(L-2)) a value is
+// v = +-mag * scale exactly, so
+//   dot:    the step sum is (sum_k +-mag_k * w_k) * scale  (scale once/step)
+//   update: h * v = +-(mag * (h * scale)) where hs = h * scale is exact
+//           whenever it stays in the normal range (checked per step), hence
+//           RN(h*v) = +-RN(mag*hs) bit for bit.
+// Per value that is: mask, I2F.F64.U32, a sign LOP3 on the high word and one
+// FP64 op. Blocks where the fast path is not exact (e_max <= L-2, where the
+// reference flushes tiny values to zero, or hs outside the normal range)
+// take the exact decoder (BlockDecoder) out of line.
+
+// Sign-magnitude codes split for the fast path: magnitude and the sign moved
+// to bit 31.
+struct Codes4 {
+    uint32_t mag[4];
+    uint32_t sgn[4];
+};
+
+__device__ __forceinline__ double signed_i2f(uint32_t mag, uint32_t sgn) {
+    const double d = __uint2double_rn(mag);
+    return __hiloint2double(__double2hiint(d) ^ static_cast<int>(sgn), __double2loint(d));
+}
+
+template <int L>
+__device__ __forceinline__ double fast_dot(const Codes4& c, uint32_t e, const double w[4]) {
+    double s = __dmul_rn(signed_i2f(c.mag[0], c.sgn[0]), w[0]);
+#pragma unroll
+    for (int k = 1; k < 4; ++k) s = fma(signed_i2f(c.mag[k], c.sgn[k]), w[k], s);
+    return __dmul_rn(s, __hiloint2double(static_cast<int>((e - (L - 2)) << 20), 0));
+}
+
+// Exact per-step decode (rare path), kept out of line.
+template <int L>
+__device__ __forceinline__ void slow_decode(const Codes4& c, uint32_t e, double v[4]) {
+    const BlockDecoder<L> d(e);
+#pragma unroll
+    for (int k = 0; k < 4; ++k) {
+        const uint32_t code = c.mag[k] | (c.sgn[k] >> (32 - L));
+        v[k] = d(code);
+    }
+}
+
+template <int L>
+__device__ __forceinline__ double frsz_dot(const Codes4& c, uint32_t e, const double w[4]) {
+    if (__builtin_expect(e > L - 2, 1)) return fast_dot<L>(c, e, w);
+    double v[4];
+    slow_decode<L>(c, e, v);
+    double s = __dmul_rn(v[0], w[0]);
+#pragma unroll
+    for (int k = 1; k < 4; ++k) s = fma(v[k], w[k], s);
+    return s;
+}
+
+// h_exp: biased exponent field of h (hoisted per column by the caller).
+template <int L>
+__device__ __forceinline__ void frsz_update(const Codes4& c, uint32_t e, double h, int h_exp, double w[4]) {
+    const int es = static_cast<int>(e) - (L - 2);          // scale's biased exponent
+    const int hse = h_exp + es - 1023;                      // exponent of h*scale
+    const bool ok = es > 0 && (h == 0.0 || (h_exp != 0 && hse >= 1 && hse <= 2046));
+    if (__builtin_expect(ok, 1)) {
+        const double hs = __dmul_rn(h, __hiloint2double(es << 20, 0));
+#pragma unroll
+        for (int k = 0; k < 4; ++k) {
+            const double p = __dmul_rn(__uint2double_rn(c.mag[k]), hs);
+            w[k] = __dsub_rn(w[k], __hiloint2double(__double2hiint(p) ^ static_cast<int>(c.sgn[k]), __double2loint(p)));
+        }
+        return;
+    }
+    double v[4];
+    slow_decode<L>(c, e, v);
+#pragma unroll
+    for (int k = 0; k < 4; ++k) w[k] = __dsub_rn(w[k], __dmul_rn(h, v[k]));
+}
+
+template <int F> struct Step;
+
+template <> struct Step<kZ32> {
+    uint4 c;
+    uint32_t e;
+    __device__ __forceinline__ void load(const BasisView& B, uint64_t col, uint64_t r) {
+        c = __ldg(reinterpret_cast<const uint4*>(B.data + col * B.col_stride_bytes) + r / 4);
+        e = __ldg(B.exp + col * B.exp_col_stride + r / 32);
+    }
+    __device__ __forceinline__ Codes4 codes() const {
+        Codes4 k;
+        const uint32_t w[4] = {c.x, c.y, c.z, c.w};
+#pragma unroll
+        for (int i = 0; i < 4; ++i) {
+            k.mag[i] = w[i] & 0x7FFFFFFFu;
+            k.sgn[i] = w[i] & 0x80000000u;
+        }
+        return k;
+    }
+    __device__ __forceinline__ double dot(const double w[4]) const { return frsz_dot<32>(codes(), e, w); }
+    __device__ __forceinline__ void update(double h, int he, double w[4]) const { frsz_update<32>(codes(), e, h, he, w); }
+};
+
+template <> struct Step<kZ16> {
+    uint2 c;
+    uint32_t e;
+    __device__ __forceinline__ void load(const BasisView& B, uint64_t col, uint64_t r) {
+        c = __ldg(reinterpret_cast<const uint2*>(B.data + col * B.col_stride_bytes) + r / 4);
+        e = __ldg(B.exp + col * B.exp_col_stride + r / 32);
+    }
+    __device__ __forceinline__ Codes4 codes() const {
+        Codes4 k;
+        k.mag[0] = c.x & 0x7FFFu;          k.sgn[0] = (c.x << 16) & 0x80000000u;
+        k.mag[1] = (c.x >> 16) & 0x7FFFu;  k.sgn[1] = c.x & 0x80000000u;
+        k.mag[2] = c.y & 0x7FFFu;          k.sgn[2] = (c.y << 16) & 0x80000000u;
+        k.mag[3] = (c.y >> 16) & 0x7FFFu;  k.sgn[3] = c.y & 0x80000000u;
+        return k;
+    }
+    __device__ __forceinline__ double dot(const double w[4]) const { return frsz_dot<16>(codes(), e, w); }
+    __device__ __forceinline__ void update(double h, int he, double w[4]) const { frsz_update<16>(codes(), e, h, he, w); }
+};
+
+template <> struct Step<kZ21> {
+    uint32_t w0, w1, w2, w3;
+    uint32_t sh, e;
+    __device__ __forceinline__ void load(const BasisView& B, uint64_t col, uint64_t r) {
+        const uint32_t* p = reinterpret_cast<const uint32_t*>(B.data + col * B.col_stride_bytes);
+        const uint32_t bit = (static_cast<uint32_t>(r) & 31u) * 21u;  // 0..588
+        const uint64_t q = (r / 32) * 21 + (bit >> 5);
+        sh = bit & 31u;
+        w0 = __ldg(p + q); w1 = __ldg(p + q + 1); w2 = __ldg(p + q + 2); w3 = __ldg(p + q + 3);
+        e = __ldg(B.exp + col * B.exp_col_stride + r / 32);
+    }
+    __device__ __forceinline__ Codes4 codes() const {
+        // code k sits at bit sh + 21k of the 128-bit little-endian window w0..w3
+        const uint32_t o1 = sh + 21, o2 = sh + 42, o3 = sh + 63;
+        uint32_t c[4];
+        c[0] = __funnelshift_r(w0, w1, sh);
+        c[1] = o1 < 32 ? __funnelshift_r(w0, w1, o1) : __funnelshift_r(w1, w2, o1 - 32);
+        c[2] = o2 < 64 ? __funnelshift_r(w1, w2, o2 - 32) : __funnelshift_r(w2, w3, o2 - 64);
+        c[3] = o3 < 64 ? __funnelshift_r(w1, w2, o3 - 32) : __funnelshift_r(w2, w3, o3 - 64);
+        Codes4 k;
+#pragma unroll
+        for (int i = 0; i < 4; ++i) {
+            k.mag[i] = c[i] & 0xFFFFFu;
+            k.sgn[i] = (c[i] << 11) & 0x80000000u;
+        }
+        return k;
+    }
+    __device__ __forceinline__ double dot(const double w[4]) const { return frsz_dot<21>(codes(), e, w); }
+    __device__ __forceinline__ void update(double h, int he, double w[4]) const { frsz_update<21>(codes(), e, h, he, w); }
+};
+
+template <> struct Step<kF64> {
+    double2 a, b;
+    __device__ __forceinline__ void load(const BasisView& B, uint64_t col, uint64_t r) {
+        const double2* p = reinterpret_cast<const double2*>(B.data + col * B.col_stride_bytes) + r / 2;
+        a = __ldg(p);
+        b = __ldg(p + 1);
+    }
+    __device__ __forceinline__ void values(double v[4]) const { v[0] = a.x; v[1] = a.y; v[2] = b.x; v[3] = b.y; }
+    __device__ __forceinline__ double dot(const double w[4]) const {
+        double v[4];
+        values(v);
+        double s = __dmul_rn(v[0], w[0]);
+#pragma unroll
+        for (int k = 1; k < 4; ++k) s = fma(v[k], w[k], s);
+        return s;
+    }
+    __device__ __forceinline__ void update(double h, int, double w[4]) const {
+        double v[4];
+        values(v);
+#pragma unroll
+        for (int k = 0; k < 4; ++k) w[k] = __dsub_rn(w[k], __dmul_rn(h, v[k]));
+    }
+};
+
+template <> struct Step<kF32> {
+    float4 c;
+    __device__ __forceinline__ void load(const BasisView& B, uint64_t col, uint64_t r) {
+        c = __ldg(reinterpret_cast<const float4*>(B.data + col * B.col_stride_bytes) + r / 4);
+    }
+    __device__ __forceinline__ void values(double v[4]) const { v[0] = c.x; v[1] = c.y; v[2] = c.z; v[3] = c.w; }
+    __device__ __forceinline__ double dot(const double w[4]) const {
+        double v[4];
+        values(v);
+        double s = __dmul_rn(v[0], w[0]);
+#pragma unroll
+        for (int k = 1; k < 4; ++k) s = fma(v[k], w[k], s);
+        return s;
+    }
+    __device__ __forceinline__ void update(double h, int, double w[4]) const {
+        double v[4];
+        values(v);
+#pragma unroll
+        for (int k = 0; k < 4; ++k) w[k] = __dsub_rn(w[k], __dmul_rn(h, v[k]));
+    }
+};
+
+template <> struct Step<kF16> {
+    uint2 c;
+    __device__ __forceinline__ void load(const BasisView& B, uint64_t col, uint64_t r) {
+        c = __ldg(reinterpret_cast<const uint2*>(B.data + col * B.col_stride_bytes) + r / 4);
+    }
+    __device__ __forceinline__ void values(double v[4]) const {
+        v[0] = half_bits_to_double(c.x & 0xFFFFu); v[1] = half_bits_to_double(c.x >> 16);
+        v[2] = half_bits_to_double(c.y & 0xFFFFu); v[3] = half_bits_to_double(c.y >> 16);
+    }
+    __device__ __forceinline__ double dot(const double w[4]) const {
+        double v[4];
+        values(v);
+        double s = __dmul_rn(v[0], w[0]);
+#pragma unroll
+        for (int k = 1; k < 4; ++k) s = fma(v[k], w[k], s);
+        return s;
+    }
+    __device__ __forceinline__ void update(double h, int, double w[4]) const {
+        double v[4];
+        values(v);
+#pragma unroll
+        for (int k = 0; k < 4; ++k) w[k] = __dsub_rn(w[k], __dmul_rn(h, v[k]));
+    }
+};
+
+// Stored bytes per value of a format (algorithmic traffic accounting).
+inline double stored_bytes_per_value(int f) {
+    switch (f) {
+    case kF64: return 8.0;
+    case kF32: return 4.0;
+    case kF16: return 2.0;
+    case kZ16: return 17.0 / 8.0;
+    case kZ21: return 22.0 / 8.0;
+    default: return 33.0 / 8.0;
+    }
+}
+
+}  // namespace cbgx

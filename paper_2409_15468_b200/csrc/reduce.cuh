@@ -1,0 +1,58 @@
+// reduce.cuh -- deterministic two-stage reduction epilogue shared by every
+// reducing kernel (CGS dot/update norms, SpMV norms, BLAS-1 dot).
+#pragma once
+
+#include <cuda_runtime.h>
+
+#include <cstdint>
+
+#include "runtime.h"
+
+namespace cbgx {
+
+// red: shared [nwarps][ncol] per-warp partials. Writes this CTA's row of
+// partials[gridDim.x][ncol]; the last CTA to arrive (ticket) sums the rows
+// in CTA order into out[ncol] and re-arms the ticket. The summation order
+// depends only on gridDim.x, so results are bit-reproducible run to run.
+__device__ __forceinline__ void block_finalize(const double* red, int nwarps, uint32_t ncol,
+                                               double* __restrict__ partials,
+                                               unsigned* __restrict__ ticket,
+                                               double* __restrict__ out) {
+    __shared__ bool s_last;
+    for (uint32_t k = threadIdx.x; k < ncol; k += blockDim.x) {
+        double s = red[k];
+        for (int w = 1; w < nwarps; ++w) s = __dadd_rn(s, red[w * ncol + k]);
+        partials[static_cast<uint64_t>(blockIdx.x) * ncol + k] = s;
+    }
+    __threadfence();
+    __syncthreads();
+    if (threadIdx.x == 0) s_last = atomicAdd(ticket, 1u) == gridDim.x - 1;
+    __syncthreads();
+    if (s_last) {
+        __threadfence();
+        for (uint32_t k = threadIdx.x; k < ncol; k += blockDim.x) {
+            double s = __ldcg(partials + k);
+            for (unsigned c = 1; c < gridDim.x; ++c)
+                s = __dadd_rn(s, __ldcg(partials + static_cast<uint64_t>(c) * ncol + k));
+            out[k] = s;
+        }
+        if (threadIdx.x == 0) *ticket = 0u;
+    }
+}
+
+// Deterministic <x, y>. REDUCE_TREE: fixed-shape tree; REDUCE_REFERENCE:
+// one thread, sequential from +0.0 (sparse.cpp:58-67).
+void launch_dot(const double* x, const double* y, uint64_t n, int reduction, double* out,
+                Workspace* ws, cudaStream_t st);
+
+void launch_cgs_dot(const cbgx_basis& V, uint64_t first, uint32_t cols, const double* w, int wn,
+                    int reduction, double* h, Workspace* ws, cudaStream_t st);
+void launch_cgs_update(const cbgx_basis& V, uint64_t first, uint32_t cols, const double* h,
+                       double sign, double* w, double* norm, int reduction, Workspace* ws,
+                       cudaStream_t st);
+void launch_basis_write(const cbgx_basis& V, uint64_t j, const double* x, const double* scale_src,
+                        int scale_mode, double* v_out, uint64_t* bad, cudaStream_t st);
+void launch_basis_read(const cbgx_basis& V, uint64_t j, uint64_t first, uint64_t count, double* out,
+                       cudaStream_t st);
+
+}  // namespace cbgx

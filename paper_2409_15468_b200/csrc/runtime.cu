@@ -1,0 +1,107 @@
+// runtime.cu -- error state, device queries and reduction workspaces for the
+// C-ABI (include/cbgx.h).
+#include <cstdio>
+#include <cstring>
+#include <mutex>
+#include <string>
+
+#include "common.cuh"
+#include "runtime.h"
+
+namespace cbgx {
+
+namespace {
+thread_local std::string t_msg;
+thread_local uint64_t t_index = 0;
+}  // namespace
+
+void set_error(int code, const std::string& msg, uint64_t index) {
+    (void)code;
+    t_msg = msg;
+    t_index = index;
+}
+
+void check_cuda(cudaError_t e, const char* what) {
+    if (e != cudaSuccess) {
+        throw Error(CBGX_ECUDA, std::string("cuda: ") + cudaGetErrorString(e) + " (" + what + ")");
+    }
+}
+
+int current_device() {
+    int d = 0;
+    CBGX_CUDA(cudaGetDevice(&d));
+    return d;
+}
+
+int sm_count() {
+    static int cache[64] = {0};
+    const int d = current_device();
+    if (d < 64 && cache[d]) return cache[d];
+    int v = 0;
+    CBGX_CUDA(cudaDeviceGetAttribute(&v, cudaDevAttrMultiProcessorCount, d));
+    if (d < 64) cache[d] = v;
+    return v;
+}
+
+Workspace::~Workspace() {
+    if (partials) cudaFree(partials);
+    if (counters) cudaFree(counters);
+}
+
+double* Workspace::get_partials(size_t doubles) {
+    if (doubles > partial_cap) {
+        if (partials) CBGX_CUDA(cudaFree(partials));
+        partials = nullptr;
+        size_t cap = partial_cap ? partial_cap : 1024;
+        while (cap < doubles) cap *= 2;
+        CBGX_CUDA(cudaMalloc(&partials, cap * sizeof(double)));
+        partial_cap = cap;
+    }
+    return partials;
+}
+
+unsigned* Workspace::get_counter() {
+    if (!counters) {
+        CBGX_CUDA(cudaMalloc(&counters, kCounters * sizeof(unsigned)));
+        CBGX_CUDA(cudaMemset(counters, 0, kCounters * sizeof(unsigned)));
+    }
+    return counters;
+}
+
+}  // namespace cbgx
+
+using namespace cbgx;
+
+extern "C" {
+
+const char* cbgx_last_error(void) { return t_msg.c_str(); }
+uint64_t cbgx_last_error_index(void) { return t_index; }
+int cbgx_version(void) { return 1; }
+
+int cbgx_device_info(int* device, int* sms, int64_t* l2) {
+    return guard([&] {
+        int d = current_device();
+        if (device) *device = d;
+        if (sms) *sms = sm_count();
+        if (l2) {
+            int v = 0;
+            CBGX_CUDA(cudaDeviceGetAttribute(&v, cudaDevAttrL2CacheSize, d));
+            *l2 = v;
+        }
+    });
+}
+
+int cbgx_workspace_create(cbgx_workspace** ws) {
+    return guard([&] {
+        if (!ws) throw Error(CBGX_EINVAL, "workspace: null output");
+        auto* w = new Workspace();
+        w->device = current_device();
+        *ws = reinterpret_cast<cbgx_workspace*>(w);
+    });
+}
+
+int cbgx_workspace_destroy(cbgx_workspace* ws) {
+    return guard([&] { delete reinterpret_cast<Workspace*>(ws); });
+}
+
+}  // extern "C"

@@ -1,0 +1,85 @@
+// solver.h -- device-resident restarted CB-GMRES driver (host control loop).
+#pragma once
+
+#include <cuda_runtime.h>
+
+#include <cstdint>
+#include <memory>
+#include <vector>
+
+#include "cbgx.h"
+#include "runtime.h"
+
+namespace cbgx {
+
+// Cross-rank plumbing for the row-partitioned solve. A null Comm means one
+// rank (single GPU).
+struct Comm {
+    virtual ~Comm() = default;
+    virtual int rank() const = 0;
+    virtual int size() const = 0;
+    // d_vals[0..count) hold this rank's partial sums. Replace them by the
+    // sum over ranks taken in rank order 0..P-1 (identical on every rank,
+    // independent of the collective's algorithm).
+    virtual void sum_partials(double* d_vals, size_t count, cudaStream_t st) = 0;
+    // Gather `bytes` from every rank into d_recv[rank * bytes].
+    virtual void allgather(const void* d_send, void* d_recv, size_t bytes, cudaStream_t st) = 0;
+    struct Msg {
+        int peer;
+        void* d_buf;
+        size_t bytes;
+    };
+    // Grouped point-to-point exchange (all sends and receives in flight together).
+    virtual void exchange(const std::vector<Msg>& sends, const std::vector<Msg>& recvs,
+                          cudaStream_t st) = 0;
+    virtual void barrier(cudaStream_t st) = 0;
+};
+
+// Halo plan: which own rows each peer needs (packed by a gather kernel),
+// and where each peer's ghosts land in the local vector (after the own rows).
+struct Halo {
+    Comm* comm = nullptr;
+    uint64_t n_local = 0;
+    uint64_t n_ghost = 0;
+    std::vector<int> send_peers, recv_peers;
+    std::vector<uint64_t> send_offsets;   // into d_send_idx / d_send_buf (size peers+1)
+    std::vector<uint64_t> recv_offsets;   // into ghost region (size peers+1)
+    int32_t* d_send_idx = nullptr;        // local row indices to pack
+    double* d_send_buf = nullptr;
+    ~Halo();
+    void exchange(double* d_vec, cudaStream_t st) const;  // fills d_vec[n_local..)
+};
+
+class Solver {
+public:
+    Solver(const cbgx_csr& A, const cbgx_gmres_config& cfg, Comm* comm, Halo* halo);
+    ~Solver();
+    void solve(const double* d_b, const double* d_x0, double* d_x, cbgx_history* hist,
+               cbgx_solve_stats* stats, cudaStream_t st);
+
+private:
+    struct PhaseTimer;
+    void reduce(double* d_vals, size_t count, cudaStream_t st);
+    double fetch_scalar(const double* d, cudaStream_t st);
+
+    cbgx_csr A_;
+    cbgx_gmres_config cfg_;
+    Comm* comm_;
+    Halo* halo_;
+    uint64_t n_;
+    cbgx_basis V_{};
+    void* d_basis_ = nullptr;
+    uint32_t* d_exp_ = nullptr;
+    double* d_r_ = nullptr;
+    double* d_v_ = nullptr;   // n + ghosts
+    double* d_w_ = nullptr;
+    double* d_scal_ = nullptr;   // [0] omega^2 [1] hn^2 [2] ||b||^2 [3] ||r||^2 [4..] h / u / y
+    double* h_pinned_ = nullptr;
+    Workspace ws_;
+};
+
+struct SolverHandle {
+    std::unique_ptr<Solver> solver;
+};
+
+}  // namespace cbgx

@@ -1,0 +1,284 @@
+// sparse.cu -- CSR SpMV (fused norm / residual epilogues), BLAS-1 and the
+// device-side 3-D stencil generators.
+//
+// Reference: sparse.cpp:43-84 (spmv, dot, norm2, scale, axpy), gmres.cpp:
+// 181-190 (explicit residual). SpMV accumulates each row left to right from
+// +0.0 with separate multiply/add roundings, so y is bit-identical to the
+// reference; only the fused norms depend on the (fixed) reduction tree.
+#include <cub/device/device_scan.cuh>
+
+#include <algorithm>
+
+#include "common.cuh"
+#include "reduce.cuh"
+#include "runtime.h"
+
+namespace cbgx {
+
+namespace {
+
+constexpr int kThreads = 256;
+constexpr int kWarps = kThreads / 32;
+
+int rows_grid(uint64_t rows) {
+    const uint64_t want = (rows + kThreads - 1) / kThreads;
+    const uint64_t cap = static_cast<uint64_t>(sm_count()) * 8;
+    return static_cast<int>(std::max<uint64_t>(1, std::min(want, cap)));
+}
+
+// MODE 0: y = A x.  MODE 1: y = b - A x.
+template <typename RP, int MODE>
+__global__ void __launch_bounds__(kThreads)
+spmv_kernel(uint64_t n_rows, const RP* __restrict__ rp, const int32_t* __restrict__ ci,
+            const double* __restrict__ va, const double* __restrict__ x,
+            const double* __restrict__ b, double* __restrict__ y, int with_norm,
+            double* __restrict__ partials, unsigned* __restrict__ ticket,
+            double* __restrict__ norm_out) {
+    __shared__ double red[kWarps];
+    double acc = 0.0;
+    for (uint64_t r = blockIdx.x * static_cast<uint64_t>(kThreads) + threadIdx.x; r < n_rows;
+         r += static_cast<uint64_t>(gridDim.x) * kThreads) {
+        const uint64_t k0 = static_cast<uint64_t>(__ldg(rp + r));
+        const uint64_t k1 = static_cast<uint64_t>(__ldg(rp + r + 1));
+        double s = 0.0;
+        for (uint64_t k = k0; k < k1; ++k) s = __dadd_rn(s, __dmul_rn(__ldg(va + k), __ldg(x + __ldg(ci + k))));
+        if (MODE == 1) s = __dsub_rn(__ldg(b + r), s);
+        y[r] = s;
+        if (with_norm) acc = __dadd_rn(acc, __dmul_rn(s, s));
+    }
+    if (!with_norm) return;
+    acc = warp_sum(acc);
+    if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = acc;
+    __syncthreads();
+    block_finalize(red, kWarps, 1, partials, ticket, norm_out);
+}
+
+__global__ void __launch_bounds__(kThreads)
+dot_kernel(const double* __restrict__ x, const double* __restrict__ y, uint64_t n,
+           double* __restrict__ partials, unsigned* __restrict__ ticket, double* __restrict__ out) {
+    __shared__ double red[kWarps];
+    double acc = 0.0;
+    for (uint64_t i = blockIdx.x * static_cast<uint64_t>(kThreads) + threadIdx.x; i < n;
+         i += static_cast<uint64_t>(gridDim.x) * kThreads)
+        acc = __dadd_rn(acc, __dmul_rn(x[i], y[i]));
+    acc = warp_sum(acc);
+    if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = acc;
+    __syncthreads();
+    block_finalize(red, kWarps, 1, partials, ticket, out);
+}
+
+__global__ void serial_dot_kernel(const double* __restrict__ x, const double* __restrict__ y,
+                                  uint64_t n, double* __restrict__ out) {
+    double s = 0.0;
+    for (uint64_t i = 0; i < n; ++i) s = __dadd_rn(s, __dmul_rn(x[i], y[i]));
+    *out = s;
+}
+
+__global__ void scale_kernel(double a, double* __restrict__ x, uint64_t n) {
+    for (uint64_t i = blockIdx.x * static_cast<uint64_t>(blockDim.x) + threadIdx.x; i < n;
+         i += static_cast<uint64_t>(gridDim.x) * blockDim.x)
+        x[i] = __dmul_rn(x[i], a);
+}
+
+__global__ void axpy_kernel(double a, const double* __restrict__ x, double* __restrict__ y, uint64_t n) {
+    for (uint64_t i = blockIdx.x * static_cast<uint64_t>(blockDim.x) + threadIdx.x; i < n;
+         i += static_cast<uint64_t>(gridDim.x) * blockDim.x)
+        y[i] = __dadd_rn(y[i], __dmul_rn(a, x[i]));
+}
+
+// ------------------------------------------------------ stencils
+struct Grid3 {
+    uint64_t nx, ny, nz;
+};
+
+__host__ __device__ __forceinline__ int stencil_count(int kind, Grid3 g, uint64_t row) {
+    const uint64_t x = row % g.nx, y = (row / g.nx) % g.ny, z = row / (g.nx * g.ny);
+    const int cx = 1 + (x > 0) + (x + 1 < g.nx);
+    const int cy = 1 + (y > 0) + (y + 1 < g.ny);
+    const int cz = 1 + (z > 0) + (z + 1 < g.nz);
+    return kind == 2 ? cx * cy * cz : (cx + cy + cz - 2);
+}
+
+template <typename RP>
+__global__ void stencil_count_kernel(int kind, Grid3 g, uint64_t row_begin, uint64_t rows,
+                                     RP* __restrict__ counts) {
+    for (uint64_t i = blockIdx.x * static_cast<uint64_t>(blockDim.x) + threadIdx.x; i <= rows;
+         i += static_cast<uint64_t>(gridDim.x) * blockDim.x)
+        counts[i] = i < rows ? static_cast<RP>(stencil_count(kind, g, row_begin + i)) : RP(0);
+}
+
+// Emits row entries in ascending column order (dz, dy, dx lexicographic),
+// the 3-D analogue of gen_convdiff's S, W, C, E, N order (sparse.cpp:265-286).
+template <typename RP>
+__global__ void stencil_fill_kernel(int kind, Grid3 g, double pe, uint64_t row_begin, uint64_t rows,
+                                    int64_t col_offset, const RP* __restrict__ rp,
+                                    int32_t* __restrict__ ci, double* __restrict__ va) {
+    const double centre = kind == 0 ? 6.0 : (kind == 1 ? 6.0 + 3.0 * pe : 26.0);
+    const double upwind = kind == 1 ? -(1.0 + pe) : -1.0;
+    for (uint64_t i = blockIdx.x * static_cast<uint64_t>(blockDim.x) + threadIdx.x; i < rows;
+         i += static_cast<uint64_t>(gridDim.x) * blockDim.x) {
+        const uint64_t row = row_begin + i;
+        const int64_t x = row % g.nx, y = (row / g.nx) % g.ny, z = row / (g.nx * g.ny);
+        uint64_t k = static_cast<uint64_t>(rp[i]);
+        for (int dz = -1; dz <= 1; ++dz)
+            for (int dy = -1; dy <= 1; ++dy)
+                for (int dx = -1; dx <= 1; ++dx) {
+                    const int nzc = (dx != 0) + (dy != 0) + (dz != 0);
+                    if (kind != 2 && nzc > 1) continue;
+                    if (x + dx < 0 || x + dx >= static_cast<int64_t>(g.nx)) continue;
+                    if (y + dy < 0 || y + dy >= static_cast<int64_t>(g.ny)) continue;
+                    if (z + dz < 0 || z + dz >= static_cast<int64_t>(g.nz)) continue;
+                    const int64_t col = static_cast<int64_t>(row) +
+                                        (dz * static_cast<int64_t>(g.ny) + dy) * static_cast<int64_t>(g.nx) + dx;
+                    double v = -1.0;
+                    if (nzc == 0) v = centre;
+                    else if (dx < 0 || dy < 0 || dz < 0) v = upwind;
+                    ci[k] = static_cast<int32_t>(col - col_offset);
+                    va[k] = v;
+                    ++k;
+                }
+    }
+}
+
+template <typename RP>
+void stencil_generate(int kind, Grid3 g, double pe, uint64_t rb, uint64_t re, int64_t col_offset,
+                      RP* rp, int32_t* ci, double* va, cudaStream_t st) {
+    const uint64_t rows = re - rb;
+    const int grid = static_cast<int>(std::min<uint64_t>((rows + 256) / 256 + 1, sm_count() * 16ull));
+    stencil_count_kernel<RP><<<grid, 256, 0, st>>>(kind, g, rb, rows, rp);
+    CBGX_CUDA(cudaGetLastError());
+    size_t tmp_bytes = 0;
+    CBGX_CUDA(cub::DeviceScan::ExclusiveSum(nullptr, tmp_bytes, rp, rp, rows + 1, st));
+    void* tmp = nullptr;
+    CBGX_CUDA(cudaMallocAsync(&tmp, tmp_bytes, st));
+    CBGX_CUDA(cub::DeviceScan::ExclusiveSum(tmp, tmp_bytes, rp, rp, rows + 1, st));
+    CBGX_CUDA(cudaFreeAsync(tmp, st));
+    stencil_fill_kernel<RP><<<grid, 256, 0, st>>>(kind, g, pe, rb, rows, col_offset, rp, ci, va);
+    CBGX_CUDA(cudaGetLastError());
+}
+
+void check_csr(const cbgx_csr* A) {
+    if (!A) throw Error(CBGX_EINVAL, "csr: null matrix");
+    if (A->row_ptr_bits != 32 && A->row_ptr_bits != 64) throw Error(CBGX_EINVAL, "csr: row_ptr_bits must be 32 or 64");
+    if (A->row_ptr_bits == 32 && A->nnz > 0x7FFFFFFFull) throw Error(CBGX_EINVAL, "csr: nnz needs 64-bit row_ptr");
+}
+
+}  // namespace
+
+void launch_spmv(const cbgx_csr& A, const double* x, const double* b, double* y, double* norm,
+                 int reduction, Workspace* ws, cudaStream_t st) {
+    const int grid = rows_grid(A.n_rows);
+    const bool fused = norm && reduction == CBGX_REDUCE_TREE;
+    double* partials = fused ? ws->get_partials(grid) : nullptr;
+    unsigned* ticket = fused ? ws->get_counter() : nullptr;
+#define CBGX_SPMV(RP, MODE)                                                                     \
+    spmv_kernel<RP, MODE><<<grid, kThreads, 0, st>>>(A.n_rows, static_cast<const RP*>(A.d_row_ptr), \
+                                                     A.d_col_idx, A.d_values, x, b, y, fused,     \
+                                                     partials, ticket, norm)
+    if (A.row_ptr_bits == 32) {
+        if (b) CBGX_SPMV(int32_t, 1); else CBGX_SPMV(int32_t, 0);
+    } else {
+        if (b) CBGX_SPMV(int64_t, 1); else CBGX_SPMV(int64_t, 0);
+    }
+#undef CBGX_SPMV
+    CBGX_CUDA(cudaGetLastError());
+    if (norm && !fused) launch_dot(y, y, A.n_rows, CBGX_REDUCE_REFERENCE, norm, ws, st);
+}
+
+void launch_dot(const double* x, const double* y, uint64_t n, int reduction, double* out,
+                Workspace* ws, cudaStream_t st) {
+    if (reduction == CBGX_REDUCE_REFERENCE) {
+        serial_dot_kernel<<<1, 1, 0, st>>>(x, y, n, out);
+    } else {
+        const int grid = rows_grid(n);
+        dot_kernel<<<grid, kThreads, 0, st>>>(x, y, n, ws->get_partials(grid), ws->get_counter(), out);
+    }
+    CBGX_CUDA(cudaGetLastError());
+}
+
+}  // namespace cbgx
+
+using namespace cbgx;
+
+extern "C" {
+
+int cbgx_csr_spmv(const cbgx_csr* A, const double* d_x, double* d_y, double* d_ynorm2, int reduction,
+                  cbgx_workspace* ws, void* stream) {
+    return guard([&] {
+        check_csr(A);
+        if (d_ynorm2 && !ws) throw Error(CBGX_EINVAL, "spmv: fused norm needs a workspace");
+        launch_spmv(*A, d_x, nullptr, d_y, d_ynorm2, reduction, ws_of(ws), as_stream(stream));
+    });
+}
+
+int cbgx_csr_residual(const cbgx_csr* A, const double* d_x, const double* d_b, double* d_r,
+                      double* d_rnorm2, int reduction, cbgx_workspace* ws, void* stream) {
+    return guard([&] {
+        check_csr(A);
+        if (!d_b) throw Error(CBGX_EINVAL, "residual: null b");
+        if (d_rnorm2 && !ws) throw Error(CBGX_EINVAL, "residual: fused norm needs a workspace");
+        launch_spmv(*A, d_x, d_b, d_r, d_rnorm2, reduction, ws_of(ws), as_stream(stream));
+    });
+}
+
+int cbgx_dot(const double* d_x, const double* d_y, uint64_t n, int reduction, double* d_out,
+             cbgx_workspace* ws, void* stream) {
+    return guard([&] {
+        if (reduction == CBGX_REDUCE_TREE && !ws) throw Error(CBGX_EINVAL, "dot: null workspace");
+        launch_dot(d_x, d_y, n, reduction, d_out, ws_of(ws), as_stream(stream));
+    });
+}
+
+int cbgx_scale(double alpha, double* d_x, uint64_t n, void* stream) {
+    return guard([&] {
+        if (!n) return;
+        scale_kernel<<<rows_grid(n), kThreads, 0, as_stream(stream)>>>(alpha, d_x, n);
+        CBGX_CUDA(cudaGetLastError());
+    });
+}
+
+int cbgx_axpy(double alpha, const double* d_x, double* d_y, uint64_t n, void* stream) {
+    return guard([&] {
+        if (!n) return;
+        axpy_kernel<<<rows_grid(n), kThreads, 0, as_stream(stream)>>>(alpha, d_x, d_y, n);
+        CBGX_CUDA(cudaGetLastError());
+    });
+}
+
+uint64_t cbgx_stencil_nnz(int kind, uint64_t nx, uint64_t ny, uint64_t nz, uint64_t rb, uint64_t re) {
+    // Partial x-lines row by row, whole x-lines in closed form:
+    // sum_x cx = 3nx - 2 (nx >= 1).
+    const Grid3 g{nx, ny, nz};
+    if (nx == 0 || ny == 0 || nz == 0 || rb >= re) return 0;
+    uint64_t total = 0;
+    uint64_t row = rb;
+    while (row < re) {
+        const uint64_t x = row % nx;
+        if (x == 0 && row + nx <= re) {
+            const uint64_t y = (row / nx) % ny, z = row / (nx * ny);
+            const uint64_t cy = 1 + (y > 0) + (y + 1 < ny), cz = 1 + (z > 0) + (z + 1 < nz);
+            const uint64_t sx = 3 * nx - 2;
+            total += kind == 2 ? sx * cy * cz : sx + nx * (cy + cz - 2);
+            row += nx;
+        } else {
+            total += static_cast<uint64_t>(stencil_count(kind, g, row));
+            ++row;
+        }
+    }
+    return total;
+}
+
+int cbgx_stencil_generate(int kind, uint64_t nx, uint64_t ny, uint64_t nz, double pe, uint64_t rb,
+                          uint64_t re, int64_t col_offset, void* d_row_ptr, uint32_t bits,
+                          int32_t* d_col_idx, double* d_values, void* stream) {
+    return guard([&] {
+        if (kind < 0 || kind > 2) throw Error(CBGX_EINVAL, "stencil: kind must be 0, 1 or 2");
+        if (rb > re || re > nx * ny * nz) throw Error(CBGX_ERANGE, "stencil: bad row range");
+        const Grid3 g{nx, ny, nz};
+        if (bits == 32) stencil_generate(kind, g, pe, rb, re, col_offset, static_cast<int32_t*>(d_row_ptr), d_col_idx, d_values, as_stream(stream));
+        else if (bits == 64) stencil_generate(kind, g, pe, rb, re, col_offset, static_cast<int64_t*>(d_row_ptr), d_col_idx, d_values, as_stream(stream));
+        else throw Error(CBGX_EINVAL, "stencil: row_ptr_bits must be 32 or 64");
+    });
+}
+
+}  // extern "C"
