@@ -44,6 +44,10 @@ const char* cbgx_last_error(void);
 /* index (non-finite value) or iteration (breakdown) attached to the last error */
 uint64_t cbgx_last_error_index(void);
 int cbgx_version(void);
+/* kernels launched by this library since load (for launch accounting) */
+uint64_t cbgx_launch_count(void);
+/* make `device` current for this library on the calling thread */
+int cbgx_set_device(int device);
 /* device ordinal, SM count and L2 bytes of the current device */
 int cbgx_device_info(int* device, int* sm_count, int64_t* l2_bytes);
 
@@ -196,6 +200,14 @@ int cbgx_stencil_generate(int kind, uint64_t nx, uint64_t ny, uint64_t nz, doubl
                           void* d_row_ptr, uint32_t row_ptr_bits, int32_t* d_col_idx,
                           double* d_values, void* stream);
 
+/* Host-side right-hand-side recipe of generate_problem (sparse.cpp:233-247):
+ * x_sol[i] = sin(i) / ||s||, s[i] = sin(i) with the C library sin and a
+ * strictly sequential norm over all n (so a row block of a partitioned
+ * problem gets bit-identical values). Fills out[k] = x_sol[first + k] for
+ * k < count; sin is evaluated on `threads` host threads (0 = all cores).
+ * Problem setup, not part of the solve. */
+int cbgx_sin_solution(uint64_t n, uint64_t first, uint64_t count, double* out, int threads);
+
 /* ------------------------------------------------------------- solver
  * Reference: gmres.hpp:17-115, gmres.cpp:141-252. Restarted GMRES with the
  * Krylov basis in `format`, CGS + at most one re-orthogonalisation pass,
@@ -213,7 +225,8 @@ typedef struct {
 } cbgx_gmres_config;
 
 enum {
-    CBGX_SOLVER_PHASE_TIMING = 1   /* record CUDA events around every phase */
+    CBGX_SOLVER_PHASE_TIMING = 1,          /* CUDA events around every phase, summed per solve */
+    CBGX_SOLVER_PHASE_TIMING_DEFERRED = 2  /* record events, collect later (no per-solve sync) */
 };
 
 typedef struct {
@@ -253,6 +266,10 @@ int cbgx_solver_destroy(cbgx_solver* s);
 int cbgx_solver_solve(cbgx_solver* s, const double* d_b, const double* d_x0, double* d_x,
                       cbgx_history* hist, cbgx_solve_stats* stats, void* stream);
 
+/* Device ms per phase (CBGX_PHASE_*) accumulated over the solves run with
+ * CBGX_SOLVER_PHASE_TIMING_DEFERRED since the last call; resets. */
+int cbgx_solver_phase_times(cbgx_solver* s, double* ms, uint64_t count);
+
 /* Host-buffer drop-in for gmres_solve(const CsrMatrix&, span b, span x0,
  * cfg) (gmres.hpp:113-115): size_t CSR as in CsrMatrix, uploads, solves on
  * the current device, downloads the solution. */
@@ -283,6 +300,8 @@ int cbgx_halo_create(cbgx_comm* c, uint64_t row_begin, uint64_t row_end, uint64_
                      cbgx_halo** out);
 int cbgx_halo_destroy(cbgx_halo* h);
 uint64_t cbgx_halo_ghosts(const cbgx_halo* h);
+/* fill d_vec[n_local .. n_local+ghosts) from the owners' rows (collective) */
+int cbgx_halo_exchange(cbgx_halo* h, double* d_vec, void* stream);
 
 /* Distributed solve: A_local has n_rows = local rows and columns already
  * remapped by cbgx_halo_create; vectors are local (own rows). */

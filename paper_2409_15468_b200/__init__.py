@@ -500,16 +500,15 @@ def norm2(x, reduction=_lib.REDUCE_TREE) -> float:
     return float(np.sqrt(dot(x, x, reduction)))
 
 
-def sin_problem_host(n: int):
-    """x_sol = s/||s||, s[i] = sin(i) with the C library sin and a
-    sequential norm -- generate_problem's recipe (sparse.cpp:233-247); b is
-    then A x_sol on the device (bit-identical SpMV)."""
-    import math
-    s = np.fromiter((math.sin(float(i)) for i in range(n)), dtype=np.float64, count=n)
-    acc = 0.0
-    for v in s.tolist():
-        acc += v * v
-    return s * (1.0 / math.sqrt(acc))
+def sin_problem_host(n: int, first: int = 0, count: int = None) -> np.ndarray:
+    """x_sol = s/||s||, s[i] = sin(i): generate_problem's recipe
+    (sparse.cpp:233-247) with the C library sin and a sequential norm over
+    all n; rows [first, first+count). b is then A x_sol on the device
+    (bit-identical SpMV)."""
+    count = n - first if count is None else count
+    out = np.empty(max(count, 1), np.float64)
+    check(lib().cbgx_sin_solution(n, first, count, out.ctypes.data, 0))
+    return out[:count]
 
 
 # ------------------------------------------------------------ solver
@@ -523,11 +522,14 @@ class GmresConfig:
     storage_format: StorageFormat = StorageFormat.f64()
     reduction: int = _lib.REDUCE_TREE
     phase_timing: bool = False
+    phase_timing_deferred: bool = False
 
     def c(self):
+        flags = (_lib.PHASE_TIMING if self.phase_timing else 0) | \
+            (_lib.PHASE_TIMING_DEFERRED if self.phase_timing_deferred else 0)
         return _lib.GmresConfig(self.restart, self.target_rrn, self.max_total_iterations, self.eta,
                                 self.storage_format.kind, self.storage_format.bit_length,
-                                self.reduction, _lib.PHASE_TIMING if self.phase_timing else 0)
+                                self.reduction, flags)
 
 
 @dataclasses.dataclass
@@ -615,6 +617,12 @@ class Solver:
         check(lib().cbgx_solver_solve(self.h, _ptr(b), _ptr(_dev(x0)), _ptr(x), ctypes.byref(hist),
                                       ctypes.byref(st), _stream()))
         return _result(st, hist, bufs, x)
+
+    def phase_times(self):
+        """{phase: device ms} over the deferred-timing solves since last call."""
+        ms = np.zeros(8, np.float64)
+        check(lib().cbgx_solver_phase_times(self.h, ms.ctypes.data, 8))
+        return dict(zip(_lib.PHASES, ms.tolist()))
 
     def __del__(self):
         try:

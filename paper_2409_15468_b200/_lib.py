@@ -12,6 +12,7 @@ OK, EINVAL, ENONFINITE, ERANGE, EBREAKDOWN, ECUDA, ENOMEM, ECOMM, EINTERNAL = ra
 F64, F32, F16, FRSZ2 = 0, 1, 2, 3
 REDUCE_TREE, REDUCE_REFERENCE = 0, 1
 PHASE_TIMING = 1
+PHASE_TIMING_DEFERRED = 2
 PHASES = ["spmv", "dot", "update", "write", "residual", "solution", "comm", "host"]
 
 u32, u64, i32, i64, dbl, vp = C.c_uint32, C.c_uint64, C.c_int32, C.c_int64, C.c_double, C.c_void_p
@@ -60,6 +61,10 @@ def lib():
             "cbgx_last_error": ([], C.c_char_p),
             "cbgx_last_error_index": ([], u64),
             "cbgx_version": ([], C.c_int),
+            "cbgx_launch_count": ([], u64),
+            "cbgx_set_device": ([C.c_int], C.c_int),
+            "cbgx_sin_solution": ([u64, u64, u64, vp, C.c_int], C.c_int),
+            "cbgx_halo_exchange": ([vp, vp, vp], C.c_int),
             "cbgx_device_info": ([P(C.c_int), P(C.c_int), P(i64)], C.c_int),
             "cbgx_frsz2_num_blocks": ([u64, u32], u64),
             "cbgx_frsz2_words_per_block": ([u32, u32], u64),
@@ -86,6 +91,7 @@ def lib():
             "cbgx_stencil_generate": ([C.c_int, u64, u64, u64, dbl, u64, u64, i64, vp, u32, vp, vp, vp], C.c_int),
             "cbgx_solver_create": ([P(Csr), P(GmresConfig), vp, P(vp)], C.c_int),
             "cbgx_solver_destroy": ([vp], C.c_int),
+            "cbgx_solver_phase_times": ([vp, vp, u64], C.c_int),
             "cbgx_solver_solve": ([vp, vp, vp, vp, P(History), P(SolveStats), vp], C.c_int),
             "cbgx_gmres_solve_host": ([u64, vp, vp, vp, vp, vp, P(GmresConfig), vp, P(History), P(SolveStats)], C.c_int),
             "cbgx_nccl_unique_id": ([vp], C.c_int),

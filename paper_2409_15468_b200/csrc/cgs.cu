@@ -18,8 +18,14 @@
 // shared memory in tile order, CTAs write partial rows in CTA order, and the
 // last CTA to finish (device ticket) sums the rows in CTA order.
 #include <algorithm>
+#include <mutex>
+#include <map>
+#include <set>
+#include <tuple>
+#include <utility>
 
 #include "basis.cuh"
+#include "pipeline.cuh"
 #include "codec.cuh"
 #include "common.cuh"
 #include "reduce.cuh"
@@ -29,14 +35,86 @@ namespace cbgx {
 
 namespace {
 
-constexpr int kThreads = 256;
-constexpr int kWarps = kThreads / 32;
-constexpr int kSteps = 4;                          // 4-row steps per thread per tile
-constexpr uint64_t kTileRows = 4ull * kThreads * kSteps;  // 4096
-static_assert(kRowAlign % kTileRows == 0, "tiles must divide the basis row padding");
+// ---- geometry -------------------------------------------------------------
+// Consumers: 8 warps; a step is 1024 rows (4 consecutive rows per thread);
+// a sub-tile is up to Geo<F>::sub steps whose w stays in registers while every
+// column's segment streams through a kStages-deep shared-memory ring filled
+// by one producer thread with cp.async.bulk.
+constexpr int kConsumerWarps = 8;
+constexpr int kConsumers = kConsumerWarps * 32;
+constexpr int kThreads = kConsumers + 32;   // + producer warp
+constexpr int kWarps = kConsumerWarps;      // reduction slots
+constexpr uint32_t kStepRows = 4 * kConsumers;  // 1024
 
-__device__ __forceinline__ void load_w(const double* __restrict__ w, uint64_t n, uint64_t r,
-                                       double out[4]) {
+// Per format: payload / exponent bytes per 1024-row step, steps per
+// sub-tile (w of a sub-tile lives in registers: sub * 4 doubles per thread)
+// and ring depth. A ring stage holds one column's segment of a sub-tile.
+template <int F> struct Geo;
+template <> struct Geo<kZ32> { static constexpr uint32_t pay = 4096, ex = 128; static constexpr int sub = 4, stages = 4; };
+template <> struct Geo<kZ16> { static constexpr uint32_t pay = 2048, ex = 128; static constexpr int sub = 4, stages = 6; };
+template <> struct Geo<kZ21> { static constexpr uint32_t pay = 2688, ex = 128; static constexpr int sub = 4, stages = 5; };
+template <> struct Geo<kF64> { static constexpr uint32_t pay = 8192, ex = 0; static constexpr int sub = 4, stages = 3; };
+template <> struct Geo<kF32> { static constexpr uint32_t pay = 4096, ex = 0; static constexpr int sub = 4, stages = 4; };
+template <> struct Geo<kF16> { static constexpr uint32_t pay = 2048, ex = 0; static constexpr int sub = 4, stages = 6; };
+static_assert(kRowAlign % (kStepRows * 8) == 0, "sub-tiles must divide the row padding");
+
+template <int F>
+__host__ __device__ constexpr uint32_t stage_bytes() {
+    return Geo<F>::sub * (Geo<F>::pay + Geo<F>::ex) + 16;  // +16: l=21 loader reads one word past
+}
+
+// Split [s0, s1) into ceil(len/sub) sub-tiles of near-equal size (so no CTA
+// ends with a 1-step remainder that costs a full ring round per column).
+struct SubTiles {
+    uint64_t s0, len, count;
+    __device__ __forceinline__ uint64_t begin(uint64_t i) const { return s0 + len * i / count; }
+    __device__ __forceinline__ uint64_t end(uint64_t i) const { return s0 + len * (i + 1) / count; }
+};
+template <int F>
+__device__ __forceinline__ SubTiles sub_tiles(uint64_t s0, uint64_t s1) {
+    const uint64_t len = s1 - s0;
+    return SubTiles{s0, len, (len + Geo<F>::sub - 1) / Geo<F>::sub};
+}
+
+// ---- shared-memory step loaders (r = local row of the thread's 4 rows) ----
+template <int F>
+__device__ __forceinline__ void step_lds(Step<F>& st, const unsigned char* pay, const uint32_t* ex, uint32_t r);
+
+template <>
+__device__ __forceinline__ void step_lds<kZ32>(Step<kZ32>& st, const unsigned char* pay, const uint32_t* ex, uint32_t r) {
+    st.c = *reinterpret_cast<const uint4*>(pay + 4u * r);
+    st.e = ex[r / 32];
+}
+template <>
+__device__ __forceinline__ void step_lds<kZ16>(Step<kZ16>& st, const unsigned char* pay, const uint32_t* ex, uint32_t r) {
+    st.c = *reinterpret_cast<const uint2*>(pay + 2u * r);
+    st.e = ex[r / 32];
+}
+template <>
+__device__ __forceinline__ void step_lds<kZ21>(Step<kZ21>& st, const unsigned char* pay, const uint32_t* ex, uint32_t r) {
+    const uint32_t* p = reinterpret_cast<const uint32_t*>(pay);
+    const uint32_t bit = (r & 31u) * 21u;
+    const uint32_t q = (r / 32) * 21 + (bit >> 5);
+    st.sh = bit & 31u;
+    st.w0 = p[q]; st.w1 = p[q + 1]; st.w2 = p[q + 2]; st.w3 = p[q + 3];
+    st.e = ex[r / 32];
+}
+template <>
+__device__ __forceinline__ void step_lds<kF64>(Step<kF64>& st, const unsigned char* pay, const uint32_t*, uint32_t r) {
+    const double2* p = reinterpret_cast<const double2*>(pay + 8u * r);
+    st.a = p[0];
+    st.b = p[1];
+}
+template <>
+__device__ __forceinline__ void step_lds<kF32>(Step<kF32>& st, const unsigned char* pay, const uint32_t*, uint32_t r) {
+    st.c = *reinterpret_cast<const float4*>(pay + 4u * r);
+}
+template <>
+__device__ __forceinline__ void step_lds<kF16>(Step<kF16>& st, const unsigned char* pay, const uint32_t*, uint32_t r) {
+    st.c = *reinterpret_cast<const uint2*>(pay + 2u * r);
+}
+
+__device__ __forceinline__ void load_w(const double* __restrict__ w, uint64_t n, uint64_t r, double out[4]) {
     if (r + 3 < n) {
         const double2 a = __ldg(reinterpret_cast<const double2*>(w + r));
         const double2 b = __ldg(reinterpret_cast<const double2*>(w + r + 2));
@@ -47,54 +125,130 @@ __device__ __forceinline__ void load_w(const double* __restrict__ w, uint64_t n,
     }
 }
 
+// This CTA's step range: steps are split evenly over the grid (balanced to
+// one 1024-row step), so no CTA owns a whole extra tile.
+__device__ __forceinline__ void cta_steps(uint64_t n, uint64_t& s0, uint64_t& s1) {
+    const uint64_t steps = (n + kStepRows - 1) / kStepRows;
+    s0 = steps * blockIdx.x / gridDim.x;
+    s1 = steps * (blockIdx.x + 1) / gridDim.x;
+}
+
+struct Ring {
+    unsigned char* stages;
+    uint64_t* full;
+    uint64_t* empty;
+};
+
+template <int F>
+__device__ __forceinline__ Ring ring_setup(unsigned char* smem) {
+    constexpr int S = Geo<F>::stages;
+    Ring r;
+    r.stages = smem;
+    r.full = reinterpret_cast<uint64_t*>(smem + S * stage_bytes<F>());
+    r.empty = r.full + S;
+    if (threadIdx.x == 0) {
+        for (int s = 0; s < S; ++s) {
+            mbar_init(r.full + s, 1);
+            mbar_init(r.empty + s, kConsumerWarps);
+        }
+        fence_barrier_init();
+    }
+    return r;
+}
+
+// Producer (one elected thread): for every sub-tile and column, wait for a
+// free stage and bulk-copy the column's payload (+ exponent) segment.
+template <int F>
+__device__ __forceinline__ void produce(const Ring& R, const BasisView& B, uint64_t first, uint32_t cols,
+                                        uint64_t s0, uint64_t s1, bool reverse) {
+    constexpr int S = Geo<F>::stages;
+    constexpr uint32_t PAY = Geo<F>::pay, EX = Geo<F>::ex;
+    const uint64_t policy = policy_evict_normal();
+    uint32_t it = 0;
+    const SubTiles T = sub_tiles<F>(s0, s1);
+    for (uint64_t t = 0; t < T.count; ++t) {
+        const uint64_t sb = T.begin(t);
+        const uint32_t steps = static_cast<uint32_t>(T.end(t) - sb);
+        const uint32_t pb = steps * PAY, eb = steps * EX;
+        for (uint32_t jj = 0; jj < cols; ++jj, ++it) {
+            const uint32_t j = reverse ? cols - 1 - jj : jj;
+            const int stage = it % S;
+            mbar_wait(R.empty + stage, ((it / S) & 1) ^ 1);
+            mbar_arrive_expect_tx(R.full + stage, pb + eb);
+            unsigned char* dst = R.stages + stage * stage_bytes<F>();
+            const unsigned char* col = B.data + (first + j) * B.col_stride_bytes;
+            bulk_g2s(dst, col + sb * PAY, pb, R.full + stage, policy);
+            if constexpr (EX > 0) {
+                const unsigned char* ecol = reinterpret_cast<const unsigned char*>(B.exp + (first + j) * B.exp_col_stride);
+                bulk_g2s(dst + Geo<F>::sub * PAY, ecol + sb * EX, eb, R.full + stage, policy);
+            }
+        }
+    }
+}
+
 // ------------------------------------------------------------------ dot
 template <int F>
-__global__ void __launch_bounds__(kThreads, 2)
+__global__ void __launch_bounds__(kThreads, 3)
 cgs_dot_kernel(BasisView B, uint64_t first, uint32_t cols, const double* __restrict__ w,
                int with_wnorm, double* __restrict__ partials, unsigned* __restrict__ ticket,
-               double* __restrict__ h_out) {
-    extern __shared__ double red[];  // [kWarps][cols + 1]
-    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+               double* __restrict__ h_out, GateArg gate) {
+    if (!gate.open()) return;  // re-orthogonalisation pass not needed
+    constexpr int S = Geo<F>::stages;
+    constexpr uint32_t PAY = Geo<F>::pay;
+    extern __shared__ __align__(128) unsigned char smem[];
     const uint32_t ncol = cols + (with_wnorm ? 1 : 0);
+    const Ring R = ring_setup<F>(smem);
+    double* red = reinterpret_cast<double*>(R.empty + S);  // [kWarps][ncol]
     for (uint32_t k = threadIdx.x; k < kWarps * ncol; k += kThreads) red[k] = 0.0;
     __syncthreads();
-
-    const uint64_t ntiles = (B.n + kTileRows - 1) / kTileRows;
-    for (uint64_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
-        const uint64_t r0 = tile * kTileRows + 4ull * threadIdx.x;
-        double wv[kSteps][4];
+    uint64_t s0, s1;
+    cta_steps(B.n, s0, s1);
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    if (warp == kConsumerWarps) {
+        if (lane == 0) produce<F>(R, B, first, cols, s0, s1, true);
+    } else {
+        uint32_t it = 0;
+        const SubTiles T = sub_tiles<F>(s0, s1);
+        for (uint64_t t = 0; t < T.count; ++t) {
+            const uint64_t sb = T.begin(t);
+            const uint32_t steps = static_cast<uint32_t>(T.end(t) - sb);
+            double wv[Geo<F>::sub][4];
 #pragma unroll
-        for (int s = 0; s < kSteps; ++s) load_w(w, B.n, r0 + s * 4ull * kThreads, wv[s]);
-        if (with_wnorm) {
-            double acc = 0.0;
+            for (int s = 0; s < Geo<F>::sub; ++s) {
+                if (s < steps) load_w(w, B.n, (sb + s) * kStepRows + 4u * threadIdx.x, wv[s]);
+                else wv[s][0] = wv[s][1] = wv[s][2] = wv[s][3] = 0.0;
+            }
+            if (with_wnorm) {
+                double acc = 0.0;
 #pragma unroll
-            for (int s = 0; s < kSteps; ++s)
+                for (int s = 0; s < Geo<F>::sub; ++s)
 #pragma unroll
-                for (int k = 0; k < 4; ++k) acc = __dadd_rn(acc, __dmul_rn(wv[s][k], wv[s][k]));
-            acc = warp_sum(acc);
-            if (lane == 0) red[warp * ncol + cols] += acc;
-        }
-        Step<F> buf[2][kSteps];
-        if (cols > 0) {
-#pragma unroll
-            for (int s = 0; s < kSteps; ++s) buf[0][s].load(B, first, r0 + s * 4ull * kThreads);
-        }
-        for (uint32_t j = 0; j < cols; j += 2) {
-            // even column in buf[0]; prefetch odd column into buf[1]
-#pragma unroll
-            for (int half = 0; half < 2; ++half) {
-                const uint32_t jj = j + half;
-                if (jj >= cols) break;
-                if (jj + 1 < cols) {
-#pragma unroll
-                    for (int s = 0; s < kSteps; ++s)
-                        buf[half ^ 1][s].load(B, first + jj + 1, r0 + s * 4ull * kThreads);
-                }
-                double acc = buf[half][0].dot(wv[0]);
-#pragma unroll
-                for (int s = 1; s < kSteps; ++s) acc = __dadd_rn(acc, buf[half][s].dot(wv[s]));
+                    for (int k = 0; k < 4; ++k) acc = fma(wv[s][k], wv[s][k], acc);
                 acc = warp_sum(acc);
-                if (lane == 0) red[warp * ncol + jj] += acc;
+                if (lane == 0) red[warp * ncol + cols] += acc;
+            }
+            // Columns stream last-to-first: the preceding update pass ended on
+            // the high columns, so they are still in L2 (and the following
+            // update starts on the low columns this pass ends with).
+            for (uint32_t jj = 0; jj < cols; ++jj, ++it) {
+                const uint32_t j = cols - 1 - jj;
+                const int stage = it % S;
+                mbar_wait(R.full + stage, (it / S) & 1);
+                const unsigned char* pay = R.stages + stage * stage_bytes<F>();
+                const uint32_t* ex = reinterpret_cast<const uint32_t*>(pay + Geo<F>::sub * PAY);
+                double acc = 0.0;
+#pragma unroll
+                for (int s = 0; s < Geo<F>::sub; ++s) {
+                    if (s < steps) {
+                        Step<F> st;
+                        step_lds<F>(st, pay, ex, s * kStepRows + 4u * threadIdx.x);
+                        acc = __dadd_rn(acc, st.dot(wv[s]));
+                    }
+                }
+                __syncwarp();
+                if (lane == 0) mbar_arrive(R.empty + stage);
+                acc = warp_sum(acc);
+                if (lane == 0) red[warp * ncol + j] += acc;
             }
         }
     }
@@ -104,67 +258,79 @@ cgs_dot_kernel(BasisView B, uint64_t first, uint32_t cols, const double* __restr
 
 // --------------------------------------------------------------- update
 template <int F>
-__global__ void __launch_bounds__(kThreads, 2)
+__global__ void __launch_bounds__(kThreads, 3)
 cgs_update_kernel(BasisView B, uint64_t first, uint32_t cols, const double* __restrict__ h,
                   double h_sign, double* __restrict__ w, int with_norm,
                   double* __restrict__ partials, unsigned* __restrict__ ticket,
-                  double* __restrict__ norm_out) {
-    extern __shared__ double sh[];  // [cols] coefficients, then [kWarps] norm partials
-    double* hs = sh;
-    double* red = sh + cols;
-    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+                  double* __restrict__ norm_out, GateArg gate) {
+    if (!gate.open()) return;
+    constexpr int S = Geo<F>::stages;
+    constexpr uint32_t PAY = Geo<F>::pay;
+    extern __shared__ __align__(128) unsigned char smem[];
+    const Ring R = ring_setup<F>(smem);
+    double* hs = reinterpret_cast<double*>(R.empty + S);  // [cols]
+    double* red = hs + cols;                               // [kWarps]
     for (uint32_t k = threadIdx.x; k < cols; k += kThreads) hs[k] = h_sign * h[k];
     if (threadIdx.x < kWarps) red[threadIdx.x] = 0.0;
     __syncthreads();
-
-    const uint64_t ntiles = (B.n + kTileRows - 1) / kTileRows;
-    for (uint64_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
-        const uint64_t r0 = tile * kTileRows + 4ull * threadIdx.x;
-        double wv[kSteps][4];
+    uint64_t s0, s1;
+    cta_steps(B.n, s0, s1);
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    if (warp == kConsumerWarps) {
+        if (lane == 0) produce<F>(R, B, first, cols, s0, s1, false);
+    } else {
+        uint32_t it = 0;
+        double nacc = 0.0;
+        const SubTiles T = sub_tiles<F>(s0, s1);
+        for (uint64_t t = 0; t < T.count; ++t) {
+            const uint64_t sb = T.begin(t);
+            const uint32_t steps = static_cast<uint32_t>(T.end(t) - sb);
+            double wv[Geo<F>::sub][4];
 #pragma unroll
-        for (int s = 0; s < kSteps; ++s) load_w(w, B.n, r0 + s * 4ull * kThreads, wv[s]);
-        Step<F> buf[2][kSteps];
-        if (cols > 0) {
-#pragma unroll
-            for (int s = 0; s < kSteps; ++s) buf[0][s].load(B, first, r0 + s * 4ull * kThreads);
-        }
-        for (uint32_t j = 0; j < cols; j += 2) {
-#pragma unroll
-            for (int half = 0; half < 2; ++half) {
-                const uint32_t jj = j + half;
-                if (jj >= cols) break;
-                if (jj + 1 < cols) {
-#pragma unroll
-                    for (int s = 0; s < kSteps; ++s)
-                        buf[half ^ 1][s].load(B, first + jj + 1, r0 + s * 4ull * kThreads);
-                }
-                const double hj = hs[jj];
+            for (int s = 0; s < Geo<F>::sub; ++s) {
+                if (s < steps) load_w(w, B.n, (sb + s) * kStepRows + 4u * threadIdx.x, wv[s]);
+                else wv[s][0] = wv[s][1] = wv[s][2] = wv[s][3] = 0.0;
+            }
+            for (uint32_t j = 0; j < cols; ++j, ++it) {
+                const int stage = it % S;
+                mbar_wait(R.full + stage, (it / S) & 1);
+                const unsigned char* pay = R.stages + stage * stage_bytes<F>();
+                const uint32_t* ex = reinterpret_cast<const uint32_t*>(pay + Geo<F>::sub * PAY);
+                const double hj = hs[j];
                 const int he = static_cast<int>(exp_field(hj));
 #pragma unroll
-                for (int s = 0; s < kSteps; ++s) buf[half][s].update(hj, he, wv[s]);
+                for (int s = 0; s < Geo<F>::sub; ++s) {
+                    if (s < steps) {
+                        Step<F> st;
+                        step_lds<F>(st, pay, ex, s * kStepRows + 4u * threadIdx.x);
+                        st.update(hj, he, wv[s]);
+                    }
+                }
+                __syncwarp();
+                if (lane == 0) mbar_arrive(R.empty + stage);
             }
-        }
-        double acc = 0.0;
 #pragma unroll
-        for (int s = 0; s < kSteps; ++s) {
-            const uint64_t r = r0 + s * 4ull * kThreads;
-            if (r + 3 < B.n) {
-                reinterpret_cast<double2*>(w + r)[0] = make_double2(wv[s][0], wv[s][1]);
-                reinterpret_cast<double2*>(w + r)[1] = make_double2(wv[s][2], wv[s][3]);
-            } else {
+            for (int s = 0; s < Geo<F>::sub; ++s) {
+                if (s >= steps) break;
+                const uint64_t r = (sb + s) * kStepRows + 4u * threadIdx.x;
+                if (r + 3 < B.n) {
+                    reinterpret_cast<double2*>(w + r)[0] = make_double2(wv[s][0], wv[s][1]);
+                    reinterpret_cast<double2*>(w + r)[1] = make_double2(wv[s][2], wv[s][3]);
+                } else {
 #pragma unroll
-                for (int k = 0; k < 4; ++k)
-                    if (r + k < B.n) w[r + k] = wv[s][k];
-            }
-            if (with_norm) {
+                    for (int k = 0; k < 4; ++k)
+                        if (r + k < B.n) w[r + k] = wv[s][k];
+                }
+                if (with_norm) {
 #pragma unroll
-                for (int k = 0; k < 4; ++k)
-                    if (r + k < B.n) acc = __dadd_rn(acc, __dmul_rn(wv[s][k], wv[s][k]));
+                    for (int k = 0; k < 4; ++k)
+                        if (r + k < B.n) nacc = fma(wv[s][k], wv[s][k], nacc);
+                }
             }
         }
         if (with_norm) {
-            acc = warp_sum(acc);
-            if (lane == 0) red[warp] += acc;
+            nacc = warp_sum(nacc);
+            if (lane == 0) red[warp] = nacc;
         }
     }
     __syncthreads();
@@ -179,7 +345,8 @@ cgs_update_kernel(BasisView B, uint64_t first, uint32_t cols, const double* __re
 template <int F>
 __global__ void serial_dot_kernel(BasisView B, uint64_t first, uint32_t cols,
                                   const double* __restrict__ w, int with_wnorm,
-                                  double* __restrict__ h_out) {
+                                  double* __restrict__ h_out, GateArg gate) {
+    if (!gate.open()) return;
     const uint32_t j = blockIdx.x * blockDim.x + threadIdx.x;
     if (j < cols) {
         double total = 0.0;
@@ -204,19 +371,14 @@ __global__ void serial_dot_kernel(BasisView B, uint64_t first, uint32_t cols,
 // --------------------------------------------------------- write / read
 template <int F>
 __global__ void write_plain_kernel(unsigned char* __restrict__ col, const double* __restrict__ x,
-                                   uint64_t n, uint64_t n_pad, const double* __restrict__ scale_src,
-                                   int scale_mode, double* __restrict__ v_out) {
-    double s = 1.0;
-    if (scale_src) {
-        const double p = *scale_src;
-        s = scale_mode == 1 ? 1.0 / sqrt(p) : p;
-    }
+                                   uint64_t n, uint64_t n_pad, ScaleArg scale, double* __restrict__ v_out) {
+    const double s = scale.value();
     for (uint64_t i = blockIdx.x * static_cast<uint64_t>(blockDim.x) + threadIdx.x; i < n_pad;
          i += static_cast<uint64_t>(gridDim.x) * blockDim.x) {
         double v = 0.0;
         if (i < n) {
             v = x[i];
-            if (scale_src) v = __dmul_rn(v, s);
+            if (scale.src) v = __dmul_rn(v, s);
             if (v_out) v_out[i] = v;
         }
         if constexpr (F == kF64) reinterpret_cast<double*>(col)[i] = v;
@@ -247,65 +409,98 @@ void dispatch_fmt(int f, A&&... a) {
     }
 }
 
-int persistent_grid(uint64_t tiles) {
-    const uint64_t cap = static_cast<uint64_t>(sm_count()) * 2;
-    return static_cast<int>(std::max<uint64_t>(1, std::min<uint64_t>(tiles, cap)));
+// Persistent grid: as many CTAs as fit (smem-limited), never more than
+// there are 1024-row steps.
+// Persistent grid: all CTAs that can be co-resident (registers and shared
+// memory via the occupancy calculator), never more than 1024-row steps.
+template <class K>
+int ring_grid(K kernel, uint64_t n, size_t smem) {
+    // occupancy query cached per (device, kernel, smem): it costs host time
+    // on every launch otherwise
+    static std::mutex mu;
+    static std::map<std::tuple<int, const void*, size_t>, int> cache;
+    const auto key = std::make_tuple(current_device(), reinterpret_cast<const void*>(kernel), smem);
+    int per_sm = 0;
+    {
+        std::lock_guard<std::mutex> lock(mu);
+        auto it = cache.find(key);
+        if (it == cache.end()) {
+            CBGX_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kernel, kThreads, smem));
+            cache.emplace(key, per_sm);
+        } else {
+            per_sm = it->second;
+        }
+    }
+    const uint64_t steps = (n + kStepRows - 1) / kStepRows;
+    const uint64_t cap = static_cast<uint64_t>(sm_count()) * std::max(per_sm, 1);
+    return static_cast<int>(std::max<uint64_t>(1, std::min<uint64_t>(steps, cap)));
+}
+
+template <int F>
+size_t ring_smem(size_t extra_doubles) {
+    return Geo<F>::stages * (stage_bytes<F>() + 16) + extra_doubles * sizeof(double);
+}
+
+// Raise the dynamic shared-memory limit once per kernel (per device).
+template <class K>
+void allow_smem(K kernel) {
+    static std::mutex mu;
+    static std::set<std::pair<int, const void*>> done;
+    const auto key = std::make_pair(current_device(), reinterpret_cast<const void*>(kernel));
+    std::lock_guard<std::mutex> lock(mu);
+    if (done.count(key)) return;
+    CBGX_CUDA(cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
+    done.insert(key);
 }
 
 template <int F> struct DotLaunch {
     static void run(const BasisView& B, uint64_t first, uint32_t cols, const double* w, int wn,
-                    int reduction, double* h, Workspace* ws, cudaStream_t st) {
+                    int reduction, double* h, Workspace* ws, cudaStream_t st, const GateArg& gate) {
         const uint32_t ncol = cols + (wn ? 1 : 0);
         if (ncol == 0) return;
         if (reduction == CBGX_REDUCE_REFERENCE) {
             const uint32_t threads = ncol;
-            serial_dot_kernel<F><<<(threads + 63) / 64, 64, 0, st>>>(B, first, cols, w, wn, h);
+            CBGX_K(serial_dot_kernel<F><<<(threads + 63) / 64, 64, 0, st>>>(B, first, cols, w, wn, h, gate));
             return;
         }
-        const int grid = persistent_grid((B.n + kTileRows - 1) / kTileRows);
-        const size_t smem = sizeof(double) * kWarps * ncol;
-        if (smem > 48 * 1024) {
-            CBGX_CUDA(cudaFuncSetAttribute(cgs_dot_kernel<F>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                           static_cast<int>(smem)));
-        }
+        const size_t smem = ring_smem<F>(static_cast<size_t>(kWarps) * ncol);
+        allow_smem(cgs_dot_kernel<F>);
+        const int grid = ring_grid(cgs_dot_kernel<F>, B.n, smem);
         double* partials = ws->get_partials(static_cast<size_t>(grid) * ncol);
-        cgs_dot_kernel<F><<<grid, kThreads, smem, st>>>(B, first, cols, w, wn, partials,
-                                                        ws->get_counter(), h);
+        CBGX_K(cgs_dot_kernel<F><<<grid, kThreads, smem, st>>>(B, first, cols, w, wn, partials,
+                                                        ws->get_counter(), h, gate));
     }
 };
 
 template <int F> struct UpdateLaunch {
     static void run(const BasisView& B, uint64_t first, uint32_t cols, const double* h, double sign,
-                    double* w, double* norm, int reduction, Workspace* ws, cudaStream_t st) {
-        const int grid = persistent_grid((B.n + kTileRows - 1) / kTileRows);
+                    double* w, double* norm, int reduction, Workspace* ws, cudaStream_t st,
+                    const GateArg& gate) {
         const bool fused_norm = norm && reduction == CBGX_REDUCE_TREE;
         if (cols > 0 || fused_norm) {
-            const size_t smem = sizeof(double) * (cols + kWarps);
-            if (smem > 48 * 1024) {
-                CBGX_CUDA(cudaFuncSetAttribute(cgs_update_kernel<F>,
-                                               cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                               static_cast<int>(smem)));
-            }
+            const size_t smem = ring_smem<F>(cols + kWarps);
+            allow_smem(cgs_update_kernel<F>);
+            const int grid = ring_grid(cgs_update_kernel<F>, B.n, smem);
             double* partials = fused_norm ? ws->get_partials(grid) : nullptr;
-            cgs_update_kernel<F><<<grid, kThreads, smem, st>>>(B, first, cols, h, sign, w, fused_norm,
-                                                               partials, ws->get_counter(), norm);
+            CBGX_K(cgs_update_kernel<F><<<grid, kThreads, smem, st>>>(B, first, cols, h, sign, w, fused_norm,
+                                                               partials, ws->get_counter(), norm, gate));
         }
-        if (norm && !fused_norm) launch_dot(w, w, B.n, CBGX_REDUCE_REFERENCE, norm, ws, st);
+        if (norm && !fused_norm) launch_dot(w, w, B.n, CBGX_REDUCE_REFERENCE, norm, ws, st, gate);
     }
 };
 
 template <int F> struct WriteLaunch {
-    static void run(const cbgx_basis& V, uint64_t j, const double* x, const double* scale_src,
-                    int scale_mode, double* v_out, uint64_t* bad, cudaStream_t st) {
+    static void run(const cbgx_basis& V, uint64_t j, const double* x, const ScaleArg& scale,
+                    double* v_out, uint64_t* bad, cudaStream_t st) {
         unsigned char* col = static_cast<unsigned char*>(V.d_data) + j * V.col_stride_bytes;
         if constexpr (FmtInfo<F>::frsz) {
             launch_compress(x, V.n, V.n_pad / 32, 32, FmtInfo<F>::L,
                             V.d_exp + j * V.exp_col_stride, reinterpret_cast<uint32_t*>(col),
-                            scale_src, scale_mode, v_out, bad, st);
+                            scale, v_out, bad, st);
         } else {
             const uint64_t blocks = std::min<uint64_t>((V.n_pad + 255) / 256, static_cast<uint64_t>(sm_count()) * 16);
-            write_plain_kernel<F><<<static_cast<int>(std::max<uint64_t>(blocks, 1)), 256, 0, st>>>(
-                col, x, V.n, V.n_pad, scale_src, scale_mode, v_out);
+            CBGX_K(write_plain_kernel<F><<<static_cast<int>(std::max<uint64_t>(blocks, 1)), 256, 0, st>>>(
+                col, x, V.n, V.n_pad, scale, v_out));
         }
     }
 };
@@ -314,7 +509,7 @@ template <int F> struct ReadLaunch {
     static void run(const BasisView& B, uint64_t j, uint64_t first, uint64_t count, double* out,
                     cudaStream_t st) {
         const uint64_t blocks = std::min<uint64_t>((count + 255) / 256, static_cast<uint64_t>(sm_count()) * 16);
-        read_kernel<F><<<static_cast<int>(std::max<uint64_t>(blocks, 1)), 256, 0, st>>>(B, j, first, count, out);
+        CBGX_K(read_kernel<F><<<static_cast<int>(std::max<uint64_t>(blocks, 1)), 256, 0, st>>>(B, j, first, count, out));
     }
 };
 
@@ -327,24 +522,24 @@ void check_basis(const cbgx_basis* V) {
 }  // namespace
 
 void launch_cgs_dot(const cbgx_basis& V, uint64_t first, uint32_t cols, const double* w, int wn,
-                    int reduction, double* h, Workspace* ws, cudaStream_t st) {
+                    int reduction, double* h, Workspace* ws, cudaStream_t st, const GateArg& gate) {
     if (first + cols > V.capacity) throw Error(CBGX_ERANGE, "basis: column index out of range");
-    dispatch_fmt<DotLaunch>(fmt_of(V), view_of(V), first, cols, w, wn, reduction, h, ws, st);
+    dispatch_fmt<DotLaunch>(fmt_of(V), view_of(V), first, cols, w, wn, reduction, h, ws, st, gate);
     CBGX_CUDA(cudaGetLastError());
 }
 
 void launch_cgs_update(const cbgx_basis& V, uint64_t first, uint32_t cols, const double* h,
                        double sign, double* w, double* norm, int reduction, Workspace* ws,
-                       cudaStream_t st) {
+                       cudaStream_t st, const GateArg& gate) {
     if (first + cols > V.capacity) throw Error(CBGX_ERANGE, "basis: column index out of range");
-    dispatch_fmt<UpdateLaunch>(fmt_of(V), view_of(V), first, cols, h, sign, w, norm, reduction, ws, st);
+    dispatch_fmt<UpdateLaunch>(fmt_of(V), view_of(V), first, cols, h, sign, w, norm, reduction, ws, st, gate);
     CBGX_CUDA(cudaGetLastError());
 }
 
-void launch_basis_write(const cbgx_basis& V, uint64_t j, const double* x, const double* scale_src,
-                        int scale_mode, double* v_out, uint64_t* bad, cudaStream_t st) {
+void launch_basis_write(const cbgx_basis& V, uint64_t j, const double* x, const ScaleArg& scale,
+                        double* v_out, uint64_t* bad, cudaStream_t st) {
     if (j >= V.capacity) throw Error(CBGX_ERANGE, "basis: cannot write column");
-    dispatch_fmt<WriteLaunch>(fmt_of(V), V, j, x, scale_src, scale_mode, v_out, bad, st);
+    dispatch_fmt<WriteLaunch>(fmt_of(V), V, j, x, scale, v_out, bad, st);
     CBGX_CUDA(cudaGetLastError());
 }
 
@@ -395,7 +590,10 @@ int cbgx_basis_write(const cbgx_basis* V, uint64_t j, const double* d_x, const d
                      int scale_mode, double* d_v_out, uint64_t* d_bad_index, void* stream) {
     return guard([&] {
         check_basis(V);
-        launch_basis_write(*V, j, d_x, d_scale_src, scale_mode, d_v_out, d_bad_index, as_stream(stream));
+        ScaleArg sc;
+        sc.src = d_scale_src;
+        sc.mode = scale_mode == 1 ? 1 : 0;
+        launch_basis_write(*V, j, d_x, sc, d_v_out, d_bad_index, as_stream(stream));
     });
 }
 

@@ -74,14 +74,10 @@ template <int L, bool kScale>
 __global__ void __launch_bounds__(kThreads)
 compress32_kernel(const double* __restrict__ x, uint64_t n, uint64_t nb_write,
                   uint32_t* __restrict__ exps, uint32_t* __restrict__ payload,
-                  const double* __restrict__ scale_src, int scale_mode,
-                  double* __restrict__ v_out, unsigned long long* __restrict__ bad) {
+                  ScaleArg scale, double* __restrict__ v_out,
+                  unsigned long long* __restrict__ bad) {
     const int lane = threadIdx.x & 31;
-    double s = 1.0;
-    if (kScale) {
-        const double p = *scale_src;
-        s = scale_mode == 1 ? 1.0 / sqrt(p) : p;
-    }
+    const double s = kScale ? scale.value() : 1.0;
     const uint64_t warp = (static_cast<uint64_t>(blockIdx.x) * kWarps) + (threadIdx.x >> 5);
     const uint64_t nwarps = static_cast<uint64_t>(gridDim.x) * kWarps;
     for (uint64_t b0 = warp * kUnroll; b0 < nb_write; b0 += nwarps * kUnroll) {
@@ -230,29 +226,29 @@ bool fast_path(uint32_t bs, uint32_t l) { return bs == 32 && (l == 16 || l == 21
 }  // namespace
 
 void launch_compress(const double* x, uint64_t n, uint64_t nb_write, uint32_t bs, uint32_t l,
-                     uint32_t* exps, uint32_t* payload, const double* scale_src, int scale_mode,
-                     double* v_out, uint64_t* bad, cudaStream_t st) {
+                     uint32_t* exps, uint32_t* payload, const ScaleArg& scale, double* v_out, uint64_t* bad,
+                     cudaStream_t st) {
     validate(bs, l);
     if (nb_write == 0) return;
     auto* badp = reinterpret_cast<unsigned long long*>(bad);
     if (fast_path(bs, l)) {
         const int grid = grid_for(nb_write, kWarps * kUnroll);
-        const bool sc = scale_src != nullptr;
+        const bool sc = scale.src != nullptr;
 #define CBGX_LAUNCH_C(LL)                                                                    \
-    if (sc) compress32_kernel<LL, true><<<grid, kThreads, 0, st>>>(x, n, nb_write, exps, payload, \
-                                                                   scale_src, scale_mode, v_out, badp); \
-    else compress32_kernel<LL, false><<<grid, kThreads, 0, st>>>(x, n, nb_write, exps, payload,   \
-                                                                 nullptr, 0, nullptr, badp)
+    if (sc) CBGX_K(compress32_kernel<LL, true><<<grid, kThreads, 0, st>>>(x, n, nb_write, exps, payload, \
+                                                                   scale, v_out, badp)); \
+    else CBGX_K(compress32_kernel<LL, false><<<grid, kThreads, 0, st>>>(x, n, nb_write, exps, payload,   \
+                                                                 ScaleArg{}, nullptr, badp))
         if (l == 32) { CBGX_LAUNCH_C(32); }
         else if (l == 16) { CBGX_LAUNCH_C(16); }
         else { CBGX_LAUNCH_C(21); }
 #undef CBGX_LAUNCH_C
     } else {
-        if (scale_src || v_out) throw Error(CBGX_EINVAL, "frsz2: fused scale needs bs=32, l in {16,21,32}");
+        if (scale.src || v_out) throw Error(CBGX_EINVAL, "frsz2: fused scale needs bs=32, l in {16,21,32}");
         const uint64_t nb = (n + bs - 1) / bs;
         if (nb_write != nb) throw Error(CBGX_EINVAL, "frsz2: generic codec writes exactly num_blocks");
-        compress_generic_kernel<<<grid_for(nb, 128), 128, 0, st>>>(x, n, bs, l, (static_cast<uint64_t>(bs) * l + 31) / 32,
-                                                                  exps, payload, badp);
+        CBGX_K(compress_generic_kernel<<<grid_for(nb, 128), 128, 0, st>>>(x, n, bs, l, (static_cast<uint64_t>(bs) * l + 31) / 32,
+                                                                  exps, payload, badp));
     }
     CBGX_CUDA(cudaGetLastError());
 }
@@ -263,12 +259,12 @@ void launch_decompress(const uint32_t* exps, const uint32_t* payload, uint64_t n
     if (count == 0) return;
     if (fast_path(bs, l) && first == 0 && count == n) {
         const int grid = grid_for((n + 31) / 32, kWarps * kUnroll);
-        if (l == 32) decompress32_kernel<32><<<grid, kThreads, 0, st>>>(exps, payload, n, out);
-        else if (l == 16) decompress32_kernel<16><<<grid, kThreads, 0, st>>>(exps, payload, n, out);
-        else decompress32_kernel<21><<<grid, kThreads, 0, st>>>(exps, payload, n, out);
+        if (l == 32) CBGX_K(decompress32_kernel<32><<<grid, kThreads, 0, st>>>(exps, payload, n, out));
+        else if (l == 16) CBGX_K(decompress32_kernel<16><<<grid, kThreads, 0, st>>>(exps, payload, n, out));
+        else CBGX_K(decompress32_kernel<21><<<grid, kThreads, 0, st>>>(exps, payload, n, out));
     } else {
-        decompress_generic_kernel<<<grid_for(count, 256), 256, 0, st>>>(
-            exps, payload, bs, l, (static_cast<uint64_t>(bs) * l + 31) / 32, first, count, out);
+        CBGX_K(decompress_generic_kernel<<<grid_for(count, 256), 256, 0, st>>>(
+            exps, payload, bs, l, (static_cast<uint64_t>(bs) * l + 31) / 32, first, count, out));
     }
     CBGX_CUDA(cudaGetLastError());
 }
@@ -318,7 +314,7 @@ int cbgx_frsz2_compress_async(const double* d_in, uint64_t n, uint32_t bs, uint3
                               void* stream) {
     return guard([&] {
         validate(bs, l);
-        launch_compress(d_in, n, cbgx_frsz2_num_blocks(n, bs), bs, l, d_exp, d_payload, nullptr, 0,
+        launch_compress(d_in, n, cbgx_frsz2_num_blocks(n, bs), bs, l, d_exp, d_payload, ScaleArg{},
                         nullptr, d_bad_index, as_stream(stream));
     });
 }
@@ -329,8 +325,8 @@ int cbgx_frsz2_compress(const double* d_in, uint64_t n, uint32_t bs, uint32_t l,
         validate(bs, l);
         cudaStream_t st = as_stream(stream);
         const uint64_t bad = sync_bad_index([&](uint64_t* d_bad) {
-            launch_compress(d_in, n, cbgx_frsz2_num_blocks(n, bs), bs, l, d_exp, d_payload, nullptr,
-                            0, nullptr, d_bad, st);
+            launch_compress(d_in, n, cbgx_frsz2_num_blocks(n, bs), bs, l, d_exp, d_payload, ScaleArg{},
+                            nullptr, d_bad, st);
         }, st);
         if (bad != ~0ull) throw_non_finite(bad);
     });
@@ -358,8 +354,8 @@ int cbgx_frsz2_encode_block(const double* d_values, uint32_t count, uint32_t l, 
         validate(count, l);
         cudaStream_t st = as_stream(stream);
         const uint64_t bad = sync_bad_index([&](uint64_t* d_bad) {
-            encode_block_kernel<<<1, 32, 0, st>>>(d_values, count, l, d_emax, d_codes,
-                                                  reinterpret_cast<unsigned long long*>(d_bad));
+            CBGX_K(encode_block_kernel<<<1, 32, 0, st>>>(d_values, count, l, d_emax, d_codes,
+                                                  reinterpret_cast<unsigned long long*>(d_bad)));
             CBGX_CUDA(cudaGetLastError());
         }, st);
         if (bad != ~0ull) throw_non_finite(bad);

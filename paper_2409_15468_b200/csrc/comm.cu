@@ -108,7 +108,7 @@ struct Scratch {
 };
 
 void sum_gathered(const double* g, int P, size_t count, double* out, cudaStream_t st) {
-    sum_ranks_kernel<<<1, 128, 0, st>>>(g, P, count, out);
+    CBGX_K(sum_ranks_kernel<<<1, 128, 0, st>>>(g, P, count, out));
     CBGX_CUDA(cudaGetLastError());
 }
 
@@ -214,8 +214,8 @@ void Halo::exchange(double* d_vec, cudaStream_t st) const {
     if (!comm || comm->size() == 1) return;
     const uint64_t total = send_offsets.empty() ? 0 : send_offsets.back();
     if (total) {
-        gather_rows_kernel<<<static_cast<int>(std::min<uint64_t>((total + 255) / 256, 1024)), 256, 0, st>>>(
-            d_vec, d_send_idx, total, d_send_buf);
+        CBGX_K(gather_rows_kernel<<<static_cast<int>(std::min<uint64_t>((total + 255) / 256, 1024)), 256, 0, st>>>(
+            d_vec, d_send_idx, total, d_send_buf));
         CBGX_CUDA(cudaGetLastError());
     }
     std::vector<Comm::Msg> sends, recvs;
@@ -399,6 +399,13 @@ int cbgx_halo_destroy(cbgx_halo* h) {
 }
 
 uint64_t cbgx_halo_ghosts(const cbgx_halo* h) { return h ? h->impl->n_ghost : 0; }
+
+int cbgx_halo_exchange(cbgx_halo* h, double* d_vec, void* stream) {
+    return guard([&] {
+        if (!h) throw Error(CBGX_EINVAL, "halo: null handle");
+        h->impl->exchange(d_vec, as_stream(stream));
+    });
+}
 
 int cbgx_solver_create_dist(const cbgx_csr* A, cbgx_halo* halo, const cbgx_gmres_config* cfg,
                             cbgx_comm* comm, cbgx_solver** out) {

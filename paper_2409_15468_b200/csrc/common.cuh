@@ -133,6 +133,36 @@ struct BlockDecoder {
     }
 };
 
+// -------------------------------------------- device-side solver decisions
+// The re-orthogonalisation test of arnoldi_orthogonalize (gmres.cpp:51):
+// h_next < eta * omega with h_next = sqrt(hn1), omega = sqrt(omega2). IEEE
+// sqrt and multiply on the device give the same bits as the host's test, so
+// kernels gated on it run exactly when the reference would run the pass.
+struct GateArg {
+    const double* hn1 = nullptr;     // ||w||^2 after the first CGS pass
+    const double* omega2 = nullptr;  // ||w||^2 before orthogonalisation
+    double eta = 0.0;
+    __device__ __forceinline__ bool open() const {
+        return hn1 == nullptr || sqrt(*hn1) < eta * sqrt(*omega2);
+    }
+};
+
+// Scale applied by the basis writer: none (src == nullptr), *src (mode 0),
+// 1/sqrt(*src) (mode 1: scale(1.0 / h_next, w) with h_next = sqrt(||w||^2)),
+// or 1/sqrt(gate.open() ? src[1] : src[0]) (mode 2: h_next of whichever CGS
+// pass ran last).
+struct ScaleArg {
+    const double* src = nullptr;
+    int mode = 0;
+    GateArg gate;
+    __device__ __forceinline__ double value() const {
+        if (src == nullptr) return 1.0;
+        if (mode == 0) return *src;
+        if (mode == 1) return 1.0 / sqrt(*src);
+        return 1.0 / sqrt(gate.open() ? src[1] : src[0]);
+    }
+};
+
 // ------------------------------------------------------ warp reductions
 __device__ __forceinline__ double warp_sum(double v) {
 #pragma unroll
@@ -141,3 +171,9 @@ __device__ __forceinline__ double warp_sum(double v) {
 }
 
 }  // namespace cbgx
+
+namespace cbgx {
+// Process-wide count of kernels this library launched (cbgx_launch_count).
+void note_launch();
+}  // namespace cbgx
+#define CBGX_K(...) (::cbgx::note_launch(), __VA_ARGS__)

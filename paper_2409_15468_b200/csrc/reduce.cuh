@@ -6,6 +6,7 @@
 
 #include <cstdint>
 
+#include "common.cuh"
 #include "runtime.h"
 
 namespace cbgx {
@@ -28,30 +29,35 @@ __device__ __forceinline__ void block_finalize(const double* red, int nwarps, ui
     __syncthreads();
     if (threadIdx.x == 0) s_last = atomicAdd(ticket, 1u) == gridDim.x - 1;
     __syncthreads();
-    if (s_last) {
-        __threadfence();
-        for (uint32_t k = threadIdx.x; k < ncol; k += blockDim.x) {
-            double s = __ldcg(partials + k);
-            for (unsigned c = 1; c < gridDim.x; ++c)
-                s = __dadd_rn(s, __ldcg(partials + static_cast<uint64_t>(c) * ncol + k));
-            out[k] = s;
-        }
-        if (threadIdx.x == 0) *ticket = 0u;
+    if (!s_last) return;
+    __threadfence();
+    // Column k: lane L sums CTA rows L, L+32, ... in order, then a fixed
+    // butterfly across the warp -- the same shape every launch.
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, nw = blockDim.x >> 5;
+    for (uint32_t k = warp; k < ncol; k += nw) {
+        double s = 0.0;
+        for (unsigned c = lane; c < gridDim.x; c += 32)
+            s = __dadd_rn(s, __ldcg(partials + static_cast<uint64_t>(c) * ncol + k));
+        s = warp_sum(s);
+        if (lane == 0) out[k] = s;
     }
+    if (threadIdx.x == 0) *ticket = 0u;
 }
 
 // Deterministic <x, y>. REDUCE_TREE: fixed-shape tree; REDUCE_REFERENCE:
 // one thread, sequential from +0.0 (sparse.cpp:58-67).
 void launch_dot(const double* x, const double* y, uint64_t n, int reduction, double* out,
-                Workspace* ws, cudaStream_t st);
+                Workspace* ws, cudaStream_t st, const GateArg& gate = GateArg{});
 
+// gate: run only when the device-side re-orthogonalisation test holds.
 void launch_cgs_dot(const cbgx_basis& V, uint64_t first, uint32_t cols, const double* w, int wn,
-                    int reduction, double* h, Workspace* ws, cudaStream_t st);
+                    int reduction, double* h, Workspace* ws, cudaStream_t st,
+                    const GateArg& gate = GateArg{});
 void launch_cgs_update(const cbgx_basis& V, uint64_t first, uint32_t cols, const double* h,
                        double sign, double* w, double* norm, int reduction, Workspace* ws,
-                       cudaStream_t st);
-void launch_basis_write(const cbgx_basis& V, uint64_t j, const double* x, const double* scale_src,
-                        int scale_mode, double* v_out, uint64_t* bad, cudaStream_t st);
+                       cudaStream_t st, const GateArg& gate = GateArg{});
+void launch_basis_write(const cbgx_basis& V, uint64_t j, const double* x, const ScaleArg& scale,
+                        double* v_out, uint64_t* bad, cudaStream_t st);
 void launch_basis_read(const cbgx_basis& V, uint64_t j, uint64_t first, uint64_t count, double* out,
                        cudaStream_t st);
 

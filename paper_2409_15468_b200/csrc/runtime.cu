@@ -1,5 +1,6 @@
 // runtime.cu -- error state, device queries and reduction workspaces for the
 // C-ABI (include/cbgx.h).
+#include <atomic>
 #include <cstdio>
 #include <cstring>
 #include <mutex>
@@ -11,9 +12,12 @@
 namespace cbgx {
 
 namespace {
+std::atomic<uint64_t> g_launches{0};
 thread_local std::string t_msg;
 thread_local uint64_t t_index = 0;
 }  // namespace
+
+void note_launch() { g_launches.fetch_add(1, std::memory_order_relaxed); }
 
 void set_error(int code, const std::string& msg, uint64_t index) {
     (void)code;
@@ -77,6 +81,11 @@ extern "C" {
 const char* cbgx_last_error(void) { return t_msg.c_str(); }
 uint64_t cbgx_last_error_index(void) { return t_index; }
 int cbgx_version(void) { return 1; }
+uint64_t cbgx_launch_count(void) { return g_launches.load(); }
+
+int cbgx_set_device(int device) {
+    return guard([&] { CBGX_CUDA(cudaSetDevice(device)); });
+}
 
 int cbgx_device_info(int* device, int* sms, int64_t* l2) {
     return guard([&] {

@@ -31,13 +31,40 @@ void launch_spmv(const cbgx_csr& A, const double* x, const double* b, double* y,
 
 namespace {
 
-constexpr size_t kHn = 0;     // ||w||^2 after the update (h_next^2)
-constexpr size_t kOmega = 1;  // ||w||^2 before orthogonalisation
-constexpr size_t kH = 2;      // h[0..m]
+// Step slot layout: [hn1, hn2, omega^2, h[0..m], u[0..m]] where hn1/hn2 are
+// ||w||^2 after the first/second CGS pass and u the second pass's
+// coefficients (host adds them to h, gmres.cpp:65-67).
+constexpr size_t kHn1 = 0;
+constexpr size_t kHn2 = 1;
+constexpr size_t kOmega = 2;
+constexpr size_t kH = 3;
+inline size_t kU(uint64_t m) { return kH + m + 1; }
+inline size_t kSlot(uint64_t m) { return (kU(m) + m + 1 + 3) / 4 * 4; }
 
 struct BreakdownError : Error {
     BreakdownError(const std::string& m, uint64_t it) : Error(CBGX_EBREAKDOWN, m, it) {}
 };
+
+__global__ void narrow_csr_kernel(const uint64_t* __restrict__ rp64, uint64_t n, int32_t* __restrict__ rp32,
+                                  const uint64_t* __restrict__ ci64, uint64_t nnz, int32_t* __restrict__ ci32,
+                                  uint64_t* __restrict__ bad) {
+    const uint64_t stride = static_cast<uint64_t>(gridDim.x) * blockDim.x;
+    for (uint64_t k = blockIdx.x * static_cast<uint64_t>(blockDim.x) + threadIdx.x; k < nnz; k += stride) {
+        const uint64_t c = ci64[k];
+        if (c >= n) *bad = 1;
+        ci32[k] = static_cast<int32_t>(c);
+    }
+    if (rp32)
+        for (uint64_t r = blockIdx.x * static_cast<uint64_t>(blockDim.x) + threadIdx.x; r <= n; r += stride)
+            rp32[r] = static_cast<int32_t>(rp64[r]);
+}
+
+void narrow_csr(const uint64_t* rp64, uint64_t n, int32_t* rp32, const uint64_t* ci64, uint64_t nnz,
+                int32_t* ci32, uint64_t* bad, cudaStream_t st) {
+    const int grid = static_cast<int>(std::min<uint64_t>((std::max(nnz, n + 1) + 255) / 256, sm_count() * 8ull));
+    CBGX_K(narrow_csr_kernel<<<std::max(grid, 1), 256, 0, st>>>(rp64, n, rp32, ci64, nnz, ci32, bad));
+    CBGX_CUDA(cudaGetLastError());
+}
 
 int fmt_from_cfg(const cbgx_gmres_config& c) {
     cbgx_basis tmp{};
@@ -122,11 +149,23 @@ Solver::Solver(const cbgx_csr& A, const cbgx_gmres_config& cfg, Comm* comm, Halo
     CBGX_CUDA(cudaMalloc(&d_r_, std::max<uint64_t>(n_, 1) * sizeof(double)));
     CBGX_CUDA(cudaMalloc(&d_v_, std::max<uint64_t>(n_ + ghosts, 1) * sizeof(double)));
     CBGX_CUDA(cudaMalloc(&d_w_, std::max<uint64_t>(n_, 1) * sizeof(double)));
-    CBGX_CUDA(cudaMalloc(&d_scal_, (3 * m + 16) * sizeof(double)));
-    CBGX_CUDA(cudaMallocHost(&h_pinned_, (3 * m + 16) * sizeof(double)));
+    const size_t scal = 2 * kSlot(m) + 2 * m + 16;
+    CBGX_CUDA(cudaMalloc(&d_scal_, scal * sizeof(double)));
+    CBGX_CUDA(cudaMemset(d_scal_, 0, scal * sizeof(double)));
+    CBGX_CUDA(cudaMallocHost(&h_pinned_, scal * sizeof(double)));
+    for (auto& e : step_ev_) CBGX_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+}
+
+void Solver::collect_phases(double* ms, size_t count) {
+    cbgx_solve_stats S{};
+    if (timer_) timer_->collect(&S);
+    for (size_t i = 0; i < count && i < CBGX_NUM_PHASES; ++i) ms[i] = S.phase_ms[i];
 }
 
 Solver::~Solver() {
+    delete timer_;
+    for (auto e : step_ev_)
+        if (e) cudaEventDestroy(e);
     cudaFree(d_basis_);
     cudaFree(d_exp_);
     cudaFree(d_r_);
@@ -150,8 +189,9 @@ void Solver::solve(const double* d_b, const double* d_x0, double* d_x, cbgx_hist
                    cbgx_solve_stats* stats, cudaStream_t st) {
     const auto t_start = std::chrono::steady_clock::now();
     cbgx_solve_stats S{};
-    PhaseTimer timer;
-    timer.on = (cfg_.flags & CBGX_SOLVER_PHASE_TIMING) != 0;
+    if (!timer_) timer_ = new PhaseTimer();
+    PhaseTimer& timer = *timer_;
+    timer.on = (cfg_.flags & (CBGX_SOLVER_PHASE_TIMING | CBGX_SOLVER_PHASE_TIMING_DEFERRED)) != 0;
     timer.st = st;
     const int red = static_cast<int>(cfg_.reduction);
     const uint64_t m = cfg_.restart;
@@ -160,6 +200,7 @@ void Solver::solve(const double* d_b, const double* d_x0, double* d_x, cbgx_hist
     const double bpv = stored_bytes_per_value(fmt);
     const double rp_bytes = A_.row_ptr_bits / 8.0;
     const double spmv_bytes = A_.nnz * 12.0 + (n + 1) * rp_bytes + 16.0 * n;
+    const bool multi = comm_ && comm_->size() > 1;
     uint64_t hist_len = 0;
     auto push = [&](uint64_t it, double rrn, bool ex) {
         if (hist && hist_len < hist->capacity) {
@@ -174,11 +215,11 @@ void Solver::solve(const double* d_b, const double* d_x0, double* d_x, cbgx_hist
         S.phase_launches[phase] += launches;
         S.kernel_launches += launches;
     };
-    double* scal = d_scal_;
-    double* h_u = scal + kH + m + 2;  // re-orthogonalisation coefficients u
-    double* h_y = h_u + m + 2;        // least-squares solution y
-    double* rn = h_y + m + 2;         // ||b||^2, then ||r||^2 at each restart
-    double* hs = h_pinned_;
+    // Device scalars: two step slots (double-buffered so step i+1 can run
+    // while the host still reads step i), then y and the restart norm.
+    const size_t slot = kSlot(m);
+    double* y_dev = d_scal_ + 2 * slot;
+    double* rn = y_dev + m + 2;
 
     // ||b|| (gmres.cpp:161)
     timer.begin(CBGX_PHASE_RESIDUAL);
@@ -198,6 +239,72 @@ void Solver::solve(const double* d_b, const double* d_x0, double* d_x, cbgx_hist
         std::vector<double> hcol(m + 2), y(m);
         uint64_t iter = 0, cycles = 0;
         double last = 0.0;
+
+        // One Arnoldi step on the device (gmres.cpp:210-234 minus the host
+        // Givens): spmv, CGS pass, gated second pass, scaled write of the
+        // next column, and one D2H of the step's slot. `used` columns are in
+        // the basis when the step starts; it writes column used+1.
+        auto enqueue_step = [&](uint64_t used, int p) {
+            double* sl = d_scal_ + p * slot;
+            const uint32_t cols = static_cast<uint32_t>(used + 1);
+            GateArg gate;
+            gate.hn1 = sl + kHn1;
+            gate.omega2 = sl + kOmega;
+            gate.eta = cfg_.eta;
+            if (halo_) {
+                timer.begin(CBGX_PHASE_COMM);
+                halo_->exchange(d_v_, st);
+                timer.end();
+            }
+            timer.begin(CBGX_PHASE_SPMV);
+            launch_spmv(A_, d_v_, nullptr, d_w_, sl + kOmega, red, &ws_, st);  // w = A v, omega^2
+            timer.end();
+            count(CBGX_PHASE_SPMV, spmv_bytes);
+            timer.begin(CBGX_PHASE_DOT);
+            launch_cgs_dot(V_, 0, cols, d_w_, 0, red, sl + kH, &ws_, st);      // h = V^T w
+            timer.end();
+            count(CBGX_PHASE_DOT, cols * bpv * n + 8.0 * n);
+            if (multi) {
+                timer.begin(CBGX_PHASE_COMM);
+                reduce(sl + kOmega, cols + 1, st);
+                timer.end();
+            }
+            timer.begin(CBGX_PHASE_UPDATE);
+            launch_cgs_update(V_, 0, cols, sl + kH, 1.0, d_w_, sl + kHn1, red, &ws_, st);  // w -= V h
+            timer.end();
+            count(CBGX_PHASE_UPDATE, cols * bpv * n + 16.0 * n);
+            if (multi) {
+                timer.begin(CBGX_PHASE_COMM);
+                reduce(sl + kHn1, 1, st);
+                timer.end();
+            }
+            // Second CGS pass, gated on the device by the reference's test
+            // h_next < eta * omega (gmres.cpp:51-68); empty launches otherwise.
+            timer.begin(CBGX_PHASE_DOT);
+            launch_cgs_dot(V_, 0, cols, d_w_, 0, red, sl + kU(m), &ws_, st, gate);
+            timer.end();
+            if (multi) reduce(sl + kU(m), cols, st);
+            timer.begin(CBGX_PHASE_UPDATE);
+            launch_cgs_update(V_, 0, cols, sl + kU(m), 1.0, d_w_, sl + kHn2, red, &ws_, st, gate);
+            timer.end();
+            if (multi) reduce(sl + kHn2, 1, st);
+            S.kernel_launches += 2;
+            // v = w / h_next of the last pass that ran; column used+1
+            // (gmres.cpp:230-234). Written even when the host will later
+            // detect a breakdown: that column is then never read.
+            ScaleArg sc;
+            sc.src = sl + kHn1;
+            sc.mode = 2;
+            sc.gate = gate;
+            timer.begin(CBGX_PHASE_WRITE);
+            launch_basis_write(V_, used + 1, d_w_, sc, d_v_, nullptr, st);
+            timer.end();
+            count(CBGX_PHASE_WRITE, 16.0 * n + bpv * n);
+            CBGX_CUDA(cudaMemcpyAsync(h_pinned_ + p * slot, sl, kU(m) * sizeof(double) + cols * sizeof(double),
+                                      cudaMemcpyDeviceToHost, st));
+            CBGX_CUDA(cudaEventRecord(step_ev_[p], st));
+        };
+
         for (;;) {
             // Explicit residual r = b - A x (gmres.cpp:181-190).
             timer.begin(CBGX_PHASE_RESIDUAL);
@@ -228,70 +335,43 @@ void Solver::solve(const double* d_b, const double* d_x0, double* d_x, cbgx_hist
             lsq.reset(beta);
             // v = r * (1/beta); column 0 (gmres.cpp:201-204)
             timer.begin(CBGX_PHASE_WRITE);
-            launch_basis_write(V_, 0, d_r_, rn, 1, d_v_, nullptr, st);
+            ScaleArg sc0;
+            sc0.src = rn;
+            sc0.mode = 1;
+            launch_basis_write(V_, 0, d_r_, sc0, d_v_, nullptr, st);
             timer.end();
             count(CBGX_PHASE_WRITE, 16.0 * n + bpv * n);
 
             uint64_t used = 0;
             bool cycle_done = false;
-            while (!cycle_done && used < m && iter < cfg_.max_total_iterations) {
+            // Steps that can run in this cycle (restart and iteration cap).
+            const uint64_t max_steps = std::min<uint64_t>(m, cfg_.max_total_iterations - iter);
+            enqueue_step(0, 0);
+            uint64_t enqueued = 1;
+            while (!cycle_done) {
+                // Look one step ahead: the device works on step used+1 while
+                // the host runs Givens on step `used`.
+                if (enqueued < max_steps) {
+                    enqueue_step(enqueued, static_cast<int>(enqueued & 1));
+                    ++enqueued;
+                }
+                const int p = static_cast<int>(used & 1);
+                CBGX_CUDA(cudaEventSynchronize(step_ev_[p]));
+                const double* hs = h_pinned_ + p * slot;
                 ++iter;
                 const uint32_t cols = static_cast<uint32_t>(used + 1);
-                // w = A v, omega^2 fused (gmres.cpp:210, :43)
-                if (halo_) {
-                    timer.begin(CBGX_PHASE_COMM);
-                    halo_->exchange(d_v_, st);
-                    timer.end();
-                }
-                timer.begin(CBGX_PHASE_SPMV);
-                launch_spmv(A_, d_v_, nullptr, d_w_, scal + kOmega, red, &ws_, st);
-                timer.end();
-                count(CBGX_PHASE_SPMV, spmv_bytes);
-                // h = V^T w (gmres.cpp:44-46)
-                timer.begin(CBGX_PHASE_DOT);
-                launch_cgs_dot(V_, 0, cols, d_w_, 0, red, scal + kH, &ws_, st);
-                timer.end();
-                count(CBGX_PHASE_DOT, cols * bpv * n + 8.0 * n);
-                if (comm_ && comm_->size() > 1) {
-                    timer.begin(CBGX_PHASE_COMM);
-                    reduce(scal + kOmega, cols + 1, st);
-                    timer.end();
-                }
-                // w -= V h, h_next^2 fused (gmres.cpp:47-50)
-                timer.begin(CBGX_PHASE_UPDATE);
-                launch_cgs_update(V_, 0, cols, scal + kH, 1.0, d_w_, scal + kHn, red, &ws_, st);
-                timer.end();
-                count(CBGX_PHASE_UPDATE, cols * bpv * n + 16.0 * n);
-                if (comm_ && comm_->size() > 1) {
-                    timer.begin(CBGX_PHASE_COMM);
-                    reduce(scal + kHn, 1, st);
-                    timer.end();
-                }
-                CBGX_CUDA(cudaMemcpyAsync(hs, scal, (kH + cols) * sizeof(double), cudaMemcpyDeviceToHost, st));
-                CBGX_CUDA(cudaStreamSynchronize(st));
                 const double omega = std::sqrt(hs[kOmega]);
-                double h_next = std::sqrt(hs[kHn]);
+                double h_next = std::sqrt(hs[kHn1]);
                 for (uint64_t i = 0; i < cols; ++i) hcol[i] = hs[kH + i];
                 bool breakdown = false;
                 if (h_next < cfg_.eta * omega) {
-                    // one re-orthogonalisation pass (gmres.cpp:53-68)
+                    // the device ran the second pass (gmres.cpp:53-68)
                     ++S.reorth_passes;
-                    const double before = h_next;
-                    timer.begin(CBGX_PHASE_DOT);
-                    launch_cgs_dot(V_, 0, cols, d_w_, 0, red, h_u, &ws_, st);
-                    reduce(h_u, cols, st);
-                    timer.end();
                     count(CBGX_PHASE_DOT, cols * bpv * n + 8.0 * n);
-                    timer.begin(CBGX_PHASE_UPDATE);
-                    launch_cgs_update(V_, 0, cols, h_u, 1.0, d_w_, scal + kHn, red, &ws_, st);
-                    reduce(scal + kHn, 1, st);
-                    timer.end();
                     count(CBGX_PHASE_UPDATE, cols * bpv * n + 16.0 * n);
-                    CBGX_CUDA(cudaMemcpyAsync(hs + kH + m + 2, h_u, cols * sizeof(double), cudaMemcpyDeviceToHost, st));
-                    CBGX_CUDA(cudaMemcpyAsync(hs + kHn, scal + kHn, sizeof(double), cudaMemcpyDeviceToHost, st));
-                    CBGX_CUDA(cudaStreamSynchronize(st));
-                    for (uint64_t i = 0; i < cols; ++i) hcol[i] += hs[kH + m + 2 + i];
-                    h_next = std::sqrt(hs[kHn]);
+                    const double before = h_next;
+                    for (uint64_t i = 0; i < cols; ++i) hcol[i] += hs[kU(m) + i];
+                    h_next = std::sqrt(hs[kHn2]);
                     breakdown = h_next < cfg_.eta * before;
                 }
                 breakdown = breakdown || h_next == 0.0;
@@ -304,35 +384,30 @@ void Solver::solve(const double* d_b, const double* d_x0, double* d_x, cbgx_hist
                 lsq.add_column(hcol.data(), used + 2, &estimate);
                 ++used;
                 const double implicit_rrn = estimate / norm_b;
-                if (!breakdown) {
-                    // v = w / h_next; column `used` (gmres.cpp:230-234)
-                    timer.begin(CBGX_PHASE_WRITE);
-                    launch_basis_write(V_, used, d_w_, scal + kHn, 1, d_v_, nullptr, st);
-                    timer.end();
-                    count(CBGX_PHASE_WRITE, 16.0 * n + bpv * n);
-                }
                 cycle_done = breakdown || implicit_rrn <= cfg_.target_rrn || used == m ||
                              iter >= cfg_.max_total_iterations;
                 if (!cycle_done) push(iter, implicit_rrn, false);
             }
+            // A speculative step beyond the cycle end may still be in flight;
+            // it only touched w, v, its scalar slot and basis column used+1..,
+            // none of which the solution update below reads.
             // x += V y (gmres.cpp:242-243, :134-139)
             const long bad = lsq.solve_y(y.data());
             if (bad >= 0) throw BreakdownError("gmres: singular triangular factor", static_cast<uint64_t>(bad));
             timer.begin(CBGX_PHASE_SOLUTION);
-            std::memcpy(hs, y.data(), used * sizeof(double));
-            CBGX_CUDA(cudaMemcpyAsync(h_y, hs, used * sizeof(double), cudaMemcpyHostToDevice, st));
-            launch_cgs_update(V_, 0, static_cast<uint32_t>(used), h_y, -1.0, d_x, nullptr, red, &ws_, st);
+            double* hy = h_pinned_ + 2 * slot;
+            std::memcpy(hy, y.data(), used * sizeof(double));
+            CBGX_CUDA(cudaMemcpyAsync(y_dev, hy, used * sizeof(double), cudaMemcpyHostToDevice, st));
+            launch_cgs_update(V_, 0, static_cast<uint32_t>(used), y_dev, -1.0, d_x, nullptr, red, &ws_, st);
             timer.end();
             count(CBGX_PHASE_SOLUTION, used * bpv * n + 16.0 * n);
-            // The H2D above reads the pinned buffer asynchronously; the next
-            // fetch synchronises before it is reused.
         }
         S.total_iterations = iter;
         S.restarts = cycles > 0 ? cycles - 1 : 0;
         S.final_rrn = last;
     }
     CBGX_CUDA(cudaStreamSynchronize(st));
-    timer.collect(&S);
+    if (cfg_.flags & CBGX_SOLVER_PHASE_TIMING) timer.collect(&S);
     S.wall_seconds = std::chrono::duration<double>(std::chrono::steady_clock::now() - t_start).count();
     if (hist) hist->length = hist_len;
     if (stats) *stats = S;
@@ -373,6 +448,13 @@ int cbgx_solver_destroy(cbgx_solver* s) {
     return guard([&] { delete reinterpret_cast<SolverHandle*>(s); });
 }
 
+int cbgx_solver_phase_times(cbgx_solver* s, double* ms, uint64_t count) {
+    return guard([&] {
+        if (!s) throw Error(CBGX_EINVAL, "solver: null handle");
+        reinterpret_cast<SolverHandle*>(s)->solver->collect_phases(ms, count);
+    });
+}
+
 int cbgx_solver_solve(cbgx_solver* s, const double* d_b, const double* d_x0, double* d_x,
                       cbgx_history* hist, cbgx_solve_stats* stats, void* stream) {
     return guard([&] {
@@ -390,41 +472,49 @@ int cbgx_gmres_solve_host(uint64_t n, const uint64_t* row_ptrs, const uint64_t* 
         if (n > 0x7FFFFFFFull) throw Error(CBGX_EINVAL, "gmres: n must fit int32 column indices");
         const uint64_t nnz = row_ptrs[n];
         const bool wide = nnz > 0x7FFFFFFFull;
-        std::vector<int32_t> ci(nnz);
-        for (uint64_t k = 0; k < nnz; ++k) {
-            if (col_idx[k] >= n) throw Error(CBGX_EINVAL, "csr: column index out of range");
-            ci[k] = static_cast<int32_t>(col_idx[k]);
-        }
-        std::vector<int32_t> rp32;
-        if (!wide) {
-            rp32.resize(n + 1);
-            for (uint64_t r = 0; r <= n; ++r) rp32[r] = static_cast<int32_t>(row_ptrs[r]);
-        }
+        // Stream-ordered staging: the size_t CSR of the reference
+        // (CsrMatrix, sparse.hpp:17-26) goes over as-is and is narrowed on the
+        // device (int32 columns, int32/int64 row offsets).
         cudaStream_t st = nullptr;
-        void* d_rp = nullptr;
-        int32_t* d_ci = nullptr;
-        double *d_va = nullptr, *d_b = nullptr, *d_x0 = nullptr, *d_x = nullptr;
+        CBGX_CUDA(cudaStreamCreateWithFlags(&st, cudaStreamNonBlocking));
+        std::vector<void*> bufs;
+        auto alloc = [&](size_t bytes) {
+            void* p = nullptr;
+            CBGX_CUDA(cudaMallocAsync(&p, std::max<size_t>(bytes, 8), st));
+            bufs.push_back(p);
+            return p;
+        };
         auto cleanup = [&] {
-            cudaFree(d_rp); cudaFree(d_ci); cudaFree(d_va); cudaFree(d_b); cudaFree(d_x0); cudaFree(d_x);
+            for (void* p : bufs) cudaFreeAsync(p, st);
+            cudaStreamSynchronize(st);
+            cudaStreamDestroy(st);
         };
         try {
-            const size_t rpb = wide ? 8 : 4;
-            CBGX_CUDA(cudaMalloc(&d_rp, (n + 1) * rpb));
-            CBGX_CUDA(cudaMalloc(&d_ci, std::max<uint64_t>(nnz, 1) * 4));
-            CBGX_CUDA(cudaMalloc(&d_va, std::max<uint64_t>(nnz, 1) * 8));
-            CBGX_CUDA(cudaMalloc(&d_b, std::max<uint64_t>(n, 1) * 8));
-            CBGX_CUDA(cudaMalloc(&d_x0, std::max<uint64_t>(n, 1) * 8));
-            CBGX_CUDA(cudaMalloc(&d_x, std::max<uint64_t>(n, 1) * 8));
-            CBGX_CUDA(cudaMemcpy(d_rp, wide ? static_cast<const void*>(row_ptrs) : static_cast<const void*>(rp32.data()),
-                                 (n + 1) * rpb, cudaMemcpyHostToDevice));
-            CBGX_CUDA(cudaMemcpy(d_ci, ci.data(), nnz * 4, cudaMemcpyHostToDevice));
-            CBGX_CUDA(cudaMemcpy(d_va, values, nnz * 8, cudaMemcpyHostToDevice));
-            CBGX_CUDA(cudaMemcpy(d_b, b, n * 8, cudaMemcpyHostToDevice));
-            CBGX_CUDA(cudaMemcpy(d_x0, x0, n * 8, cudaMemcpyHostToDevice));
+            auto* d_rp64 = static_cast<uint64_t*>(alloc((n + 1) * 8));
+            auto* d_ci64 = static_cast<uint64_t*>(alloc(nnz * 8));
+            auto* d_va = static_cast<double*>(alloc(nnz * 8));
+            auto* d_b = static_cast<double*>(alloc(n * 8));
+            auto* d_x0 = static_cast<double*>(alloc(n * 8));
+            auto* d_x = static_cast<double*>(alloc(n * 8));
+            auto* d_ci = static_cast<int32_t*>(alloc(nnz * 4));
+            void* d_rp = wide ? static_cast<void*>(d_rp64) : alloc((n + 1) * 4);
+            auto* d_bad = static_cast<uint64_t*>(alloc(8));
+            CBGX_CUDA(cudaMemsetAsync(d_bad, 0, 8, st));
+            CBGX_CUDA(cudaMemcpyAsync(d_rp64, row_ptrs, (n + 1) * 8, cudaMemcpyHostToDevice, st));
+            CBGX_CUDA(cudaMemcpyAsync(d_ci64, col_idx, nnz * 8, cudaMemcpyHostToDevice, st));
+            CBGX_CUDA(cudaMemcpyAsync(d_va, values, nnz * 8, cudaMemcpyHostToDevice, st));
+            CBGX_CUDA(cudaMemcpyAsync(d_b, b, n * 8, cudaMemcpyHostToDevice, st));
+            CBGX_CUDA(cudaMemcpyAsync(d_x0, x0, n * 8, cudaMemcpyHostToDevice, st));
+            narrow_csr(d_rp64, n, wide ? nullptr : static_cast<int32_t*>(d_rp), d_ci64, nnz, d_ci, d_bad, st);
+            uint64_t bad = 0;
+            CBGX_CUDA(cudaMemcpyAsync(&bad, d_bad, 8, cudaMemcpyDeviceToHost, st));
+            CBGX_CUDA(cudaStreamSynchronize(st));
+            if (bad) throw Error(CBGX_EINVAL, "csr: column index out of range");
             cbgx_csr A{n, n, nnz, d_rp, wide ? 64u : 32u, d_ci, d_va};
             Solver solver(A, c, nullptr, nullptr);
             solver.solve(d_b, d_x0, d_x, hist, stats, st);
-            CBGX_CUDA(cudaMemcpy(x_out, d_x, n * 8, cudaMemcpyDeviceToHost));
+            CBGX_CUDA(cudaMemcpyAsync(x_out, d_x, n * 8, cudaMemcpyDeviceToHost, st));
+            CBGX_CUDA(cudaStreamSynchronize(st));
         } catch (...) {
             cleanup();
             throw;

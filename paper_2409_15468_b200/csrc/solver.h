@@ -57,8 +57,12 @@ public:
     void solve(const double* d_b, const double* d_x0, double* d_x, cbgx_history* hist,
                cbgx_solve_stats* stats, cudaStream_t st);
 
+    // Device time per phase accumulated over deferred-timing solves (resets).
+    void collect_phases(double* ms, size_t count);
+
 private:
     struct PhaseTimer;
+    PhaseTimer* timer_ = nullptr;
     void reduce(double* d_vals, size_t count, cudaStream_t st);
     double fetch_scalar(const double* d, cudaStream_t st);
 
@@ -75,6 +79,7 @@ private:
     double* d_w_ = nullptr;
     double* d_scal_ = nullptr;   // [0] omega^2 [1] hn^2 [2] ||b||^2 [3] ||r||^2 [4..] h / u / y
     double* h_pinned_ = nullptr;
+    cudaEvent_t step_ev_[2] = {nullptr, nullptr};
     Workspace ws_;
 };
 

@@ -55,7 +55,9 @@ spmv_kernel(uint64_t n_rows, const RP* __restrict__ rp, const int32_t* __restric
 
 __global__ void __launch_bounds__(kThreads)
 dot_kernel(const double* __restrict__ x, const double* __restrict__ y, uint64_t n,
-           double* __restrict__ partials, unsigned* __restrict__ ticket, double* __restrict__ out) {
+           double* __restrict__ partials, unsigned* __restrict__ ticket, double* __restrict__ out,
+           GateArg gate) {
+    if (!gate.open()) return;
     __shared__ double red[kWarps];
     double acc = 0.0;
     for (uint64_t i = blockIdx.x * static_cast<uint64_t>(kThreads) + threadIdx.x; i < n;
@@ -68,7 +70,8 @@ dot_kernel(const double* __restrict__ x, const double* __restrict__ y, uint64_t 
 }
 
 __global__ void serial_dot_kernel(const double* __restrict__ x, const double* __restrict__ y,
-                                  uint64_t n, double* __restrict__ out) {
+                                  uint64_t n, double* __restrict__ out, GateArg gate) {
+    if (!gate.open()) return;
     double s = 0.0;
     for (uint64_t i = 0; i < n; ++i) s = __dadd_rn(s, __dmul_rn(x[i], y[i]));
     *out = s;
@@ -145,7 +148,7 @@ void stencil_generate(int kind, Grid3 g, double pe, uint64_t rb, uint64_t re, in
                       RP* rp, int32_t* ci, double* va, cudaStream_t st) {
     const uint64_t rows = re - rb;
     const int grid = static_cast<int>(std::min<uint64_t>((rows + 256) / 256 + 1, sm_count() * 16ull));
-    stencil_count_kernel<RP><<<grid, 256, 0, st>>>(kind, g, rb, rows, rp);
+    CBGX_K(stencil_count_kernel<RP><<<grid, 256, 0, st>>>(kind, g, rb, rows, rp));
     CBGX_CUDA(cudaGetLastError());
     size_t tmp_bytes = 0;
     CBGX_CUDA(cub::DeviceScan::ExclusiveSum(nullptr, tmp_bytes, rp, rp, rows + 1, st));
@@ -153,7 +156,7 @@ void stencil_generate(int kind, Grid3 g, double pe, uint64_t rb, uint64_t re, in
     CBGX_CUDA(cudaMallocAsync(&tmp, tmp_bytes, st));
     CBGX_CUDA(cub::DeviceScan::ExclusiveSum(tmp, tmp_bytes, rp, rp, rows + 1, st));
     CBGX_CUDA(cudaFreeAsync(tmp, st));
-    stencil_fill_kernel<RP><<<grid, 256, 0, st>>>(kind, g, pe, rb, rows, col_offset, rp, ci, va);
+    CBGX_K(stencil_fill_kernel<RP><<<grid, 256, 0, st>>>(kind, g, pe, rb, rows, col_offset, rp, ci, va));
     CBGX_CUDA(cudaGetLastError());
 }
 
@@ -172,9 +175,9 @@ void launch_spmv(const cbgx_csr& A, const double* x, const double* b, double* y,
     double* partials = fused ? ws->get_partials(grid) : nullptr;
     unsigned* ticket = fused ? ws->get_counter() : nullptr;
 #define CBGX_SPMV(RP, MODE)                                                                     \
-    spmv_kernel<RP, MODE><<<grid, kThreads, 0, st>>>(A.n_rows, static_cast<const RP*>(A.d_row_ptr), \
+    CBGX_K(spmv_kernel<RP, MODE><<<grid, kThreads, 0, st>>>(A.n_rows, static_cast<const RP*>(A.d_row_ptr), \
                                                      A.d_col_idx, A.d_values, x, b, y, fused,     \
-                                                     partials, ticket, norm)
+                                                     partials, ticket, norm))
     if (A.row_ptr_bits == 32) {
         if (b) CBGX_SPMV(int32_t, 1); else CBGX_SPMV(int32_t, 0);
     } else {
@@ -186,12 +189,12 @@ void launch_spmv(const cbgx_csr& A, const double* x, const double* b, double* y,
 }
 
 void launch_dot(const double* x, const double* y, uint64_t n, int reduction, double* out,
-                Workspace* ws, cudaStream_t st) {
+                Workspace* ws, cudaStream_t st, const GateArg& gate) {
     if (reduction == CBGX_REDUCE_REFERENCE) {
-        serial_dot_kernel<<<1, 1, 0, st>>>(x, y, n, out);
+        CBGX_K(serial_dot_kernel<<<1, 1, 0, st>>>(x, y, n, out, gate));
     } else {
         const int grid = rows_grid(n);
-        dot_kernel<<<grid, kThreads, 0, st>>>(x, y, n, ws->get_partials(grid), ws->get_counter(), out);
+        CBGX_K(dot_kernel<<<grid, kThreads, 0, st>>>(x, y, n, ws->get_partials(grid), ws->get_counter(), out, gate));
     }
     CBGX_CUDA(cudaGetLastError());
 }
@@ -232,7 +235,7 @@ int cbgx_dot(const double* d_x, const double* d_y, uint64_t n, int reduction, do
 int cbgx_scale(double alpha, double* d_x, uint64_t n, void* stream) {
     return guard([&] {
         if (!n) return;
-        scale_kernel<<<rows_grid(n), kThreads, 0, as_stream(stream)>>>(alpha, d_x, n);
+        CBGX_K(scale_kernel<<<rows_grid(n), kThreads, 0, as_stream(stream)>>>(alpha, d_x, n));
         CBGX_CUDA(cudaGetLastError());
     });
 }
@@ -240,7 +243,7 @@ int cbgx_scale(double alpha, double* d_x, uint64_t n, void* stream) {
 int cbgx_axpy(double alpha, const double* d_x, double* d_y, uint64_t n, void* stream) {
     return guard([&] {
         if (!n) return;
-        axpy_kernel<<<rows_grid(n), kThreads, 0, as_stream(stream)>>>(alpha, d_x, d_y, n);
+        CBGX_K(axpy_kernel<<<rows_grid(n), kThreads, 0, as_stream(stream)>>>(alpha, d_x, d_y, n));
         CBGX_CUDA(cudaGetLastError());
     });
 }
