@@ -48,6 +48,13 @@ int cbgx_version(void);
 uint64_t cbgx_launch_count(void);
 /* make `device` current for this library on the calling thread */
 int cbgx_set_device(int device);
+/* Device memory for callers that do not link the CUDA runtime themselves
+ * (the C++ drop-in): synchronous allocate / free / copy / fill.
+ * kind: 0 host->device, 1 device->host, 2 device->device. */
+int cbgx_malloc(void** d_ptr, uint64_t bytes);
+int cbgx_free(void* d_ptr);
+int cbgx_memcpy(void* dst, const void* src, uint64_t bytes, int kind);
+int cbgx_memset(void* d_ptr, int value, uint64_t bytes);
 /* device ordinal, SM count and L2 bytes of the current device */
 int cbgx_device_info(int* device, int* sm_count, int64_t* l2_bytes);
 
@@ -299,6 +306,20 @@ int cbgx_halo_create(cbgx_comm* c, uint64_t row_begin, uint64_t row_end, uint64_
                      const int64_t* d_global_cols, uint64_t nnz, int32_t* d_local_cols_out,
                      cbgx_halo** out);
 int cbgx_halo_destroy(cbgx_halo* h);
+/* Pure host pieces of the halo plan (what cbgx_halo_create runs between its
+ * collectives), exposed so the partition logic can be tested without GPUs:
+ * row_ranges = [begin_0, end_0, begin_1, ...]; outputs the remapped local
+ * columns (nnz), the sorted ghost list (<= nnz entries) and need_per_rank
+ * (ghosts owned by each rank). */
+int cbgx_halo_plan(int nranks, int rank, const uint64_t* row_ranges, uint64_t n_global,
+                   const int64_t* gcols, uint64_t nnz, int32_t* local_cols_out,
+                   int64_t* ghosts_out, uint64_t* n_ghosts, uint64_t* need_per_rank);
+/* Owner side: global rows requested by a peer -> local row indices to pack. */
+int cbgx_halo_send_index(uint64_t row_begin, uint64_t row_end, const int64_t* requested,
+                         uint64_t count, int32_t* send_idx_out);
+/* Host form of the rank-ordered combine the device runs after an
+ * all-gather: out[k] = sum_r gathered[r*count + k], r = 0..nranks-1 in order. */
+int cbgx_sum_ranks_host(int nranks, uint64_t count, const double* gathered, double* out);
 uint64_t cbgx_halo_ghosts(const cbgx_halo* h);
 /* fill d_vec[n_local .. n_local+ghosts) from the owners' rows (collective) */
 int cbgx_halo_exchange(cbgx_halo* h, double* d_vec, void* stream);

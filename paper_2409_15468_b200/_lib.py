@@ -101,6 +101,13 @@ def lib():
             "cbgx_halo_create": ([vp, u64, u64, u64, vp, u64, vp, P(vp)], C.c_int),
             "cbgx_halo_destroy": ([vp], C.c_int),
             "cbgx_halo_ghosts": ([vp], u64),
+            "cbgx_halo_plan": ([C.c_int, C.c_int, vp, u64, vp, u64, vp, vp, P(u64), vp], C.c_int),
+            "cbgx_halo_send_index": ([u64, u64, vp, u64, vp], C.c_int),
+            "cbgx_sum_ranks_host": ([C.c_int, u64, vp, vp], C.c_int),
+            "cbgx_malloc": ([P(vp), u64], C.c_int),
+            "cbgx_free": ([vp], C.c_int),
+            "cbgx_memcpy": ([vp, vp, u64, C.c_int], C.c_int),
+            "cbgx_memset": ([vp, C.c_int, u64], C.c_int),
             "cbgx_solver_create_dist": ([P(Csr), vp, P(GmresConfig), vp, P(vp)], C.c_int),
             "cbgx_gmres_solve_partitioned_local": ([u64, vp, vp, vp, vp, vp, P(GmresConfig), C.c_int, vp,
                                                     P(History), P(SolveStats)], C.c_int),
@@ -109,6 +116,7 @@ def lib():
             f = getattr(L, name)
             f.argtypes = args
             f.restype = res
+        L.cbgx_signatures = frozenset(sigs)
         _lib = L
     return _lib
 

@@ -228,6 +228,67 @@ void Halo::exchange(double* d_vec, cudaStream_t st) const {
     comm->exchange(sends, recvs, st);
 }
 
+// ------------------------------------------------ pure host halo planning
+// (no device calls; exposed through the C-ABI so the partition logic is
+// testable on CPU with a gloo communicator, tests/test_dist_cpu.py)
+struct HaloPlan {
+    std::vector<int64_t> ghosts;     // sorted global indices not owned here
+    std::vector<uint64_t> need;      // need[o]: ghosts owned by rank o
+    std::vector<int32_t> local_cols; // remapped columns
+};
+
+HaloPlan plan_halo(int P, int me, const uint64_t* ranges, uint64_t n_global, const int64_t* cols, uint64_t nnz) {
+    for (int r = 0; r < P; ++r) {
+        if (ranges[2 * r] > ranges[2 * r + 1] || (r > 0 && ranges[2 * r] != ranges[2 * r - 1]))
+            throw Error(CBGX_EINVAL, "halo: row blocks must be contiguous and ordered by rank");
+    }
+    if (ranges[0] != 0 || ranges[2 * P - 1] != n_global) throw Error(CBGX_EINVAL, "halo: row blocks must cover the matrix");
+    const uint64_t rb = ranges[2 * me], re = ranges[2 * me + 1];
+    auto owner = [&](int64_t c) {
+        int lo = 0, hi = P - 1;
+        while (lo < hi) {
+            const int mid = (lo + hi + 1) / 2;
+            if (static_cast<uint64_t>(c) >= ranges[2 * mid]) lo = mid; else hi = mid - 1;
+        }
+        return lo;
+    };
+    HaloPlan H;
+    for (uint64_t k = 0; k < nnz; ++k) {
+        const int64_t c = cols[k];
+        if (c < 0 || static_cast<uint64_t>(c) >= n_global) throw Error(CBGX_EINVAL, "csr: column index out of range");
+        if (static_cast<uint64_t>(c) < rb || static_cast<uint64_t>(c) >= re) H.ghosts.push_back(c);
+    }
+    std::sort(H.ghosts.begin(), H.ghosts.end());
+    H.ghosts.erase(std::unique(H.ghosts.begin(), H.ghosts.end()), H.ghosts.end());
+    H.need.assign(P, 0);
+    for (int64_t g : H.ghosts) ++H.need[owner(g)];
+    // own -> c - rb; ghost -> n_local + position (ghosts sorted by global
+    // index == grouped by owner rank); each row keeps its nonzero order, so
+    // the local SpMV accumulates in the reference's order.
+    H.local_cols.resize(nnz);
+    const uint64_t n_local = re - rb;
+    for (uint64_t k = 0; k < nnz; ++k) {
+        const int64_t c = cols[k];
+        if (static_cast<uint64_t>(c) >= rb && static_cast<uint64_t>(c) < re) {
+            H.local_cols[k] = static_cast<int32_t>(c - static_cast<int64_t>(rb));
+        } else {
+            const auto it = std::lower_bound(H.ghosts.begin(), H.ghosts.end(), c);
+            H.local_cols[k] = static_cast<int32_t>(n_local + static_cast<uint64_t>(it - H.ghosts.begin()));
+        }
+    }
+    return H;
+}
+
+std::vector<int32_t> send_index(uint64_t rb, uint64_t re, const int64_t* requested, uint64_t count) {
+    std::vector<int32_t> idx(count);
+    for (uint64_t k = 0; k < count; ++k) {
+        if (requested[k] < static_cast<int64_t>(rb) || requested[k] >= static_cast<int64_t>(re))
+            throw Error(CBGX_EINTERNAL, "halo: request for a row this rank does not own");
+        idx[k] = static_cast<int32_t>(requested[k] - static_cast<int64_t>(rb));
+    }
+    return idx;
+}
+
 // Collective: builds the halo plan and remaps columns (see cbgx.h).
 std::unique_ptr<Halo> make_halo(Comm* comm, uint64_t rb, uint64_t re, uint64_t n_global,
                                 const int64_t* d_gcols, uint64_t nnz, int32_t* d_lcols,
@@ -249,35 +310,13 @@ std::unique_ptr<Halo> make_halo(Comm* comm, uint64_t rb, uint64_t re, uint64_t n
         CBGX_CUDA(cudaStreamSynchronize(st));
         CBGX_CUDA(cudaMemcpy(ranges.data(), d, 2 * P * sizeof(uint64_t), cudaMemcpyDeviceToHost));
     }
-    for (int r = 0; r < P; ++r) {
-        if (ranges[2 * r] > ranges[2 * r + 1] || (r > 0 && ranges[2 * r] != ranges[2 * r - 1]))
-            throw Error(CBGX_EINVAL, "halo: row blocks must be contiguous and ordered by rank");
-    }
-    if (ranges[0] != 0 || ranges[2 * P - 1] != n_global) throw Error(CBGX_EINVAL, "halo: row blocks must cover the matrix");
-    auto owner = [&](int64_t c) {
-        int lo = 0, hi = P - 1;
-        while (lo < hi) {
-            const int mid = (lo + hi + 1) / 2;
-            if (static_cast<uint64_t>(c) >= ranges[2 * mid]) lo = mid; else hi = mid - 1;
-        }
-        return lo;
-    };
-    std::vector<int64_t> ghosts;
-    for (int64_t c : cols) {
-        if (c < 0 || static_cast<uint64_t>(c) >= n_global) throw Error(CBGX_EINVAL, "csr: column index out of range");
-        if (static_cast<uint64_t>(c) < rb || static_cast<uint64_t>(c) >= re) ghosts.push_back(c);
-    }
-    std::sort(ghosts.begin(), ghosts.end());
-    ghosts.erase(std::unique(ghosts.begin(), ghosts.end()), ghosts.end());
-    H->n_ghost = ghosts.size();
-    // requests per owner (ghosts sorted by index == grouped by owner rank)
-    std::vector<uint64_t> need(P, 0);
-    for (int64_t g : ghosts) ++need[owner(g)];
+    HaloPlan plan = plan_halo(P, me, ranges.data(), n_global, cols.data(), nnz);
+    H->n_ghost = plan.ghosts.size();
     std::vector<uint64_t> counts(static_cast<size_t>(P) * P);
     {
         Scratch s;
         uint64_t* d = static_cast<uint64_t*>(s.get((static_cast<size_t>(P) * P + P) * sizeof(uint64_t)));
-        CBGX_CUDA(cudaMemcpy(d + static_cast<size_t>(P) * P, need.data(), P * sizeof(uint64_t), cudaMemcpyHostToDevice));
+        CBGX_CUDA(cudaMemcpy(d + static_cast<size_t>(P) * P, plan.need.data(), P * sizeof(uint64_t), cudaMemcpyHostToDevice));
         comm->allgather(d + static_cast<size_t>(P) * P, d, P * sizeof(uint64_t), st);
         CBGX_CUDA(cudaStreamSynchronize(st));
         CBGX_CUDA(cudaMemcpy(counts.data(), d, counts.size() * sizeof(uint64_t), cudaMemcpyDeviceToHost));
@@ -286,9 +325,9 @@ std::unique_ptr<Halo> make_halo(Comm* comm, uint64_t rb, uint64_t re, uint64_t n
     uint64_t off = 0;
     H->recv_offsets.push_back(0);
     for (int o = 0; o < P; ++o) {
-        if (o == me || !need[o]) continue;
+        if (o == me || !plan.need[o]) continue;
         H->recv_peers.push_back(o);
-        off += need[o];
+        off += plan.need[o];
         H->recv_offsets.push_back(off);
     }
     H->send_offsets.push_back(0);
@@ -302,9 +341,10 @@ std::unique_ptr<Halo> make_halo(Comm* comm, uint64_t rb, uint64_t re, uint64_t n
     }
     // exchange request lists (global indices) with the owners
     Scratch req_s, req_r;
-    int64_t* d_req = static_cast<int64_t*>(req_s.get(std::max<size_t>(ghosts.size(), 1) * 8));
+    int64_t* d_req = static_cast<int64_t*>(req_s.get(std::max<size_t>(plan.ghosts.size(), 1) * 8));
     int64_t* d_got = static_cast<int64_t*>(req_r.get(std::max<uint64_t>(soff, 1) * 8));
-    if (!ghosts.empty()) CBGX_CUDA(cudaMemcpy(d_req, ghosts.data(), ghosts.size() * 8, cudaMemcpyHostToDevice));
+    if (!plan.ghosts.empty())
+        CBGX_CUDA(cudaMemcpy(d_req, plan.ghosts.data(), plan.ghosts.size() * 8, cudaMemcpyHostToDevice));
     {
         std::vector<Comm::Msg> sends, recvs;
         for (size_t i = 0; i < H->recv_peers.size(); ++i)
@@ -316,27 +356,11 @@ std::unique_ptr<Halo> make_halo(Comm* comm, uint64_t rb, uint64_t re, uint64_t n
     }
     std::vector<int64_t> got(soff);
     if (soff) CBGX_CUDA(cudaMemcpy(got.data(), d_got, soff * 8, cudaMemcpyDeviceToHost));
-    std::vector<int32_t> send_idx(soff);
-    for (uint64_t k = 0; k < soff; ++k) {
-        if (static_cast<uint64_t>(got[k]) < rb || static_cast<uint64_t>(got[k]) >= re)
-            throw Error(CBGX_EINTERNAL, "halo: request for a row this rank does not own");
-        send_idx[k] = static_cast<int32_t>(got[k] - static_cast<int64_t>(rb));
-    }
+    const std::vector<int32_t> sidx = send_index(rb, re, got.data(), soff);
     CBGX_CUDA(cudaMalloc(&H->d_send_idx, std::max<uint64_t>(soff, 1) * 4));
     CBGX_CUDA(cudaMalloc(&H->d_send_buf, std::max<uint64_t>(soff, 1) * 8));
-    if (soff) CBGX_CUDA(cudaMemcpy(H->d_send_idx, send_idx.data(), soff * 4, cudaMemcpyHostToDevice));
-    // remap columns: own -> c - rb, ghost -> n_local + rank in sorted ghosts
-    std::vector<int32_t> lc(nnz);
-    for (uint64_t k = 0; k < nnz; ++k) {
-        const int64_t c = cols[k];
-        if (static_cast<uint64_t>(c) >= rb && static_cast<uint64_t>(c) < re) {
-            lc[k] = static_cast<int32_t>(c - static_cast<int64_t>(rb));
-        } else {
-            const auto it = std::lower_bound(ghosts.begin(), ghosts.end(), c);
-            lc[k] = static_cast<int32_t>(H->n_local + static_cast<uint64_t>(it - ghosts.begin()));
-        }
-    }
-    if (nnz) CBGX_CUDA(cudaMemcpy(d_lcols, lc.data(), nnz * 4, cudaMemcpyHostToDevice));
+    if (soff) CBGX_CUDA(cudaMemcpy(H->d_send_idx, sidx.data(), soff * 4, cudaMemcpyHostToDevice));
+    if (nnz) CBGX_CUDA(cudaMemcpy(d_lcols, plan.local_cols.data(), nnz * 4, cudaMemcpyHostToDevice));
     return H;
 }
 
@@ -391,6 +415,38 @@ int cbgx_halo_create(cbgx_comm* c, uint64_t row_begin, uint64_t row_end, uint64_
         if (!c || !out) throw Error(CBGX_EINVAL, "halo: null argument");
         *out = new cbgx_halo{make_halo(c->impl.get(), row_begin, row_end, n_global, d_global_cols, nnz,
                                        d_local_cols_out, nullptr)};
+    });
+}
+
+int cbgx_halo_plan(int nranks, int rank, const uint64_t* row_ranges, uint64_t n_global, const int64_t* gcols,
+                   uint64_t nnz, int32_t* local_cols_out, int64_t* ghosts_out, uint64_t* n_ghosts,
+                   uint64_t* need_per_rank) {
+    return guard([&] {
+        if (nranks < 1 || rank < 0 || rank >= nranks) throw Error(CBGX_EINVAL, "halo: bad rank");
+        const HaloPlan p = plan_halo(nranks, rank, row_ranges, n_global, gcols, nnz);
+        if (local_cols_out) std::copy(p.local_cols.begin(), p.local_cols.end(), local_cols_out);
+        if (ghosts_out) std::copy(p.ghosts.begin(), p.ghosts.end(), ghosts_out);
+        if (n_ghosts) *n_ghosts = p.ghosts.size();
+        if (need_per_rank) std::copy(p.need.begin(), p.need.end(), need_per_rank);
+    });
+}
+
+int cbgx_halo_send_index(uint64_t row_begin, uint64_t row_end, const int64_t* requested, uint64_t count,
+                         int32_t* send_idx_out) {
+    return guard([&] {
+        const auto idx = send_index(row_begin, row_end, requested, count);
+        std::copy(idx.begin(), idx.end(), send_idx_out);
+    });
+}
+
+int cbgx_sum_ranks_host(int nranks, uint64_t count, const double* gathered, double* out) {
+    return guard([&] {
+        // the rank-order combine of sum_ranks_kernel, on the host
+        for (uint64_t k = 0; k < count; ++k) {
+            double s = gathered[k];
+            for (int r = 1; r < nranks; ++r) s += gathered[static_cast<uint64_t>(r) * count + k];
+            out[k] = s;
+        }
     });
 }
 

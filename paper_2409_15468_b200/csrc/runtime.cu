@@ -87,6 +87,35 @@ int cbgx_set_device(int device) {
     return guard([&] { CBGX_CUDA(cudaSetDevice(device)); });
 }
 
+int cbgx_malloc(void** d_ptr, uint64_t bytes) {
+    return guard([&] {
+        if (!d_ptr) throw Error(CBGX_EINVAL, "malloc: null output");
+        *d_ptr = nullptr;
+        CBGX_CUDA(cudaMalloc(d_ptr, bytes ? bytes : 8));
+    });
+}
+
+int cbgx_free(void* d_ptr) {
+    return guard([&] {
+        if (d_ptr) CBGX_CUDA(cudaFree(d_ptr));
+    });
+}
+
+int cbgx_memcpy(void* dst, const void* src, uint64_t bytes, int kind) {
+    return guard([&] {
+        if (!bytes) return;
+        const cudaMemcpyKind k = kind == 0 ? cudaMemcpyHostToDevice
+                                 : kind == 1 ? cudaMemcpyDeviceToHost : cudaMemcpyDeviceToDevice;
+        CBGX_CUDA(cudaMemcpy(dst, src, bytes, k));
+    });
+}
+
+int cbgx_memset(void* d_ptr, int value, uint64_t bytes) {
+    return guard([&] {
+        if (bytes) CBGX_CUDA(cudaMemset(d_ptr, value, bytes));
+    });
+}
+
 int cbgx_device_info(int* device, int* sms, int64_t* l2) {
     return guard([&] {
         int d = current_device();

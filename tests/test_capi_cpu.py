@@ -31,6 +31,11 @@ def test_exports_every_declared_symbol(L):
     assert not missing, missing
 
 
+def test_every_symbol_has_a_ctypes_signature(L):
+    missing = [s for s in declared_symbols() if s not in L.cbgx_signatures]
+    assert not missing, missing
+
+
 def test_pure_host_functions(L):
     assert L.cbgx_frsz2_storage_bytes(64, 32, 32) == 264        # acceptance.cpp:141-149
     assert L.cbgx_frsz2_storage_bytes(32, 32, 21) == 88         # test_frsz2.cpp:301
