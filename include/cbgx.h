@@ -233,7 +233,8 @@ typedef struct {
 
 enum {
     CBGX_SOLVER_PHASE_TIMING = 1,          /* CUDA events around every phase, summed per solve */
-    CBGX_SOLVER_PHASE_TIMING_DEFERRED = 2  /* record events, collect later (no per-solve sync) */
+    CBGX_SOLVER_PHASE_TIMING_DEFERRED = 2, /* record events, collect later (no per-solve sync) */
+    CBGX_SOLVER_NO_FUSION = 4              /* always use the split dot/update/write kernels */
 };
 
 typedef struct {
@@ -244,8 +245,10 @@ typedef struct {
     uint64_t length;       /* out: records produced (may exceed capacity) */
 } cbgx_history;
 
+/* ORTHO: the fused single-GPU orthogonalisation kernel (dot + update + gated
+ * second pass + next-column write in one cooperative launch). */
 enum { CBGX_PHASE_SPMV = 0, CBGX_PHASE_DOT, CBGX_PHASE_UPDATE, CBGX_PHASE_WRITE,
-       CBGX_PHASE_RESIDUAL, CBGX_PHASE_SOLUTION, CBGX_PHASE_COMM, CBGX_PHASE_HOST,
+       CBGX_PHASE_RESIDUAL, CBGX_PHASE_SOLUTION, CBGX_PHASE_COMM, CBGX_PHASE_ORTHO,
        CBGX_NUM_PHASES };
 
 typedef struct {
@@ -259,6 +262,8 @@ typedef struct {
     double phase_bytes[CBGX_NUM_PHASES];   /* algorithmic HBM bytes per phase */
     uint64_t phase_launches[CBGX_NUM_PHASES];
     uint64_t kernel_launches;          /* kernels this solve launched */
+    double host_enqueue_ms;            /* host time spent issuing Arnoldi steps */
+    double host_wait_ms;               /* host time blocked on step results */
 } cbgx_solve_stats;
 
 typedef struct cbgx_comm cbgx_comm;
@@ -284,6 +289,10 @@ int cbgx_gmres_solve_host(uint64_t n, const uint64_t* row_ptrs, const uint64_t* 
                           const double* values, const double* b, const double* x0,
                           const cbgx_gmres_config* cfg, double* x_out, cbgx_history* hist,
                           cbgx_solve_stats* stats);
+
+/* Debug: globaltimer stamps of CTA 0 in the last fused orthogonalisation
+ * launch (requires CBGX_TRACE_FUSED=1 in the environment). */
+int cbgx_debug_fused_trace(uint64_t* out, int count);
 
 /* ---------------------------------------------- multi-GPU row partition
  * One process per GPU; each rank owns rows [row_begin, row_end) (multiples

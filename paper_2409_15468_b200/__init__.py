@@ -523,10 +523,12 @@ class GmresConfig:
     reduction: int = _lib.REDUCE_TREE
     phase_timing: bool = False
     phase_timing_deferred: bool = False
+    fusion: bool = True   # fused single-GPU orthogonalisation kernel when eligible
 
     def c(self):
         flags = (_lib.PHASE_TIMING if self.phase_timing else 0) | \
-            (_lib.PHASE_TIMING_DEFERRED if self.phase_timing_deferred else 0)
+            (_lib.PHASE_TIMING_DEFERRED if self.phase_timing_deferred else 0) | \
+            (0 if self.fusion else _lib.NO_FUSION)
         return _lib.GmresConfig(self.restart, self.target_rrn, self.max_total_iterations, self.eta,
                                 self.storage_format.kind, self.storage_format.bit_length,
                                 self.reduction, flags)

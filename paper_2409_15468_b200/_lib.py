@@ -13,7 +13,8 @@ F64, F32, F16, FRSZ2 = 0, 1, 2, 3
 REDUCE_TREE, REDUCE_REFERENCE = 0, 1
 PHASE_TIMING = 1
 PHASE_TIMING_DEFERRED = 2
-PHASES = ["spmv", "dot", "update", "write", "residual", "solution", "comm", "host"]
+NO_FUSION = 4
+PHASES = ["spmv", "dot", "update", "write", "residual", "solution", "comm", "ortho"]
 
 u32, u64, i32, i64, dbl, vp = C.c_uint32, C.c_uint64, C.c_int32, C.c_int64, C.c_double, C.c_void_p
 
@@ -44,7 +45,7 @@ class SolveStats(C.Structure):
     _fields_ = [("converged", C.c_int), ("total_iterations", u64), ("restarts", u64),
                 ("final_rrn", dbl), ("wall_seconds", dbl), ("reorth_passes", u64),
                 ("phase_ms", dbl * 8), ("phase_bytes", dbl * 8), ("phase_launches", u64 * 8),
-                ("kernel_launches", u64)]
+                ("kernel_launches", u64), ("host_enqueue_ms", dbl), ("host_wait_ms", dbl)]
 
 
 _lib = None
@@ -65,6 +66,7 @@ def lib():
             "cbgx_set_device": ([C.c_int], C.c_int),
             "cbgx_sin_solution": ([u64, u64, u64, vp, C.c_int], C.c_int),
             "cbgx_halo_exchange": ([vp, vp, vp], C.c_int),
+            "cbgx_debug_fused_trace": ([vp, C.c_int], C.c_int),
             "cbgx_device_info": ([P(C.c_int), P(C.c_int), P(i64)], C.c_int),
             "cbgx_frsz2_num_blocks": ([u64, u32], u64),
             "cbgx_frsz2_words_per_block": ([u32, u32], u64),

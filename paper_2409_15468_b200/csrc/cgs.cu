@@ -18,6 +18,7 @@
 // shared memory in tile order, CTAs write partial rows in CTA order, and the
 // last CTA to finish (device ticket) sums the rows in CTA order.
 #include <algorithm>
+#include <cstdlib>
 #include <mutex>
 #include <map>
 #include <set>
@@ -413,24 +414,25 @@ void dispatch_fmt(int f, A&&... a) {
 // there are 1024-row steps.
 // Persistent grid: all CTAs that can be co-resident (registers and shared
 // memory via the occupancy calculator), never more than 1024-row steps.
+// Occupancy query cached per (device, kernel, smem): it costs host time on
+// every launch otherwise.
 template <class K>
-int ring_grid(K kernel, uint64_t n, size_t smem) {
-    // occupancy query cached per (device, kernel, smem): it costs host time
-    // on every launch otherwise
+int occupancy(K kernel, size_t smem) {
     static std::mutex mu;
     static std::map<std::tuple<int, const void*, size_t>, int> cache;
     const auto key = std::make_tuple(current_device(), reinterpret_cast<const void*>(kernel), smem);
+    std::lock_guard<std::mutex> lock(mu);
+    auto it = cache.find(key);
+    if (it != cache.end()) return it->second;
     int per_sm = 0;
-    {
-        std::lock_guard<std::mutex> lock(mu);
-        auto it = cache.find(key);
-        if (it == cache.end()) {
-            CBGX_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kernel, kThreads, smem));
-            cache.emplace(key, per_sm);
-        } else {
-            per_sm = it->second;
-        }
-    }
+    CBGX_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kernel, kThreads, smem));
+    cache.emplace(key, per_sm);
+    return per_sm;
+}
+
+template <class K>
+int ring_grid(K kernel, uint64_t n, size_t smem) {
+    const int per_sm = occupancy(kernel, smem);
     const uint64_t steps = (n + kStepRows - 1) / kStepRows;
     const uint64_t cap = static_cast<uint64_t>(sm_count()) * std::max(per_sm, 1);
     return static_cast<int>(std::max<uint64_t>(1, std::min<uint64_t>(steps, cap)));
@@ -513,6 +515,451 @@ template <int F> struct ReadLaunch {
     }
 };
 
+// ============================================================================
+// Fused single-GPU Arnoldi orthogonalisation (persistent, co-resident grid).
+//
+// One launch replaces dot -> update -> [gated dot -> update] -> scaled write
+// of the next basis column (gmres.cpp:211-234 minus the host Givens). Every
+// CTA owns a fixed row range for the whole launch, so w stays in registers
+// across all passes; passes are separated by a grid barrier among the
+// consumer warps while the producer warp keeps streaming the next pass's
+// columns through the shared-memory ring (the basis does not depend on the
+// barrier). Dot passes run last-to-first and update passes first-to-last, so
+// each pass starts on the columns the previous one left in L2.
+// Eligible when every CTA's rows fit in kFusedMaxSteps 1024-row steps
+// (n <= 8192 * co-resident CTAs, ~2.4M rows on a B200).
+constexpr int kFusedMaxSteps = 8;
+
+// Ring stage = one column's segment of `chunk` steps (the whole CTA range
+// when it fits, so a column-pass is one ring round).
+template <int F> struct FGeo;
+template <> struct FGeo<kZ32> { static constexpr int chunk = 8, stages = 3; };
+template <> struct FGeo<kZ16> { static constexpr int chunk = 8, stages = 4; };
+template <> struct FGeo<kZ21> { static constexpr int chunk = 8, stages = 3; };
+template <> struct FGeo<kF64> { static constexpr int chunk = 4, stages = 3; };
+template <> struct FGeo<kF32> { static constexpr int chunk = 8, stages = 3; };
+template <> struct FGeo<kF16> { static constexpr int chunk = 8, stages = 4; };
+
+template <int F>
+__host__ __device__ constexpr uint32_t fstage_bytes() {
+    return FGeo<F>::chunk * (Geo<F>::pay + Geo<F>::ex) + 16;
+}
+
+struct FusedArgs {
+    BasisView B;
+    uint32_t cols;             // columns 0..cols-1 orthogonalise w; column `cols` is written
+    unsigned char* out_pay;    // column `cols` payload / values
+    uint32_t* out_exp;         // column `cols` exponents (FRSZ2)
+    const double* w;           // SpMV output (rows [0, n))
+    double* v_out;             // next SpMV input
+    double* slot;              // [hn1, hn2, omega2, h[0..m], u[0..m]]; omega2 set by the SpMV
+    uint32_t u_off;            // index of u in slot
+    double eta;
+    double* partials;          // gridDim.x * (cols + 1)
+    unsigned* bar;             // [count, generation], zero-initialised
+    unsigned long long* trace; // optional: CTA 0 phase timestamps (debug)
+};
+
+__device__ __forceinline__ unsigned long long global_ns() {
+    unsigned long long t;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+    return t;
+}
+#define FTRACE(i) do { if (a.trace && blockIdx.x == 0 && threadIdx.x == 0) a.trace[i] = global_ns(); } while (0)
+
+__device__ __forceinline__ void consumer_sync() {
+    asm volatile("bar.sync 1, %0;" ::"n"(kConsumers) : "memory");
+}
+
+// Grid barrier among the consumer warps of all (co-resident) CTAs.
+__device__ __forceinline__ void grid_sync(unsigned* bar) {
+    consumer_sync();
+    if (threadIdx.x == 0) {
+        volatile unsigned* gen = bar + 1;
+        const unsigned g = *gen;
+        __threadfence();
+        if (atomicAdd(bar, 1u) == gridDim.x - 1) {
+            bar[0] = 0;
+            __threadfence();
+            atomicAdd(bar + 1, 1u);
+        } else {
+            while (*gen == g) __nanosleep(32);
+        }
+        __threadfence();
+    }
+    consumer_sync();
+}
+
+// Grid barrier fused with the cross-CTA reduction: the LAST CTA to arrive
+// sums the CTA partial rows of `count` values (fixed order: lane-strided
+// over CTAs, then a warp butterfly -- deterministic whichever CTA it is),
+// publishes them to `result` (global) and releases the others, who read
+// back only `count` values. One CTA reads the partials instead of every CTA
+// hammering the same lines in L2.
+__device__ __forceinline__ void grid_reduce(unsigned* bar, const double* partials, uint32_t stride, uint32_t count,
+                                            double* result, double* out_smem, double* part, int* s_flag) {
+    consumer_sync();
+    if (threadIdx.x == 0) {
+        volatile unsigned* gen = bar + 1;
+        const unsigned g = *gen;
+        __threadfence();
+        const bool last = atomicAdd(bar, 1u) == gridDim.x - 1;
+        s_flag[0] = last ? 1 : 0;
+        s_flag[1] = static_cast<int>(g);
+    }
+    consumer_sync();
+    if (s_flag[0]) {
+        __threadfence();
+        // R threads per value: thread t sums CTA rows g, g+R, g+2R, ... of
+        // value k = t % count (g = t / count), loads issued back to back;
+        // then the R partials of each value are added in g order.
+        const uint32_t R = count >= kConsumers ? 1u : kConsumers / count;
+        const uint32_t t = threadIdx.x;
+        for (uint32_t k0 = 0; k0 < count; k0 += kConsumers) {
+            const uint32_t k = k0 + t % (count < kConsumers ? count : kConsumers);
+            const uint32_t g = count < kConsumers ? t / count : 0;
+            double v = 0.0;
+            if (g < R && k < count) {
+                constexpr int kMax = 32;
+                double x[kMax];
+#pragma unroll
+                for (int i = 0; i < kMax; ++i) {
+                    const unsigned c = g + R * i;
+                    x[i] = c < gridDim.x ? __ldcg(partials + static_cast<uint64_t>(c) * stride + k) : 0.0;
+                }
+#pragma unroll
+                for (int i = 0; i < kMax; ++i)
+                    if (g + R * i < gridDim.x) v = __dadd_rn(v, x[i]);
+                for (unsigned c = g + R * kMax; c < gridDim.x; c += R)
+                    v = __dadd_rn(v, __ldcg(partials + static_cast<uint64_t>(c) * stride + k));
+                part[g * count + k] = v;
+            }
+            consumer_sync();
+            if (t < count && k0 + t < count) {
+                const uint32_t kk = k0 + t;
+                double s = part[kk];
+                for (uint32_t gg = 1; gg < R; ++gg) s = __dadd_rn(s, part[gg * count + kk]);
+                out_smem[kk] = s;
+                result[kk] = s;
+            }
+            consumer_sync();
+        }
+        consumer_sync();
+        if (threadIdx.x == 0) {
+            __threadfence();
+            bar[0] = 0;
+            __threadfence();
+            atomicAdd(bar + 1, 1u);
+        }
+    } else {
+        if (threadIdx.x == 0) {
+            volatile unsigned* gen = bar + 1;
+            while (*gen == static_cast<unsigned>(s_flag[1])) __nanosleep(20);
+            __threadfence();
+        }
+        consumer_sync();
+        for (uint32_t k = threadIdx.x; k < count; k += kConsumers) out_smem[k] = __ldcg(result + k);
+    }
+    consumer_sync();
+}
+
+// Every CTA sums the CTA partial rows of `count` values in the same fixed
+// order (lane-strided over CTAs, then a warp butterfly), result in smem.
+__device__ __forceinline__ void reduce_all(const double* partials, uint32_t stride, uint32_t count, double* out) {
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    for (uint32_t k = warp; k < count; k += kConsumerWarps) {
+        const double s = warp_sum(lane_sum_rows(partials, stride, k, gridDim.x, lane));
+        if (lane == 0) out[k] = s;
+    }
+    consumer_sync();
+}
+
+template <int F>
+__device__ __forceinline__ void fused_write(const FusedArgs& a, uint64_t s0, uint32_t steps, double wv[][4],
+                                            double scale, uint32_t* scratch) {
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+#pragma unroll
+    for (int s = 0; s < kFusedMaxSteps; ++s) {
+        if (s >= static_cast<int>(steps)) break;
+        const uint64_t r = (s0 + s) * kStepRows + 4u * threadIdx.x;
+        double v[4];
+#pragma unroll
+        for (int k = 0; k < 4; ++k) v[k] = r + k < a.B.n ? __dmul_rn(wv[s][k], scale) : 0.0;
+        if (r + 3 < a.B.n) {
+            reinterpret_cast<double2*>(a.v_out + r)[0] = make_double2(v[0], v[1]);
+            reinterpret_cast<double2*>(a.v_out + r)[1] = make_double2(v[2], v[3]);
+        } else {
+#pragma unroll
+            for (int k = 0; k < 4; ++k)
+                if (r + k < a.B.n) a.v_out[r + k] = v[k];
+        }
+        if constexpr (FmtInfo<F>::frsz) {
+            constexpr int L = FmtInfo<F>::L;
+            uint32_t e = 0;
+#pragma unroll
+            for (int k = 0; k < 4; ++k) e = max(e, exp_field(v[k]));
+            e = max(e, __shfl_xor_sync(0xFFFFFFFFu, e, 1));
+            e = max(e, __shfl_xor_sync(0xFFFFFFFFu, e, 2));
+            e = max(e, __shfl_xor_sync(0xFFFFFFFFu, e, 4));
+            uint32_t c[4];
+#pragma unroll
+            for (int k = 0; k < 4; ++k) c[k] = encode32<L>(v[k], e);
+            if ((lane & 7) == 0) a.out_exp[r / 32] = e;
+            if constexpr (L == 32) {
+                reinterpret_cast<uint4*>(a.out_pay)[r / 4] = make_uint4(c[0], c[1], c[2], c[3]);
+            } else if constexpr (L == 16) {
+                reinterpret_cast<uint2*>(a.out_pay)[r / 4] = make_uint2(c[0] | (c[1] << 16), c[2] | (c[3] << 16));
+            } else {
+                // 4 blocks (84 words) per warp per step, assembled in smem
+                uint32_t* wbuf = scratch + warp * 84;
+                for (int i = lane; i < 84; i += 32) wbuf[i] = 0u;
+                __syncwarp();
+                const uint32_t bit0 = (lane >> 3) * 672u + (lane & 7) * 84u;
+#pragma unroll
+                for (int k = 0; k < 4; ++k) {
+                    const uint32_t b = bit0 + 21u * k, q = b >> 5, sh = b & 31u;
+                    atomicOr(wbuf + q, c[k] << sh);
+                    if (sh > 11) atomicOr(wbuf + q + 1, c[k] >> (32 - sh));
+                }
+                __syncwarp();
+                uint32_t* dst = reinterpret_cast<uint32_t*>(a.out_pay) + ((s0 + s) * kStepRows + warp * 128u) / 32 * 21;
+                for (int i = lane; i < 84; i += 32) dst[i] = wbuf[i];
+                __syncwarp();
+            }
+        } else if constexpr (F == kF64) {
+            reinterpret_cast<double2*>(a.out_pay)[r / 2] = make_double2(v[0], v[1]);
+            reinterpret_cast<double2*>(a.out_pay)[r / 2 + 1] = make_double2(v[2], v[3]);
+        } else if constexpr (F == kF32) {
+            reinterpret_cast<float4*>(a.out_pay)[r / 4] =
+                make_float4(__double2float_rn(v[0]), __double2float_rn(v[1]), __double2float_rn(v[2]), __double2float_rn(v[3]));
+        } else {
+            reinterpret_cast<uint2*>(a.out_pay)[r / 4] =
+                make_uint2(double_to_half_bits(v[0]) | (static_cast<uint32_t>(double_to_half_bits(v[1])) << 16),
+                           double_to_half_bits(v[2]) | (static_cast<uint32_t>(double_to_half_bits(v[3])) << 16));
+        }
+    }
+}
+
+template <int F>
+__global__ void __launch_bounds__(kThreads, 2) arnoldi_fused_kernel(FusedArgs a) {
+    constexpr int S = FGeo<F>::stages;
+    constexpr uint32_t PAY = Geo<F>::pay, EX = Geo<F>::ex, SB = fstage_bytes<F>();
+    extern __shared__ __align__(128) unsigned char smem[];
+    const uint32_t cols = a.cols;
+    unsigned char* stages = smem;
+    uint64_t* full = reinterpret_cast<uint64_t*>(smem + S * SB);
+    uint64_t* empty = full + S;
+    double* red = reinterpret_cast<double*>(empty + S);        // [kWarps][cols]
+    double* hsm = red + kWarps * (cols + 1);                    // reduced h / u (cols)
+    double* scal = hsm + cols + 1;                              // [hn1, hn2, gate]
+    double* part = scal + 4;                                    // grid_reduce scratch (kConsumers)
+    uint32_t* scratch = reinterpret_cast<uint32_t*>(part + kConsumers);  // l=21 write: 8 warps x 84 words
+    volatile int* s_gate = reinterpret_cast<volatile int*>(scratch + kConsumerWarps * 84);
+    int* s_flag = const_cast<int*>(s_gate) + 2;
+    if (threadIdx.x == 0) {
+        for (int s = 0; s < S; ++s) {
+            mbar_init(full + s, 1);
+            mbar_init(empty + s, kConsumerWarps);
+        }
+        fence_barrier_init();
+        *s_gate = -1;
+    }
+    __syncthreads();
+    uint64_t s0, s1;
+    cta_steps(a.B.n, s0, s1);
+    const uint32_t steps = static_cast<uint32_t>(s1 - s0);
+    constexpr int kChunkSteps = FGeo<F>::chunk, kChunks = kFusedMaxSteps / kChunkSteps;
+    const uint32_t nch = (steps + kChunkSteps - 1) / kChunkSteps;
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+
+    if (warp == kConsumerWarps) {
+        // ---------------- producer: dot1 (rev), update1, [dot2 (rev), update2]
+        if (lane != 0) return;
+        const uint64_t policy = policy_evict_normal();
+        uint32_t it = 0;
+        for (int pass = 0; pass < 4; ++pass) {
+            if (pass == 2) {
+                while (*s_gate < 0) __nanosleep(64);
+                if (*s_gate == 0) break;
+            }
+            const bool rev = (pass & 1) == 0;
+            for (uint32_t jj = 0; jj < cols; ++jj) {
+                const uint32_t j = rev ? cols - 1 - jj : jj;
+                for (uint32_t ch = 0; ch < nch; ++ch, ++it) {
+                    const uint64_t sb = s0 + ch * kChunkSteps;
+                    const uint32_t cs = static_cast<uint32_t>(min(static_cast<uint64_t>(kChunkSteps), s1 - sb));
+                    const int stage = it % S;
+                    mbar_wait(empty + stage, ((it / S) & 1) ^ 1);
+                    mbar_arrive_expect_tx(full + stage, cs * (PAY + EX));
+                    unsigned char* dst = stages + stage * SB;
+                    bulk_g2s(dst, a.B.data + j * a.B.col_stride_bytes + sb * PAY, cs * PAY, full + stage, policy);
+                    if constexpr (EX > 0)
+                        bulk_g2s(dst + kChunkSteps * PAY,
+                                 reinterpret_cast<const unsigned char*>(a.B.exp + j * a.B.exp_col_stride) + sb * EX,
+                                 cs * EX, full + stage, policy);
+                }
+            }
+        }
+        return;
+    }
+
+    // ---------------- consumers
+    FTRACE(0);
+    if (a.trace && threadIdx.x == 0) a.trace[16 + 2048 + blockIdx.x] = global_ns();
+    double wv[kFusedMaxSteps][4];
+#pragma unroll
+    for (int s = 0; s < kFusedMaxSteps; ++s) {
+        if (s < static_cast<int>(steps)) load_w(a.w, a.B.n, (s0 + s) * kStepRows + 4u * threadIdx.x, wv[s]);
+        else wv[s][0] = wv[s][1] = wv[s][2] = wv[s][3] = 0.0;
+    }
+    FTRACE(1);
+    uint32_t it = 0;
+    const uint32_t stride = cols + 1;
+    double hn[2] = {0.0, 0.0};
+    bool gate = false;
+    for (int pass = 0; pass < 4; ++pass) {
+        if (pass == 2 && !gate) break;
+        const bool dotpass = (pass & 1) == 0;
+        if (dotpass) {
+            for (uint32_t k = threadIdx.x; k < kWarps * cols; k += kConsumers) red[k] = 0.0;
+            consumer_sync();
+        }
+        double nacc = 0.0;
+        for (uint32_t jj = 0; jj < cols; ++jj) {
+            const uint32_t j = dotpass ? cols - 1 - jj : jj;
+            const double hj = dotpass ? 0.0 : hsm[j];
+            const int he = static_cast<int>(exp_field(hj));
+            double acc = 0.0, acc2 = 0.0;
+#pragma unroll
+            for (int ch = 0; ch < kChunks; ++ch) {
+                if (ch >= static_cast<int>(nch)) break;
+                const int stage = it % S;
+                mbar_wait(full + stage, (it / S) & 1);
+                const unsigned char* pay = stages + stage * SB;
+                const uint32_t* ex = reinterpret_cast<const uint32_t*>(pay + kChunkSteps * PAY);
+#pragma unroll
+                for (int s = 0; s < kChunkSteps; ++s) {
+                    const int gs = ch * kChunkSteps + s;
+                    if (gs < static_cast<int>(steps)) {
+                        Step<F> st;
+                        step_lds<F>(st, pay, ex, s * kStepRows + 4u * threadIdx.x);
+                        if (dotpass) {
+                            if (s & 1) acc2 = __dadd_rn(acc2, st.dot(wv[gs]));
+                            else acc = __dadd_rn(acc, st.dot(wv[gs]));
+                        } else {
+                            st.update(hj, he, wv[gs]);
+                        }
+                    }
+                }
+                __syncwarp();
+                if (lane == 0) mbar_arrive(empty + stage);
+                ++it;
+            }
+            if (dotpass) {
+                acc = warp_sum(__dadd_rn(acc, acc2));
+                if (lane == 0) red[warp * cols + j] = acc;
+            }
+        }
+        FTRACE(2 + 3 * pass);
+        if (a.trace && threadIdx.x == 0 && pass < 2) a.trace[16 + pass * 1024 + blockIdx.x] = global_ns();
+        if (dotpass) {
+            consumer_sync();
+            for (uint32_t j = threadIdx.x; j < cols; j += kConsumers) {
+                double s = red[j];
+                for (int w = 1; w < kWarps; ++w) s = __dadd_rn(s, red[w * cols + j]);
+                a.partials[static_cast<uint64_t>(blockIdx.x) * stride + j] = s;
+            }
+            FTRACE(3 + 3 * pass);
+            grid_reduce(a.bar, a.partials, stride, cols, a.slot + (pass == 0 ? 3u : a.u_off), hsm, part, s_flag);
+            FTRACE(4 + 3 * pass);
+        } else {
+#pragma unroll
+            for (int s = 0; s < kFusedMaxSteps; ++s)
+#pragma unroll
+                for (int k = 0; k < 4; ++k) nacc = fma(wv[s][k], wv[s][k], nacc);
+            nacc = warp_sum(nacc);
+            if (lane == 0) red[warp] = nacc;
+            consumer_sync();
+            if (threadIdx.x == 0) {
+                double s = red[0];
+                for (int w = 1; w < kWarps; ++w) s = __dadd_rn(s, red[w]);
+                a.partials[static_cast<uint64_t>(blockIdx.x) * stride + cols] = s;
+            }
+            FTRACE(3 + 3 * pass);
+            const int which = pass == 1 ? 0 : 1;
+            grid_reduce(a.bar, a.partials + cols, stride, 1, a.slot + which, scal + which, part, s_flag);
+            FTRACE(4 + 3 * pass);
+            hn[which] = scal[which];
+            if (pass == 1) {
+                // gmres.cpp:51 on the device (same IEEE ops as the host)
+                gate = sqrt(hn[0]) < a.eta * sqrt(a.slot[2]);
+                if (threadIdx.x == 0) {
+                    *s_gate = gate ? 1 : 0;
+                    __threadfence_block();
+                }
+            }
+        }
+    }
+    // v = w / h_next of the last pass, written as the next basis column
+    const double scale = 1.0 / sqrt(gate ? hn[1] : hn[0]);
+    fused_write<F>(a, s0, steps, wv, scale, scratch);
+    FTRACE(14);
+}
+
+// Debug timeline of the fused kernel (CTA 0): enabled by CBGX_TRACE_FUSED=1,
+// read back with cbgx_debug_fused_trace.
+unsigned long long* g_trace = nullptr;
+unsigned long long* fused_trace_buffer() {
+    static const bool on = [] {
+        const char* e = getenv("CBGX_TRACE_FUSED");
+        return e && e[0] == '1';
+    }();
+    if (!on) return nullptr;
+    if (!g_trace) {
+        CBGX_CUDA(cudaMalloc(&g_trace, (16 + 3 * 1024) * sizeof(unsigned long long)));
+        CBGX_CUDA(cudaMemset(g_trace, 0, (16 + 3 * 1024) * sizeof(unsigned long long)));
+    }
+    return g_trace;
+}
+
+template <int F>
+size_t fused_smem(uint32_t cols) {
+    return FGeo<F>::stages * (fstage_bytes<F>() + 16) +
+           (kWarps * (cols + 1) + (cols + 1) + 4 + kConsumers + 2 * 128) * sizeof(double) + kConsumerWarps * 84 * 4 + 32;
+}
+
+template <int F> struct FusedLaunch {
+    static void run(const cbgx_basis& V, uint32_t cols, const double* w, double* v_out, double* slot,
+                    uint32_t u_off, double eta, Workspace* ws, cudaStream_t st, bool* done) {
+        const size_t smem = fused_smem<F>(cols);
+        allow_smem(arnoldi_fused_kernel<F>);
+        const int per_sm = occupancy(arnoldi_fused_kernel<F>, smem);
+        const uint64_t G = static_cast<uint64_t>(sm_count()) * static_cast<uint64_t>(per_sm);
+        const uint64_t steps = (V.n + kStepRows - 1) / kStepRows;
+        *done = false;
+        if (per_sm < 1 || steps > G * kFusedMaxSteps) return;  // not eligible: caller uses the split kernels
+        const int grid = static_cast<int>(std::min<uint64_t>(G, steps));
+        FusedArgs a;
+        a.B = view_of(V);
+        a.cols = cols;
+        a.out_pay = static_cast<unsigned char*>(V.d_data) + static_cast<uint64_t>(cols) * V.col_stride_bytes;
+        a.out_exp = V.d_exp ? V.d_exp + static_cast<uint64_t>(cols) * V.exp_col_stride : nullptr;
+        a.w = w;
+        a.v_out = v_out;
+        a.slot = slot;
+        a.u_off = u_off;
+        a.eta = eta;
+        a.partials = ws->get_partials(static_cast<size_t>(grid) * (cols + 1));
+        a.bar = ws->get_counter() + 8;
+        a.trace = fused_trace_buffer();
+        void* args[] = {&a};
+        note_launch();
+        CBGX_CUDA(cudaLaunchCooperativeKernel(reinterpret_cast<void*>(arnoldi_fused_kernel<F>), dim3(grid),
+                                              dim3(kThreads), args, smem, st));
+        *done = true;
+    }
+};
+
 void check_basis(const cbgx_basis* V) {
     if (!V) throw Error(CBGX_EINVAL, "basis: null descriptor");
     if (V->n_pad < V->n || V->n_pad % kRowAlign) throw Error(CBGX_EINVAL, "basis: bad row padding");
@@ -541,6 +988,37 @@ void launch_basis_write(const cbgx_basis& V, uint64_t j, const double* x, const 
     if (j >= V.capacity) throw Error(CBGX_ERANGE, "basis: cannot write column");
     dispatch_fmt<WriteLaunch>(fmt_of(V), V, j, x, scale, v_out, bad, st);
     CBGX_CUDA(cudaGetLastError());
+}
+
+namespace {
+template <int F> struct FusedProbe {
+    static void run(const cbgx_basis& V, uint64_t max_cols, bool* ok) {
+        const size_t smem = fused_smem<F>(static_cast<uint32_t>(max_cols));
+        allow_smem(arnoldi_fused_kernel<F>);
+        int per_sm = 0;
+        CBGX_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, arnoldi_fused_kernel<F>, kThreads, smem));
+        int coop = 0;
+        CBGX_CUDA(cudaDeviceGetAttribute(&coop, cudaDevAttrCooperativeLaunch, current_device()));
+        const uint64_t G = static_cast<uint64_t>(sm_count()) * static_cast<uint64_t>(per_sm);
+        const uint64_t steps = (V.n + kStepRows - 1) / kStepRows;
+        *ok = coop && per_sm >= 1 && steps <= G * kFusedMaxSteps;
+    }
+};
+}  // namespace
+
+bool fused_eligible(const cbgx_basis& V, uint64_t max_cols) {
+    bool ok = false;
+    dispatch_fmt<FusedProbe>(fmt_of(V), V, max_cols, &ok);
+    return ok;
+}
+
+bool launch_arnoldi_fused(const cbgx_basis& V, uint32_t cols, const double* w, double* v_out, double* slot,
+                          uint32_t u_off, double eta, Workspace* ws, cudaStream_t st) {
+    if (cols + 1 > V.capacity) throw Error(CBGX_ERANGE, "basis: cannot write column");
+    bool done = false;
+    dispatch_fmt<FusedLaunch>(fmt_of(V), V, cols, w, v_out, slot, u_off, eta, ws, st, &done);
+    CBGX_CUDA(cudaGetLastError());
+    return done;
 }
 
 void launch_basis_read(const cbgx_basis& V, uint64_t j, uint64_t first, uint64_t count, double* out,
@@ -621,6 +1099,13 @@ int cbgx_cgs_update(const cbgx_basis* V, uint64_t first, uint32_t cols, const do
         if (!ws) throw Error(CBGX_EINVAL, "cgs: null workspace");
         launch_cgs_update(*V, first, cols, d_h, h_sign < 0 ? -1.0 : 1.0, d_w, d_wnorm2, reduction,
                           ws_of(ws), as_stream(stream));
+    });
+}
+
+int cbgx_debug_fused_trace(uint64_t* out, int count) {
+    return guard([&] {
+        if (!g_trace) throw Error(CBGX_EINVAL, "trace: set CBGX_TRACE_FUSED=1 before the first fused launch");
+        CBGX_CUDA(cudaMemcpy(out, g_trace, std::min(count, 16 + 3 * 1024) * sizeof(uint64_t), cudaMemcpyDeviceToHost));
     });
 }
 

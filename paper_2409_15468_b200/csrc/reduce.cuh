@@ -11,6 +11,28 @@
 
 namespace cbgx {
 
+// Lane L's share of column k over `rows` CTA partial rows: rows L, L+32, ...
+// summed in that order. All loads are issued before the first add (the
+// partials sit in L2; a dependent load-add loop would pay one L2 round trip
+// per row).
+__device__ __forceinline__ double lane_sum_rows(const double* __restrict__ partials, uint32_t stride, uint32_t k,
+                                                unsigned rows, int lane) {
+    constexpr int kMax = 24;  // up to 768 CTAs
+    double v[kMax];
+#pragma unroll
+    for (int i = 0; i < kMax; ++i) {
+        const unsigned c = lane + 32u * i;
+        v[i] = c < rows ? __ldcg(partials + static_cast<uint64_t>(c) * stride + k) : 0.0;
+    }
+    double s = 0.0;
+#pragma unroll
+    for (int i = 0; i < kMax; ++i)
+        if (lane + 32u * i < rows) s = __dadd_rn(s, v[i]);
+    for (unsigned c = lane + 32u * kMax; c < rows; c += 32)
+        s = __dadd_rn(s, __ldcg(partials + static_cast<uint64_t>(c) * stride + k));
+    return s;
+}
+
 // red: shared [nwarps][ncol] per-warp partials. Writes this CTA's row of
 // partials[gridDim.x][ncol]; the last CTA to arrive (ticket) sums the rows
 // in CTA order into out[ncol] and re-arms the ticket. The summation order
@@ -35,10 +57,7 @@ __device__ __forceinline__ void block_finalize(const double* red, int nwarps, ui
     // butterfly across the warp -- the same shape every launch.
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, nw = blockDim.x >> 5;
     for (uint32_t k = warp; k < ncol; k += nw) {
-        double s = 0.0;
-        for (unsigned c = lane; c < gridDim.x; c += 32)
-            s = __dadd_rn(s, __ldcg(partials + static_cast<uint64_t>(c) * ncol + k));
-        s = warp_sum(s);
+        const double s = warp_sum(lane_sum_rows(partials, ncol, k, gridDim.x, lane));
         if (lane == 0) out[k] = s;
     }
     if (threadIdx.x == 0) *ticket = 0u;
@@ -56,6 +75,12 @@ void launch_cgs_dot(const cbgx_basis& V, uint64_t first, uint32_t cols, const do
 void launch_cgs_update(const cbgx_basis& V, uint64_t first, uint32_t cols, const double* h,
                        double sign, double* w, double* norm, int reduction, Workspace* ws,
                        cudaStream_t st, const GateArg& gate = GateArg{});
+// Fused single-GPU orthogonalisation + next-column write (one cooperative
+// launch; see cgs.cu). Returns false (nothing launched) when the problem is
+// too large for the register-resident w of a co-resident grid.
+bool fused_eligible(const cbgx_basis& V, uint64_t max_cols);
+bool launch_arnoldi_fused(const cbgx_basis& V, uint32_t cols, const double* w, double* v_out, double* slot,
+                          uint32_t u_off, double eta, Workspace* ws, cudaStream_t st);
 void launch_basis_write(const cbgx_basis& V, uint64_t j, const double* x, const ScaleArg& scale,
                         double* v_out, uint64_t* bad, cudaStream_t st);
 void launch_basis_read(const cbgx_basis& V, uint64_t j, uint64_t first, uint64_t count, double* out,

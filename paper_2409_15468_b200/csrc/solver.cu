@@ -240,11 +240,18 @@ void Solver::solve(const double* d_b, const double* d_x0, double* d_x, cbgx_hist
         uint64_t iter = 0, cycles = 0;
         double last = 0.0;
 
+        // Fused orthogonalisation: single GPU, tree reductions, and a grid
+        // that can hold every row's w in registers (probed once per solver).
+        if (fused_state_ == 0) {
+            fused_state_ = (!multi && !halo_ && red == CBGX_REDUCE_TREE && fused_eligible(V_, m)) ? 1 : 2;
+        }
+        const bool use_fused = fused_state_ == 1 && !(cfg_.flags & CBGX_SOLVER_NO_FUSION);
         // One Arnoldi step on the device (gmres.cpp:210-234 minus the host
         // Givens): spmv, CGS pass, gated second pass, scaled write of the
         // next column, and one D2H of the step's slot. `used` columns are in
         // the basis when the step starts; it writes column used+1.
         auto enqueue_step = [&](uint64_t used, int p) {
+            const auto te = std::chrono::steady_clock::now();
             double* sl = d_scal_ + p * slot;
             const uint32_t cols = static_cast<uint32_t>(used + 1);
             GateArg gate;
@@ -260,49 +267,61 @@ void Solver::solve(const double* d_b, const double* d_x0, double* d_x, cbgx_hist
             launch_spmv(A_, d_v_, nullptr, d_w_, sl + kOmega, red, &ws_, st);  // w = A v, omega^2
             timer.end();
             count(CBGX_PHASE_SPMV, spmv_bytes);
-            timer.begin(CBGX_PHASE_DOT);
-            launch_cgs_dot(V_, 0, cols, d_w_, 0, red, sl + kH, &ws_, st);      // h = V^T w
-            timer.end();
-            count(CBGX_PHASE_DOT, cols * bpv * n + 8.0 * n);
-            if (multi) {
-                timer.begin(CBGX_PHASE_COMM);
-                reduce(sl + kOmega, cols + 1, st);
+            if (use_fused) {
+                // one cooperative launch: dot, update, gated second pass and
+                // the scaled write of column used+1, w register-resident
+                timer.begin(CBGX_PHASE_ORTHO);
+                const bool ok = launch_arnoldi_fused(V_, cols, d_w_, d_v_, sl, static_cast<uint32_t>(kU(m)), cfg_.eta,
+                                                     &ws_, st);
                 timer.end();
-            }
-            timer.begin(CBGX_PHASE_UPDATE);
-            launch_cgs_update(V_, 0, cols, sl + kH, 1.0, d_w_, sl + kHn1, red, &ws_, st);  // w -= V h
-            timer.end();
-            count(CBGX_PHASE_UPDATE, cols * bpv * n + 16.0 * n);
-            if (multi) {
-                timer.begin(CBGX_PHASE_COMM);
-                reduce(sl + kHn1, 1, st);
+                if (!ok) throw Error(CBGX_EINTERNAL, "fused orthogonalisation became ineligible");
+                count(CBGX_PHASE_ORTHO, 2.0 * cols * bpv * n + 8.0 * n + 8.0 * n + bpv * n);
+            } else {
+                timer.begin(CBGX_PHASE_DOT);
+                launch_cgs_dot(V_, 0, cols, d_w_, 0, red, sl + kH, &ws_, st);      // h = V^T w
                 timer.end();
+                count(CBGX_PHASE_DOT, cols * bpv * n + 8.0 * n);
+                if (multi) {
+                    timer.begin(CBGX_PHASE_COMM);
+                    reduce(sl + kOmega, cols + 1, st);
+                    timer.end();
+                }
+                timer.begin(CBGX_PHASE_UPDATE);
+                launch_cgs_update(V_, 0, cols, sl + kH, 1.0, d_w_, sl + kHn1, red, &ws_, st);  // w -= V h
+                timer.end();
+                count(CBGX_PHASE_UPDATE, cols * bpv * n + 16.0 * n);
+                if (multi) {
+                    timer.begin(CBGX_PHASE_COMM);
+                    reduce(sl + kHn1, 1, st);
+                    timer.end();
+                }
+                // Second CGS pass, gated on the device by the reference's test
+                // h_next < eta * omega (gmres.cpp:51-68); empty launches otherwise.
+                timer.begin(CBGX_PHASE_DOT);
+                launch_cgs_dot(V_, 0, cols, d_w_, 0, red, sl + kU(m), &ws_, st, gate);
+                timer.end();
+                if (multi) reduce(sl + kU(m), cols, st);
+                timer.begin(CBGX_PHASE_UPDATE);
+                launch_cgs_update(V_, 0, cols, sl + kU(m), 1.0, d_w_, sl + kHn2, red, &ws_, st, gate);
+                timer.end();
+                if (multi) reduce(sl + kHn2, 1, st);
+                S.kernel_launches += 2;
+                // v = w / h_next of the last pass that ran; column used+1
+                // (gmres.cpp:230-234). Written even when the host will later
+                // detect a breakdown: that column is then never read.
+                ScaleArg sc;
+                sc.src = sl + kHn1;
+                sc.mode = 2;
+                sc.gate = gate;
+                timer.begin(CBGX_PHASE_WRITE);
+                launch_basis_write(V_, used + 1, d_w_, sc, d_v_, nullptr, st);
+                timer.end();
+                count(CBGX_PHASE_WRITE, 16.0 * n + bpv * n);
             }
-            // Second CGS pass, gated on the device by the reference's test
-            // h_next < eta * omega (gmres.cpp:51-68); empty launches otherwise.
-            timer.begin(CBGX_PHASE_DOT);
-            launch_cgs_dot(V_, 0, cols, d_w_, 0, red, sl + kU(m), &ws_, st, gate);
-            timer.end();
-            if (multi) reduce(sl + kU(m), cols, st);
-            timer.begin(CBGX_PHASE_UPDATE);
-            launch_cgs_update(V_, 0, cols, sl + kU(m), 1.0, d_w_, sl + kHn2, red, &ws_, st, gate);
-            timer.end();
-            if (multi) reduce(sl + kHn2, 1, st);
-            S.kernel_launches += 2;
-            // v = w / h_next of the last pass that ran; column used+1
-            // (gmres.cpp:230-234). Written even when the host will later
-            // detect a breakdown: that column is then never read.
-            ScaleArg sc;
-            sc.src = sl + kHn1;
-            sc.mode = 2;
-            sc.gate = gate;
-            timer.begin(CBGX_PHASE_WRITE);
-            launch_basis_write(V_, used + 1, d_w_, sc, d_v_, nullptr, st);
-            timer.end();
-            count(CBGX_PHASE_WRITE, 16.0 * n + bpv * n);
             CBGX_CUDA(cudaMemcpyAsync(h_pinned_ + p * slot, sl, kU(m) * sizeof(double) + cols * sizeof(double),
                                       cudaMemcpyDeviceToHost, st));
             CBGX_CUDA(cudaEventRecord(step_ev_[p], st));
+            S.host_enqueue_ms += std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - te).count();
         };
 
         for (;;) {
@@ -356,7 +375,9 @@ void Solver::solve(const double* d_b, const double* d_x0, double* d_x, cbgx_hist
                     ++enqueued;
                 }
                 const int p = static_cast<int>(used & 1);
+                const auto tw = std::chrono::steady_clock::now();
                 CBGX_CUDA(cudaEventSynchronize(step_ev_[p]));
+                S.host_wait_ms += std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - tw).count();
                 const double* hs = h_pinned_ + p * slot;
                 ++iter;
                 const uint32_t cols = static_cast<uint32_t>(used + 1);
@@ -367,8 +388,12 @@ void Solver::solve(const double* d_b, const double* d_x0, double* d_x, cbgx_hist
                 if (h_next < cfg_.eta * omega) {
                     // the device ran the second pass (gmres.cpp:53-68)
                     ++S.reorth_passes;
-                    count(CBGX_PHASE_DOT, cols * bpv * n + 8.0 * n);
-                    count(CBGX_PHASE_UPDATE, cols * bpv * n + 16.0 * n);
+                    if (use_fused) {
+                        S.phase_bytes[CBGX_PHASE_ORTHO] += 2.0 * cols * bpv * n;
+                    } else {
+                        count(CBGX_PHASE_DOT, cols * bpv * n + 8.0 * n);
+                        count(CBGX_PHASE_UPDATE, cols * bpv * n + 16.0 * n);
+                    }
                     const double before = h_next;
                     for (uint64_t i = 0; i < cols; ++i) hcol[i] += hs[kU(m) + i];
                     h_next = std::sqrt(hs[kHn2]);

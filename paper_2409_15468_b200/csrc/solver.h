@@ -80,6 +80,7 @@ private:
     double* d_scal_ = nullptr;   // [0] omega^2 [1] hn^2 [2] ||b||^2 [3] ||r||^2 [4..] h / u / y
     double* h_pinned_ = nullptr;
     cudaEvent_t step_ev_[2] = {nullptr, nullptr};
+    int fused_state_ = 0;  // 0 unknown, 1 fused orthogonalisation kernel, 2 split kernels
     Workspace ws_;
 };
 

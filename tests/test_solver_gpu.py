@@ -92,6 +92,19 @@ def _parse(text):
     return out
 
 
+@pytest.mark.parametrize("case", ["convdiff100_pe1/frsz2-32", "p7_16/frsz2-21", "cd7_12_pe1/f64",
+                                  "convdiff12_pe1_m20/frsz2-32"])
+def test_split_kernels_within_tolerance(cbg, port, case):
+    """The split dot/update/write kernels (large-n / multi-GPU path) on the
+    same cases as the fused single-GPU kernel."""
+    s = SOLVES[case]
+    rp, ci, va, b = problem(port, s)
+    r = solve(cbg, rp, ci, va, b, s["fmt"], s["restart"], reduction=0, fusion=False)
+    want = s["iterations"]
+    assert abs(r.total_iterations - want) <= max(2, 0.02 * want), (r.total_iterations, want)
+    assert r.converged == s["converged"]
+
+
 def test_pinned_counts_fast_path(cbg, port):
     # acceptance.cpp:278-312 criterion 7 instance on the fast (tree) path
     rp, ci, va = port.convdiff(100, 100, 1.0)
