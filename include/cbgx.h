@@ -177,6 +177,7 @@ typedef struct {
     uint32_t row_ptr_bits;
     const int32_t* d_col_idx;
     const double* d_values;
+    uint32_t max_row_nnz;  /* longest row (0 = unknown; picks the SpMV staging size) */
 } cbgx_csr;
 
 /* y = A x; if d_ynorm2, also <y, y> (fused epilogue). */
@@ -234,7 +235,8 @@ typedef struct {
 enum {
     CBGX_SOLVER_PHASE_TIMING = 1,          /* CUDA events around every phase, summed per solve */
     CBGX_SOLVER_PHASE_TIMING_DEFERRED = 2, /* record events, collect later (no per-solve sync) */
-    CBGX_SOLVER_NO_FUSION = 4              /* always use the split dot/update/write kernels */
+    CBGX_SOLVER_NO_FUSION = 4,             /* always use the split dot/update/write kernels */
+    CBGX_SOLVER_NO_SELL = 8                /* SpMV directly on the CSR (no SELL-32 copy) */
 };
 
 typedef struct {

@@ -524,11 +524,12 @@ class GmresConfig:
     phase_timing: bool = False
     phase_timing_deferred: bool = False
     fusion: bool = True   # fused single-GPU orthogonalisation kernel when eligible
+    sell: bool = True     # SELL-32 copy of A for the SpMV when memory allows
 
     def c(self):
         flags = (_lib.PHASE_TIMING if self.phase_timing else 0) | \
             (_lib.PHASE_TIMING_DEFERRED if self.phase_timing_deferred else 0) | \
-            (0 if self.fusion else _lib.NO_FUSION)
+            (0 if self.fusion else _lib.NO_FUSION) | (0 if self.sell else _lib.NO_SELL)
         return _lib.GmresConfig(self.restart, self.target_rrn, self.max_total_iterations, self.eta,
                                 self.storage_format.kind, self.storage_format.bit_length,
                                 self.reduction, flags)

@@ -14,6 +14,7 @@ REDUCE_TREE, REDUCE_REFERENCE = 0, 1
 PHASE_TIMING = 1
 PHASE_TIMING_DEFERRED = 2
 NO_FUSION = 4
+NO_SELL = 8
 PHASES = ["spmv", "dot", "update", "write", "residual", "solution", "comm", "ortho"]
 
 u32, u64, i32, i64, dbl, vp = C.c_uint32, C.c_uint64, C.c_int32, C.c_int64, C.c_double, C.c_void_p
@@ -27,7 +28,7 @@ class Basis(C.Structure):
 
 class Csr(C.Structure):
     _fields_ = [("n_rows", u64), ("n_cols", u64), ("nnz", u64), ("d_row_ptr", vp),
-                ("row_ptr_bits", u32), ("d_col_idx", vp), ("d_values", vp)]
+                ("row_ptr_bits", u32), ("d_col_idx", vp), ("d_values", vp), ("max_row_nnz", u32)]
 
 
 class GmresConfig(C.Structure):

@@ -5,6 +5,7 @@
 #include <cuda_runtime.h>
 
 #include <cstdint>
+#include <memory>
 
 #include "common.cuh"
 #include "runtime.h"
@@ -62,6 +63,20 @@ __device__ __forceinline__ void block_finalize(const double* red, int nwarps, ui
     }
     if (threadIdx.x == 0) *ticket = 0u;
 }
+
+// SELL-32 copy of a CSR matrix (see sparse.cu).
+struct Sell {
+    double* val = nullptr;
+    int32_t* col = nullptr;
+    uint64_t* soff = nullptr;
+    uint64_t nslices = 0;
+    uint64_t entries = 0;
+    ~Sell();
+};
+// nullptr when the copy would take more than max_fraction_of_free of free memory.
+std::unique_ptr<Sell> build_sell(const cbgx_csr& A, double max_fraction_of_free, cudaStream_t st);
+void launch_spmv_sell(const cbgx_csr& A, const Sell& S, const double* x, const double* b, double* y, double* norm,
+                      int reduction, Workspace* ws, cudaStream_t st);
 
 // Deterministic <x, y>. REDUCE_TREE: fixed-shape tree; REDUCE_REFERENCE:
 // one thread, sequential from +0.0 (sparse.cpp:58-67).

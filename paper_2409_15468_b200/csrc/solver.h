@@ -8,6 +8,7 @@
 #include <vector>
 
 #include "cbgx.h"
+#include "reduce.cuh"
 #include "runtime.h"
 
 namespace cbgx {
@@ -64,6 +65,7 @@ private:
     struct PhaseTimer;
     PhaseTimer* timer_ = nullptr;
     void reduce(double* d_vals, size_t count, cudaStream_t st);
+    void spmv(const double* x, const double* b, double* y, double* norm, cudaStream_t st);
     double fetch_scalar(const double* d, cudaStream_t st);
 
     cbgx_csr A_;
@@ -80,7 +82,8 @@ private:
     double* d_scal_ = nullptr;   // [0] omega^2 [1] hn^2 [2] ||b||^2 [3] ||r||^2 [4..] h / u / y
     double* h_pinned_ = nullptr;
     cudaEvent_t step_ev_[2] = {nullptr, nullptr};
-    int fused_state_ = 0;  // 0 unknown, 1 fused orthogonalisation kernel, 2 split kernels
+    int fused_state_ = 0;
+    std::unique_ptr<Sell> sell_;  // 0 unknown, 1 fused orthogonalisation kernel, 2 split kernels
     Workspace ws_;
 };
 

@@ -41,7 +41,23 @@ spmv_kernel(uint64_t n_rows, const RP* __restrict__ rp, const int32_t* __restric
         const uint64_t k0 = static_cast<uint64_t>(__ldg(rp + r));
         const uint64_t k1 = static_cast<uint64_t>(__ldg(rp + r + 1));
         double s = 0.0;
-        for (uint64_t k = k0; k < k1; ++k) s = __dadd_rn(s, __dmul_rn(__ldg(va + k), __ldg(x + __ldg(ci + k))));
+        // batches of 8 entries: all index/value loads, then all gathers, then
+        // the in-order multiply-adds (sparse.cpp:50-52 order, two roundings)
+        for (uint64_t k = k0; k < k1; k += 8) {
+            int32_t c[8];
+            double v[8], xv[8];
+#pragma unroll
+            for (int i = 0; i < 8; ++i) {
+                const bool in = k + i < k1;
+                c[i] = in ? __ldg(ci + k + i) : 0;
+                v[i] = in ? __ldg(va + k + i) : 0.0;
+            }
+#pragma unroll
+            for (int i = 0; i < 8; ++i) xv[i] = k + i < k1 ? __ldg(x + c[i]) : 0.0;
+#pragma unroll
+            for (int i = 0; i < 8; ++i)
+                if (k + i < k1) s = __dadd_rn(s, __dmul_rn(v[i], xv[i]));
+        }
         if (MODE == 1) s = __dsub_rn(__ldg(b + r), s);
         y[r] = s;
         if (with_norm) acc = __dadd_rn(acc, __dmul_rn(s, s));
@@ -51,6 +67,96 @@ spmv_kernel(uint64_t n_rows, const RP* __restrict__ rp, const int32_t* __restric
     if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = acc;
     __syncthreads();
     block_finalize(red, kWarps, 1, partials, ticket, norm_out);
+}
+
+// ---------------------------------------------------------------- SELL-32
+// Sliced ELLPACK copy of a CSR matrix built once at solver setup: slice s
+// holds rows 32s..32s+31; entry k of every row of the slice is stored at
+// off[s] + 32k + lane, so a warp streams the slice with fully coalesced
+// loads. Entries keep their in-row order and padding is never added, so
+// y is bit-identical to the CSR SpMV (and to the reference).
+template <typename RP>
+__global__ void sell_len_kernel(const RP* __restrict__ rp, uint64_t n, uint64_t nslices, uint64_t* __restrict__ slen) {
+    for (uint64_t sl = (blockIdx.x * static_cast<uint64_t>(blockDim.x) + threadIdx.x) / 32; sl < nslices + 1;
+         sl += static_cast<uint64_t>(gridDim.x) * blockDim.x / 32) {
+        const int lane = threadIdx.x & 31;
+        const uint64_t r = sl * 32 + lane;
+        const unsigned len = (sl < nslices && r < n) ? static_cast<unsigned>(rp[r + 1] - rp[r]) : 0u;
+        const unsigned m = __reduce_max_sync(0xFFFFFFFFu, len);
+        if (lane == 0) slen[sl] = static_cast<uint64_t>(m) * 32;
+    }
+}
+
+template <typename RP>
+__global__ void sell_fill_kernel(const RP* __restrict__ rp, const int32_t* __restrict__ ci,
+                                 const double* __restrict__ va, uint64_t n, const uint64_t* __restrict__ soff,
+                                 double* __restrict__ sv, int32_t* __restrict__ sc) {
+    for (uint64_t r = blockIdx.x * static_cast<uint64_t>(blockDim.x) + threadIdx.x; r < (n + 31) / 32 * 32;
+         r += static_cast<uint64_t>(gridDim.x) * blockDim.x) {
+        const uint64_t sl = r / 32, lane = r % 32;
+        const uint64_t off = soff[sl], ml = (soff[sl + 1] - off) / 32;
+        const uint64_t k0 = r < n ? static_cast<uint64_t>(rp[r]) : 0, len = r < n ? static_cast<uint64_t>(rp[r + 1]) - k0 : 0;
+        for (uint64_t k = 0; k < ml; ++k) {
+            sv[off + k * 32 + lane] = k < len ? va[k0 + k] : 0.0;
+            sc[off + k * 32 + lane] = k < len ? ci[k0 + k] : 0;
+        }
+    }
+}
+
+template <typename RP, int MODE>
+__global__ void __launch_bounds__(kThreads)
+sell_spmv_kernel(uint64_t n_rows, const RP* __restrict__ rp, const uint64_t* __restrict__ soff,
+                 const int32_t* __restrict__ sc, const double* __restrict__ sv, const double* __restrict__ x,
+                 const double* __restrict__ b, double* __restrict__ y, int with_norm,
+                 double* __restrict__ partials, unsigned* __restrict__ ticket, double* __restrict__ norm_out) {
+    __shared__ double red[kWarps];
+    const int lane = threadIdx.x & 31;
+    double acc = 0.0;
+    const uint64_t nsl = (n_rows + 31) / 32;
+    for (uint64_t sl = (blockIdx.x * static_cast<uint64_t>(kThreads) + threadIdx.x) / 32; sl < nsl;
+         sl += static_cast<uint64_t>(gridDim.x) * kWarps) {
+        const uint64_t r = sl * 32 + lane;
+        const bool live = r < n_rows;
+        const uint32_t len = live ? static_cast<uint32_t>(__ldg(rp + r + 1) - __ldg(rp + r)) : 0u;
+        const uint64_t off = __ldg(soff + sl);
+        const uint32_t ml = static_cast<uint32_t>((__ldg(soff + sl + 1) - off) / 32);
+        const double* v = sv + off + lane;
+        const int32_t* c = sc + off + lane;
+        double s = 0.0;
+        for (uint32_t k = 0; k < ml; k += 8) {
+            double vv[8], xv[8];
+#pragma unroll
+            for (int i = 0; i < 8; ++i) {
+                const bool in = k + i < ml;
+                const int32_t col = in ? __ldcs(c + (k + i) * 32) : 0;
+                vv[i] = in ? __ldcs(v + (k + i) * 32) : 0.0;
+                xv[i] = k + i < len ? __ldg(x + col) : 0.0;
+            }
+#pragma unroll
+            for (int i = 0; i < 8; ++i)
+                if (k + i < len) s = __dadd_rn(s, __dmul_rn(vv[i], xv[i]));
+        }
+        if (live) {
+            if (MODE == 1) s = __dsub_rn(__ldg(b + r), s);
+            y[r] = s;
+            if (with_norm) acc = __dadd_rn(acc, __dmul_rn(s, s));
+        }
+    }
+    if (!with_norm) return;
+    acc = warp_sum(acc);
+    if (lane == 0) red[threadIdx.x >> 5] = acc;
+    __syncthreads();
+    block_finalize(red, kWarps, 1, partials, ticket, norm_out);
+}
+
+template <typename RP>
+__global__ void max_row_kernel(const RP* __restrict__ rp, uint64_t n, unsigned* __restrict__ out) {
+    unsigned m = 0;
+    for (uint64_t r = blockIdx.x * static_cast<uint64_t>(blockDim.x) + threadIdx.x; r < n;
+         r += static_cast<uint64_t>(gridDim.x) * blockDim.x)
+        m = max(m, static_cast<unsigned>(rp[r + 1] - rp[r]));
+    m = __reduce_max_sync(0xFFFFFFFFu, m);
+    if ((threadIdx.x & 31) == 0) atomicMax(out, m);
 }
 
 __global__ void __launch_bounds__(kThreads)
@@ -186,6 +292,83 @@ void launch_spmv(const cbgx_csr& A, const double* x, const double* b, double* y,
 #undef CBGX_SPMV
     CBGX_CUDA(cudaGetLastError());
     if (norm && !fused) launch_dot(y, y, A.n_rows, CBGX_REDUCE_REFERENCE, norm, ws, st);
+}
+
+Sell::~Sell() {
+    if (val) cudaFree(val);
+    if (col) cudaFree(col);
+    if (soff) cudaFree(soff);
+}
+
+template <typename RP>
+static void sell_build(const cbgx_csr& A, Sell& S, cudaStream_t st) {
+    const RP* rp = static_cast<const RP*>(A.d_row_ptr);
+    S.nslices = (A.n_rows + 31) / 32;
+    CBGX_CUDA(cudaMalloc(&S.soff, (S.nslices + 1) * sizeof(uint64_t)));
+    const int g1 = static_cast<int>(std::min<uint64_t>((S.nslices + 1 + 7) / 8 + 1, sm_count() * 16ull));
+    CBGX_K(sell_len_kernel<RP><<<g1, 256, 0, st>>>(rp, A.n_rows, S.nslices, S.soff));
+    size_t tmp_bytes = 0;
+    CBGX_CUDA(cub::DeviceScan::ExclusiveSum(nullptr, tmp_bytes, S.soff, S.soff, S.nslices + 1, st));
+    void* tmp = nullptr;
+    CBGX_CUDA(cudaMallocAsync(&tmp, tmp_bytes, st));
+    CBGX_CUDA(cub::DeviceScan::ExclusiveSum(tmp, tmp_bytes, S.soff, S.soff, S.nslices + 1, st));
+    CBGX_CUDA(cudaFreeAsync(tmp, st));
+    uint64_t total = 0;
+    CBGX_CUDA(cudaMemcpyAsync(&total, S.soff + S.nslices, sizeof(uint64_t), cudaMemcpyDeviceToHost, st));
+    CBGX_CUDA(cudaStreamSynchronize(st));
+    S.entries = total;
+    CBGX_CUDA(cudaMalloc(&S.val, std::max<uint64_t>(total, 1) * 8));
+    CBGX_CUDA(cudaMalloc(&S.col, std::max<uint64_t>(total, 1) * 4));
+    const int g2 = rows_grid(S.nslices * 32);
+    CBGX_K(sell_fill_kernel<RP><<<g2, kThreads, 0, st>>>(rp, A.d_col_idx, A.d_values, A.n_rows, S.soff, S.val, S.col));
+    CBGX_CUDA(cudaStreamSynchronize(st));
+}
+
+std::unique_ptr<Sell> build_sell(const cbgx_csr& A, double max_fraction_of_free, cudaStream_t st) {
+    size_t free_b = 0, total_b = 0;
+    CBGX_CUDA(cudaMemGetInfo(&free_b, &total_b));
+    const double need = (A.nnz * 1.05 + 32.0 * ((A.n_rows + 31) / 32)) * 12.0;
+    if (need > max_fraction_of_free * static_cast<double>(free_b)) return nullptr;
+    auto S = std::make_unique<Sell>();
+    if (A.row_ptr_bits == 32) sell_build<int32_t>(A, *S, st);
+    else sell_build<int64_t>(A, *S, st);
+    return S;
+}
+
+void launch_spmv_sell(const cbgx_csr& A, const Sell& S, const double* x, const double* b, double* y, double* norm,
+                      int reduction, Workspace* ws, cudaStream_t st) {
+    const int grid = rows_grid(A.n_rows);
+    const bool fused = norm && reduction == CBGX_REDUCE_TREE;
+    double* partials = fused ? ws->get_partials(grid) : nullptr;
+    unsigned* ticket = fused ? ws->get_counter() : nullptr;
+#define CBGX_SELL(RP, MODE)                                                                                   \
+    CBGX_K(sell_spmv_kernel<RP, MODE><<<grid, kThreads, 0, st>>>(A.n_rows, static_cast<const RP*>(A.d_row_ptr), \
+                                                                S.soff, S.col, S.val, x, b, y, fused, partials, \
+                                                                ticket, norm))
+    if (A.row_ptr_bits == 32) {
+        if (b) CBGX_SELL(int32_t, 1); else CBGX_SELL(int32_t, 0);
+    } else {
+        if (b) CBGX_SELL(int64_t, 1); else CBGX_SELL(int64_t, 0);
+    }
+#undef CBGX_SELL
+    CBGX_CUDA(cudaGetLastError());
+    if (norm && !fused) launch_dot(y, y, A.n_rows, CBGX_REDUCE_REFERENCE, norm, ws, st);
+}
+
+uint32_t csr_max_row_nnz(const cbgx_csr& A, cudaStream_t st) {
+    unsigned* d = nullptr;
+    CBGX_CUDA(cudaMallocAsync(reinterpret_cast<void**>(&d), sizeof(unsigned), st));
+    CBGX_CUDA(cudaMemsetAsync(d, 0, sizeof(unsigned), st));
+    const int grid = rows_grid(A.n_rows);
+    if (A.row_ptr_bits == 32)
+        CBGX_K(max_row_kernel<int32_t><<<grid, kThreads, 0, st>>>(static_cast<const int32_t*>(A.d_row_ptr), A.n_rows, d));
+    else
+        CBGX_K(max_row_kernel<int64_t><<<grid, kThreads, 0, st>>>(static_cast<const int64_t*>(A.d_row_ptr), A.n_rows, d));
+    unsigned h = 0;
+    CBGX_CUDA(cudaMemcpyAsync(&h, d, sizeof(unsigned), cudaMemcpyDeviceToHost, st));
+    CBGX_CUDA(cudaFreeAsync(d, st));
+    CBGX_CUDA(cudaStreamSynchronize(st));
+    return h;
 }
 
 void launch_dot(const double* x, const double* y, uint64_t n, int reduction, double* out,

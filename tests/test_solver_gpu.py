@@ -99,7 +99,7 @@ def test_split_kernels_within_tolerance(cbg, port, case):
     same cases as the fused single-GPU kernel."""
     s = SOLVES[case]
     rp, ci, va, b = problem(port, s)
-    r = solve(cbg, rp, ci, va, b, s["fmt"], s["restart"], reduction=0, fusion=False)
+    r = solve(cbg, rp, ci, va, b, s["fmt"], s["restart"], reduction=0, fusion=False, sell=False)
     want = s["iterations"]
     assert abs(r.total_iterations - want) <= max(2, 0.02 * want), (r.total_iterations, want)
     assert r.converged == s["converged"]
@@ -159,6 +159,17 @@ def test_device_stencils_match_oracle(cbg, port):
         assert np.array_equal(A.values.cpu().numpy(), va)
         x = np.random.default_rng(kind).standard_normal(rp.size - 1)
         assert cbg.spmv(A, x).cpu().numpy().tobytes() == port.spmv(rp, ci, va, x).tobytes()
+
+
+def test_sell_and_csr_spmv_paths_agree(cbg, port):
+    """SELL-32 and CSR SpMV give bit-identical y, so the two solves agree
+    exactly (same reduction trees elsewhere)."""
+    rp, ci, va = port.stencil(2, 13, 11, 9)
+    b, _ = port.generate_problem(rp, ci, va)
+    r1 = solve(cbg, rp, ci, va, b, "frsz2-32", 30, reduction=0, sell=True)
+    r2 = solve(cbg, rp, ci, va, b, "frsz2-32", 30, reduction=0, sell=False)
+    assert hist(r1) == hist(r2)
+    assert np.asarray(r1.solution).tobytes() == np.asarray(r2.solution).tobytes()
 
 
 def test_device_solver_determinism(cbg, port):
