@@ -542,17 +542,28 @@ class ResidualRecord:
     is_explicit: bool
 
 
-@dataclasses.dataclass
 class SolveResult:
-    """gmres.hpp:37-45 (+ device statistics)."""
-    converged: bool
-    total_iterations: int
-    restarts: int
-    final_rrn: float
-    residual_history: List[ResidualRecord]
-    wall_seconds: float
-    solution: object
-    stats: object = None
+    """gmres.hpp:37-45 (+ device statistics). The residual history is
+    materialised lazily from the raw arrays the C-ABI filled."""
+
+    def __init__(self, converged, total_iterations, restarts, final_rrn, history_arrays, wall_seconds, solution,
+                 stats=None):
+        self.converged = converged
+        self.total_iterations = total_iterations
+        self.restarts = restarts
+        self.final_rrn = final_rrn
+        self.wall_seconds = wall_seconds
+        self.solution = solution
+        self.stats = stats
+        self._hist = history_arrays
+        self._records = None
+
+    @property
+    def residual_history(self) -> List[ResidualRecord]:
+        if self._records is None:
+            hi, hr, he, k = self._hist
+            self._records = [ResidualRecord(int(hi[i]), float(hr[i]), bool(he[i])) for i in range(k)]
+        return self._records
 
 
 def _history_buffers(cap):
@@ -566,9 +577,8 @@ def _history_buffers(cap):
 def _result(st: "_lib.SolveStats", hist, bufs, x) -> SolveResult:
     hi, hr, he = bufs
     k = min(hist.length, hist.capacity)
-    recs = [ResidualRecord(int(hi[i]), float(hr[i]), bool(he[i])) for i in range(k)]
     return SolveResult(bool(st.converged), int(st.total_iterations), int(st.restarts), float(st.final_rrn),
-                       recs, float(st.wall_seconds), x, st)
+                       (hi[:k].copy(), hr[:k].copy(), he[:k].copy(), k), float(st.wall_seconds), x, st)
 
 
 def gmres_solve(a: CsrMatrix, b, x0, cfg: GmresConfig = GmresConfig()) -> SolveResult:
@@ -612,10 +622,15 @@ class Solver:
         n = self.a.desc.n_rows
         b = _dev(b)
         if x0 is None:
-            x0 = torch.zeros(n, dtype=torch.float64, device="cuda")
+            if getattr(self, "_zeros", None) is None:
+                self._zeros = torch.zeros(n, dtype=torch.float64, device="cuda")
+            x0 = self._zeros
         if x is None:
             x = torch.empty(n, dtype=torch.float64, device="cuda")
-        hist, bufs = _history_buffers(2 * self.cfg.max_total_iterations + 4)
+        if getattr(self, "_hbufs", None) is None:
+            self._hbufs = _history_buffers(2 * self.cfg.max_total_iterations + 4)
+        hist, bufs = self._hbufs
+        hist.length = 0
         st = _lib.SolveStats()
         check(lib().cbgx_solver_solve(self.h, _ptr(b), _ptr(_dev(x0)), _ptr(x), ctypes.byref(hist),
                                       ctypes.byref(st), _stream()))

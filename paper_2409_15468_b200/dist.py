@@ -120,10 +120,15 @@ class DistSolver:
         torch = _torch()
         rows = self.prob.re - self.prob.rb
         if x0 is None:
-            x0 = torch.zeros(rows, dtype=torch.float64, device="cuda")
+            if getattr(self, "_zeros", None) is None:
+                self._zeros = torch.zeros(rows, dtype=torch.float64, device="cuda")
+            x0 = self._zeros
         if x is None:
             x = torch.empty(rows, dtype=torch.float64, device="cuda")
-        hist, bufs = _history_buffers(2 * self.cfg.max_total_iterations + 4)
+        if getattr(self, "_hbufs", None) is None:
+            self._hbufs = _history_buffers(2 * self.cfg.max_total_iterations + 4)
+        hist, bufs = self._hbufs
+        hist.length = 0
         st = _lib.SolveStats()
         check(lib().cbgx_solver_solve(self.h, _ptr(b), _ptr(x0), _ptr(x), ctypes.byref(hist), ctypes.byref(st),
                                       _stream()))
