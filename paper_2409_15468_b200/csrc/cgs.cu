@@ -555,10 +555,16 @@ struct FusedArgs {
     double* slot;              // [hn1, hn2, omega2, h[0..m], u[0..m]]; omega2 set by the SpMV
     uint32_t u_off;            // index of u in slot
     double eta;
-    double* partials;          // gridDim.x * (cols + 1)
-    unsigned* bar;             // [count, generation], zero-initialised
+    double* partials;          // kRegions regions of gridDim.x * (cols + 1)
+    unsigned* bar;             // this launch's arrival counter (zero at launch)
+    unsigned* bar_next;        // the next launch's counter: zeroed here (CTA 0)
+    unsigned* gate_hist;       // previous launch's gate: 0 open (speculate), 1 closed
     unsigned long long* trace; // optional: CTA 0 phase timestamps (debug)
 };
+
+// Partial-row regions, one per grid reduction of a launch, so a CTA that
+// runs ahead never overwrites rows a slower CTA is still reading.
+constexpr int kRegions = 4;
 
 __device__ __forceinline__ unsigned long long global_ns() {
     unsigned long long t;
@@ -571,107 +577,76 @@ __device__ __forceinline__ void consumer_sync() {
     asm volatile("bar.sync 1, %0;" ::"n"(kConsumers) : "memory");
 }
 
-// Grid barrier among the consumer warps of all (co-resident) CTAs.
-__device__ __forceinline__ void grid_sync(unsigned* bar) {
+__device__ __forceinline__ void red_release_add(unsigned* p, unsigned v) {
+    asm volatile("red.release.gpu.global.add.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
+}
+
+__device__ __forceinline__ unsigned ld_acquire(const unsigned* p) {
+    unsigned v;
+    asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+    return v;
+}
+
+// Grid all-reduce among the consumer warps of all (co-resident) CTAs, one
+// barrier hop: every CTA has written its partial row (`count` values at
+// rows + cta * stride); thread 0 arrives with a release add on the launch's
+// monotonic counter and waits (acquire) until all gridDim.x CTAs of barrier
+// number `seq` have arrived; then EVERY CTA sums the rows itself in one
+// fixed order -- R = 2^i <= 32 adjacent lanes per value, lane g summing
+// rows g, g+R, ... (loads batched so they are all in flight), then a
+// butterfly over the R lanes -- so all CTAs hold bit-identical results and
+// no CTA waits for another to publish them. count <= kConsumers.
+__device__ __forceinline__ void grid_allreduce(unsigned* bar, unsigned seq, const double* rows, uint32_t stride,
+                                               uint32_t count, double* out_smem,
+                                               unsigned long long* trace = nullptr) {
     consumer_sync();
     if (threadIdx.x == 0) {
-        volatile unsigned* gen = bar + 1;
-        const unsigned g = *gen;
-        __threadfence();
-        if (atomicAdd(bar, 1u) == gridDim.x - 1) {
-            bar[0] = 0;
-            __threadfence();
-            atomicAdd(bar + 1, 1u);
-        } else {
-            while (*gen == g) __nanosleep(32);
+        if (trace && blockIdx.x == 0) trace[11 + 2 * seq] = global_ns();
+        red_release_add(bar, 1u);
+        const unsigned target = (seq + 1) * gridDim.x;
+        while (ld_acquire(bar) < target) {
         }
-        __threadfence();
+        if (trace && blockIdx.x == 0) trace[12 + 2 * seq] = global_ns();
     }
+    consumer_sync();
+    uint32_t R = 32;
+    while (R > 1 && R * count > static_cast<uint32_t>(kConsumers)) R >>= 1;
+    const uint32_t t = threadIdx.x, k = t / R, g = t % R;
+    const unsigned G = gridDim.x;
+    double v = 0.0;
+    if (k < count) {
+        constexpr int kB = 8;
+        for (unsigned c0 = g; c0 < G; c0 += R * kB) {
+            double x[kB];
+#pragma unroll
+            for (int i = 0; i < kB; ++i) {
+                const unsigned c = c0 + R * i;
+                x[i] = c < G ? __ldcg(rows + static_cast<uint64_t>(c) * stride + k) : 0.0;
+            }
+#pragma unroll
+            for (int i = 0; i < kB; ++i)
+                if (c0 + R * i < G) v = __dadd_rn(v, x[i]);
+        }
+    }
+    for (uint32_t off = R >> 1; off >= 1; off >>= 1) v = __dadd_rn(v, __shfl_xor_sync(0xFFFFFFFFu, v, off));
+    if (g == 0 && k < count) out_smem[k] = v;
     consumer_sync();
 }
 
-// Grid barrier fused with the cross-CTA reduction: the LAST CTA to arrive
-// sums the CTA partial rows of `count` values (fixed order: lane-strided
-// over CTAs, then a warp butterfly -- deterministic whichever CTA it is),
-// publishes them to `result` (global) and releases the others, who read
-// back only `count` values. One CTA reads the partials instead of every CTA
-// hammering the same lines in L2.
-__device__ __forceinline__ void grid_reduce(unsigned* bar, const double* partials, uint32_t stride, uint32_t count,
-                                            double* result, double* out_smem, double* part, int* s_flag) {
-    consumer_sync();
-    if (threadIdx.x == 0) {
-        volatile unsigned* gen = bar + 1;
-        const unsigned g = *gen;
-        __threadfence();
-        const bool last = atomicAdd(bar, 1u) == gridDim.x - 1;
-        s_flag[0] = last ? 1 : 0;
-        s_flag[1] = static_cast<int>(g);
-    }
-    consumer_sync();
-    if (s_flag[0]) {
-        __threadfence();
-        // R threads per value: thread t sums CTA rows g, g+R, g+2R, ... of
-        // value k = t % count (g = t / count), loads issued back to back;
-        // then the R partials of each value are added in g order.
-        const uint32_t R = count >= kConsumers ? 1u : kConsumers / count;
-        const uint32_t t = threadIdx.x;
-        for (uint32_t k0 = 0; k0 < count; k0 += kConsumers) {
-            const uint32_t k = k0 + t % (count < kConsumers ? count : kConsumers);
-            const uint32_t g = count < kConsumers ? t / count : 0;
-            double v = 0.0;
-            if (g < R && k < count) {
-                constexpr int kMax = 32;
-                double x[kMax];
-#pragma unroll
-                for (int i = 0; i < kMax; ++i) {
-                    const unsigned c = g + R * i;
-                    x[i] = c < gridDim.x ? __ldcg(partials + static_cast<uint64_t>(c) * stride + k) : 0.0;
-                }
-#pragma unroll
-                for (int i = 0; i < kMax; ++i)
-                    if (g + R * i < gridDim.x) v = __dadd_rn(v, x[i]);
-                for (unsigned c = g + R * kMax; c < gridDim.x; c += R)
-                    v = __dadd_rn(v, __ldcg(partials + static_cast<uint64_t>(c) * stride + k));
-                part[g * count + k] = v;
-            }
-            consumer_sync();
-            if (t < count && k0 + t < count) {
-                const uint32_t kk = k0 + t;
-                double s = part[kk];
-                for (uint32_t gg = 1; gg < R; ++gg) s = __dadd_rn(s, part[gg * count + kk]);
-                out_smem[kk] = s;
-                result[kk] = s;
-            }
-            consumer_sync();
-        }
-        consumer_sync();
-        if (threadIdx.x == 0) {
-            __threadfence();
-            bar[0] = 0;
-            __threadfence();
-            atomicAdd(bar + 1, 1u);
-        }
-    } else {
-        if (threadIdx.x == 0) {
-            volatile unsigned* gen = bar + 1;
-            while (*gen == static_cast<unsigned>(s_flag[1])) __nanosleep(20);
-            __threadfence();
-        }
-        consumer_sync();
-        for (uint32_t k = threadIdx.x; k < count; k += kConsumers) out_smem[k] = __ldcg(result + k);
-    }
-    consumer_sync();
-}
-
-// Every CTA sums the CTA partial rows of `count` values in the same fixed
-// order (lane-strided over CTAs, then a warp butterfly), result in smem.
-__device__ __forceinline__ void reduce_all(const double* partials, uint32_t stride, uint32_t count, double* out) {
+// This CTA's <w, w> over its register-resident rows (fixed order).
+__device__ __forceinline__ double cta_wnorm2(double wv[][4], double* nred) {
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    for (uint32_t k = warp; k < count; k += kConsumerWarps) {
-        const double s = warp_sum(lane_sum_rows(partials, stride, k, gridDim.x, lane));
-        if (lane == 0) out[k] = s;
-    }
+    double nacc = 0.0;
+#pragma unroll
+    for (int s = 0; s < kFusedMaxSteps; ++s)
+#pragma unroll
+        for (int k = 0; k < 4; ++k) nacc = fma(wv[s][k], wv[s][k], nacc);
+    nacc = warp_sum(nacc);
+    if (lane == 0) nred[warp] = nacc;
     consumer_sync();
+    double s = nred[0];
+    for (int w = 1; w < kWarps; ++w) s = __dadd_rn(s, nred[w]);
+    return s;  // valid in every thread
 }
 
 template <int F>
@@ -740,6 +715,73 @@ __device__ __forceinline__ void fused_write(const FusedArgs& a, uint64_t s0, uin
     }
 }
 
+// One column pass over the CTA's rows: dot (partials into red[warp][j]) or
+// update (w -= h_j v_j) for columns in the given order.
+template <int F, bool kDot>
+__device__ __forceinline__ void fused_pass(uint32_t cols, uint32_t steps, uint32_t nch, unsigned char* stages,
+                                           uint64_t* full, uint64_t* empty, uint32_t& it, double wv[][4],
+                                           double* red, const double* hsm) {
+    constexpr int S = FGeo<F>::stages;
+    constexpr uint32_t PAY = Geo<F>::pay, SB = fstage_bytes<F>();
+    constexpr int kChunkSteps = FGeo<F>::chunk, kChunks = kFusedMaxSteps / kChunkSteps;
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    for (uint32_t jj = 0; jj < cols; ++jj) {
+        const uint32_t j = kDot ? cols - 1 - jj : jj;
+        const double hj = kDot ? 0.0 : hsm[j];
+        const int he = static_cast<int>(exp_field(hj));
+        double acc = 0.0, acc2 = 0.0;
+#pragma unroll
+        for (int ch = 0; ch < kChunks; ++ch) {
+            if (ch >= static_cast<int>(nch)) break;
+            const int stage = it % S;
+            mbar_wait(full + stage, (it / S) & 1);
+            const unsigned char* pay = stages + stage * SB;
+            const uint32_t* ex = reinterpret_cast<const uint32_t*>(pay + kChunkSteps * PAY);
+#pragma unroll
+            for (int s = 0; s < kChunkSteps; ++s) {
+                const int gs = ch * kChunkSteps + s;
+                if (gs < static_cast<int>(steps)) {
+                    Step<F> st;
+                    step_lds<F>(st, pay, ex, s * kStepRows + 4u * threadIdx.x);
+                    if constexpr (kDot) {
+                        if (s & 1) acc2 = __dadd_rn(acc2, st.dot(wv[gs]));
+                        else acc = __dadd_rn(acc, st.dot(wv[gs]));
+                    } else {
+                        st.update(hj, he, wv[gs]);
+                    }
+                }
+            }
+            __syncwarp();
+            if (lane == 0) mbar_arrive(empty + stage);
+            ++it;
+        }
+        if constexpr (kDot) {
+            acc = warp_sum(__dadd_rn(acc, acc2));
+            if (lane == 0) red[warp * cols + j] = acc;
+        }
+    }
+}
+
+// CTA row of the dot pass partials: red[warp][j] summed over warps in order.
+__device__ __forceinline__ void dot_partials_out(const double* red, uint32_t cols, double* row) {
+    consumer_sync();
+    for (uint32_t j = threadIdx.x; j < cols; j += kConsumers) {
+        double s = red[j];
+        for (int w = 1; w < kWarps; ++w) s = __dadd_rn(s, red[w * cols + j]);
+        row[j] = s;
+    }
+}
+
+// Pass schedule (gmres.cpp:36-71, CGS with the reference's gated second
+// pass), 3 grid reductions when the second pass runs, 2 when it does not:
+//   dot1 -> R0[h] -> update1 -> (speculative dot2) -> R1[u.., hn1] -> gate
+//   -> update2 -> R2[hn2] -> scaled write of column `cols`.
+// The second dot pass needs only the CTA's own rows of the updated w, so it
+// runs before the gate is known when the previous launch's gate was open
+// (re-orthogonalisation tends to persist), saving one grid reduction; if
+// the gate turns out closed its coefficients are simply not used. With the
+// previous gate closed the dot2 pass waits for the gate (R1 = [hn1] only,
+// then R2'[u] in region 2).
 template <int F>
 __global__ void __launch_bounds__(kThreads, 2) arnoldi_fused_kernel(FusedArgs a) {
     constexpr int S = FGeo<F>::stages;
@@ -750,12 +792,11 @@ __global__ void __launch_bounds__(kThreads, 2) arnoldi_fused_kernel(FusedArgs a)
     uint64_t* full = reinterpret_cast<uint64_t*>(smem + S * SB);
     uint64_t* empty = full + S;
     double* red = reinterpret_cast<double*>(empty + S);        // [kWarps][cols]
-    double* hsm = red + kWarps * (cols + 1);                    // reduced h / u (cols)
-    double* scal = hsm + cols + 1;                              // [hn1, hn2, gate]
-    double* part = scal + 4;                                    // grid_reduce scratch (kConsumers)
-    uint32_t* scratch = reinterpret_cast<uint32_t*>(part + kConsumers);  // l=21 write: 8 warps x 84 words
+    double* hsm = red + kWarps * (cols + 1);                    // reduced h / u (+ hn1 at [cols])
+    double* scal = hsm + cols + 1;                              // [hn2]
+    double* nred = scal + 4;                                    // [kWarps] norm partials
+    uint32_t* scratch = reinterpret_cast<uint32_t*>(nred + kConsumers);  // l=21 write: 8 warps x 84 words
     volatile int* s_gate = reinterpret_cast<volatile int*>(scratch + kConsumerWarps * 84);
-    int* s_flag = const_cast<int*>(s_gate) + 2;
     if (threadIdx.x == 0) {
         for (int s = 0; s < S; ++s) {
             mbar_init(full + s, 1);
@@ -764,11 +805,15 @@ __global__ void __launch_bounds__(kThreads, 2) arnoldi_fused_kernel(FusedArgs a)
         fence_barrier_init();
         *s_gate = -1;
     }
+    // previous launch's gate (written by CTA 0 at its end, after every CTA
+    // of that launch had read it); CTA-uniform
+    const bool spec = *reinterpret_cast<volatile unsigned*>(a.gate_hist) == 0u;
+    if (blockIdx.x == 0 && threadIdx.x == 0) *a.bar_next = 0u;
     __syncthreads();
     uint64_t s0, s1;
     cta_steps(a.B.n, s0, s1);
     const uint32_t steps = static_cast<uint32_t>(s1 - s0);
-    constexpr int kChunkSteps = FGeo<F>::chunk, kChunks = kFusedMaxSteps / kChunkSteps;
+    constexpr int kChunkSteps = FGeo<F>::chunk;
     const uint32_t nch = (steps + kChunkSteps - 1) / kChunkSteps;
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
 
@@ -778,7 +823,7 @@ __global__ void __launch_bounds__(kThreads, 2) arnoldi_fused_kernel(FusedArgs a)
         const uint64_t policy = policy_evict_normal();
         uint32_t it = 0;
         for (int pass = 0; pass < 4; ++pass) {
-            if (pass == 2) {
+            if (pass == (spec ? 3 : 2)) {
                 while (*s_gate < 0) __nanosleep(64);
                 if (*s_gate == 0) break;
             }
@@ -805,7 +850,7 @@ __global__ void __launch_bounds__(kThreads, 2) arnoldi_fused_kernel(FusedArgs a)
 
     // ---------------- consumers
     FTRACE(0);
-    if (a.trace && threadIdx.x == 0) a.trace[16 + 2048 + blockIdx.x] = global_ns();
+    if (a.trace && threadIdx.x == 0) a.trace[32 + 2048 + blockIdx.x] = global_ns();
     double wv[kFusedMaxSteps][4];
 #pragma unroll
     for (int s = 0; s < kFusedMaxSteps; ++s) {
@@ -815,95 +860,71 @@ __global__ void __launch_bounds__(kThreads, 2) arnoldi_fused_kernel(FusedArgs a)
     FTRACE(1);
     uint32_t it = 0;
     const uint32_t stride = cols + 1;
-    double hn[2] = {0.0, 0.0};
-    bool gate = false;
-    for (int pass = 0; pass < 4; ++pass) {
-        if (pass == 2 && !gate) break;
-        const bool dotpass = (pass & 1) == 0;
-        if (dotpass) {
-            for (uint32_t k = threadIdx.x; k < kWarps * cols; k += kConsumers) red[k] = 0.0;
-            consumer_sync();
-        }
-        double nacc = 0.0;
-        for (uint32_t jj = 0; jj < cols; ++jj) {
-            const uint32_t j = dotpass ? cols - 1 - jj : jj;
-            const double hj = dotpass ? 0.0 : hsm[j];
-            const int he = static_cast<int>(exp_field(hj));
-            double acc = 0.0, acc2 = 0.0;
-#pragma unroll
-            for (int ch = 0; ch < kChunks; ++ch) {
-                if (ch >= static_cast<int>(nch)) break;
-                const int stage = it % S;
-                mbar_wait(full + stage, (it / S) & 1);
-                const unsigned char* pay = stages + stage * SB;
-                const uint32_t* ex = reinterpret_cast<const uint32_t*>(pay + kChunkSteps * PAY);
-#pragma unroll
-                for (int s = 0; s < kChunkSteps; ++s) {
-                    const int gs = ch * kChunkSteps + s;
-                    if (gs < static_cast<int>(steps)) {
-                        Step<F> st;
-                        step_lds<F>(st, pay, ex, s * kStepRows + 4u * threadIdx.x);
-                        if (dotpass) {
-                            if (s & 1) acc2 = __dadd_rn(acc2, st.dot(wv[gs]));
-                            else acc = __dadd_rn(acc, st.dot(wv[gs]));
-                        } else {
-                            st.update(hj, he, wv[gs]);
-                        }
-                    }
-                }
-                __syncwarp();
-                if (lane == 0) mbar_arrive(empty + stage);
-                ++it;
-            }
-            if (dotpass) {
-                acc = warp_sum(__dadd_rn(acc, acc2));
-                if (lane == 0) red[warp * cols + j] = acc;
-            }
-        }
-        FTRACE(2 + 3 * pass);
-        if (a.trace && threadIdx.x == 0 && pass < 2) a.trace[16 + pass * 1024 + blockIdx.x] = global_ns();
-        if (dotpass) {
-            consumer_sync();
-            for (uint32_t j = threadIdx.x; j < cols; j += kConsumers) {
-                double s = red[j];
-                for (int w = 1; w < kWarps; ++w) s = __dadd_rn(s, red[w * cols + j]);
-                a.partials[static_cast<uint64_t>(blockIdx.x) * stride + j] = s;
-            }
-            FTRACE(3 + 3 * pass);
-            grid_reduce(a.bar, a.partials, stride, cols, a.slot + (pass == 0 ? 3u : a.u_off), hsm, part, s_flag);
-            FTRACE(4 + 3 * pass);
-        } else {
-#pragma unroll
-            for (int s = 0; s < kFusedMaxSteps; ++s)
-#pragma unroll
-                for (int k = 0; k < 4; ++k) nacc = fma(wv[s][k], wv[s][k], nacc);
-            nacc = warp_sum(nacc);
-            if (lane == 0) red[warp] = nacc;
-            consumer_sync();
-            if (threadIdx.x == 0) {
-                double s = red[0];
-                for (int w = 1; w < kWarps; ++w) s = __dadd_rn(s, red[w]);
-                a.partials[static_cast<uint64_t>(blockIdx.x) * stride + cols] = s;
-            }
-            FTRACE(3 + 3 * pass);
-            const int which = pass == 1 ? 0 : 1;
-            grid_reduce(a.bar, a.partials + cols, stride, 1, a.slot + which, scal + which, part, s_flag);
-            FTRACE(4 + 3 * pass);
-            hn[which] = scal[which];
-            if (pass == 1) {
-                // gmres.cpp:51 on the device (same IEEE ops as the host)
-                gate = sqrt(hn[0]) < a.eta * sqrt(a.slot[2]);
-                if (threadIdx.x == 0) {
-                    *s_gate = gate ? 1 : 0;
-                    __threadfence_block();
-                }
-            }
-        }
+    const uint64_t region = static_cast<uint64_t>(gridDim.x) * stride;
+    double* myrow = a.partials + static_cast<uint64_t>(blockIdx.x) * stride;
+    const bool cta0 = blockIdx.x == 0;
+    unsigned seq = 0;
+
+    // dot1 -> h
+    fused_pass<F, true>(cols, steps, nch, stages, full, empty, it, wv, red, hsm);
+    FTRACE(2);
+    if (a.trace && threadIdx.x == 0) a.trace[32 + blockIdx.x] = global_ns();
+    dot_partials_out(red, cols, myrow);
+    grid_allreduce(a.bar, seq++, a.partials, stride, cols, hsm, a.trace);
+    if (cta0)
+        for (uint32_t j = threadIdx.x; j < cols; j += kConsumers) a.slot[3 + j] = hsm[j];
+    FTRACE(3);
+    // update1
+    fused_pass<F, false>(cols, steps, nch, stages, full, empty, it, wv, red, hsm);
+    FTRACE(4);
+    if (a.trace && threadIdx.x == 0) a.trace[32 + 1024 + blockIdx.x] = global_ns();
+    const double hn1_part = cta_wnorm2(wv, nred);
+    double* row1 = myrow + region;
+    if (spec) {
+        // speculative dot2 -> u, reduced together with hn1
+        fused_pass<F, true>(cols, steps, nch, stages, full, empty, it, wv, red, hsm);
+        FTRACE(5);
+        dot_partials_out(red, cols, row1);
     }
+    if (threadIdx.x == 0) row1[cols] = hn1_part;
+    if (spec) grid_allreduce(a.bar, seq++, a.partials + region, stride, cols + 1, hsm, a.trace);
+    else grid_allreduce(a.bar, seq++, a.partials + region + cols, stride, 1, hsm + cols);
+    FTRACE(6);
+    const double hn1 = hsm[cols];
+    // gmres.cpp:51 on the device (same IEEE ops as the host)
+    const bool gate = sqrt(hn1) < a.eta * sqrt(a.slot[2]);
+    if (threadIdx.x == 0) {
+        *s_gate = gate ? 1 : 0;
+        __threadfence_block();
+    }
+    if (cta0 && threadIdx.x == 0) a.slot[0] = hn1;
+    double hn2 = hn1;
+    if (gate) {
+        if (!spec) {
+            fused_pass<F, true>(cols, steps, nch, stages, full, empty, it, wv, red, hsm);
+            FTRACE(5);
+            dot_partials_out(red, cols, myrow + 2 * region);
+            grid_allreduce(a.bar, seq++, a.partials + 2 * region, stride, cols, hsm);
+        }
+        if (cta0)
+            for (uint32_t j = threadIdx.x; j < cols; j += kConsumers) a.slot[a.u_off + j] = hsm[j];
+        FTRACE(7);
+        // update2 (u in hsm)
+        fused_pass<F, false>(cols, steps, nch, stages, full, empty, it, wv, red, hsm);
+        FTRACE(8);
+        const double p = cta_wnorm2(wv, nred);
+        double* row3 = myrow + 3 * region;
+        if (threadIdx.x == 0) row3[0] = p;
+        grid_allreduce(a.bar, seq++, a.partials + 3 * region, stride, 1, scal, a.trace);
+        hn2 = scal[0];
+        if (cta0 && threadIdx.x == 0) a.slot[1] = hn2;
+        FTRACE(9);
+    }
+    if (cta0 && threadIdx.x == 0) *a.gate_hist = gate ? 0u : 1u;
     // v = w / h_next of the last pass, written as the next basis column
-    const double scale = 1.0 / sqrt(gate ? hn[1] : hn[0]);
+    const double scale = 1.0 / sqrt(hn2);
     fused_write<F>(a, s0, steps, wv, scale, scratch);
-    FTRACE(14);
+    FTRACE(10);
 }
 
 // Debug timeline of the fused kernel (CTA 0): enabled by CBGX_TRACE_FUSED=1,
@@ -916,8 +937,8 @@ unsigned long long* fused_trace_buffer() {
     }();
     if (!on) return nullptr;
     if (!g_trace) {
-        CBGX_CUDA(cudaMalloc(&g_trace, (16 + 3 * 1024) * sizeof(unsigned long long)));
-        CBGX_CUDA(cudaMemset(g_trace, 0, (16 + 3 * 1024) * sizeof(unsigned long long)));
+        CBGX_CUDA(cudaMalloc(&g_trace, (32 + 3 * 1024) * sizeof(unsigned long long)));
+        CBGX_CUDA(cudaMemset(g_trace, 0, (32 + 3 * 1024) * sizeof(unsigned long long)));
     }
     return g_trace;
 }
@@ -949,8 +970,14 @@ template <int F> struct FusedLaunch {
         a.slot = slot;
         a.u_off = u_off;
         a.eta = eta;
-        a.partials = ws->get_partials(static_cast<size_t>(grid) * (cols + 1));
-        a.bar = ws->get_counter() + 8;
+        a.partials = ws->get_partials(static_cast<size_t>(kRegions) * grid * (cols + 1));
+        // two arrival counters used by alternate launches: each launch
+        // zeroes the other one (the previous launch has completed)
+        unsigned* c = ws->get_counter();
+        const uint64_t seq = ws->fused_launches++;
+        a.bar = c + Workspace::kFusedBar + (seq & 1) * 32;
+        a.bar_next = c + Workspace::kFusedBar + ((seq + 1) & 1) * 32;
+        a.gate_hist = c + Workspace::kFusedGate;
         a.trace = fused_trace_buffer();
         void* args[] = {&a};
         note_launch();
@@ -1001,7 +1028,7 @@ template <int F> struct FusedProbe {
         CBGX_CUDA(cudaDeviceGetAttribute(&coop, cudaDevAttrCooperativeLaunch, current_device()));
         const uint64_t G = static_cast<uint64_t>(sm_count()) * static_cast<uint64_t>(per_sm);
         const uint64_t steps = (V.n + kStepRows - 1) / kStepRows;
-        *ok = coop && per_sm >= 1 && steps <= G * kFusedMaxSteps;
+        *ok = coop && per_sm >= 1 && steps <= G * kFusedMaxSteps && max_cols + 1 <= static_cast<uint64_t>(kConsumers);
     }
 };
 }  // namespace
@@ -1105,7 +1132,7 @@ int cbgx_cgs_update(const cbgx_basis* V, uint64_t first, uint32_t cols, const do
 int cbgx_debug_fused_trace(uint64_t* out, int count) {
     return guard([&] {
         if (!g_trace) throw Error(CBGX_EINVAL, "trace: set CBGX_TRACE_FUSED=1 before the first fused launch");
-        CBGX_CUDA(cudaMemcpy(out, g_trace, std::min(count, 16 + 3 * 1024) * sizeof(uint64_t), cudaMemcpyDeviceToHost));
+        CBGX_CUDA(cudaMemcpy(out, g_trace, std::min(count, 32 + 3 * 1024) * sizeof(uint64_t), cudaMemcpyDeviceToHost));
     });
 }
 

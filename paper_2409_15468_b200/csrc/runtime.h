@@ -12,7 +12,12 @@ namespace cbgx {
 // partial row per CTA into `partials`; the last CTA to finish (ticket from
 // a device counter) sums the rows in CTA order and resets the counter.
 struct Workspace {
-    static constexpr int kCounters = 16;
+    // [0, 16): reduction tickets; kFusedBar, kFusedBar + 32: the fused
+    // kernel's alternating grid-barrier counters; kFusedGate: its last gate.
+    static constexpr int kFusedBar = 32;
+    static constexpr int kFusedGate = 96;
+    static constexpr int kCounters = 128;
+    uint64_t fused_launches = 0;
     int device = 0;
     double* partials = nullptr;
     size_t partial_cap = 0;
