@@ -183,6 +183,13 @@ typedef struct {
 /* y = A x; if d_ynorm2, also <y, y> (fused epilogue). */
 int cbgx_csr_spmv(const cbgx_csr* A, const double* d_x, double* d_y, double* d_ynorm2,
                   int reduction, cbgx_workspace* ws, void* stream);
+/* Staged CSR SpMV (row tiles bulk-copied into shared memory; bit-identical
+ * to cbgx_csr_spmv). cbgx_csr_spmv_plan returns the tile height (32..256
+ * rows) or 0 when some tile exceeds the stage capacity (then use
+ * cbgx_csr_spmv). d_b != NULL computes r = b - A x instead. */
+int cbgx_csr_spmv_plan(const cbgx_csr* A, uint32_t* tile_rows, void* stream);
+int cbgx_csr_spmv_staged(const cbgx_csr* A, uint32_t tile_rows, const double* d_x, const double* d_b,
+                         double* d_y, double* d_ynorm2, int reduction, cbgx_workspace* ws, void* stream);
 /* r = b - A x (gmres.cpp:181-184); if d_rnorm2, also <r, r>. */
 int cbgx_csr_residual(const cbgx_csr* A, const double* d_x, const double* d_b, double* d_r,
                       double* d_rnorm2, int reduction, cbgx_workspace* ws, void* stream);
@@ -236,7 +243,8 @@ enum {
     CBGX_SOLVER_PHASE_TIMING = 1,          /* CUDA events around every phase, summed per solve */
     CBGX_SOLVER_PHASE_TIMING_DEFERRED = 2, /* record events, collect later (no per-solve sync) */
     CBGX_SOLVER_NO_FUSION = 4,             /* always use the split dot/update/write kernels */
-    CBGX_SOLVER_NO_SELL = 8                /* SpMV directly on the CSR (no SELL-32 copy) */
+    CBGX_SOLVER_NO_SELL = 8,               /* SpMV directly on the CSR (no SELL-32 copy) */
+    CBGX_SOLVER_NO_TMA_SPMV = 16           /* no staged (bulk-copy) CSR SpMV */
 };
 
 typedef struct {

@@ -486,6 +486,27 @@ def spmv(a: DeviceCsr, x, y=None, want_norm=False, reduction=_lib.REDUCE_TREE):
     return (y[:a.desc.n_rows], nrm) if want_norm else y[:a.desc.n_rows]
 
 
+def spmv_plan(a: DeviceCsr) -> int:
+    """Tile height of the staged SpMV for this matrix (0: not stageable)."""
+    import ctypes
+    t = ctypes.c_uint32(0)
+    check(lib().cbgx_csr_spmv_plan(ctypes.byref(a.desc), ctypes.byref(t), _stream()))
+    return t.value
+
+
+def spmv_staged(a: DeviceCsr, x, tile_rows: int, b=None, want_norm=False, reduction=_lib.REDUCE_TREE):
+    """Staged (bulk-copy) CSR SpMV: y = A x, or r = b - A x when b is given."""
+    import ctypes
+    torch = _torch()
+    x = _dev(x)
+    bb = _dev(b) if b is not None else None
+    y = torch.empty(max(a.desc.n_rows, 1), dtype=torch.float64, device="cuda")
+    nrm = torch.empty(1, dtype=torch.float64, device="cuda") if want_norm else None
+    check(lib().cbgx_csr_spmv_staged(ctypes.byref(a.desc), tile_rows, _ptr(x), _ptr(bb), _ptr(y), _ptr(nrm),
+                                     reduction, _ws(), _stream()))
+    return (y[:a.desc.n_rows], nrm) if want_norm else y[:a.desc.n_rows]
+
+
 def dot(x, y, reduction=_lib.REDUCE_TREE) -> float:
     torch = _torch()
     x, y = _dev(x), _dev(y)
@@ -525,11 +546,13 @@ class GmresConfig:
     phase_timing_deferred: bool = False
     fusion: bool = True   # fused single-GPU orthogonalisation kernel when eligible
     sell: bool = True     # SELL-32 copy of A for the SpMV when memory allows
+    tma_spmv: bool = True  # staged (bulk-copy) CSR SpMV when every row tile fits
 
     def c(self):
         flags = (_lib.PHASE_TIMING if self.phase_timing else 0) | \
             (_lib.PHASE_TIMING_DEFERRED if self.phase_timing_deferred else 0) | \
-            (0 if self.fusion else _lib.NO_FUSION) | (0 if self.sell else _lib.NO_SELL)
+            (0 if self.fusion else _lib.NO_FUSION) | (0 if self.sell else _lib.NO_SELL) | \
+            (0 if self.tma_spmv else _lib.NO_TMA_SPMV)
         return _lib.GmresConfig(self.restart, self.target_rrn, self.max_total_iterations, self.eta,
                                 self.storage_format.kind, self.storage_format.bit_length,
                                 self.reduction, flags)

@@ -78,6 +78,12 @@ std::unique_ptr<Sell> build_sell(const cbgx_csr& A, double max_fraction_of_free,
 void launch_spmv_sell(const cbgx_csr& A, const Sell& S, const double* x, const double* b, double* y, double* norm,
                       int reduction, Workspace* ws, cudaStream_t st);
 
+// Staged (TMA) CSR SpMV: plan_spmv_tiles returns the tile height (32..256
+// rows, 0 when some tile would exceed the stage capacity).
+uint32_t plan_spmv_tiles(const cbgx_csr& A, cudaStream_t st);
+void launch_spmv_tma(const cbgx_csr& A, uint32_t tile_rows, const double* x, const double* b, double* y,
+                     double* norm, int reduction, Workspace* ws, cudaStream_t st);
+
 // Deterministic <x, y>. REDUCE_TREE: fixed-shape tree; REDUCE_REFERENCE:
 // one thread, sequential from +0.0 (sparse.cpp:58-67).
 void launch_dot(const double* x, const double* y, uint64_t n, int reduction, double* out,

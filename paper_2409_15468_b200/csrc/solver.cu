@@ -139,7 +139,14 @@ Solver::Solver(const cbgx_csr& A, const cbgx_gmres_config& cfg, Comm* comm, Halo
     // basis is allocated below, so leave room for it).
     // Measured on B200: SELL wins for long rows (27-pt: 4.8 vs 5.4 ms/solve
     // of SpMV at 128^3); the batched CSR kernel wins for 7-pt rows.
-    if (!(cfg.flags & CBGX_SOLVER_NO_SELL) && A_.max_row_nnz >= 16) {
+    // Staged (TMA bulk-copy) CSR SpMV when every row tile fits a stage;
+    // else a SELL-32 copy for long rows, else the plain CSR kernel.
+    // Measured on B200 (scripts/spmv_micro.py): staged wins for short rows
+    // (256-row tiles: 7-pt 128^3 57 vs 65 us, 256^3 93% vs 81% of HBM peak);
+    // for long rows (27-pt, 64-row tiles) SELL-32 is kept.
+    if (!(cfg.flags & CBGX_SOLVER_NO_TMA_SPMV)) tile_rows_ = plan_spmv_tiles(A_, nullptr);
+    if (tile_rows_ && tile_rows_ < 256 && !(cfg.flags & CBGX_SOLVER_NO_SELL) && A_.max_row_nnz >= 16) tile_rows_ = 0;
+    if (!tile_rows_ && !(cfg.flags & CBGX_SOLVER_NO_SELL) && A_.max_row_nnz >= 16) {
         uint64_t db = 0, eb = 0;
         cbgx_basis tmp{};
         cbgx_basis_layout(cfg.format_kind, cfg.bit_length, n_, cfg.restart + 1, &tmp, &db, &eb);
@@ -191,7 +198,8 @@ Solver::~Solver() {
 }
 
 void Solver::spmv(const double* x, const double* b, double* y, double* norm, cudaStream_t st) {
-    if (sell_) launch_spmv_sell(A_, *sell_, x, b, y, norm, static_cast<int>(cfg_.reduction), &ws_, st);
+    if (tile_rows_) launch_spmv_tma(A_, tile_rows_, x, b, y, norm, static_cast<int>(cfg_.reduction), &ws_, st);
+    else if (sell_) launch_spmv_sell(A_, *sell_, x, b, y, norm, static_cast<int>(cfg_.reduction), &ws_, st);
     else launch_spmv(A_, x, b, y, norm, static_cast<int>(cfg_.reduction), &ws_, st);
 }
 

@@ -83,7 +83,8 @@ private:
     double* h_pinned_ = nullptr;
     cudaEvent_t step_ev_[2] = {nullptr, nullptr};
     int fused_state_ = 0;
-    std::unique_ptr<Sell> sell_;  // 0 unknown, 1 fused orthogonalisation kernel, 2 split kernels
+    std::unique_ptr<Sell> sell_;
+    uint32_t tile_rows_ = 0;      // staged SpMV tile height (0: not used)
     Workspace ws_;
 };
 

@@ -10,6 +10,7 @@
 #include <algorithm>
 
 #include "common.cuh"
+#include "pipeline.cuh"
 #include "reduce.cuh"
 #include "runtime.h"
 
@@ -147,6 +148,249 @@ sell_spmv_kernel(uint64_t n_rows, const RP* __restrict__ rp, const uint64_t* __r
     if (lane == 0) red[threadIdx.x >> 5] = acc;
     __syncthreads();
     block_finalize(red, kWarps, 1, partials, ticket, norm_out);
+}
+
+
+// ------------------------------------------------------- staged CSR (TMA)
+// Row tiles of TR rows (a power of two <= 256 chosen at setup so that no
+// tile holds more than kTileEntries entries). One producer thread per CTA
+// bulk-copies (cp.async.bulk, SASS UBLKCP) each tile's column indices,
+// values and row offsets -- contiguous CSR segments -- into a kStages-deep
+// shared-memory ring, keeping ~100 KB per CTA in flight independent of how
+// many loads the consumer threads have outstanding. The consumers then
+//   1. entry-parallel: p_k = RN(values[k] * x[col[k]]) for every entry of
+//      the tile (conflict-free shared reads, x gathered through L2), written
+//      back in place;
+//   2. row-parallel: y[r] = ((0 + p_k0) + p_k0+1) + ... in row order.
+// That is exactly the reference's mul-then-add sequence (sparse.cpp:50-52),
+// so y is bit-identical to spmv(). The last <16 B of an array that a bulk
+// copy cannot cover (end of allocation) is read directly from global.
+constexpr int kTileEntries = 2048;
+constexpr int kSpmvStages = 4;
+constexpr int kSpmvConsumers = 256;
+// Consumer groups take alternate tiles (measured on B200: one group of 8
+// warps with 256-row tiles beats two groups with 128-row tiles -- the
+// producer's per-tile cost dominates at smaller tiles).
+constexpr int kSpmvGroups = 1;
+constexpr int kGroupThreads = kSpmvConsumers / kSpmvGroups;
+constexpr int kSpmvThreads = kSpmvConsumers + 32;
+
+template <typename RP>
+struct TileGeo {
+    static constexpr uint32_t val_bytes = (kTileEntries + 2) * 8;
+    static constexpr uint32_t col_bytes = (kTileEntries + 4) * 4;
+    static constexpr uint32_t rp_bytes = (kGroupThreads + 1 + 16 / sizeof(RP)) * sizeof(RP) + 16;
+    static constexpr uint32_t stage = (val_bytes + col_bytes + rp_bytes + 127) / 128 * 128;
+};
+
+__device__ __forceinline__ void spmv_group_sync(int g) {
+    if (g == 0) asm volatile("bar.sync 1, %0;" ::"n"(kGroupThreads) : "memory");
+    else asm volatile("bar.sync 2, %0;" ::"n"(kGroupThreads) : "memory");
+}
+
+// Aligned window of a contiguous array segment [b, e) of element size ES:
+// start aligned down to 16 B; bytes rounded down so the copy never reads
+// past the array end `total` (elements beyond `got` are read from global).
+template <int ES>
+__device__ __forceinline__ void seg_window(uint64_t b, uint64_t e, uint64_t total, uint64_t& a0, uint32_t& bytes) {
+    constexpr uint64_t per = 16 / ES;
+    a0 = b / per * per;
+    uint64_t a1 = (e + per - 1) / per * per;
+    if (a1 > total) a1 = total / per * per;
+    bytes = a1 > a0 ? static_cast<uint32_t>((a1 - a0) * ES) : 0u;
+}
+
+template <typename RP, int MODE>
+__global__ void __launch_bounds__(kSpmvThreads)
+spmv_tma_kernel(uint64_t n_rows, uint64_t nnz, uint32_t tile_rows, const RP* __restrict__ rp,
+                const int32_t* __restrict__ ci, const double* __restrict__ va, const double* __restrict__ x,
+                const double* __restrict__ b, double* __restrict__ y, int with_norm,
+                double* __restrict__ partials, unsigned* __restrict__ ticket, double* __restrict__ norm_out) {
+    using G = TileGeo<RP>;
+    extern __shared__ __align__(128) unsigned char smem[];
+    uint64_t* full = reinterpret_cast<uint64_t*>(smem + kSpmvStages * G::stage);
+    uint64_t* empty = full + kSpmvStages;
+    double* red = reinterpret_cast<double*>(empty + kSpmvStages);
+    if (threadIdx.x == 0) {
+        for (int s = 0; s < kSpmvStages; ++s) {
+            mbar_init(full + s, 1);
+            mbar_init(empty + s, kGroupThreads / 32);
+        }
+        fence_barrier_init();
+    }
+    __syncthreads();
+    const uint64_t ntiles = (n_rows + tile_rows - 1) / tile_rows;
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    if (warp == kSpmvConsumers / 32) {
+        // Producer warp: the entry ranges of the next 32 tiles are fetched
+        // together (lane j: tile i0 + j), so issuing a tile never waits on a
+        // dependent global load; lane 0 issues the bulk copies.
+        const uint64_t policy = policy_evict_first();
+        uint32_t i = 0;
+        for (uint64_t tb = blockIdx.x; tb < ntiles; tb += 32ull * gridDim.x) {
+            const uint64_t mt = tb + static_cast<uint64_t>(lane) * gridDim.x;
+            uint64_t mk0 = 0, mk1 = 0;
+            if (mt < ntiles) {
+                const uint64_t r0 = mt * tile_rows, r1 = min(n_rows, r0 + tile_rows);
+                mk0 = static_cast<uint64_t>(__ldg(rp + r0));
+                mk1 = static_cast<uint64_t>(__ldg(rp + r1));
+            }
+            for (int j = 0; j < 32; ++j, ++i) {
+                const uint64_t tile = tb + static_cast<uint64_t>(j) * gridDim.x;
+                if (tile >= ntiles) break;
+                const uint64_t k0 = __shfl_sync(0xFFFFFFFFu, mk0, j), k1 = __shfl_sync(0xFFFFFFFFu, mk1, j);
+                if (lane == 0) {
+                    const uint64_t r0 = tile * tile_rows, r1 = min(n_rows, r0 + tile_rows);
+                    const int stage = i % kSpmvStages;
+                    mbar_wait(empty + stage, ((i / kSpmvStages) & 1) ^ 1);
+                    unsigned char* dst = smem + stage * G::stage;
+                    uint64_t av, ac, ar;
+                    uint32_t bv, bc, br;
+                    seg_window<8>(k0, k1, nnz, av, bv);
+                    seg_window<4>(k0, k1, nnz, ac, bc);
+                    seg_window<sizeof(RP)>(r0, r1 + 1, n_rows + 1, ar, br);
+                    mbar_arrive_expect_tx(full + stage, bv + bc + br);
+                    if (bv) bulk_g2s(dst, va + av, bv, full + stage, policy);
+                    if (bc) bulk_g2s(dst + G::val_bytes, ci + ac, bc, full + stage, policy);
+                    if (br) bulk_g2s(dst + G::val_bytes + G::col_bytes, rp + ar, br, full + stage, policy);
+                }
+                __syncwarp();
+            }
+        }
+        return;
+    }
+    double acc = 0.0;
+    const int g = warp / (kGroupThreads / 32);
+    const uint32_t t = threadIdx.x % kGroupThreads;
+    uint32_t i = g;
+    for (uint64_t tile = blockIdx.x + static_cast<uint64_t>(g) * gridDim.x; tile < ntiles;
+         tile += static_cast<uint64_t>(kSpmvGroups) * gridDim.x, i += kSpmvGroups) {
+        const uint64_t r0 = tile * tile_rows, r1 = min(n_rows, r0 + tile_rows);
+        const uint32_t nrows = static_cast<uint32_t>(r1 - r0);
+        const int stage = i % kSpmvStages;
+        unsigned char* st = smem + stage * G::stage;
+        double* sv = reinterpret_cast<double*>(st);
+        const int32_t* sc = reinterpret_cast<const int32_t*>(st + G::val_bytes);
+        const RP* sr = reinterpret_cast<const RP*>(st + G::val_bytes + G::col_bytes);
+        constexpr uint64_t pr = 16 / sizeof(RP);
+        const uint32_t orr = static_cast<uint32_t>(r0 % pr);   // rp[r0] at sr[orr]
+        mbar_wait(full + stage, (i / kSpmvStages) & 1);
+        // Tail tile of the arrays (the bulk copies stop at the last whole
+        // 16 B): uniform slow path straight from global memory.
+        const bool tail = r1 + 1 > (n_rows + 1) / pr * pr;
+        uint64_t k0, k1;
+        if (!tail) {
+            k0 = static_cast<uint64_t>(sr[orr]);
+            k1 = static_cast<uint64_t>(sr[orr + nrows]);
+        } else {
+            k0 = static_cast<uint64_t>(__ldg(rp + r0));
+            k1 = static_cast<uint64_t>(__ldg(rp + r1));
+        }
+        const bool gtail = tail || (k1 + 1) / 2 * 2 > nnz / 2 * 2 || (k1 + 3) / 4 * 4 > nnz / 4 * 4;
+        if (gtail) {
+            for (uint64_t r = r0 + t; r < r1; r += kGroupThreads) {
+                const uint64_t a = static_cast<uint64_t>(__ldg(rp + r)), e = static_cast<uint64_t>(__ldg(rp + r + 1));
+                double s = 0.0;
+                for (uint64_t k = a; k < e; ++k) s = __dadd_rn(s, __dmul_rn(__ldg(va + k), __ldg(x + __ldg(ci + k))));
+                if (MODE == 1) s = __dsub_rn(__ldg(b + r), s);
+                y[r] = s;
+                if (with_norm) acc = __dadd_rn(acc, __dmul_rn(s, s));
+            }
+        } else {
+            const uint32_t ov = static_cast<uint32_t>(k0 & 1), oc = static_cast<uint32_t>(k0 & 3);
+            const uint32_t base = static_cast<uint32_t>(k0);  // low bits: in-tile offsets only
+            if constexpr (true) {
+                if (tile_rows == kGroupThreads) {
+                    // short rows: one thread per row, loads for up to 8
+                    // entries issued together, products added in row order
+                    for (uint32_t lr = t; lr < nrows; lr += kGroupThreads) {
+                        const uint32_t a = static_cast<uint32_t>(sr[orr + lr]) - base;
+                        const uint32_t e = static_cast<uint32_t>(sr[orr + lr + 1]) - base;
+                        double s = 0.0;
+                        for (uint32_t k = a; k < e; k += 8) {
+                            int32_t c[8];
+                            double v[8], xv[8];
+#pragma unroll
+                            for (int u = 0; u < 8; ++u) {
+                                const bool in = k + u < e;
+                                c[u] = in ? sc[k + u + oc] : 0;
+                                v[u] = in ? sv[k + u + ov] : 0.0;
+                            }
+#pragma unroll
+                            for (int u = 0; u < 8; ++u) xv[u] = k + u < e ? __ldg(x + c[u]) : 0.0;
+#pragma unroll
+                            for (int u = 0; u < 8; ++u)
+                                if (k + u < e) s = __dadd_rn(s, __dmul_rn(v[u], xv[u]));
+                        }
+                        const uint64_t r = r0 + lr;
+                        if (MODE == 1) s = __dsub_rn(__ldg(b + r), s);
+                        y[r] = s;
+                        if (with_norm) acc = __dadd_rn(acc, __dmul_rn(s, s));
+                    }
+                } else {
+                    // long rows: products entry-parallel (in place), then
+                    // the row sums in order
+                    const uint32_t cnt = static_cast<uint32_t>(k1 - k0);
+                    for (uint32_t e0 = t; e0 < cnt; e0 += 8 * kGroupThreads) {
+                        int32_t c[8];
+                        double v[8], xv[8];
+#pragma unroll
+                        for (int u = 0; u < 8; ++u) {
+                            const uint32_t e = e0 + u * kGroupThreads;
+                            c[u] = e < cnt ? sc[e + oc] : 0;
+                            v[u] = e < cnt ? sv[e + ov] : 0.0;
+                        }
+#pragma unroll
+                        for (int u = 0; u < 8; ++u) xv[u] = e0 + u * kGroupThreads < cnt ? __ldg(x + c[u]) : 0.0;
+#pragma unroll
+                        for (int u = 0; u < 8; ++u) {
+                            const uint32_t e = e0 + u * kGroupThreads;
+                            if (e < cnt) sv[e + ov] = __dmul_rn(v[u], xv[u]);
+                        }
+                    }
+                    spmv_group_sync(g);
+                    for (uint32_t lr = t; lr < nrows; lr += kGroupThreads) {
+                        const uint32_t a = static_cast<uint32_t>(sr[orr + lr]) - base + ov;
+                        const uint32_t e = static_cast<uint32_t>(sr[orr + lr + 1]) - base + ov;
+                        double s = 0.0;
+                        for (uint32_t k = a; k < e; ++k) s = __dadd_rn(s, sv[k]);
+                        const uint64_t r = r0 + lr;
+                        if (MODE == 1) s = __dsub_rn(__ldg(b + r), s);
+                        y[r] = s;
+                        if (with_norm) acc = __dadd_rn(acc, __dmul_rn(s, s));
+                    }
+                }
+            }
+        }
+        __syncwarp();
+        if (lane == 0) mbar_arrive(empty + stage);
+    }
+    if (!with_norm) return;
+    acc = warp_sum(acc);
+    if (lane == 0) red[warp] = acc;
+    // the producer warp has exited (or exits without waiting on anything):
+    // __syncthreads counts only the remaining threads
+    __syncthreads();
+    block_finalize(red, kSpmvConsumers / 32, 1, partials, ticket, norm_out);
+}
+
+// Largest entry count over row tiles of 32/64/128/256 rows.
+template <typename RP>
+__global__ void tile_nnz_kernel(const RP* __restrict__ rp, uint64_t n, unsigned long long* __restrict__ out) {
+    unsigned long long m[4] = {0, 0, 0, 0};
+    for (uint64_t t = blockIdx.x * static_cast<uint64_t>(blockDim.x) + threadIdx.x; t * 256 < n;
+         t += static_cast<uint64_t>(gridDim.x) * blockDim.x) {
+        unsigned long long c[8];
+        for (int g = 0; g < 8; ++g) {
+            const uint64_t a = min(n, t * 256 + g * 32), e = min(n, t * 256 + g * 32 + 32);
+            c[g] = static_cast<unsigned long long>(rp[e] - rp[a]);
+        }
+        for (int g = 0; g < 8; ++g) m[0] = max(m[0], c[g]);
+        for (int g = 0; g < 8; g += 2) m[1] = max(m[1], c[g] + c[g + 1]);
+        for (int g = 0; g < 8; g += 4) m[2] = max(m[2], c[g] + c[g + 1] + c[g + 2] + c[g + 3]);
+        m[3] = max(m[3], c[0] + c[1] + c[2] + c[3] + c[4] + c[5] + c[6] + c[7]);
+    }
+    for (int i = 0; i < 4; ++i) atomicMax(out + i, m[i]);
 }
 
 template <typename RP>
@@ -355,6 +599,60 @@ void launch_spmv_sell(const cbgx_csr& A, const Sell& S, const double* x, const d
     if (norm && !fused) launch_dot(y, y, A.n_rows, CBGX_REDUCE_REFERENCE, norm, ws, st);
 }
 
+
+uint32_t plan_spmv_tiles(const cbgx_csr& A, cudaStream_t st) {
+    if (A.n_rows == 0) return 0;
+    unsigned long long* d = nullptr;
+    CBGX_CUDA(cudaMallocAsync(reinterpret_cast<void**>(&d), 4 * sizeof(unsigned long long), st));
+    CBGX_CUDA(cudaMemsetAsync(d, 0, 4 * sizeof(unsigned long long), st));
+    const int grid = rows_grid((A.n_rows + 255) / 256);
+    if (A.row_ptr_bits == 32)
+        CBGX_K(tile_nnz_kernel<int32_t><<<grid, kThreads, 0, st>>>(static_cast<const int32_t*>(A.d_row_ptr), A.n_rows, d));
+    else
+        CBGX_K(tile_nnz_kernel<int64_t><<<grid, kThreads, 0, st>>>(static_cast<const int64_t*>(A.d_row_ptr), A.n_rows, d));
+    unsigned long long h[4] = {0, 0, 0, 0};
+    CBGX_CUDA(cudaMemcpyAsync(h, d, sizeof(h), cudaMemcpyDeviceToHost, st));
+    CBGX_CUDA(cudaFreeAsync(d, st));
+    CBGX_CUDA(cudaStreamSynchronize(st));
+    for (int i = 3; i >= 0; --i)
+        if ((32 << i) <= kGroupThreads && h[i] <= static_cast<unsigned long long>(kTileEntries)) return 32u << i;
+    return 0;
+}
+
+template <typename RP, int MODE>
+static void spmv_tma_launch(const cbgx_csr& A, uint32_t tile_rows, const double* x, const double* b, double* y,
+                            int fused, double* norm, Workspace* ws, cudaStream_t st) {
+    static int per_sm = -1;  // per (RP, MODE) instantiation; one device geometry
+    const size_t smem = kSpmvStages * (TileGeo<RP>::stage + 16) + 64;
+    if (per_sm < 0) {
+        CBGX_CUDA(cudaFuncSetAttribute(spmv_tma_kernel<RP, MODE>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                       static_cast<int>(smem)));
+        CBGX_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, spmv_tma_kernel<RP, MODE>, kSpmvThreads, smem));
+        per_sm = std::max(per_sm, 1);
+    }
+    const uint64_t ntiles = (A.n_rows + tile_rows - 1) / tile_rows;
+    const int grid = static_cast<int>(std::max<uint64_t>(1, std::min<uint64_t>(ntiles, static_cast<uint64_t>(sm_count()) * per_sm)));
+    double* partials = fused ? ws->get_partials(grid) : nullptr;
+    unsigned* ticket = fused ? ws->get_counter() : nullptr;
+    CBGX_K(spmv_tma_kernel<RP, MODE><<<grid, kSpmvThreads, smem, st>>>(
+        A.n_rows, A.nnz, tile_rows, static_cast<const RP*>(A.d_row_ptr), A.d_col_idx, A.d_values, x, b, y, fused,
+        partials, ticket, norm));
+}
+
+void launch_spmv_tma(const cbgx_csr& A, uint32_t tile_rows, const double* x, const double* b, double* y,
+                     double* norm, int reduction, Workspace* ws, cudaStream_t st) {
+    const int fused = norm && reduction == CBGX_REDUCE_TREE;
+    if (A.row_ptr_bits == 32) {
+        if (b) spmv_tma_launch<int32_t, 1>(A, tile_rows, x, b, y, fused, norm, ws, st);
+        else spmv_tma_launch<int32_t, 0>(A, tile_rows, x, b, y, fused, norm, ws, st);
+    } else {
+        if (b) spmv_tma_launch<int64_t, 1>(A, tile_rows, x, b, y, fused, norm, ws, st);
+        else spmv_tma_launch<int64_t, 0>(A, tile_rows, x, b, y, fused, norm, ws, st);
+    }
+    CBGX_CUDA(cudaGetLastError());
+    if (norm && !fused) launch_dot(y, y, A.n_rows, CBGX_REDUCE_REFERENCE, norm, ws, st);
+}
+
 uint32_t csr_max_row_nnz(const cbgx_csr& A, cudaStream_t st) {
     unsigned* d = nullptr;
     CBGX_CUDA(cudaMallocAsync(reinterpret_cast<void**>(&d), sizeof(unsigned), st));
@@ -394,6 +692,26 @@ int cbgx_csr_spmv(const cbgx_csr* A, const double* d_x, double* d_y, double* d_y
         check_csr(A);
         if (d_ynorm2 && !ws) throw Error(CBGX_EINVAL, "spmv: fused norm needs a workspace");
         launch_spmv(*A, d_x, nullptr, d_y, d_ynorm2, reduction, ws_of(ws), as_stream(stream));
+    });
+}
+
+int cbgx_csr_spmv_plan(const cbgx_csr* A, uint32_t* tile_rows, void* stream) {
+    return guard([&] {
+        check_csr(A);
+        if (!tile_rows) throw Error(CBGX_EINVAL, "spmv: null output");
+        *tile_rows = plan_spmv_tiles(*A, as_stream(stream));
+    });
+}
+
+int cbgx_csr_spmv_staged(const cbgx_csr* A, uint32_t tile_rows, const double* d_x, const double* d_b,
+                         double* d_y, double* d_ynorm2, int reduction, cbgx_workspace* ws, void* stream) {
+    return guard([&] {
+        check_csr(A);
+        if (tile_rows < 32 || tile_rows > static_cast<uint32_t>(kGroupThreads) || (tile_rows & (tile_rows - 1)))
+            throw Error(CBGX_EINVAL, "spmv: tile_rows must be a power of two in [32, 256]");
+        if (d_ynorm2 && !ws) throw Error(CBGX_EINVAL, "spmv: fused norm needs a workspace");
+        if (A->n_rows == 0) return;
+        launch_spmv_tma(*A, tile_rows, d_x, d_b, d_y, d_ynorm2, reduction, ws_of(ws), as_stream(stream));
     });
 }
 

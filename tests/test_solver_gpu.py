@@ -204,3 +204,60 @@ def test_partitioned_local_matches_single(cbg, port, parts):
     assert r.converged
     assert abs(r.total_iterations - single.total_iterations) <= 2
     assert np.allclose(r.solution, single.solution, rtol=1e-7, atol=1e-12)
+
+
+def _ragged_csr(rng, n, max_len, empty_frac=0.1, long_rows=()):
+    lens = rng.integers(0, max_len + 1, size=n)
+    lens[rng.random(n) < empty_frac] = 0
+    for r, L in long_rows:
+        lens[r] = L
+    rp = np.zeros(n + 1, dtype=np.uint64)
+    rp[1:] = np.cumsum(lens)
+    nnz = int(rp[-1])
+    ci = np.concatenate([np.sort(rng.choice(n, size=int(L), replace=L > n)) for L in lens]).astype(np.uint64) \
+        if nnz else np.zeros(0, np.uint64)
+    va = rng.standard_normal(nnz)
+    return rp, ci, va
+
+
+@pytest.mark.parametrize("n,max_len,tile", [(1, 3, 32), (37, 9, 256), (1000, 7, 256), (4099, 27, 64),
+                                            (5000, 40, 32), (70001, 7, 256)])
+def test_staged_spmv_bit_exact(cbg, port, n, max_len, tile):
+    """Staged (bulk-copy) CSR SpMV: y and b - A x bit-identical to the
+    reference spmv on ragged rows (empty rows, tails that end mid-tile,
+    arrays whose last <16 B are read directly); the planner picks the
+    largest tile that fits."""
+    rng = np.random.default_rng(n)
+    rp, ci, va = _ragged_csr(rng, n, max_len)
+    A = cbg.DeviceCsr.from_host(cbg.CsrMatrix(n, n, rp, ci, va))
+    t = cbg.spmv_plan(A)
+    assert t >= tile
+    x = rng.standard_normal(n)
+    ref = port.spmv(rp, ci, va, x)
+    for rows in sorted({32, tile, t}):
+        y, nrm = cbg.spmv_staged(A, x, rows, want_norm=True)
+        assert y.cpu().numpy().tobytes() == ref.tobytes(), rows
+        assert abs(nrm.item() - float(ref @ ref)) <= 1e-12 * max(1.0, float(ref @ ref))
+        b = rng.standard_normal(n)
+        r = cbg.spmv_staged(A, x, rows, b=b)
+        assert r.cpu().numpy().tobytes() == (b - ref).tobytes(), rows
+
+
+def test_staged_spmv_plan_limits(cbg):
+    rng = np.random.default_rng(3)
+    # one 3000-entry row: no tile fits a stage -> 0 (solver falls back)
+    rp, ci, va = _ragged_csr(rng, 5000, 5, long_rows=[(123, 3000)])
+    A = cbg.DeviceCsr.from_host(cbg.CsrMatrix(5000, 5000, rp, ci, va))
+    assert cbg.spmv_plan(A) == 0
+    # 27-point rows: 64-row tiles (64 * 27 <= 2048 < 128 * 27)
+    assert cbg.spmv_plan(cbg.stencil(2, 20)) == 64
+    assert cbg.spmv_plan(cbg.stencil(0, 20)) == 256
+
+
+def test_staged_and_csr_solves_agree(cbg, port):
+    rp, ci, va = port.stencil(0, 14, 13, 11)
+    b, _ = port.generate_problem(rp, ci, va)
+    r1 = solve(cbg, rp, ci, va, b, "frsz2-32", 30, reduction=0, tma_spmv=True)
+    r2 = solve(cbg, rp, ci, va, b, "frsz2-32", 30, reduction=0, tma_spmv=False)
+    assert hist(r1) == hist(r2)
+    assert np.asarray(r1.solution).tobytes() == np.asarray(r2.solution).tobytes()
