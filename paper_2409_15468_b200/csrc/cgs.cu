@@ -32,6 +32,10 @@
 #include "reduce.cuh"
 #include "runtime.h"
 
+#ifndef FUSED_CTAS_PER_SM
+#define FUSED_CTAS_PER_SM 2
+#endif
+
 namespace cbgx {
 
 namespace {
@@ -519,30 +523,56 @@ template <int F> struct ReadLaunch {
 // Fused single-GPU Arnoldi orthogonalisation (persistent, co-resident grid).
 //
 // One launch replaces dot -> update -> [gated dot -> update] -> scaled write
-// of the next basis column (gmres.cpp:211-234 minus the host Givens). Every
-// CTA owns a fixed row range for the whole launch, so w stays in registers
-// across all passes; passes are separated by a grid barrier among the
-// consumer warps while the producer warp keeps streaming the next pass's
-// columns through the shared-memory ring (the basis does not depend on the
-// barrier). Dot passes run last-to-first and update passes first-to-last, so
-// each pass starts on the columns the previous one left in L2.
-// Eligible when every CTA's rows fit in kFusedMaxSteps 1024-row steps
-// (n <= 8192 * co-resident CTAs, ~2.4M rows on a B200).
+// of the next basis column (gmres.cpp:211-234 minus the host Givens). One CTA
+// per SM (16 consumer warps + 1 producer warp) owns a fixed, contiguous row
+// range for the whole launch, so w stays in registers across all passes;
+// passes are separated by grid all-reductions among the consumer warps while
+// the producer warp keeps streaming the next pass's columns through the
+// shared-memory ring (the basis does not depend on the reduction). Dot passes
+// run last-to-first and update passes first-to-last, so each pass starts on
+// the columns the previous one left in L2.
+//
+// Rows are split over the CTAs in 128-row units (16-B aligned segments for
+// every format), so CTAs differ by at most one unit (<1% at 128^3) and every
+// grid reduction waits on a balanced grid. One CTA per SM halves the number
+// of partial rows each reduction has to read compared with two.
+// Eligible when every CTA's rows fit in kFusedMaxSteps 2048-row steps
+// (n <= 16384 * SMs, ~2.4M rows on a B200).
 constexpr int kFusedMaxSteps = 8;
+constexpr int kFCtasPerSM = FUSED_CTAS_PER_SM;
+constexpr int kFWarps = 16 / kFCtasPerSM;       // consumer warps
+constexpr int kFConsumers = kFWarps * 32;
+constexpr int kFThreads = kFConsumers + 32;     // + producer warp
+constexpr uint32_t kFStepRows = 4 * kFConsumers;
+constexpr uint32_t kUnitRows = 128;
 
-// Ring stage = one column's segment of `chunk` steps (the whole CTA range
-// when it fits, so a column-pass is one ring round).
+// Ring stage = one column's segment of `chunk` 2048-row steps.
 template <int F> struct FGeo;
+#if FUSED_CTAS_PER_SM == 1
+template <> struct FGeo<kZ32> { static constexpr int chunk = 4, stages = 5; };
+template <> struct FGeo<kZ16> { static constexpr int chunk = 8, stages = 5; };
+template <> struct FGeo<kZ21> { static constexpr int chunk = 4, stages = 7; };
+template <> struct FGeo<kF64> { static constexpr int chunk = 2, stages = 5; };
+template <> struct FGeo<kF32> { static constexpr int chunk = 4, stages = 5; };
+template <> struct FGeo<kF16> { static constexpr int chunk = 8, stages = 5; };
+#else
 template <> struct FGeo<kZ32> { static constexpr int chunk = 8, stages = 3; };
 template <> struct FGeo<kZ16> { static constexpr int chunk = 8, stages = 4; };
 template <> struct FGeo<kZ21> { static constexpr int chunk = 8, stages = 3; };
 template <> struct FGeo<kF64> { static constexpr int chunk = 4, stages = 3; };
 template <> struct FGeo<kF32> { static constexpr int chunk = 8, stages = 3; };
 template <> struct FGeo<kF16> { static constexpr int chunk = 8, stages = 4; };
+#endif
+
+// payload / exponent bytes per 2048-row step and per 128-row unit
+template <int F> struct FBytes {
+    static constexpr uint32_t pay = Geo<F>::pay * kFStepRows / 1024, ex = Geo<F>::ex * kFStepRows / 1024;
+    static constexpr uint32_t upay = Geo<F>::pay / 8, uex = Geo<F>::ex / 8;
+};
 
 template <int F>
 __host__ __device__ constexpr uint32_t fstage_bytes() {
-    return FGeo<F>::chunk * (Geo<F>::pay + Geo<F>::ex) + 16;
+    return FGeo<F>::chunk * (FBytes<F>::pay + FBytes<F>::ex) + 16;
 }
 
 struct FusedArgs {
@@ -555,15 +585,16 @@ struct FusedArgs {
     double* slot;              // [hn1, hn2, omega2, h[0..m], u[0..m]]; omega2 set by the SpMV
     uint32_t u_off;            // index of u in slot
     double eta;
-    double* partials;          // kRegions regions of gridDim.x * (cols + 1)
+    double* partials;          // kRegions regions of (cols + 1) x gs doubles (value-major)
+    uint32_t gs;               // gridDim.x rounded up to even
     unsigned* bar;             // this launch's arrival counter (zero at launch)
     unsigned* bar_next;        // the next launch's counter: zeroed here (CTA 0)
     unsigned* gate_hist;       // previous launch's gate: 0 open (speculate), 1 closed
     unsigned long long* trace; // optional: CTA 0 phase timestamps (debug)
 };
 
-// Partial-row regions, one per grid reduction of a launch, so a CTA that
-// runs ahead never overwrites rows a slower CTA is still reading.
+// Partial regions, one per grid reduction of a launch, so a CTA that runs
+// ahead never overwrites partials a slower CTA is still reading.
 constexpr int kRegions = 4;
 
 __device__ __forceinline__ unsigned long long global_ns() {
@@ -574,7 +605,7 @@ __device__ __forceinline__ unsigned long long global_ns() {
 #define FTRACE(i) do { if (a.trace && blockIdx.x == 0 && threadIdx.x == 0) a.trace[i] = global_ns(); } while (0)
 
 __device__ __forceinline__ void consumer_sync() {
-    asm volatile("bar.sync 1, %0;" ::"n"(kConsumers) : "memory");
+    asm volatile("bar.sync 1, %0;" ::"n"(kFConsumers) : "memory");
 }
 
 __device__ __forceinline__ void red_release_add(unsigned* p, unsigned v) {
@@ -587,16 +618,23 @@ __device__ __forceinline__ unsigned ld_acquire(const unsigned* p) {
     return v;
 }
 
+// This CTA's rows: [r0, r1) in 128-row units, balanced over the grid.
+__device__ __forceinline__ void fused_rows(uint64_t n, uint64_t& r0, uint64_t& r1) {
+    const uint64_t units = (n + kUnitRows - 1) / kUnitRows;
+    r0 = units * blockIdx.x / gridDim.x * kUnitRows;
+    r1 = units * (blockIdx.x + 1) / gridDim.x * kUnitRows;
+}
+
 // Grid all-reduce among the consumer warps of all (co-resident) CTAs, one
-// barrier hop: every CTA has written its partial row (`count` values at
-// rows + cta * stride); thread 0 arrives with a release add on the launch's
-// monotonic counter and waits (acquire) until all gridDim.x CTAs of barrier
-// number `seq` have arrived; then EVERY CTA sums the rows itself in one
-// fixed order -- R = 2^i <= 32 adjacent lanes per value, lane g summing
-// rows g, g+R, ... (loads batched so they are all in flight), then a
+// barrier hop. Partials are value-major: value k of CTA c at
+// region[k * gs + c]. Thread 0 arrives with a release add on the launch's
+// monotonic counter and waits (acquire) until all CTAs of barrier number
+// `seq` have arrived; then EVERY CTA sums the partials itself in one fixed
+// order -- R = 2^i <= 32 adjacent lanes per value, lane g adding the
+// 16-B pairs g, g+R, ... (loads batched so they are all in flight), then a
 // butterfly over the R lanes -- so all CTAs hold bit-identical results and
-// no CTA waits for another to publish them. count <= kConsumers.
-__device__ __forceinline__ void grid_allreduce(unsigned* bar, unsigned seq, const double* rows, uint32_t stride,
+// nobody waits for another CTA to publish them. count <= kFConsumers.
+__device__ __forceinline__ void grid_allreduce(unsigned* bar, unsigned seq, const double* region, uint32_t gs,
                                                uint32_t count, double* out_smem,
                                                unsigned long long* trace = nullptr) {
     consumer_sync();
@@ -610,22 +648,28 @@ __device__ __forceinline__ void grid_allreduce(unsigned* bar, unsigned seq, cons
     }
     consumer_sync();
     uint32_t R = 32;
-    while (R > 1 && R * count > static_cast<uint32_t>(kConsumers)) R >>= 1;
+    while (R > 1 && R * count > static_cast<uint32_t>(kFConsumers)) R >>= 1;
     const uint32_t t = threadIdx.x, k = t / R, g = t % R;
-    const unsigned G = gridDim.x;
+    const unsigned G = gridDim.x, pairs = (G + 1) / 2;
     double v = 0.0;
     if (k < count) {
-        constexpr int kB = 8;
-        for (unsigned c0 = g; c0 < G; c0 += R * kB) {
-            double x[kB];
+        const double2* base = reinterpret_cast<const double2*>(region + static_cast<uint64_t>(k) * gs);
+        constexpr int kB = 4;
+        for (unsigned p0 = g; p0 < pairs; p0 += R * kB) {
+            double2 x[kB];
 #pragma unroll
             for (int i = 0; i < kB; ++i) {
-                const unsigned c = c0 + R * i;
-                x[i] = c < G ? __ldcg(rows + static_cast<uint64_t>(c) * stride + k) : 0.0;
+                const unsigned p = p0 + R * i;
+                x[i] = p < pairs ? __ldcg(base + p) : make_double2(0.0, 0.0);
             }
 #pragma unroll
-            for (int i = 0; i < kB; ++i)
-                if (c0 + R * i < G) v = __dadd_rn(v, x[i]);
+            for (int i = 0; i < kB; ++i) {
+                const unsigned p = p0 + R * i;
+                if (p < pairs) {
+                    v = __dadd_rn(v, x[i].x);
+                    if (2 * p + 1 < G) v = __dadd_rn(v, x[i].y);
+                }
+            }
         }
     }
     for (uint32_t off = R >> 1; off >= 1; off >>= 1) v = __dadd_rn(v, __shfl_xor_sync(0xFFFFFFFFu, v, off));
@@ -633,7 +677,8 @@ __device__ __forceinline__ void grid_allreduce(unsigned* bar, unsigned seq, cons
     consumer_sync();
 }
 
-// This CTA's <w, w> over its register-resident rows (fixed order).
+// This CTA's <w, w> over its register-resident rows (fixed order); the
+// value is returned in every thread.
 __device__ __forceinline__ double cta_wnorm2(double wv[][4], double* nred) {
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     double nacc = 0.0;
@@ -645,18 +690,19 @@ __device__ __forceinline__ double cta_wnorm2(double wv[][4], double* nred) {
     if (lane == 0) nred[warp] = nacc;
     consumer_sync();
     double s = nred[0];
-    for (int w = 1; w < kWarps; ++w) s = __dadd_rn(s, nred[w]);
-    return s;  // valid in every thread
+    for (int w = 1; w < kFWarps; ++w) s = __dadd_rn(s, nred[w]);
+    return s;
 }
 
 template <int F>
-__device__ __forceinline__ void fused_write(const FusedArgs& a, uint64_t s0, uint32_t steps, double wv[][4],
-                                            double scale, uint32_t* scratch) {
+__device__ __forceinline__ void fused_write(const FusedArgs& a, uint64_t r0, uint64_t r1, uint32_t steps,
+                                            double wv[][4], double scale, uint32_t* scratch) {
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
 #pragma unroll
     for (int s = 0; s < kFusedMaxSteps; ++s) {
         if (s >= static_cast<int>(steps)) break;
-        const uint64_t r = (s0 + s) * kStepRows + 4u * threadIdx.x;
+        const uint64_t r = r0 + s * kFStepRows + 4u * threadIdx.x;
+        if (r >= r1) continue;  // warp-uniform: r1 is a multiple of 128
         double v[4];
 #pragma unroll
         for (int k = 0; k < 4; ++k) v[k] = r + k < a.B.n ? __dmul_rn(wv[s][k], scale) : 0.0;
@@ -697,7 +743,7 @@ __device__ __forceinline__ void fused_write(const FusedArgs& a, uint64_t s0, uin
                     if (sh > 11) atomicOr(wbuf + q + 1, c[k] >> (32 - sh));
                 }
                 __syncwarp();
-                uint32_t* dst = reinterpret_cast<uint32_t*>(a.out_pay) + ((s0 + s) * kStepRows + warp * 128u) / 32 * 21;
+                uint32_t* dst = reinterpret_cast<uint32_t*>(a.out_pay) + (r - 4u * lane) / 32 * 21;
                 for (int i = lane; i < 84; i += 32) dst[i] = wbuf[i];
                 __syncwarp();
             }
@@ -716,13 +762,14 @@ __device__ __forceinline__ void fused_write(const FusedArgs& a, uint64_t s0, uin
 }
 
 // One column pass over the CTA's rows: dot (partials into red[warp][j]) or
-// update (w -= h_j v_j) for columns in the given order.
+// update (w -= h_j v_j) for columns in the given order. `lim` = number of
+// the CTA's rows; a thread's 4 rows are skipped past it (its w stays 0).
 template <int F, bool kDot>
-__device__ __forceinline__ void fused_pass(uint32_t cols, uint32_t steps, uint32_t nch, unsigned char* stages,
+__device__ __forceinline__ void fused_pass(uint32_t cols, uint32_t lim, uint32_t nch, unsigned char* stages,
                                            uint64_t* full, uint64_t* empty, uint32_t& it, double wv[][4],
                                            double* red, const double* hsm) {
     constexpr int S = FGeo<F>::stages;
-    constexpr uint32_t PAY = Geo<F>::pay, SB = fstage_bytes<F>();
+    constexpr uint32_t PAY = FBytes<F>::pay, SB = fstage_bytes<F>();
     constexpr int kChunkSteps = FGeo<F>::chunk, kChunks = kFusedMaxSteps / kChunkSteps;
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     for (uint32_t jj = 0; jj < cols; ++jj) {
@@ -740,9 +787,10 @@ __device__ __forceinline__ void fused_pass(uint32_t cols, uint32_t steps, uint32
 #pragma unroll
             for (int s = 0; s < kChunkSteps; ++s) {
                 const int gs = ch * kChunkSteps + s;
-                if (gs < static_cast<int>(steps)) {
+                const uint32_t lr = s * kFStepRows + 4u * threadIdx.x;
+                if (static_cast<uint32_t>(gs) * kFStepRows + 4u * threadIdx.x < lim) {
                     Step<F> st;
-                    step_lds<F>(st, pay, ex, s * kStepRows + 4u * threadIdx.x);
+                    step_lds<F>(st, pay, ex, lr);
                     if constexpr (kDot) {
                         if (s & 1) acc2 = __dadd_rn(acc2, st.dot(wv[gs]));
                         else acc = __dadd_rn(acc, st.dot(wv[gs]));
@@ -762,13 +810,14 @@ __device__ __forceinline__ void fused_pass(uint32_t cols, uint32_t steps, uint32
     }
 }
 
-// CTA row of the dot pass partials: red[warp][j] summed over warps in order.
-__device__ __forceinline__ void dot_partials_out(const double* red, uint32_t cols, double* row) {
+// This CTA's dot-pass partials (red[warp][j] summed over warps in order)
+// into the value-major region: region[j * gs + cta].
+__device__ __forceinline__ void dot_partials_out(const double* red, uint32_t cols, double* region, uint32_t gs) {
     consumer_sync();
-    for (uint32_t j = threadIdx.x; j < cols; j += kConsumers) {
+    for (uint32_t j = threadIdx.x; j < cols; j += kFConsumers) {
         double s = red[j];
-        for (int w = 1; w < kWarps; ++w) s = __dadd_rn(s, red[w * cols + j]);
-        row[j] = s;
+        for (int w = 1; w < kFWarps; ++w) s = __dadd_rn(s, red[w * cols + j]);
+        region[static_cast<uint64_t>(j) * gs + blockIdx.x] = s;
     }
 }
 
@@ -783,24 +832,24 @@ __device__ __forceinline__ void dot_partials_out(const double* red, uint32_t col
 // previous gate closed the dot2 pass waits for the gate (R1 = [hn1] only,
 // then R2'[u] in region 2).
 template <int F>
-__global__ void __launch_bounds__(kThreads, 2) arnoldi_fused_kernel(FusedArgs a) {
+__global__ void __launch_bounds__(kFThreads, kFCtasPerSM) arnoldi_fused_kernel(FusedArgs a) {
     constexpr int S = FGeo<F>::stages;
-    constexpr uint32_t PAY = Geo<F>::pay, EX = Geo<F>::ex, SB = fstage_bytes<F>();
+    constexpr uint32_t PAY = FBytes<F>::pay, UPAY = FBytes<F>::upay, UEX = FBytes<F>::uex, SB = fstage_bytes<F>();
     extern __shared__ __align__(128) unsigned char smem[];
     const uint32_t cols = a.cols;
     unsigned char* stages = smem;
     uint64_t* full = reinterpret_cast<uint64_t*>(smem + S * SB);
     uint64_t* empty = full + S;
-    double* red = reinterpret_cast<double*>(empty + S);        // [kWarps][cols]
-    double* hsm = red + kWarps * (cols + 1);                    // reduced h / u (+ hn1 at [cols])
+    double* red = reinterpret_cast<double*>(empty + S);        // [kFWarps][cols]
+    double* hsm = red + kFWarps * (cols + 1);                   // reduced h / u (+ hn1 at [cols])
     double* scal = hsm + cols + 1;                              // [hn2]
-    double* nred = scal + 4;                                    // [kWarps] norm partials
-    uint32_t* scratch = reinterpret_cast<uint32_t*>(nred + kConsumers);  // l=21 write: 8 warps x 84 words
-    volatile int* s_gate = reinterpret_cast<volatile int*>(scratch + kConsumerWarps * 84);
+    double* nred = scal + 4;                                    // [kFWarps] norm partials
+    uint32_t* scratch = reinterpret_cast<uint32_t*>(nred + kFWarps);  // l=21 write: 16 warps x 84 words
+    volatile int* s_gate = reinterpret_cast<volatile int*>(scratch + kFWarps * 84);
     if (threadIdx.x == 0) {
         for (int s = 0; s < S; ++s) {
             mbar_init(full + s, 1);
-            mbar_init(empty + s, kConsumerWarps);
+            mbar_init(empty + s, kFWarps);
         }
         fence_barrier_init();
         *s_gate = -1;
@@ -810,17 +859,20 @@ __global__ void __launch_bounds__(kThreads, 2) arnoldi_fused_kernel(FusedArgs a)
     const bool spec = *reinterpret_cast<volatile unsigned*>(a.gate_hist) == 0u;
     if (blockIdx.x == 0 && threadIdx.x == 0) *a.bar_next = 0u;
     __syncthreads();
-    uint64_t s0, s1;
-    cta_steps(a.B.n, s0, s1);
-    const uint32_t steps = static_cast<uint32_t>(s1 - s0);
+    uint64_t r0, r1;
+    fused_rows(a.B.n, r0, r1);
+    const uint32_t lim = static_cast<uint32_t>(r1 - r0);
+    const uint32_t steps = (lim + kFStepRows - 1) / kFStepRows;
     constexpr int kChunkSteps = FGeo<F>::chunk;
-    const uint32_t nch = (steps + kChunkSteps - 1) / kChunkSteps;
+    constexpr uint32_t kChunkRows = kChunkSteps * kFStepRows;
+    const uint32_t nch = (lim + kChunkRows - 1) / kChunkRows;
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
 
-    if (warp == kConsumerWarps) {
+    if (warp == kFWarps) {
         // ---------------- producer: dot1 (rev), update1, [dot2 (rev), update2]
         if (lane != 0) return;
         const uint64_t policy = policy_evict_normal();
+        const uint64_t u0 = r0 / kUnitRows;
         uint32_t it = 0;
         for (int pass = 0; pass < 4; ++pass) {
             if (pass == (spec ? 3 : 2)) {
@@ -830,18 +882,18 @@ __global__ void __launch_bounds__(kThreads, 2) arnoldi_fused_kernel(FusedArgs a)
             const bool rev = (pass & 1) == 0;
             for (uint32_t jj = 0; jj < cols; ++jj) {
                 const uint32_t j = rev ? cols - 1 - jj : jj;
+                const unsigned char* col = a.B.data + j * a.B.col_stride_bytes;
+                const unsigned char* ecol = reinterpret_cast<const unsigned char*>(a.B.exp + j * a.B.exp_col_stride);
                 for (uint32_t ch = 0; ch < nch; ++ch, ++it) {
-                    const uint64_t sb = s0 + ch * kChunkSteps;
-                    const uint32_t cs = static_cast<uint32_t>(min(static_cast<uint64_t>(kChunkSteps), s1 - sb));
+                    const uint32_t ub = ch * (kChunkRows / kUnitRows);
+                    const uint32_t un = min(kChunkRows, lim - ch * kChunkRows) / kUnitRows;
                     const int stage = it % S;
                     mbar_wait(empty + stage, ((it / S) & 1) ^ 1);
-                    mbar_arrive_expect_tx(full + stage, cs * (PAY + EX));
+                    mbar_arrive_expect_tx(full + stage, un * (UPAY + UEX));
                     unsigned char* dst = stages + stage * SB;
-                    bulk_g2s(dst, a.B.data + j * a.B.col_stride_bytes + sb * PAY, cs * PAY, full + stage, policy);
-                    if constexpr (EX > 0)
-                        bulk_g2s(dst + kChunkSteps * PAY,
-                                 reinterpret_cast<const unsigned char*>(a.B.exp + j * a.B.exp_col_stride) + sb * EX,
-                                 cs * EX, full + stage, policy);
+                    bulk_g2s(dst, col + (u0 + ub) * UPAY, un * UPAY, full + stage, policy);
+                    if constexpr (UEX > 0)
+                        bulk_g2s(dst + kChunkSteps * PAY, ecol + (u0 + ub) * UEX, un * UEX, full + stage, policy);
                 }
             }
         }
@@ -852,43 +904,44 @@ __global__ void __launch_bounds__(kThreads, 2) arnoldi_fused_kernel(FusedArgs a)
     FTRACE(0);
     if (a.trace && threadIdx.x == 0) a.trace[32 + 2048 + blockIdx.x] = global_ns();
     double wv[kFusedMaxSteps][4];
+    const uint64_t wend = min(r1, a.B.n);
 #pragma unroll
     for (int s = 0; s < kFusedMaxSteps; ++s) {
-        if (s < static_cast<int>(steps)) load_w(a.w, a.B.n, (s0 + s) * kStepRows + 4u * threadIdx.x, wv[s]);
+        if (s < static_cast<int>(steps)) load_w(a.w, wend, r0 + s * kFStepRows + 4u * threadIdx.x, wv[s]);
         else wv[s][0] = wv[s][1] = wv[s][2] = wv[s][3] = 0.0;
     }
     FTRACE(1);
     uint32_t it = 0;
-    const uint32_t stride = cols + 1;
-    const uint64_t region = static_cast<uint64_t>(gridDim.x) * stride;
-    double* myrow = a.partials + static_cast<uint64_t>(blockIdx.x) * stride;
+    const uint32_t gs = a.gs;
+    const uint64_t region = static_cast<uint64_t>(cols + 1) * gs;
+    double* const P = a.partials;
     const bool cta0 = blockIdx.x == 0;
     unsigned seq = 0;
 
     // dot1 -> h
-    fused_pass<F, true>(cols, steps, nch, stages, full, empty, it, wv, red, hsm);
+    fused_pass<F, true>(cols, lim, nch, stages, full, empty, it, wv, red, hsm);
     FTRACE(2);
     if (a.trace && threadIdx.x == 0) a.trace[32 + blockIdx.x] = global_ns();
-    dot_partials_out(red, cols, myrow);
-    grid_allreduce(a.bar, seq++, a.partials, stride, cols, hsm, a.trace);
+    dot_partials_out(red, cols, P, gs);
+    grid_allreduce(a.bar, seq++, P, gs, cols, hsm, a.trace);
     if (cta0)
-        for (uint32_t j = threadIdx.x; j < cols; j += kConsumers) a.slot[3 + j] = hsm[j];
+        for (uint32_t j = threadIdx.x; j < cols; j += kFConsumers) a.slot[3 + j] = hsm[j];
     FTRACE(3);
     // update1
-    fused_pass<F, false>(cols, steps, nch, stages, full, empty, it, wv, red, hsm);
+    fused_pass<F, false>(cols, lim, nch, stages, full, empty, it, wv, red, hsm);
     FTRACE(4);
     if (a.trace && threadIdx.x == 0) a.trace[32 + 1024 + blockIdx.x] = global_ns();
     const double hn1_part = cta_wnorm2(wv, nred);
-    double* row1 = myrow + region;
+    double* const P1 = P + region;
     if (spec) {
         // speculative dot2 -> u, reduced together with hn1
-        fused_pass<F, true>(cols, steps, nch, stages, full, empty, it, wv, red, hsm);
+        fused_pass<F, true>(cols, lim, nch, stages, full, empty, it, wv, red, hsm);
         FTRACE(5);
-        dot_partials_out(red, cols, row1);
+        dot_partials_out(red, cols, P1, gs);
     }
-    if (threadIdx.x == 0) row1[cols] = hn1_part;
-    if (spec) grid_allreduce(a.bar, seq++, a.partials + region, stride, cols + 1, hsm, a.trace);
-    else grid_allreduce(a.bar, seq++, a.partials + region + cols, stride, 1, hsm + cols);
+    if (threadIdx.x == 0) P1[static_cast<uint64_t>(cols) * gs + blockIdx.x] = hn1_part;
+    if (spec) grid_allreduce(a.bar, seq++, P1, gs, cols + 1, hsm, a.trace);
+    else grid_allreduce(a.bar, seq++, P1 + static_cast<uint64_t>(cols) * gs, gs, 1, hsm + cols);
     FTRACE(6);
     const double hn1 = hsm[cols];
     // gmres.cpp:51 on the device (same IEEE ops as the host)
@@ -901,21 +954,21 @@ __global__ void __launch_bounds__(kThreads, 2) arnoldi_fused_kernel(FusedArgs a)
     double hn2 = hn1;
     if (gate) {
         if (!spec) {
-            fused_pass<F, true>(cols, steps, nch, stages, full, empty, it, wv, red, hsm);
+            fused_pass<F, true>(cols, lim, nch, stages, full, empty, it, wv, red, hsm);
             FTRACE(5);
-            dot_partials_out(red, cols, myrow + 2 * region);
-            grid_allreduce(a.bar, seq++, a.partials + 2 * region, stride, cols, hsm);
+            dot_partials_out(red, cols, P + 2 * region, gs);
+            grid_allreduce(a.bar, seq++, P + 2 * region, gs, cols, hsm);
         }
         if (cta0)
-            for (uint32_t j = threadIdx.x; j < cols; j += kConsumers) a.slot[a.u_off + j] = hsm[j];
+            for (uint32_t j = threadIdx.x; j < cols; j += kFConsumers) a.slot[a.u_off + j] = hsm[j];
         FTRACE(7);
         // update2 (u in hsm)
-        fused_pass<F, false>(cols, steps, nch, stages, full, empty, it, wv, red, hsm);
+        fused_pass<F, false>(cols, lim, nch, stages, full, empty, it, wv, red, hsm);
         FTRACE(8);
         const double p = cta_wnorm2(wv, nred);
-        double* row3 = myrow + 3 * region;
-        if (threadIdx.x == 0) row3[0] = p;
-        grid_allreduce(a.bar, seq++, a.partials + 3 * region, stride, 1, scal, a.trace);
+        double* const P3 = P + 3 * region;
+        if (threadIdx.x == 0) P3[blockIdx.x] = p;
+        grid_allreduce(a.bar, seq++, P3, gs, 1, scal, a.trace);
         hn2 = scal[0];
         if (cta0 && threadIdx.x == 0) a.slot[1] = hn2;
         FTRACE(9);
@@ -923,7 +976,7 @@ __global__ void __launch_bounds__(kThreads, 2) arnoldi_fused_kernel(FusedArgs a)
     if (cta0 && threadIdx.x == 0) *a.gate_hist = gate ? 0u : 1u;
     // v = w / h_next of the last pass, written as the next basis column
     const double scale = 1.0 / sqrt(hn2);
-    fused_write<F>(a, s0, steps, wv, scale, scratch);
+    fused_write<F>(a, r0, r1, steps, wv, scale, scratch);
     FTRACE(10);
 }
 
@@ -946,20 +999,51 @@ unsigned long long* fused_trace_buffer() {
 template <int F>
 size_t fused_smem(uint32_t cols) {
     return FGeo<F>::stages * (fstage_bytes<F>() + 16) +
-           (kWarps * (cols + 1) + (cols + 1) + 4 + kConsumers + 2 * 128) * sizeof(double) + kConsumerWarps * 84 * 4 + 32;
+           (kFWarps * (cols + 1) + (cols + 1) + 4 + kFWarps) * sizeof(double) + kFWarps * 84 * 4 + 32;
+}
+
+// Grid size of the fused kernel (0 when not eligible): one CTA per SM,
+// every CTA's rows within kFusedMaxSteps steps, cols + 1 <= kFConsumers.
+template <int F>
+int fused_grid(uint64_t n, uint32_t max_cols) {
+    if (max_cols + 1 > static_cast<uint32_t>(kFConsumers)) return 0;
+    const size_t smem = fused_smem<F>(max_cols);
+    if (smem > 227 * 1024) return 0;
+    static std::mutex mu;
+    static std::map<std::pair<int, size_t>, int> cache;
+    const auto key = std::make_pair(current_device(), smem);
+    int per_sm = 0;
+    {
+        std::lock_guard<std::mutex> lock(mu);
+        auto it = cache.find(key);
+        if (it != cache.end()) {
+            per_sm = it->second;
+        } else {
+            // the attribute is per kernel, not per size: set the maximum once
+            CBGX_CUDA(cudaFuncSetAttribute(arnoldi_fused_kernel<F>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                           227 * 1024));
+            CBGX_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, arnoldi_fused_kernel<F>, kFThreads, smem));
+            int coop = 0;
+            CBGX_CUDA(cudaDeviceGetAttribute(&coop, cudaDevAttrCooperativeLaunch, current_device()));
+            if (!coop) per_sm = 0;
+            cache.emplace(key, per_sm);
+        }
+    }
+    if (per_sm < 1) return 0;
+    const uint64_t units = (n + kUnitRows - 1) / kUnitRows;
+    const uint64_t G = std::min<uint64_t>(static_cast<uint64_t>(sm_count()) * std::min(per_sm, kFCtasPerSM), std::max<uint64_t>(units, 1));
+    if ((units + G - 1) / G * kUnitRows > static_cast<uint64_t>(kFusedMaxSteps) * kFStepRows) return 0;
+    return static_cast<int>(G);
 }
 
 template <int F> struct FusedLaunch {
     static void run(const cbgx_basis& V, uint32_t cols, const double* w, double* v_out, double* slot,
-                    uint32_t u_off, double eta, Workspace* ws, cudaStream_t st, bool* done) {
-        const size_t smem = fused_smem<F>(cols);
-        allow_smem(arnoldi_fused_kernel<F>);
-        const int per_sm = occupancy(arnoldi_fused_kernel<F>, smem);
-        const uint64_t G = static_cast<uint64_t>(sm_count()) * static_cast<uint64_t>(per_sm);
-        const uint64_t steps = (V.n + kStepRows - 1) / kStepRows;
+                    uint32_t u_off, double eta, uint32_t max_cols, Workspace* ws, cudaStream_t st, bool* done) {
+        // geometry fixed by the solver's capacity so it never changes mid-solve
+        const int grid = fused_grid<F>(V.n, max_cols);
         *done = false;
-        if (per_sm < 1 || steps > G * kFusedMaxSteps) return;  // not eligible: caller uses the split kernels
-        const int grid = static_cast<int>(std::min<uint64_t>(G, steps));
+        if (grid < 1 || cols > max_cols) return;  // not eligible: caller uses the split kernels
+        const size_t smem = fused_smem<F>(max_cols);
         FusedArgs a;
         a.B = view_of(V);
         a.cols = cols;
@@ -970,7 +1054,8 @@ template <int F> struct FusedLaunch {
         a.slot = slot;
         a.u_off = u_off;
         a.eta = eta;
-        a.partials = ws->get_partials(static_cast<size_t>(kRegions) * grid * (cols + 1));
+        a.gs = static_cast<uint32_t>((grid + 1) / 2 * 2);
+        a.partials = ws->get_partials(static_cast<size_t>(kRegions) * a.gs * (cols + 1));
         // two arrival counters used by alternate launches: each launch
         // zeroes the other one (the previous launch has completed)
         unsigned* c = ws->get_counter();
@@ -982,7 +1067,7 @@ template <int F> struct FusedLaunch {
         void* args[] = {&a};
         note_launch();
         CBGX_CUDA(cudaLaunchCooperativeKernel(reinterpret_cast<void*>(arnoldi_fused_kernel<F>), dim3(grid),
-                                              dim3(kThreads), args, smem, st));
+                                              dim3(kFThreads), args, smem, st));
         *done = true;
     }
 };
@@ -1020,15 +1105,7 @@ void launch_basis_write(const cbgx_basis& V, uint64_t j, const double* x, const 
 namespace {
 template <int F> struct FusedProbe {
     static void run(const cbgx_basis& V, uint64_t max_cols, bool* ok) {
-        const size_t smem = fused_smem<F>(static_cast<uint32_t>(max_cols));
-        allow_smem(arnoldi_fused_kernel<F>);
-        int per_sm = 0;
-        CBGX_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, arnoldi_fused_kernel<F>, kThreads, smem));
-        int coop = 0;
-        CBGX_CUDA(cudaDeviceGetAttribute(&coop, cudaDevAttrCooperativeLaunch, current_device()));
-        const uint64_t G = static_cast<uint64_t>(sm_count()) * static_cast<uint64_t>(per_sm);
-        const uint64_t steps = (V.n + kStepRows - 1) / kStepRows;
-        *ok = coop && per_sm >= 1 && steps <= G * kFusedMaxSteps && max_cols + 1 <= static_cast<uint64_t>(kConsumers);
+        *ok = fused_grid<F>(V.n, static_cast<uint32_t>(max_cols)) > 0;
     }
 };
 }  // namespace
@@ -1040,10 +1117,10 @@ bool fused_eligible(const cbgx_basis& V, uint64_t max_cols) {
 }
 
 bool launch_arnoldi_fused(const cbgx_basis& V, uint32_t cols, const double* w, double* v_out, double* slot,
-                          uint32_t u_off, double eta, Workspace* ws, cudaStream_t st) {
+                          uint32_t u_off, double eta, uint32_t max_cols, Workspace* ws, cudaStream_t st) {
     if (cols + 1 > V.capacity) throw Error(CBGX_ERANGE, "basis: cannot write column");
     bool done = false;
-    dispatch_fmt<FusedLaunch>(fmt_of(V), V, cols, w, v_out, slot, u_off, eta, ws, st, &done);
+    dispatch_fmt<FusedLaunch>(fmt_of(V), V, cols, w, v_out, slot, u_off, eta, max_cols, ws, st, &done);
     CBGX_CUDA(cudaGetLastError());
     return done;
 }

@@ -101,7 +101,7 @@ void launch_cgs_update(const cbgx_basis& V, uint64_t first, uint32_t cols, const
 // too large for the register-resident w of a co-resident grid.
 bool fused_eligible(const cbgx_basis& V, uint64_t max_cols);
 bool launch_arnoldi_fused(const cbgx_basis& V, uint32_t cols, const double* w, double* v_out, double* slot,
-                          uint32_t u_off, double eta, Workspace* ws, cudaStream_t st);
+                          uint32_t u_off, double eta, uint32_t max_cols, Workspace* ws, cudaStream_t st);
 void launch_basis_write(const cbgx_basis& V, uint64_t j, const double* x, const ScaleArg& scale,
                         double* v_out, uint64_t* bad, cudaStream_t st);
 void launch_basis_read(const cbgx_basis& V, uint64_t j, uint64_t first, uint64_t count, double* out,

@@ -300,7 +300,7 @@ void Solver::solve(const double* d_b, const double* d_x0, double* d_x, cbgx_hist
                 // the scaled write of column used+1, w register-resident
                 timer.begin(CBGX_PHASE_ORTHO);
                 const bool ok = launch_arnoldi_fused(V_, cols, d_w_, d_v_, sl, static_cast<uint32_t>(kU(m)), cfg_.eta,
-                                                     &ws_, st);
+                                                     static_cast<uint32_t>(m), &ws_, st);
                 timer.end();
                 if (!ok) throw Error(CBGX_EINTERNAL, "fused orthogonalisation became ineligible");
                 count(CBGX_PHASE_ORTHO, 2.0 * cols * bpv * n + 8.0 * n + 8.0 * n + bpv * n);
