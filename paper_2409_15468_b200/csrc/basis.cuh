@@ -158,7 +158,7 @@ struct Codes4 {
 };
 
 __device__ __forceinline__ double signed_i2f(uint32_t mag, uint32_t sgn) {
-    const double d = __uint2double_rn(mag);
+    const double d = u32_to_f64(mag);
     return __hiloint2double(__double2hiint(d) ^ static_cast<int>(sgn), __double2loint(d));
 }
 
@@ -197,12 +197,16 @@ template <int L>
 __device__ __forceinline__ void frsz_update(const Codes4& c, uint32_t e, double h, int h_exp, double w[4]) {
     const int es = static_cast<int>(e) - (L - 2);          // scale's biased exponent
     const int hse = h_exp + es - 1023;                      // exponent of h*scale
-    const bool ok = es > 0 && (h == 0.0 || (h_exp != 0 && hse >= 1 && hse <= 2046));
+    // hse <= 1994: 2^52 * hs stays finite, so c0 below is exact
+    const bool ok = es > 0 && (h == 0.0 || (h_exp != 0 && hse >= 1 && hse <= 1994));
     if (__builtin_expect(ok, 1)) {
         const double hs = __dmul_rn(h, __hiloint2double(es << 20, 0));
+        const double c0 = __dmul_rn(hs, -0x1p52);
 #pragma unroll
         for (int k = 0; k < 4; ++k) {
-            const double p = __dmul_rn(__uint2double_rn(c.mag[k]), hs);
+            // RN(mag * hs) as one FMA on the FP64 pipe: (2^52 + mag) * hs
+            // - 2^52 * hs is exactly mag * hs before the single rounding
+            const double p = fma(__hiloint2double(0x43300000, static_cast<int>(c.mag[k])), hs, c0);
             w[k] = __dsub_rn(w[k], __hiloint2double(__double2hiint(p) ^ static_cast<int>(c.sgn[k]), __double2loint(p)));
         }
         return;

@@ -98,10 +98,18 @@ __device__ __forceinline__ double decode_any(uint64_t code, uint32_t e_max, uint
     return __longlong_as_double(static_cast<long long>((neg << 63) | (static_cast<uint64_t>(e) << 52) | f52));
 }
 
+// Exact u32 -> double on the FP64 pipe: (2^52 + m) - 2^52. The conversion
+// instruction (I2F.F64.U32) issues on the XU pipe, 16 lanes/clk/SM, which
+// the FRSZ2 decode saturated (ncu: XU pipe 74% in the fused CGS kernel);
+// DADD runs at the FP64 rate.
+__device__ __forceinline__ double u32_to_f64(uint32_t m) {
+    return __dsub_rn(__hiloint2double(0x43300000, static_cast<int>(m)), 0x1p52);
+}
+
 // Per-block decode context for the fixed-rate formats (L <= 32).
 // Fast path (e_max > L-2, i.e. no decoded value can fall below 2^-1022):
 //   value = (double)mag * 2^(e_max-1023-(L-2)), exact (power-of-two scale of
-//   an integer < 2^31), sign folded into the scale -> I2F + LOP3 + DMUL.
+//   an integer < 2^31), sign folded into the scale -> DADD + LOP3 + DMUL.
 // Slow path (e_max <= L-2): the integer exponent-add with the reference's
 // flush of e <= 0 to a signed zero (kernels_avx2.cpp:83-118 formulation,
 // bit-identical to decode_one).
@@ -120,7 +128,7 @@ struct BlockDecoder {
         constexpr uint32_t kMagMask = (L == 32) ? 0x7FFFFFFFu : ((1u << (L - 1)) - 1u);
         const uint32_t mag = code & kMagMask;
         const uint32_t sbit = (code >> (L - 1)) << 31;
-        const double dm = __uint2double_rn(mag);
+        const double dm = u32_to_f64(mag);
         if (fast) {
             return __dmul_rn(dm, __hiloint2double(static_cast<int>(scale_hi | sbit), 0));
         }
