@@ -299,6 +299,10 @@ int cbgx_gmres_solve_host(uint64_t n, const uint64_t* row_ptrs, const uint64_t* 
                           const double* values, const double* b, const double* x0,
                           const cbgx_gmres_config* cfg, double* x_out, cbgx_history* hist,
                           cbgx_solve_stats* stats);
+/* cbgx_gmres_solve_host keeps its device staging buffers, stream and last
+ * solver (basis + workspaces) between calls on the same device; this frees
+ * them. */
+int cbgx_host_cache_release(void);
 
 /* Debug: globaltimer stamps of CTA 0 in the last fused orthogonalisation
  * launch (requires CBGX_TRACE_FUSED=1 in the environment). */

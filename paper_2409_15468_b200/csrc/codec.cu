@@ -3,13 +3,8 @@
 // Reference semantics: frsz2.cpp:155-266 (compress, compress_block,
 // decompress*, LSB-first packing :42-71) and kernels.hpp:18-58.
 //
-// Fast path (block size 32, l in {16, 21, 32}): one warp per 32-value block,
-// lane j owns value j. The block exponent is one warp max-reduction
-// (__reduce_max_sync -> CREDUX), codes are produced in registers and packed
-// with shuffles into coalesced stores: 128 B (l=32), 64 B (l=16) or 84 B
-// (l=21: word w of the block's bit stream gathers the <= 3 codes that overlap
-// it). Decompression is the mirror image. Each warp keeps kUnroll blocks in
-// flight so enough loads are outstanding to saturate HBM.
+// Fast path (block size 32, l in {16, 21, 32}): a warp step is 4 blocks,
+// each lane owns 4 consecutive values of one block (see compress4_kernel).
 //
 // Generic path (any block size, 2 <= l <= 64): one thread per block on
 // encode (blocks own disjoint words, so no atomics), one thread per value on
@@ -26,109 +21,171 @@ namespace {
 
 constexpr int kThreads = 256;
 constexpr int kWarps = kThreads / 32;
-constexpr int kUnroll = 4;
 
-template <int L>
-__device__ __forceinline__ void store_block(uint32_t code, uint32_t* __restrict__ words, int lane) {
-    if constexpr (L == 32) {
-        words[lane] = code;
-    } else if constexpr (L == 16) {
-        const uint32_t hi = __shfl_down_sync(0xFFFFFFFFu, code, 1);
-        if ((lane & 1) == 0) words[lane >> 1] = code | (hi << 16);
-    } else {
-        static_assert(L == 21, "fast codec handles l in {16, 21, 32}");
-        // Output word w covers stream bits [32w, 32w+32); codes j0..j0+2
-        // with j0 = floor(32w/21) overlap it.
-        const int w = lane;
-        const int j0 = (32 * w) / 21;
-        const uint32_t c0 = __shfl_sync(0xFFFFFFFFu, code, j0 & 31);
-        const uint32_t c1 = __shfl_sync(0xFFFFFFFFu, code, (j0 + 1) & 31);
-        const uint32_t c2 = __shfl_sync(0xFFFFFFFFu, code, (j0 + 2) & 31);
-        const uint64_t win = static_cast<uint64_t>(c0) |
-                             (static_cast<uint64_t>(j0 + 1 < 32 ? c1 : 0u) << 21) |
-                             (static_cast<uint64_t>(j0 + 2 < 32 ? c2 : 0u) << 42);
-        if (w < 21) words[w] = static_cast<uint32_t>(win >> (32 * w - 21 * j0));
-    }
-}
+// ---- 4-values-per-lane codec (the fast path) -----------------------------
+// A warp step covers 128 rows = 4 blocks; lane l owns rows 4l..4l+3 (all in
+// block l/8), so every lane moves 16-32 B per global access: 2x16 B of fp64
+// and 16 B (l=32) / 8 B (l=16) of codes, the block exponent reduced over 8
+// lanes with 3 shuffles. l=21 codes are assembled (compress) or unpacked
+// (decompress) through an 84-word per-warp shared-memory window so the
+// global side stays coalesced. kSteps warp steps are in flight per
+// iteration to keep enough bytes outstanding per SM.
+constexpr int kSteps = 4;
 
-template <int L>
-__device__ __forceinline__ uint32_t load_code(const uint32_t* __restrict__ words, int lane) {
-    if constexpr (L == 32) {
-        return __ldg(words + lane);
-    } else if constexpr (L == 16) {
-        return __ldg(reinterpret_cast<const uint16_t*>(words) + lane);
-    } else {
-        const uint32_t mine = lane < 21 ? __ldg(words + lane) : 0u;
-        const int bit = 21 * lane;
-        const int q = bit >> 5;
-        const uint32_t w0 = __shfl_sync(0xFFFFFFFFu, mine, q);
-        const uint32_t w1 = __shfl_sync(0xFFFFFFFFu, mine, (q + 1) & 31);
-        const uint64_t win = (static_cast<uint64_t>(w1) << 32) | w0;
-        return static_cast<uint32_t>(win >> (bit & 31)) & 0x1FFFFFu;
-    }
-}
-
-// Encodes blocks [0, nb_write) of s*x (rows >= n read as 0.0 -- the tail
-// zero padding of frsz2.cpp:187-191).
 template <int L, bool kScale>
 __global__ void __launch_bounds__(kThreads)
-compress32_kernel(const double* __restrict__ x, uint64_t n, uint64_t nb_write,
-                  uint32_t* __restrict__ exps, uint32_t* __restrict__ payload,
-                  ScaleArg scale, double* __restrict__ v_out,
-                  unsigned long long* __restrict__ bad) {
+compress4_kernel(const double* __restrict__ x, uint64_t n, uint64_t nb_write,
+                 uint32_t* __restrict__ exps, uint32_t* __restrict__ payload,
+                 ScaleArg scale, double* __restrict__ v_out,
+                 unsigned long long* __restrict__ bad) {
+    __shared__ uint32_t wbuf_all[kWarps][84];
     const int lane = threadIdx.x & 31;
+    uint32_t* wbuf = wbuf_all[threadIdx.x >> 5];
     const double s = kScale ? scale.value() : 1.0;
+    const uint64_t nsteps = (nb_write + 3) / 4;
     const uint64_t warp = (static_cast<uint64_t>(blockIdx.x) * kWarps) + (threadIdx.x >> 5);
     const uint64_t nwarps = static_cast<uint64_t>(gridDim.x) * kWarps;
-    for (uint64_t b0 = warp * kUnroll; b0 < nb_write; b0 += nwarps * kUnroll) {
-        double v[kUnroll];
+    for (uint64_t s0 = warp * kSteps; s0 < nsteps; s0 += nwarps * kSteps) {
+        double v[kSteps][4];
 #pragma unroll
-        for (int u = 0; u < kUnroll; ++u) {
-            const uint64_t row = (b0 + u) * 32 + lane;
-            v[u] = (b0 + u < nb_write && row < n) ? x[row] : 0.0;
+        for (int u = 0; u < kSteps; ++u) {
+            const uint64_t r = (s0 + u) * 128 + 4u * lane;
+            if (s0 + u < nsteps && r + 3 < n) {
+                const double2 a = __ldcs(reinterpret_cast<const double2*>(x + r));
+                const double2 b = __ldcs(reinterpret_cast<const double2*>(x + r + 2));
+                v[u][0] = a.x; v[u][1] = a.y; v[u][2] = b.x; v[u][3] = b.y;
+            } else {
+#pragma unroll
+                for (int k = 0; k < 4; ++k) v[u][k] = (s0 + u < nsteps && r + k < n) ? x[r + k] : 0.0;
+            }
         }
 #pragma unroll
-        for (int u = 0; u < kUnroll; ++u) {
-            const uint64_t b = b0 + u;
-            if (b >= nb_write) break;  // warp-uniform
-            const uint64_t row = b * 32 + lane;
-            double val = v[u];
-            if (kScale) {
-                val = __dmul_rn(val, s);
-                if (v_out && row < n) v_out[row] = val;
+        for (int u = 0; u < kSteps; ++u) {
+            if (s0 + u >= nsteps) break;  // warp-uniform
+            const uint64_t r = (s0 + u) * 128 + 4u * lane;
+            const uint64_t blk = r / 32;
+            const bool live = blk < nb_write;  // 8-lane-uniform
+            uint32_t e = 0;
+#pragma unroll
+            for (int k = 0; k < 4; ++k) {
+                if (kScale) v[u][k] = __dmul_rn(v[u][k], s);
+                const uint32_t ek = exp_field(v[u][k]);
+                if (ek == 0x7FFu && r + k < n) atomicMin(bad, static_cast<unsigned long long>(r + k));
+                e = max(e, ek);
             }
-            const uint32_t e = exp_field(val);
-            if (e == 0x7FFu) atomicMin(bad, static_cast<unsigned long long>(row));
-            const uint32_t e_max = __reduce_max_sync(0xFFFFFFFFu, e);
-            const uint32_t code = encode32<L>(val, e_max);
-            if (lane == 0) exps[b] = e_max;
-            store_block<L>(code, payload + b * L, lane);
+            if (kScale && v_out) {
+                if (r + 3 < n) {
+                    reinterpret_cast<double2*>(v_out + r)[0] = make_double2(v[u][0], v[u][1]);
+                    reinterpret_cast<double2*>(v_out + r)[1] = make_double2(v[u][2], v[u][3]);
+                } else {
+#pragma unroll
+                    for (int k = 0; k < 4; ++k)
+                        if (r + k < n) v_out[r + k] = v[u][k];
+                }
+            }
+            e = max(e, __shfl_xor_sync(0xFFFFFFFFu, e, 1));
+            e = max(e, __shfl_xor_sync(0xFFFFFFFFu, e, 2));
+            e = max(e, __shfl_xor_sync(0xFFFFFFFFu, e, 4));
+            uint32_t c[4];
+#pragma unroll
+            for (int k = 0; k < 4; ++k) c[k] = encode32<L>(v[u][k], e);
+            if (live && (lane & 7) == 0) exps[blk] = e;
+            if constexpr (L == 32) {
+                if (live) reinterpret_cast<uint4*>(payload)[r / 4] = make_uint4(c[0], c[1], c[2], c[3]);
+            } else if constexpr (L == 16) {
+                if (live) reinterpret_cast<uint2*>(payload)[r / 4] = make_uint2(c[0] | (c[1] << 16), c[2] | (c[3] << 16));
+            } else {
+                for (int i = lane; i < 84; i += 32) wbuf[i] = 0u;
+                __syncwarp();
+                const uint32_t bit0 = (lane >> 3) * 672u + (lane & 7) * 84u;
+#pragma unroll
+                for (int k = 0; k < 4; ++k) {
+                    const uint32_t b = bit0 + 21u * k, q = b >> 5, sh = b & 31u;
+                    atomicOr(wbuf + q, c[k] << sh);
+                    if (sh > 11) atomicOr(wbuf + q + 1, c[k] >> (32 - sh));
+                }
+                __syncwarp();
+                const uint64_t b0 = (s0 + u) * 4;  // first block of the step
+                uint32_t* dst = payload + b0 * 21;
+                const uint64_t words = (min(nb_write, b0 + 4) - b0) * 21;
+                for (int i = lane; i < 84; i += 32)
+                    if (static_cast<uint64_t>(i) < words) dst[i] = wbuf[i];
+                __syncwarp();
+            }
         }
     }
 }
 
 template <int L>
 __global__ void __launch_bounds__(kThreads)
-decompress32_kernel(const uint32_t* __restrict__ exps, const uint32_t* __restrict__ payload,
-                    uint64_t n, double* __restrict__ out) {
+decompress4_kernel(const uint32_t* __restrict__ exps, const uint32_t* __restrict__ payload,
+                   uint64_t n, double* __restrict__ out) {
+    __shared__ uint32_t wbuf_all[kWarps][84 + 4];
     const int lane = threadIdx.x & 31;
+    uint32_t* wbuf = wbuf_all[threadIdx.x >> 5];
     const uint64_t nb = (n + 31) / 32;
+    const uint64_t nsteps = (nb + 3) / 4;
     const uint64_t warp = (static_cast<uint64_t>(blockIdx.x) * kWarps) + (threadIdx.x >> 5);
     const uint64_t nwarps = static_cast<uint64_t>(gridDim.x) * kWarps;
-    for (uint64_t b0 = warp * kUnroll; b0 < nb; b0 += nwarps * kUnroll) {
-        uint32_t code[kUnroll], em[kUnroll];
+    for (uint64_t s0 = warp * kSteps; s0 < nsteps; s0 += nwarps * kSteps) {
+        uint32_t em[kSteps];
+        uint4 cw[kSteps];  // l=32: 4 codes; l=16: x,y = 4 packed codes; l=21: 3 loaded words
 #pragma unroll
-        for (int u = 0; u < kUnroll; ++u) {
-            const uint64_t b = b0 + u < nb ? b0 + u : nb - 1;
-            em[u] = __ldg(exps + b);
-            code[u] = load_code<L>(payload + b * L, lane);
+        for (int u = 0; u < kSteps; ++u) {
+            const uint64_t r = (s0 + u) * 128 + 4u * lane;
+            const uint64_t blk = min(r / 32, nb - 1);
+            em[u] = __ldg(exps + blk);
+            if constexpr (L == 32) {
+                cw[u] = r / 32 < nb ? __ldcs(reinterpret_cast<const uint4*>(payload) + r / 4) : make_uint4(0, 0, 0, 0);
+            } else if constexpr (L == 16) {
+                const uint2 t = r / 32 < nb ? __ldcs(reinterpret_cast<const uint2*>(payload) + r / 4) : make_uint2(0, 0);
+                cw[u] = make_uint4(t.x, t.y, 0, 0);
+            } else {
+                const uint64_t b0 = (s0 + u) * 4;
+                const uint64_t words = b0 < nb ? (min(nb, b0 + 4) - b0) * 21 : 0;
+                const uint32_t* src = payload + b0 * 21;
+                cw[u].x = static_cast<uint64_t>(lane) < words ? __ldcs(src + lane) : 0u;
+                cw[u].y = static_cast<uint64_t>(lane + 32) < words ? __ldcs(src + lane + 32) : 0u;
+                cw[u].z = static_cast<uint64_t>(lane + 64) < words && lane + 64 < 84 ? __ldcs(src + lane + 64) : 0u;
+            }
         }
 #pragma unroll
-        for (int u = 0; u < kUnroll; ++u) {
-            const uint64_t row = (b0 + u) * 32 + lane;
+        for (int u = 0; u < kSteps; ++u) {
+            if (s0 + u >= nsteps) break;  // warp-uniform
+            const uint64_t r = (s0 + u) * 128 + 4u * lane;
+            uint32_t code[4];
+            if constexpr (L == 32) {
+                code[0] = cw[u].x; code[1] = cw[u].y; code[2] = cw[u].z; code[3] = cw[u].w;
+            } else if constexpr (L == 16) {
+                code[0] = cw[u].x & 0xFFFFu; code[1] = cw[u].x >> 16;
+                code[2] = cw[u].y & 0xFFFFu; code[3] = cw[u].y >> 16;
+            } else {
+                wbuf[lane] = cw[u].x;
+                wbuf[lane + 32] = cw[u].y;
+                if (lane + 64 < 88) wbuf[lane + 64] = lane + 64 < 84 ? cw[u].z : 0u;
+                __syncwarp();
+                const uint32_t bit = (lane >> 3) * 672u + (lane & 7) * 84u;
+                const uint32_t q = bit >> 5, sh = bit & 31u;
+                const uint32_t w0 = wbuf[q], w1 = wbuf[q + 1], w2 = wbuf[q + 2], w3 = wbuf[q + 3];
+                __syncwarp();
+                const uint32_t o1 = sh + 21, o2 = sh + 42, o3 = sh + 63;
+                code[0] = __funnelshift_r(w0, w1, sh) & 0x1FFFFFu;
+                code[1] = (o1 < 32 ? __funnelshift_r(w0, w1, o1) : __funnelshift_r(w1, w2, o1 - 32)) & 0x1FFFFFu;
+                code[2] = (o2 < 64 ? __funnelshift_r(w1, w2, o2 - 32) : __funnelshift_r(w2, w3, o2 - 64)) & 0x1FFFFFu;
+                code[3] = (o3 < 64 ? __funnelshift_r(w1, w2, o3 - 32) : __funnelshift_r(w2, w3, o3 - 64)) & 0x1FFFFFu;
+            }
             const BlockDecoder<L> dec(em[u]);
-            const double val = dec(code[u]);
-            if (b0 + u < nb && row < n) out[row] = val;
+            double v[4];
+#pragma unroll
+            for (int k = 0; k < 4; ++k) v[k] = dec(code[k]);
+            if (r + 3 < n) {
+                __stcs(reinterpret_cast<double2*>(out + r), make_double2(v[0], v[1]));
+                __stcs(reinterpret_cast<double2*>(out + r) + 1, make_double2(v[2], v[3]));
+            } else {
+#pragma unroll
+                for (int k = 0; k < 4; ++k)
+                    if (r + k < n) out[r + k] = v[k];
+            }
         }
     }
 }
@@ -232,12 +289,12 @@ void launch_compress(const double* x, uint64_t n, uint64_t nb_write, uint32_t bs
     if (nb_write == 0) return;
     auto* badp = reinterpret_cast<unsigned long long*>(bad);
     if (fast_path(bs, l)) {
-        const int grid = grid_for(nb_write, kWarps * kUnroll);
+        const int grid = grid_for((nb_write + 3) / 4, kWarps * kSteps);
         const bool sc = scale.src != nullptr;
 #define CBGX_LAUNCH_C(LL)                                                                    \
-    if (sc) CBGX_K(compress32_kernel<LL, true><<<grid, kThreads, 0, st>>>(x, n, nb_write, exps, payload, \
+    if (sc) CBGX_K(compress4_kernel<LL, true><<<grid, kThreads, 0, st>>>(x, n, nb_write, exps, payload, \
                                                                    scale, v_out, badp)); \
-    else CBGX_K(compress32_kernel<LL, false><<<grid, kThreads, 0, st>>>(x, n, nb_write, exps, payload,   \
+    else CBGX_K(compress4_kernel<LL, false><<<grid, kThreads, 0, st>>>(x, n, nb_write, exps, payload,   \
                                                                  ScaleArg{}, nullptr, badp))
         if (l == 32) { CBGX_LAUNCH_C(32); }
         else if (l == 16) { CBGX_LAUNCH_C(16); }
@@ -258,10 +315,10 @@ void launch_decompress(const uint32_t* exps, const uint32_t* payload, uint64_t n
     validate(bs, l);
     if (count == 0) return;
     if (fast_path(bs, l) && first == 0 && count == n) {
-        const int grid = grid_for((n + 31) / 32, kWarps * kUnroll);
-        if (l == 32) CBGX_K(decompress32_kernel<32><<<grid, kThreads, 0, st>>>(exps, payload, n, out));
-        else if (l == 16) CBGX_K(decompress32_kernel<16><<<grid, kThreads, 0, st>>>(exps, payload, n, out));
-        else CBGX_K(decompress32_kernel<21><<<grid, kThreads, 0, st>>>(exps, payload, n, out));
+        const int grid = grid_for(((n + 31) / 32 + 3) / 4, kWarps * kSteps);
+        if (l == 32) CBGX_K(decompress4_kernel<32><<<grid, kThreads, 0, st>>>(exps, payload, n, out));
+        else if (l == 16) CBGX_K(decompress4_kernel<16><<<grid, kThreads, 0, st>>>(exps, payload, n, out));
+        else CBGX_K(decompress4_kernel<21><<<grid, kThreads, 0, st>>>(exps, payload, n, out));
     } else {
         CBGX_K(decompress_generic_kernel<<<grid_for(count, 256), 256, 0, st>>>(
             exps, payload, bs, l, (static_cast<uint64_t>(bs) * l + 31) / 32, first, count, out));

@@ -68,6 +68,7 @@ unsigned* Workspace::get_counter() {
     if (!counters) {
         CBGX_CUDA(cudaMalloc(&counters, kCounters * sizeof(unsigned)));
         CBGX_CUDA(cudaMemset(counters, 0, kCounters * sizeof(unsigned)));
+        CBGX_CUDA(cudaStreamSynchronize(nullptr));  // users may launch on non-blocking streams
     }
     return counters;
 }
@@ -112,7 +113,10 @@ int cbgx_memcpy(void* dst, const void* src, uint64_t bytes, int kind) {
 
 int cbgx_memset(void* d_ptr, int value, uint64_t bytes) {
     return guard([&] {
-        if (bytes) CBGX_CUDA(cudaMemset(d_ptr, value, bytes));
+        if (bytes) {
+            CBGX_CUDA(cudaMemset(d_ptr, value, bytes));
+            CBGX_CUDA(cudaStreamSynchronize(nullptr));  // complete before any stream uses it
+        }
     });
 }
 

@@ -16,6 +16,8 @@
 #include <chrono>
 #include <cmath>
 #include <cstring>
+#include <memory>
+#include <mutex>
 #include <string>
 
 #include "basis.cuh"
@@ -134,27 +136,7 @@ Solver::Solver(const cbgx_csr& A, const cbgx_gmres_config& cfg, Comm* comm, Halo
     if (!halo && A.n_rows != A.n_cols) throw Error(CBGX_EINVAL, "gmres: matrix must be square");
     (void)fmt_from_cfg(cfg);
     ws_.device = current_device();
-    if (A_.max_row_nnz == 0) A_.max_row_nnz = csr_max_row_nnz(A_, nullptr);
-    // SELL-32 copy of A for coalesced SpMV when device memory allows (the
-    // basis is allocated below, so leave room for it).
-    // Measured on B200: SELL wins for long rows (27-pt: 4.8 vs 5.4 ms/solve
-    // of SpMV at 128^3); the batched CSR kernel wins for 7-pt rows.
-    // Staged (TMA bulk-copy) CSR SpMV when every row tile fits a stage;
-    // else a SELL-32 copy for long rows, else the plain CSR kernel.
-    // Measured on B200 (scripts/spmv_micro.py): staged wins for short rows
-    // (256-row tiles: 7-pt 128^3 57 vs 65 us, 256^3 93% vs 81% of HBM peak);
-    // for long rows (27-pt, 64-row tiles) SELL-32 is kept.
-    if (!(cfg.flags & CBGX_SOLVER_NO_TMA_SPMV)) tile_rows_ = plan_spmv_tiles(A_, nullptr);
-    if (tile_rows_ && tile_rows_ < 256 && !(cfg.flags & CBGX_SOLVER_NO_SELL) && A_.max_row_nnz >= 16) tile_rows_ = 0;
-    if (!tile_rows_ && !(cfg.flags & CBGX_SOLVER_NO_SELL) && A_.max_row_nnz >= 16) {
-        uint64_t db = 0, eb = 0;
-        cbgx_basis tmp{};
-        cbgx_basis_layout(cfg.format_kind, cfg.bit_length, n_, cfg.restart + 1, &tmp, &db, &eb);
-        size_t free_b = 0, total_b = 0;
-        CBGX_CUDA(cudaMemGetInfo(&free_b, &total_b));
-        const double after_basis = static_cast<double>(free_b) - static_cast<double>(db + eb) - 64.0 * n_ * 8;
-        if (after_basis > 0) sell_ = build_sell(A_, 0.8 * after_basis / static_cast<double>(free_b), nullptr);
-    }
+    setup_matrix(true, nullptr);
     const uint64_t m = cfg.restart;
     uint64_t data_bytes = 0, exp_bytes = 0;
     const int st = cbgx_basis_layout(cfg.format_kind, cfg.bit_length, n_, m + 1, &V_, &data_bytes, &exp_bytes);
@@ -176,6 +158,42 @@ Solver::Solver(const cbgx_csr& A, const cbgx_gmres_config& cfg, Comm* comm, Halo
     CBGX_CUDA(cudaMemset(d_scal_, 0, scal * sizeof(double)));
     CBGX_CUDA(cudaMallocHost(&h_pinned_, scal * sizeof(double)));
     for (auto& e : step_ev_) CBGX_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+    // The zero-fills above run on the legacy stream; solves may run on a
+    // non-blocking stream that does not order after it.
+    CBGX_CUDA(cudaStreamSynchronize(nullptr));
+}
+
+// Matrix-dependent SpMV state: longest row, staged-tile plan, SELL-32 copy.
+// Staged (TMA bulk-copy) CSR SpMV when every 256-row tile fits a stage
+// (measured on B200, scripts/spmv_micro.py: 7-pt 128^3 57 vs 65 us, 256^3
+// 93% vs 81% of HBM peak); for long rows a SELL-32 copy when memory allows
+// (27-pt 128^3: 4.8 vs 5.4 ms/solve of SpMV), else staged with smaller
+// tiles, else the plain CSR kernel.
+void Solver::setup_matrix(bool before_basis, cudaStream_t st) {
+    sell_.reset();
+    tile_rows_ = 0;
+    if (A_.max_row_nnz == 0) A_.max_row_nnz = csr_max_row_nnz(A_, st);
+    uint32_t plan = 0;
+    if (!(cfg_.flags & CBGX_SOLVER_NO_TMA_SPMV)) plan = plan_spmv_tiles(A_, st);
+    if (plan == 256) tile_rows_ = plan;
+    if (!tile_rows_ && !(cfg_.flags & CBGX_SOLVER_NO_SELL) && A_.max_row_nnz >= 16) {
+        uint64_t db = 0, eb = 0;
+        if (before_basis) {
+            cbgx_basis tmp{};
+            cbgx_basis_layout(cfg_.format_kind, cfg_.bit_length, n_, cfg_.restart + 1, &tmp, &db, &eb);
+        }
+        size_t free_b = 0, total_b = 0;
+        CBGX_CUDA(cudaMemGetInfo(&free_b, &total_b));
+        const double after_basis = static_cast<double>(free_b) - static_cast<double>(db + eb) - 64.0 * n_ * 8;
+        if (after_basis > 0) sell_ = build_sell(A_, 0.8 * after_basis / static_cast<double>(free_b), st);
+    }
+    if (!tile_rows_ && !sell_) tile_rows_ = plan;  // no SELL copy (memory): staged if any tile fits
+}
+
+void Solver::rebind(const cbgx_csr& A, cudaStream_t st) {
+    if (A.n_rows != n_ || A.n_cols != A_.n_cols) throw Error(CBGX_EINVAL, "solver: rebind needs the same shape");
+    A_ = A;
+    setup_matrix(false, st);
 }
 
 void Solver::collect_phases(double* ms, size_t count) {
@@ -477,6 +495,81 @@ cbgx_gmres_config checked(const cbgx_gmres_config* cfg) {
     return *cfg;
 }
 
+
+// Per-device state kept between cbgx_gmres_solve_host calls: the staging
+// buffers (grown to the largest problem seen), a stream, and the last
+// solver. Every call still copies its host inputs and result; only the
+// allocations are reused (cudaMalloc/cudaFree, pinned allocations and the
+// basis set-up are what a fresh call would otherwise pay). Released by
+// cbgx_host_cache_release.
+struct HostSolveCache {
+    std::mutex mu;
+    cudaStream_t st = nullptr;
+    uint64_t cap_n = 0, cap_nnz = 0;
+    uint64_t* d_rp64 = nullptr;
+    uint64_t* d_ci64 = nullptr;
+    double* d_va = nullptr;
+    double* d_b = nullptr;
+    double* d_x0 = nullptr;
+    double* d_x = nullptr;
+    int32_t* d_ci = nullptr;
+    int32_t* d_rp32 = nullptr;
+    uint64_t* d_bad = nullptr;
+    uint64_t* h_bad = nullptr;
+    std::unique_ptr<Solver> solver;
+    void free_buffers() {
+        for (void* p : {static_cast<void*>(d_rp64), static_cast<void*>(d_ci64), static_cast<void*>(d_va),
+                        static_cast<void*>(d_b), static_cast<void*>(d_x0), static_cast<void*>(d_x),
+                        static_cast<void*>(d_ci), static_cast<void*>(d_rp32), static_cast<void*>(d_bad)})
+            if (p) cudaFree(p);
+        d_rp64 = d_ci64 = d_bad = nullptr;
+        d_va = d_b = d_x0 = d_x = nullptr;
+        d_ci = d_rp32 = nullptr;
+        cap_n = cap_nnz = 0;
+    }
+    void release() {
+        solver.reset();
+        free_buffers();
+        if (h_bad) cudaFreeHost(h_bad);
+        h_bad = nullptr;
+        if (st) cudaStreamDestroy(st);
+        st = nullptr;
+    }
+    void ensure(uint64_t n, uint64_t nnz, bool wide) {
+        (void)wide;
+        if (!st) CBGX_CUDA(cudaStreamCreateWithFlags(&st, cudaStreamNonBlocking));
+        if (!h_bad) CBGX_CUDA(cudaMallocHost(&h_bad, sizeof(uint64_t)));
+        if (n <= cap_n && nnz <= cap_nnz && d_bad) return;
+        solver.reset();  // it points into the buffers
+        free_buffers();
+        const uint64_t N = std::max<uint64_t>(n, 1), Z = std::max<uint64_t>(nnz, 1);
+        CBGX_CUDA(cudaMalloc(&d_rp64, (N + 1) * 8));
+        CBGX_CUDA(cudaMalloc(&d_ci64, Z * 8));
+        CBGX_CUDA(cudaMalloc(&d_va, Z * 8));
+        CBGX_CUDA(cudaMalloc(&d_b, N * 8));
+        CBGX_CUDA(cudaMalloc(&d_x0, N * 8));
+        CBGX_CUDA(cudaMalloc(&d_x, N * 8));
+        CBGX_CUDA(cudaMalloc(&d_ci, Z * 4));
+        CBGX_CUDA(cudaMalloc(&d_rp32, (N + 1) * 4));
+        CBGX_CUDA(cudaMalloc(&d_bad, 8));
+        cap_n = n;
+        cap_nnz = nnz;
+    }
+};
+
+bool same_config(const cbgx_gmres_config& a, const cbgx_gmres_config& b) {
+    return a.restart == b.restart && a.target_rrn == b.target_rrn && a.max_total_iterations == b.max_total_iterations &&
+           a.eta == b.eta && a.format_kind == b.format_kind && a.bit_length == b.bit_length &&
+           a.reduction == b.reduction && a.flags == b.flags;
+}
+
+HostSolveCache& host_cache() {
+    static HostSolveCache* caches = new HostSolveCache[64];  // never destroyed: no CUDA calls at exit
+    const int d = current_device();
+    if (d < 0 || d >= 64) throw Error(CBGX_EINVAL, "device index out of range");
+    return caches[d];
+}
+
 }  // namespace
 
 extern "C" {
@@ -525,54 +618,45 @@ int cbgx_gmres_solve_host(uint64_t n, const uint64_t* row_ptrs, const uint64_t* 
         if (n > 0x7FFFFFFFull) throw Error(CBGX_EINVAL, "gmres: n must fit int32 column indices");
         const uint64_t nnz = row_ptrs[n];
         const bool wide = nnz > 0x7FFFFFFFull;
+        HostSolveCache& H = host_cache();
+        std::lock_guard<std::mutex> lock(H.mu);
+        H.ensure(n, nnz, wide);
+        cudaStream_t st = H.st;
         // Stream-ordered staging: the size_t CSR of the reference
         // (CsrMatrix, sparse.hpp:17-26) goes over as-is and is narrowed on the
         // device (int32 columns, int32/int64 row offsets).
-        cudaStream_t st = nullptr;
-        CBGX_CUDA(cudaStreamCreateWithFlags(&st, cudaStreamNonBlocking));
-        std::vector<void*> bufs;
-        auto alloc = [&](size_t bytes) {
-            void* p = nullptr;
-            CBGX_CUDA(cudaMallocAsync(&p, std::max<size_t>(bytes, 8), st));
-            bufs.push_back(p);
-            return p;
-        };
-        auto cleanup = [&] {
-            for (void* p : bufs) cudaFreeAsync(p, st);
-            cudaStreamSynchronize(st);
-            cudaStreamDestroy(st);
-        };
-        try {
-            auto* d_rp64 = static_cast<uint64_t*>(alloc((n + 1) * 8));
-            auto* d_ci64 = static_cast<uint64_t*>(alloc(nnz * 8));
-            auto* d_va = static_cast<double*>(alloc(nnz * 8));
-            auto* d_b = static_cast<double*>(alloc(n * 8));
-            auto* d_x0 = static_cast<double*>(alloc(n * 8));
-            auto* d_x = static_cast<double*>(alloc(n * 8));
-            auto* d_ci = static_cast<int32_t*>(alloc(nnz * 4));
-            void* d_rp = wide ? static_cast<void*>(d_rp64) : alloc((n + 1) * 4);
-            auto* d_bad = static_cast<uint64_t*>(alloc(8));
-            CBGX_CUDA(cudaMemsetAsync(d_bad, 0, 8, st));
-            CBGX_CUDA(cudaMemcpyAsync(d_rp64, row_ptrs, (n + 1) * 8, cudaMemcpyHostToDevice, st));
-            CBGX_CUDA(cudaMemcpyAsync(d_ci64, col_idx, nnz * 8, cudaMemcpyHostToDevice, st));
-            CBGX_CUDA(cudaMemcpyAsync(d_va, values, nnz * 8, cudaMemcpyHostToDevice, st));
-            CBGX_CUDA(cudaMemcpyAsync(d_b, b, n * 8, cudaMemcpyHostToDevice, st));
-            CBGX_CUDA(cudaMemcpyAsync(d_x0, x0, n * 8, cudaMemcpyHostToDevice, st));
-            narrow_csr(d_rp64, n, wide ? nullptr : static_cast<int32_t*>(d_rp), d_ci64, nnz, d_ci, d_bad, st);
-            uint64_t bad = 0;
-            CBGX_CUDA(cudaMemcpyAsync(&bad, d_bad, 8, cudaMemcpyDeviceToHost, st));
-            CBGX_CUDA(cudaStreamSynchronize(st));
-            if (bad) throw Error(CBGX_EINVAL, "csr: column index out of range");
-            cbgx_csr A{n, n, nnz, d_rp, wide ? 64u : 32u, d_ci, d_va};
-            Solver solver(A, c, nullptr, nullptr);
-            solver.solve(d_b, d_x0, d_x, hist, stats, st);
-            CBGX_CUDA(cudaMemcpyAsync(x_out, d_x, n * 8, cudaMemcpyDeviceToHost, st));
-            CBGX_CUDA(cudaStreamSynchronize(st));
-        } catch (...) {
-            cleanup();
-            throw;
+        CBGX_CUDA(cudaMemsetAsync(H.d_bad, 0, 8, st));
+        CBGX_CUDA(cudaMemcpyAsync(H.d_rp64, row_ptrs, (n + 1) * 8, cudaMemcpyHostToDevice, st));
+        CBGX_CUDA(cudaMemcpyAsync(H.d_ci64, col_idx, nnz * 8, cudaMemcpyHostToDevice, st));
+        CBGX_CUDA(cudaMemcpyAsync(H.d_va, values, nnz * 8, cudaMemcpyHostToDevice, st));
+        CBGX_CUDA(cudaMemcpyAsync(H.d_b, b, n * 8, cudaMemcpyHostToDevice, st));
+        CBGX_CUDA(cudaMemcpyAsync(H.d_x0, x0, n * 8, cudaMemcpyHostToDevice, st));
+        void* d_rp = wide ? static_cast<void*>(H.d_rp64) : static_cast<void*>(H.d_rp32);
+        narrow_csr(H.d_rp64, n, wide ? nullptr : H.d_rp32, H.d_ci64, nnz, H.d_ci, H.d_bad, st);
+        CBGX_CUDA(cudaMemcpyAsync(H.h_bad, H.d_bad, 8, cudaMemcpyDeviceToHost, st));
+        CBGX_CUDA(cudaStreamSynchronize(st));
+        if (*H.h_bad) throw Error(CBGX_EINVAL, "csr: column index out of range");
+        cbgx_csr A{n, n, nnz, d_rp, wide ? 64u : 32u, H.d_ci, H.d_va};
+        // One solver per configuration and shape, kept between calls (its
+        // basis, vectors and workspaces); only the matrix-dependent SpMV
+        // state is recomputed for the new contents.
+        if (H.solver && H.solver->rows() == n && same_config(H.solver->config(), c)) {
+            H.solver->rebind(A, st);
+        } else {
+            H.solver.reset();
+            H.solver = std::make_unique<Solver>(A, c, nullptr, nullptr);
         }
-        cleanup();
+        H.solver->solve(H.d_b, H.d_x0, H.d_x, hist, stats, st);
+        CBGX_CUDA(cudaMemcpyAsync(x_out, H.d_x, n * 8, cudaMemcpyDeviceToHost, st));
+        CBGX_CUDA(cudaStreamSynchronize(st));
+    });
+}
+
+int cbgx_host_cache_release(void) {
+    return guard([&] {
+        HostSolveCache& H = host_cache();
+        std::lock_guard<std::mutex> lock(H.mu);
+        H.release();
     });
 }
 
