@@ -604,8 +604,10 @@ def _result(st: "_lib.SolveStats", hist, bufs, x) -> SolveResult:
                        (hi[:k].copy(), hr[:k].copy(), he[:k].copy(), k), float(st.wall_seconds), x, st)
 
 
-def gmres_solve(a: CsrMatrix, b, x0, cfg: GmresConfig = GmresConfig()) -> SolveResult:
-    """gmres.hpp:113-115 drop-in: host CSR / host vectors in, host solution out."""
+def gmres_solve(a: CsrMatrix, b, x0, cfg: GmresConfig = GmresConfig(), out=None) -> SolveResult:
+    """gmres.hpp:113-115 drop-in: host CSR / host vectors in, host solution out.
+    `out` (optional, float64[n], e.g. pinned) receives the solution instead of
+    a fresh array."""
     import ctypes
     n = a.n_rows
     if a.n_rows != a.n_cols:
@@ -617,7 +619,12 @@ def gmres_solve(a: CsrMatrix, b, x0, cfg: GmresConfig = GmresConfig()) -> SolveR
     rp = np.ascontiguousarray(a.row_ptrs, np.uint64)
     ci = np.ascontiguousarray(a.col_idx, np.uint64)
     va = np.ascontiguousarray(a.values, np.float64)
-    x = np.zeros(max(n, 1), np.float64)
+    if out is not None:
+        x = out
+        if not (isinstance(x, np.ndarray) and x.dtype == np.float64 and x.flags.c_contiguous and x.size >= max(n, 1)):
+            raise ValueError("gmres: out must be a contiguous float64 array of n values")
+    else:
+        x = np.zeros(max(n, 1), np.float64)
     hist, bufs = _history_buffers(2 * cfg.max_total_iterations + 4)
     st = _lib.SolveStats()
     c = cfg.c()

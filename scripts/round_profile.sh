@@ -1,6 +1,7 @@
 #!/usr/bin/env bash
-# Round evidence on one B200: tests, bench (both arms), config-4 micro-bench,
-# ncu launch list of one solve, and full ncu captures of the hot kernels.
+# Round evidence on one B200: tests, bench (both arms), config-4 CGS micro,
+# SpMV micro, ncu launch list of one solve (with DRAM bytes per launch), and
+# full ncu captures of the hot kernels.
 # Usage (via gpurun): bash scripts/round_profile.sh <tag>
 set -u
 TAG=${1:-r01}
@@ -12,17 +13,19 @@ tail -3 "$OUT/pytest_gpu.txt"
 timeout 900 python bench.py > "$OUT/bench.json" 2> "$OUT/bench.err"; tail -c 600 "$OUT/bench.json"; echo
 timeout 600 python bench.py --impl reference --steps 3 --warmup 1 > "$OUT/bench_reference.json" 2>&1; tail -c 300 "$OUT/bench_reference.json"; echo
 timeout 600 python scripts/cgs_micro.py --k 10,20,50,100,150,200 --formats frsz2-32,frsz2-21,frsz2-16,f32,f64 > "$OUT/cgs_micro.txt" 2>&1
-timeout 300 python scripts/cgs_micro.py --n 2097152 --k 1,5,20,40,80 --formats frsz2-32,f64 > "$OUT/cgs_micro_n2m.txt" 2>&1
-# launch list of one timed solve (cold-cache, serialised: compare shares)
-timeout 900 ncu --metrics gpu__time_duration.sum,dram__bytes_read.sum,dram__bytes_write.sum --clock-control none -c 600 --csv \
-    --log-file "$OUT/ncu_launches.csv" python bench.py --steps 1 --warmup 1 --no-fp64 --no-e2e --no-codec --no-cpu-baseline > /dev/null 2>&1
-# full captures: fused orthogonalisation in the solve, SpMV, codec, CGS micro at n = 2^26
-timeout 600 ncu --set full --clock-control none --import-source on -k regex:arnoldi_fused -s 60 -c 1 -o "$OUT/ncu_fused" \
-    python bench.py --steps 1 --warmup 1 --no-fp64 --no-e2e --no-codec --no-cpu-baseline > /dev/null 2>&1
-timeout 600 ncu --set full --clock-control none --import-source on -k regex:spmv_kernel -s 60 -c 1 -o "$OUT/ncu_spmv" \
-    python bench.py --steps 1 --warmup 1 --no-fp64 --no-e2e --no-codec --no-cpu-baseline > /dev/null 2>&1
-timeout 600 ncu --set full --clock-control none --import-source on -k regex:decompress32_kernel -s 3 -c 1 -o "$OUT/ncu_decompress" \
-    python bench.py --steps 1 --warmup 1 --no-fp64 --no-e2e --no-cpu-baseline > /dev/null 2>&1
+timeout 300 python scripts/spmv_micro.py > "$OUT/spmv_micro.txt" 2>&1
+# launch list of one solve (cold-cache, serialised: compare shares, not absolutes)
+timeout 900 ncu --metrics gpu__time_duration.sum,dram__bytes_read.sum,dram__bytes_write.sum --clock-control none --csv \
+    --log-file "$OUT/ncu_launches.csv" python scripts/one_solve.py poisson128 frsz2-32 > /dev/null 2>&1
+# full captures: fused orthogonalisation (mid-cycle launch), staged SpMV, codec, CGS micro at n = 2^26
+timeout 600 ncu --set full --clock-control none --import-source on -k regex:arnoldi_fused -s 63 -c 1 -o "$OUT/ncu_fused" \
+    python scripts/one_solve.py poisson128 frsz2-32 > /dev/null 2>&1
+timeout 600 ncu --set full --clock-control none --import-source on -k regex:spmv_tma -s 66 -c 1 -o "$OUT/ncu_spmv" \
+    python scripts/one_solve.py poisson128 frsz2-32 > /dev/null 2>&1
+timeout 600 ncu --set full --clock-control none --import-source on -k regex:decompress4 -s 3 -c 1 -o "$OUT/ncu_decompress" \
+    python scripts/quick_perf.py > /dev/null 2>&1
+timeout 600 ncu --set full --clock-control none --import-source on -k regex:compress4 -s 3 -c 1 -o "$OUT/ncu_compress" \
+    python scripts/quick_perf.py > /dev/null 2>&1
 timeout 600 ncu --set full --clock-control none --import-source on -k regex:cgs_dot_kernel -s 2 -c 1 -o "$OUT/ncu_cgs_dot_2p26" \
     python scripts/cgs_micro.py --k 100 --formats frsz2-32 --reps 1 > /dev/null 2>&1
 timeout 600 ncu --set full --clock-control none --import-source on -k regex:cgs_update_kernel -s 2 -c 1 -o "$OUT/ncu_cgs_update_2p26" \
