@@ -181,9 +181,11 @@ __device__ __forceinline__ void slow_decode(const Codes4& c, uint32_t e, double 
     }
 }
 
+// The fast/exact split is decided per warp (all 32 lanes must be active):
+// a warp-uniform branch costs no divergence bookkeeping in the hot loop.
 template <int L>
 __device__ __forceinline__ double frsz_dot(const Codes4& c, uint32_t e, const double w[4]) {
-    if (__builtin_expect(e > L - 2, 1)) return fast_dot<L>(c, e, w);
+    if (__builtin_expect(__all_sync(0xFFFFFFFFu, e > L - 2), 1)) return fast_dot<L>(c, e, w);
     double v[4];
     slow_decode<L>(c, e, v);
     double s = __dmul_rn(v[0], w[0]);
@@ -199,7 +201,7 @@ __device__ __forceinline__ void frsz_update(const Codes4& c, uint32_t e, double 
     const int hse = h_exp + es - 1023;                      // exponent of h*scale
     // hse <= 1994: 2^52 * hs stays finite, so c0 below is exact
     const bool ok = es > 0 && (h == 0.0 || (h_exp != 0 && hse >= 1 && hse <= 1994));
-    if (__builtin_expect(ok, 1)) {
+    if (__builtin_expect(__all_sync(0xFFFFFFFFu, ok), 1)) {
         const double hs = __dmul_rn(h, __hiloint2double(es << 20, 0));
         const double c0 = __dmul_rn(hs, -0x1p52);
 #pragma unroll

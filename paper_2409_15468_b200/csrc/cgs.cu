@@ -545,6 +545,7 @@ constexpr int kFConsumers = kFWarps * 32;
 constexpr int kFThreads = kFConsumers + 32;     // + producer warp
 constexpr uint32_t kFStepRows = 4 * kFConsumers;
 constexpr uint32_t kUnitRows = 128;
+static_assert(kColTail >= kFStepRows, "column tail must cover one fused step");
 
 // Ring stage = one column's segment of `chunk` 2048-row steps.
 template <int F> struct FGeo;
@@ -590,6 +591,7 @@ struct FusedArgs {
     unsigned* bar;             // this launch's arrival counter (zero at launch)
     unsigned* bar_next;        // the next launch's counter: zeroed here (CTA 0)
     unsigned* gate_hist;       // previous launch's gate: 0 open (speculate), 1 closed
+    double* host_slot;         // optional mapped pinned copy of the slot (read by the host)
     unsigned long long* trace; // optional: CTA 0 phase timestamps (debug)
 };
 
@@ -765,7 +767,7 @@ __device__ __forceinline__ void fused_write(const FusedArgs& a, uint64_t r0, uin
 // update (w -= h_j v_j) for columns in the given order. `lim` = number of
 // the CTA's rows; a thread's 4 rows are skipped past it (its w stays 0).
 template <int F, bool kDot>
-__device__ __forceinline__ void fused_pass(uint32_t cols, uint32_t lim, uint32_t nch, unsigned char* stages,
+__device__ __forceinline__ void fused_pass(uint32_t cols, uint32_t lim, uint32_t steps, uint32_t nch, unsigned char* stages,
                                            uint64_t* full, uint64_t* empty, uint32_t& it, double wv[][4],
                                            double* red, const double* hsm) {
     constexpr int S = FGeo<F>::stages;
@@ -788,7 +790,9 @@ __device__ __forceinline__ void fused_pass(uint32_t cols, uint32_t lim, uint32_t
             for (int s = 0; s < kChunkSteps; ++s) {
                 const int gs = ch * kChunkSteps + s;
                 const uint32_t lr = s * kFStepRows + 4u * threadIdx.x;
-                if (static_cast<uint32_t>(gs) * kFStepRows + 4u * threadIdx.x < lim) {
+                // whole steps (warp-uniform): rows past the CTA's range hold
+                // valid FRSZ2 data of the next range and w = 0 there
+                if (static_cast<uint32_t>(gs) < steps) {
                     Step<F> st;
                     step_lds<F>(st, pay, ex, lr);
                     if constexpr (kDot) {
@@ -807,6 +811,13 @@ __device__ __forceinline__ void fused_pass(uint32_t cols, uint32_t lim, uint32_t
             acc = warp_sum(__dadd_rn(acc, acc2));
             if (lane == 0) red[warp * cols + j] = acc;
         }
+    }
+    if constexpr (!kDot) {
+        // the update also touched the rows past the CTA's range: w = 0 there
+#pragma unroll
+        for (int s = 0; s < kFusedMaxSteps; ++s)
+            if (static_cast<uint32_t>(s) * kFStepRows + 4u * threadIdx.x >= lim)
+                wv[s][0] = wv[s][1] = wv[s][2] = wv[s][3] = 0.0;
     }
 }
 
@@ -854,6 +865,9 @@ __global__ void __launch_bounds__(kFThreads, kFCtasPerSM) arnoldi_fused_kernel(F
         fence_barrier_init();
         *s_gate = -1;
     }
+    // launched as a programmatic dependent of the SpMV: everything below
+    // reads what earlier kernels wrote
+    pdl_wait();
     // previous launch's gate (written by CTA 0 at its end, after every CTA
     // of that launch had read it); CTA-uniform
     const bool spec = *reinterpret_cast<volatile unsigned*>(a.gate_hist) == 0u;
@@ -885,8 +899,10 @@ __global__ void __launch_bounds__(kFThreads, kFCtasPerSM) arnoldi_fused_kernel(F
                 const unsigned char* col = a.B.data + j * a.B.col_stride_bytes;
                 const unsigned char* ecol = reinterpret_cast<const unsigned char*>(a.B.exp + j * a.B.exp_col_stride);
                 for (uint32_t ch = 0; ch < nch; ++ch, ++it) {
+                    // whole steps: the last one may run past r1 (into the next
+                    // range, or the allocation's slack after the last column)
                     const uint32_t ub = ch * (kChunkRows / kUnitRows);
-                    const uint32_t un = min(kChunkRows, lim - ch * kChunkRows) / kUnitRows;
+                    const uint32_t un = min(kChunkSteps, static_cast<int>(steps - ch * kChunkSteps)) * (kFStepRows / kUnitRows);
                     const int stage = it % S;
                     mbar_wait(empty + stage, ((it / S) & 1) ^ 1);
                     mbar_arrive_expect_tx(full + stage, un * (UPAY + UEX));
@@ -919,23 +935,26 @@ __global__ void __launch_bounds__(kFThreads, kFCtasPerSM) arnoldi_fused_kernel(F
     unsigned seq = 0;
 
     // dot1 -> h
-    fused_pass<F, true>(cols, lim, nch, stages, full, empty, it, wv, red, hsm);
+    fused_pass<F, true>(cols, lim, steps, nch, stages, full, empty, it, wv, red, hsm);
     FTRACE(2);
     if (a.trace && threadIdx.x == 0) a.trace[32 + blockIdx.x] = global_ns();
     dot_partials_out(red, cols, P, gs);
     grid_allreduce(a.bar, seq++, P, gs, cols, hsm, a.trace);
     if (cta0)
-        for (uint32_t j = threadIdx.x; j < cols; j += kFConsumers) a.slot[3 + j] = hsm[j];
+        for (uint32_t j = threadIdx.x; j < cols; j += kFConsumers) {
+            a.slot[3 + j] = hsm[j];
+            if (a.host_slot) a.host_slot[3 + j] = hsm[j];
+        }
     FTRACE(3);
     // update1
-    fused_pass<F, false>(cols, lim, nch, stages, full, empty, it, wv, red, hsm);
+    fused_pass<F, false>(cols, lim, steps, nch, stages, full, empty, it, wv, red, hsm);
     FTRACE(4);
     if (a.trace && threadIdx.x == 0) a.trace[32 + 1024 + blockIdx.x] = global_ns();
     const double hn1_part = cta_wnorm2(wv, nred);
     double* const P1 = P + region;
     if (spec) {
         // speculative dot2 -> u, reduced together with hn1
-        fused_pass<F, true>(cols, lim, nch, stages, full, empty, it, wv, red, hsm);
+        fused_pass<F, true>(cols, lim, steps, nch, stages, full, empty, it, wv, red, hsm);
         FTRACE(5);
         dot_partials_out(red, cols, P1, gs);
     }
@@ -950,30 +969,43 @@ __global__ void __launch_bounds__(kFThreads, kFCtasPerSM) arnoldi_fused_kernel(F
         *s_gate = gate ? 1 : 0;
         __threadfence_block();
     }
-    if (cta0 && threadIdx.x == 0) a.slot[0] = hn1;
+    if (cta0 && threadIdx.x == 0) {
+        a.slot[0] = hn1;
+        if (a.host_slot) {
+            a.host_slot[0] = hn1;
+            a.host_slot[2] = a.slot[2];
+        }
+    }
     double hn2 = hn1;
     if (gate) {
         if (!spec) {
-            fused_pass<F, true>(cols, lim, nch, stages, full, empty, it, wv, red, hsm);
+            fused_pass<F, true>(cols, lim, steps, nch, stages, full, empty, it, wv, red, hsm);
             FTRACE(5);
             dot_partials_out(red, cols, P + 2 * region, gs);
             grid_allreduce(a.bar, seq++, P + 2 * region, gs, cols, hsm);
         }
         if (cta0)
-            for (uint32_t j = threadIdx.x; j < cols; j += kFConsumers) a.slot[a.u_off + j] = hsm[j];
+            for (uint32_t j = threadIdx.x; j < cols; j += kFConsumers) {
+                a.slot[a.u_off + j] = hsm[j];
+                if (a.host_slot) a.host_slot[a.u_off + j] = hsm[j];
+            }
         FTRACE(7);
         // update2 (u in hsm)
-        fused_pass<F, false>(cols, lim, nch, stages, full, empty, it, wv, red, hsm);
+        fused_pass<F, false>(cols, lim, steps, nch, stages, full, empty, it, wv, red, hsm);
         FTRACE(8);
         const double p = cta_wnorm2(wv, nred);
         double* const P3 = P + 3 * region;
         if (threadIdx.x == 0) P3[blockIdx.x] = p;
         grid_allreduce(a.bar, seq++, P3, gs, 1, scal, a.trace);
         hn2 = scal[0];
-        if (cta0 && threadIdx.x == 0) a.slot[1] = hn2;
+        if (cta0 && threadIdx.x == 0) {
+            a.slot[1] = hn2;
+            if (a.host_slot) a.host_slot[1] = hn2;
+        }
         FTRACE(9);
     }
     if (cta0 && threadIdx.x == 0) *a.gate_hist = gate ? 0u : 1u;
+    pdl_trigger();  // the next SpMV may launch (it waits for this grid)
     // v = w / h_next of the last pass, written as the next basis column
     const double scale = 1.0 / sqrt(hn2);
     fused_write<F>(a, r0, r1, steps, wv, scale, scratch);
@@ -1038,7 +1070,8 @@ int fused_grid(uint64_t n, uint32_t max_cols) {
 
 template <int F> struct FusedLaunch {
     static void run(const cbgx_basis& V, uint32_t cols, const double* w, double* v_out, double* slot,
-                    uint32_t u_off, double eta, uint32_t max_cols, Workspace* ws, cudaStream_t st, bool* done) {
+                    uint32_t u_off, double eta, uint32_t max_cols, double* host_slot, bool pdl, Workspace* ws,
+                    cudaStream_t st, bool* done) {
         // geometry fixed by the solver's capacity so it never changes mid-solve
         const int grid = fused_grid<F>(V.n, max_cols);
         *done = false;
@@ -1064,10 +1097,21 @@ template <int F> struct FusedLaunch {
         a.bar_next = c + Workspace::kFusedBar + ((seq + 1) & 1) * 32;
         a.gate_hist = c + Workspace::kFusedGate;
         a.trace = fused_trace_buffer();
-        void* args[] = {&a};
+        a.host_slot = host_slot;
+        cudaLaunchConfig_t lc = {};
+        lc.gridDim = dim3(grid);
+        lc.blockDim = dim3(kFThreads);
+        lc.dynamicSmemBytes = smem;
+        lc.stream = st;
+        cudaLaunchAttribute at[2];
+        at[0].id = cudaLaunchAttributeCooperative;
+        at[0].val.cooperative = 1;
+        at[1].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+        at[1].val.programmaticStreamSerializationAllowed = 1;
+        lc.attrs = at;
+        lc.numAttrs = pdl ? 2 : 1;
         note_launch();
-        CBGX_CUDA(cudaLaunchCooperativeKernel(reinterpret_cast<void*>(arnoldi_fused_kernel<F>), dim3(grid),
-                                              dim3(kFThreads), args, smem, st));
+        CBGX_CUDA(cudaLaunchKernelEx(&lc, arnoldi_fused_kernel<F>, a));
         *done = true;
     }
 };
@@ -1117,10 +1161,12 @@ bool fused_eligible(const cbgx_basis& V, uint64_t max_cols) {
 }
 
 bool launch_arnoldi_fused(const cbgx_basis& V, uint32_t cols, const double* w, double* v_out, double* slot,
-                          uint32_t u_off, double eta, uint32_t max_cols, Workspace* ws, cudaStream_t st) {
+                          uint32_t u_off, double eta, uint32_t max_cols, double* host_slot, bool pdl,
+                          Workspace* ws, cudaStream_t st) {
     if (cols + 1 > V.capacity) throw Error(CBGX_ERANGE, "basis: cannot write column");
     bool done = false;
-    dispatch_fmt<FusedLaunch>(fmt_of(V), V, cols, w, v_out, slot, u_off, eta, max_cols, ws, st, &done);
+    dispatch_fmt<FusedLaunch>(fmt_of(V), V, cols, w, v_out, slot, u_off, eta, max_cols, host_slot, pdl, ws, st,
+                              &done);
     CBGX_CUDA(cudaGetLastError());
     return done;
 }
@@ -1149,19 +1195,25 @@ int cbgx_basis_layout(uint32_t kind, uint32_t l, uint64_t n, uint64_t capacity, 
         B.n_pad = pad_rows(std::max<uint64_t>(n, 1));
         B.capacity = capacity;
         const int f = fmt_of(B);
+        // Each column is followed by kColTail zero rows that no kernel writes:
+        // the fused kernel streams whole steps, and the last range's last
+        // step may run up to one step past n_pad -- it then reads zeros of
+        // the same column (finite, and multiplied by w = 0) instead of the
+        // next column's possibly stale data.
+        const uint64_t rows = B.n_pad + kColTail;
         uint64_t col_bytes = 0, exp_words = 0;
         switch (f) {
-        case kF64: col_bytes = B.n_pad * 8; break;
-        case kF32: col_bytes = B.n_pad * 4; break;
-        case kF16: col_bytes = B.n_pad * 2; break;
+        case kF64: col_bytes = rows * 8; break;
+        case kF32: col_bytes = rows * 4; break;
+        case kF16: col_bytes = rows * 2; break;
         default:
-            col_bytes = B.n_pad / 32 * l * 4;
-            exp_words = B.n_pad / 32;
+            col_bytes = rows / 32 * l * 4;
+            exp_words = rows / 32;
         }
         B.col_stride_bytes = col_bytes;
         B.exp_col_stride = exp_words;
         *out = B;
-        // +64 B slack: the l=21 step loader reads up to 3 words past a
+        // + 64 B slack: the l=21 step loader reads up to 3 words past a
         // block's last word.
         if (data_bytes) *data_bytes = col_bytes * capacity + 64;
         if (exp_bytes) *exp_bytes = exp_words * capacity * 4;

@@ -49,6 +49,8 @@ inline cudaStream_t as_stream(void* s) { return reinterpret_cast<cudaStream_t>(s
 // Rows of a basis column are padded to a multiple of this, so the fused
 // CGS kernels stream whole tiles without tail predication on the basis.
 constexpr uint64_t kRowAlign = 8192;
+// Zero rows after each basis column's n_pad rows (see cbgx_basis_layout).
+constexpr uint64_t kColTail = 2048;
 inline uint64_t pad_rows(uint64_t n) { return (n + kRowAlign - 1) / kRowAlign * kRowAlign; }
 
 // --------------------------------------------------------- device codec

@@ -50,6 +50,31 @@ __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
     } while (!done);
 }
 
+// Consumer-side wait: try_wait with a suspend-time hint parks the warp
+// until the phase completes instead of spinning on issue slots the other
+// consumer warps need.
+__device__ __forceinline__ void mbar_wait_sleep(uint64_t* bar, uint32_t parity) {
+    const uint32_t addr = smem_u32(bar);
+    uint32_t done = 0;
+    do {
+        asm volatile(
+            "{\n\t.reg .pred p;\n\t"
+            "mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2, %3;\n\t"
+            "selp.u32 %0, 1, 0, p;\n\t}"
+            : "=r"(done)
+            : "r"(addr), "r"(parity), "r"(0x989680u)
+            : "memory");
+    } while (!done);
+}
+
+// Programmatic dependent launch (sm_90+): a kernel launched with the
+// programmatic-stream-serialization attribute may start while its
+// predecessor drains; pdl_wait() blocks until the predecessor grid has
+// completed and its writes are visible (a no-op for a normal launch), and
+// pdl_trigger() lets the successor launch early.
+__device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+__device__ __forceinline__ void pdl_trigger() { asm volatile("griddepcontrol.launch_dependents;" ::: "memory"); }
+
 // Global -> shared bulk copy (bytes % 16 == 0, both addresses 16-B aligned),
 // completing `bytes` transaction bytes on `bar`. Streamed data is read once:
 // evict-first keeps it from displacing reusable lines in L2.

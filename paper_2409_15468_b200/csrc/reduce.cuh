@@ -82,7 +82,7 @@ void launch_spmv_sell(const cbgx_csr& A, const Sell& S, const double* x, const d
 // rows, 0 when some tile would exceed the stage capacity).
 uint32_t plan_spmv_tiles(const cbgx_csr& A, cudaStream_t st);
 void launch_spmv_tma(const cbgx_csr& A, uint32_t tile_rows, const double* x, const double* b, double* y,
-                     double* norm, int reduction, Workspace* ws, cudaStream_t st);
+                     double* norm, int reduction, Workspace* ws, cudaStream_t st, bool pdl = false);
 
 // Deterministic <x, y>. REDUCE_TREE: fixed-shape tree; REDUCE_REFERENCE:
 // one thread, sequential from +0.0 (sparse.cpp:58-67).
@@ -100,8 +100,11 @@ void launch_cgs_update(const cbgx_basis& V, uint64_t first, uint32_t cols, const
 // launch; see cgs.cu). Returns false (nothing launched) when the problem is
 // too large for the register-resident w of a co-resident grid.
 bool fused_eligible(const cbgx_basis& V, uint64_t max_cols);
+// host_slot: mapped pinned copy of the step slot written by the kernel (no
+// D2H copy in the stream); pdl: programmatic dependent of the SpMV before.
 bool launch_arnoldi_fused(const cbgx_basis& V, uint32_t cols, const double* w, double* v_out, double* slot,
-                          uint32_t u_off, double eta, uint32_t max_cols, Workspace* ws, cudaStream_t st);
+                          uint32_t u_off, double eta, uint32_t max_cols, double* host_slot, bool pdl,
+                          Workspace* ws, cudaStream_t st);
 void launch_basis_write(const cbgx_basis& V, uint64_t j, const double* x, const ScaleArg& scale,
                         double* v_out, uint64_t* bad, cudaStream_t st);
 void launch_basis_read(const cbgx_basis& V, uint64_t j, uint64_t first, uint64_t count, double* out,

@@ -156,7 +156,10 @@ Solver::Solver(const cbgx_csr& A, const cbgx_gmres_config& cfg, Comm* comm, Halo
     const size_t scal = 2 * kSlot(m) + 2 * m + 16;
     CBGX_CUDA(cudaMalloc(&d_scal_, scal * sizeof(double)));
     CBGX_CUDA(cudaMemset(d_scal_, 0, scal * sizeof(double)));
-    CBGX_CUDA(cudaMallocHost(&h_pinned_, scal * sizeof(double)));
+    // mapped: the fused orthogonalisation writes the step slot straight into
+    // it (no device-to-host copy between the step's kernels)
+    CBGX_CUDA(cudaHostAlloc(&h_pinned_, scal * sizeof(double), cudaHostAllocMapped));
+    CBGX_CUDA(cudaHostGetDevicePointer(reinterpret_cast<void**>(&d_hpinned_), h_pinned_, 0));
     for (auto& e : step_ev_) CBGX_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
     // The zero-fills above run on the legacy stream; solves may run on a
     // non-blocking stream that does not order after it.
@@ -215,8 +218,8 @@ Solver::~Solver() {
     cudaFreeHost(h_pinned_);
 }
 
-void Solver::spmv(const double* x, const double* b, double* y, double* norm, cudaStream_t st) {
-    if (tile_rows_) launch_spmv_tma(A_, tile_rows_, x, b, y, norm, static_cast<int>(cfg_.reduction), &ws_, st);
+void Solver::spmv(const double* x, const double* b, double* y, double* norm, cudaStream_t st, bool pdl) {
+    if (tile_rows_) launch_spmv_tma(A_, tile_rows_, x, b, y, norm, static_cast<int>(cfg_.reduction), &ws_, st, pdl);
     else if (sell_) launch_spmv_sell(A_, *sell_, x, b, y, norm, static_cast<int>(cfg_.reduction), &ws_, st);
     else launch_spmv(A_, x, b, y, norm, static_cast<int>(cfg_.reduction), &ws_, st);
 }
@@ -309,8 +312,12 @@ void Solver::solve(const double* d_b, const double* d_x0, double* d_x, cbgx_hist
                 halo_->exchange(d_v_, st);
                 timer.end();
             }
+            // In the fused path the SpMV and the orthogonalisation are
+            // programmatic dependent launches (each starts while the previous
+            // kernel drains) unless phase timing puts events between them.
+            const bool pdl = use_fused && !timer.on;
             timer.begin(CBGX_PHASE_SPMV);
-            spmv(d_v_, nullptr, d_w_, sl + kOmega, st);  // w = A v, omega^2
+            spmv(d_v_, nullptr, d_w_, sl + kOmega, st, pdl);  // w = A v, omega^2
             timer.end();
             count(CBGX_PHASE_SPMV, spmv_bytes);
             if (use_fused) {
@@ -318,7 +325,7 @@ void Solver::solve(const double* d_b, const double* d_x0, double* d_x, cbgx_hist
                 // the scaled write of column used+1, w register-resident
                 timer.begin(CBGX_PHASE_ORTHO);
                 const bool ok = launch_arnoldi_fused(V_, cols, d_w_, d_v_, sl, static_cast<uint32_t>(kU(m)), cfg_.eta,
-                                                     static_cast<uint32_t>(m), &ws_, st);
+                                                     static_cast<uint32_t>(m), d_hpinned_ + p * slot, pdl, &ws_, st);
                 timer.end();
                 if (!ok) throw Error(CBGX_EINTERNAL, "fused orthogonalisation became ineligible");
                 count(CBGX_PHASE_ORTHO, 2.0 * cols * bpv * n + 8.0 * n + 8.0 * n + bpv * n);
@@ -364,8 +371,9 @@ void Solver::solve(const double* d_b, const double* d_x0, double* d_x, cbgx_hist
                 timer.end();
                 count(CBGX_PHASE_WRITE, 16.0 * n + bpv * n);
             }
-            CBGX_CUDA(cudaMemcpyAsync(h_pinned_ + p * slot, sl, kU(m) * sizeof(double) + cols * sizeof(double),
-                                      cudaMemcpyDeviceToHost, st));
+            if (!use_fused)  // the fused kernel wrote the mapped slot itself
+                CBGX_CUDA(cudaMemcpyAsync(h_pinned_ + p * slot, sl, kU(m) * sizeof(double) + cols * sizeof(double),
+                                          cudaMemcpyDeviceToHost, st));
             CBGX_CUDA(cudaEventRecord(step_ev_[p], st));
             S.host_enqueue_ms += std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - te).count();
         };

@@ -70,7 +70,7 @@ private:
     struct PhaseTimer;
     PhaseTimer* timer_ = nullptr;
     void reduce(double* d_vals, size_t count, cudaStream_t st);
-    void spmv(const double* x, const double* b, double* y, double* norm, cudaStream_t st);
+    void spmv(const double* x, const double* b, double* y, double* norm, cudaStream_t st, bool pdl = false);
     double fetch_scalar(const double* d, cudaStream_t st);
     void setup_matrix(bool before_basis, cudaStream_t st);
 
@@ -87,6 +87,7 @@ private:
     double* d_w_ = nullptr;
     double* d_scal_ = nullptr;   // [0] omega^2 [1] hn^2 [2] ||b||^2 [3] ||r||^2 [4..] h / u / y
     double* h_pinned_ = nullptr;
+    double* d_hpinned_ = nullptr;  // device alias of the mapped h_pinned_
     cudaEvent_t step_ev_[2] = {nullptr, nullptr};
     int fused_state_ = 0;
     std::unique_ptr<Sell> sell_;

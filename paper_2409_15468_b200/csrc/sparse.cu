@@ -219,6 +219,7 @@ spmv_tma_kernel(uint64_t n_rows, uint64_t nnz, uint32_t tile_rows, const RP* __r
         fence_barrier_init();
     }
     __syncthreads();
+    pdl_trigger();  // the orthogonalisation after us may launch (it waits for this grid)
     const uint64_t ntiles = (n_rows + tile_rows - 1) / tile_rows;
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     if (warp == kSpmvConsumers / 32) {
@@ -259,6 +260,10 @@ spmv_tma_kernel(uint64_t n_rows, uint64_t nnz, uint32_t tile_rows, const RP* __r
         }
         return;
     }
+    // programmatic dependent of the orthogonalisation that wrote x: the
+    // producer streams the (constant) matrix right away, the consumers wait
+    // for the predecessor before gathering x or writing y
+    pdl_wait();
     double acc = 0.0;
     const int g = warp / (kGroupThreads / 32);
     const uint32_t t = threadIdx.x % kGroupThreads;
@@ -621,7 +626,7 @@ uint32_t plan_spmv_tiles(const cbgx_csr& A, cudaStream_t st) {
 
 template <typename RP, int MODE>
 static void spmv_tma_launch(const cbgx_csr& A, uint32_t tile_rows, const double* x, const double* b, double* y,
-                            int fused, double* norm, Workspace* ws, cudaStream_t st) {
+                            int fused, double* norm, Workspace* ws, cudaStream_t st, bool pdl) {
     static int per_sm = -1;  // per (RP, MODE) instantiation; one device geometry
     const size_t smem = kSpmvStages * (TileGeo<RP>::stage + 16) + 64;
     if (per_sm < 0) {
@@ -634,20 +639,31 @@ static void spmv_tma_launch(const cbgx_csr& A, uint32_t tile_rows, const double*
     const int grid = static_cast<int>(std::max<uint64_t>(1, std::min<uint64_t>(ntiles, static_cast<uint64_t>(sm_count()) * per_sm)));
     double* partials = fused ? ws->get_partials(grid) : nullptr;
     unsigned* ticket = fused ? ws->get_counter() : nullptr;
-    CBGX_K(spmv_tma_kernel<RP, MODE><<<grid, kSpmvThreads, smem, st>>>(
-        A.n_rows, A.nnz, tile_rows, static_cast<const RP*>(A.d_row_ptr), A.d_col_idx, A.d_values, x, b, y, fused,
-        partials, ticket, norm));
+    cudaLaunchConfig_t lc = {};
+    lc.gridDim = dim3(grid);
+    lc.blockDim = dim3(kSpmvThreads);
+    lc.dynamicSmemBytes = smem;
+    lc.stream = st;
+    cudaLaunchAttribute at[1];
+    at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    at[0].val.programmaticStreamSerializationAllowed = 1;
+    lc.attrs = at;
+    lc.numAttrs = pdl ? 1 : 0;
+    note_launch();
+    CBGX_CUDA(cudaLaunchKernelEx(&lc, spmv_tma_kernel<RP, MODE>, A.n_rows, A.nnz, tile_rows,
+                                 static_cast<const RP*>(A.d_row_ptr), A.d_col_idx, A.d_values, x, b, y, fused,
+                                 partials, ticket, norm));
 }
 
 void launch_spmv_tma(const cbgx_csr& A, uint32_t tile_rows, const double* x, const double* b, double* y,
-                     double* norm, int reduction, Workspace* ws, cudaStream_t st) {
+                     double* norm, int reduction, Workspace* ws, cudaStream_t st, bool pdl) {
     const int fused = norm && reduction == CBGX_REDUCE_TREE;
     if (A.row_ptr_bits == 32) {
-        if (b) spmv_tma_launch<int32_t, 1>(A, tile_rows, x, b, y, fused, norm, ws, st);
-        else spmv_tma_launch<int32_t, 0>(A, tile_rows, x, b, y, fused, norm, ws, st);
+        if (b) spmv_tma_launch<int32_t, 1>(A, tile_rows, x, b, y, fused, norm, ws, st, pdl);
+        else spmv_tma_launch<int32_t, 0>(A, tile_rows, x, b, y, fused, norm, ws, st, pdl);
     } else {
-        if (b) spmv_tma_launch<int64_t, 1>(A, tile_rows, x, b, y, fused, norm, ws, st);
-        else spmv_tma_launch<int64_t, 0>(A, tile_rows, x, b, y, fused, norm, ws, st);
+        if (b) spmv_tma_launch<int64_t, 1>(A, tile_rows, x, b, y, fused, norm, ws, st, pdl);
+        else spmv_tma_launch<int64_t, 0>(A, tile_rows, x, b, y, fused, norm, ws, st, pdl);
     }
     CBGX_CUDA(cudaGetLastError());
     if (norm && !fused) launch_dot(y, y, A.n_rows, CBGX_REDUCE_REFERENCE, norm, ws, st);
