@@ -27,6 +27,9 @@ ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 # exactly like the reference build (no -march, src/CMakeLists.txt).
 NVFLAGS = ARCH + ["-O3", "-lineinfo", "-std=c++20", "-Xcompiler", "-fPIC,-ffp-contract=off",
                   "-I" + INCLUDE, "-I" + CSRC, "--expt-relaxed-constexpr"]
+# Development only: extra -D geometry flags for A/B builds (e.g.
+# CBGX_NVFLAGS_EXTRA="-DFUSED_WARPS=12 -DFUSED_STEPS=5").
+NVFLAGS += os.environ.get("CBGX_NVFLAGS_EXTRA", "").split()
 
 
 def _headers_digest() -> str:

@@ -534,41 +534,43 @@ template <int F> struct ReadLaunch {
 //
 // Rows are split over the CTAs in 128-row units (16-B aligned segments for
 // every format), so CTAs differ by at most one unit (<1% at 128^3) and every
-// grid reduction waits on a balanced grid. One CTA per SM halves the number
-// of partial rows each reduction has to read compared with two.
-// Eligible when every CTA's rows fit in kFusedMaxSteps 2048-row steps
-// (n <= 16384 * SMs, ~2.4M rows on a B200).
-constexpr int kFusedMaxSteps = 8;
+// grid reduction waits on a balanced grid. Geometry (build-time, measured on
+// B200 with scripts/ab_fused.sh): FUSED_CTAS CTAs per SM of FUSED_WARPS
+// consumer warps, each thread holding 4 rows x FUSED_STEPS steps of w in
+// registers. 2 x 12 warps x 5 steps (1536-row steps) beat 2 x 8 x 8 (7.94 vs
+// 8.19 ms per 128^3 solve) and 2 x 10 x 6: more warps hide the decode and
+// shared-memory latency of the column passes. Eligible when every
+// CTA's rows fit (n <= 4 * 32 * FUSED_WARPS * FUSED_STEPS * CTAs).
+#ifndef FUSED_WARPS
+#define FUSED_WARPS 12
+#endif
+#ifndef FUSED_STEPS
+#define FUSED_STEPS 5
+#endif
+constexpr int kFusedMaxSteps = FUSED_STEPS;
 constexpr int kFCtasPerSM = FUSED_CTAS_PER_SM;
-constexpr int kFWarps = 16 / kFCtasPerSM;       // consumer warps
+constexpr int kFWarps = FUSED_WARPS;            // consumer warps
 constexpr int kFConsumers = kFWarps * 32;
 constexpr int kFThreads = kFConsumers + 32;     // + producer warp
 constexpr uint32_t kFStepRows = 4 * kFConsumers;
 constexpr uint32_t kUnitRows = 128;
 static_assert(kColTail >= kFStepRows, "column tail must cover one fused step");
+static_assert(kFStepRows % kUnitRows == 0, "steps are whole 128-row units");
 
-// Ring stage = one column's segment of `chunk` 2048-row steps.
-template <int F> struct FGeo;
-#if FUSED_CTAS_PER_SM == 1
-template <> struct FGeo<kZ32> { static constexpr int chunk = 4, stages = 5; };
-template <> struct FGeo<kZ16> { static constexpr int chunk = 8, stages = 5; };
-template <> struct FGeo<kZ21> { static constexpr int chunk = 4, stages = 7; };
-template <> struct FGeo<kF64> { static constexpr int chunk = 2, stages = 5; };
-template <> struct FGeo<kF32> { static constexpr int chunk = 4, stages = 5; };
-template <> struct FGeo<kF16> { static constexpr int chunk = 8, stages = 5; };
-#else
-template <> struct FGeo<kZ32> { static constexpr int chunk = 8, stages = 3; };
-template <> struct FGeo<kZ16> { static constexpr int chunk = 8, stages = 4; };
-template <> struct FGeo<kZ21> { static constexpr int chunk = 8, stages = 3; };
-template <> struct FGeo<kF64> { static constexpr int chunk = 4, stages = 3; };
-template <> struct FGeo<kF32> { static constexpr int chunk = 8, stages = 3; };
-template <> struct FGeo<kF16> { static constexpr int chunk = 8, stages = 4; };
-#endif
-
-// payload / exponent bytes per 2048-row step and per 128-row unit
+// payload / exponent bytes per step and per 128-row unit
 template <int F> struct FBytes {
     static constexpr uint32_t pay = Geo<F>::pay * kFStepRows / 1024, ex = Geo<F>::ex * kFStepRows / 1024;
     static constexpr uint32_t upay = Geo<F>::pay / 8, uex = Geo<F>::ex / 8;
+};
+
+// Ring stage = one column's segment of `chunk` steps (~32 KB), `stages` deep
+// (~100 KB of shared memory per CTA at two CTAs per SM).
+template <int F> struct FGeo {
+    static constexpr int chunk_raw = static_cast<int>(32768 / (FBytes<F>::pay + FBytes<F>::ex));
+    static constexpr int chunk = chunk_raw < 1 ? 1 : (chunk_raw > kFusedMaxSteps ? kFusedMaxSteps : chunk_raw);
+    static constexpr int stages_raw = static_cast<int>((kFCtasPerSM == 1 ? 170000 : 100000) /
+                                                       (chunk * (FBytes<F>::pay + FBytes<F>::ex) + 32));
+    static constexpr int stages = stages_raw < 2 ? 2 : stages_raw;
 };
 
 template <int F>
@@ -772,7 +774,7 @@ __device__ __forceinline__ void fused_pass(uint32_t cols, uint32_t lim, uint32_t
                                            double* red, const double* hsm) {
     constexpr int S = FGeo<F>::stages;
     constexpr uint32_t PAY = FBytes<F>::pay, SB = fstage_bytes<F>();
-    constexpr int kChunkSteps = FGeo<F>::chunk, kChunks = kFusedMaxSteps / kChunkSteps;
+    constexpr int kChunkSteps = FGeo<F>::chunk, kChunks = (kFusedMaxSteps + kChunkSteps - 1) / kChunkSteps;
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     for (uint32_t jj = 0; jj < cols; ++jj) {
         const uint32_t j = kDot ? cols - 1 - jj : jj;
@@ -792,7 +794,7 @@ __device__ __forceinline__ void fused_pass(uint32_t cols, uint32_t lim, uint32_t
                 const uint32_t lr = s * kFStepRows + 4u * threadIdx.x;
                 // whole steps (warp-uniform): rows past the CTA's range hold
                 // valid FRSZ2 data of the next range and w = 0 there
-                if (static_cast<uint32_t>(gs) < steps) {
+                if (gs < kFusedMaxSteps && static_cast<uint32_t>(gs) < steps) {
                     Step<F> st;
                     step_lds<F>(st, pay, ex, lr);
                     if constexpr (kDot) {
