@@ -171,15 +171,19 @@ constexpr int kSpmvConsumers = 256;
 // Consumer groups take alternate tiles (measured on B200: one group of 8
 // warps with 256-row tiles beats two groups with 128-row tiles -- the
 // producer's per-tile cost dominates at smaller tiles).
-constexpr int kSpmvGroups = 1;
+#ifndef SPMV_GROUPS
+#define SPMV_GROUPS 2
+#endif
+constexpr int kSpmvGroups = SPMV_GROUPS;
 constexpr int kGroupThreads = kSpmvConsumers / kSpmvGroups;
+constexpr int kTileRowsMax = 256;  // a group thread owns up to 256 / kGroupThreads rows of a tile
 constexpr int kSpmvThreads = kSpmvConsumers + 32;
 
 template <typename RP>
 struct TileGeo {
     static constexpr uint32_t val_bytes = (kTileEntries + 2) * 8;
     static constexpr uint32_t col_bytes = (kTileEntries + 4) * 4;
-    static constexpr uint32_t rp_bytes = (kGroupThreads + 1 + 16 / sizeof(RP)) * sizeof(RP) + 16;
+    static constexpr uint32_t rp_bytes = (kTileRowsMax + 1 + 16 / sizeof(RP)) * sizeof(RP) + 16;
     static constexpr uint32_t stage = (val_bytes + col_bytes + rp_bytes + 127) / 128 * 128;
 };
 
@@ -305,32 +309,52 @@ spmv_tma_kernel(uint64_t n_rows, uint64_t nnz, uint32_t tile_rows, const RP* __r
             const uint32_t ov = static_cast<uint32_t>(k0 & 1), oc = static_cast<uint32_t>(k0 & 3);
             const uint32_t base = static_cast<uint32_t>(k0);  // low bits: in-tile offsets only
             if constexpr (true) {
-                if (tile_rows == kGroupThreads) {
-                    // short rows: one thread per row, loads for up to 8
-                    // entries issued together, products added in row order
-                    for (uint32_t lr = t; lr < nrows; lr += kGroupThreads) {
+                if (tile_rows >= static_cast<uint32_t>(kGroupThreads)) {
+                    // short rows: one thread per row (two interleaved rows,
+                    // lr and lr + kGroupThreads, when the tile has 2x the
+                    // group's threads), loads for up to 8 entries of each row
+                    // issued together, products added in row order
+                    for (uint32_t lr = t; lr < nrows; lr += 2 * kGroupThreads) {
+                        const uint32_t lr2 = lr + kGroupThreads;
+                        const bool two = lr2 < nrows;
                         const uint32_t a = static_cast<uint32_t>(sr[orr + lr]) - base;
                         const uint32_t e = static_cast<uint32_t>(sr[orr + lr + 1]) - base;
-                        double s = 0.0;
-                        for (uint32_t k = a; k < e; k += 8) {
-                            int32_t c[8];
-                            double v[8], xv[8];
+                        const uint32_t a2 = two ? static_cast<uint32_t>(sr[orr + lr2]) - base : 0u;
+                        const uint32_t e2 = two ? static_cast<uint32_t>(sr[orr + lr2 + 1]) - base : 0u;
+                        double s = 0.0, s2 = 0.0;
+                        const uint32_t len = max(e - a, e2 - a2);
+                        for (uint32_t k = 0; k < len; k += 8) {
+                            int32_t c[8], c2[8];
+                            double v[8], xv[8], v2[8], xv2[8];
 #pragma unroll
                             for (int u = 0; u < 8; ++u) {
-                                const bool in = k + u < e;
-                                c[u] = in ? sc[k + u + oc] : 0;
-                                v[u] = in ? sv[k + u + ov] : 0.0;
+                                const bool in = a + k + u < e, in2 = a2 + k + u < e2;
+                                c[u] = in ? sc[a + k + u + oc] : 0;
+                                v[u] = in ? sv[a + k + u + ov] : 0.0;
+                                c2[u] = in2 ? sc[a2 + k + u + oc] : 0;
+                                v2[u] = in2 ? sv[a2 + k + u + ov] : 0.0;
                             }
 #pragma unroll
-                            for (int u = 0; u < 8; ++u) xv[u] = k + u < e ? __ldg(x + c[u]) : 0.0;
+                            for (int u = 0; u < 8; ++u) {
+                                xv[u] = a + k + u < e ? __ldg(x + c[u]) : 0.0;
+                                xv2[u] = a2 + k + u < e2 ? __ldg(x + c2[u]) : 0.0;
+                            }
 #pragma unroll
-                            for (int u = 0; u < 8; ++u)
-                                if (k + u < e) s = __dadd_rn(s, __dmul_rn(v[u], xv[u]));
+                            for (int u = 0; u < 8; ++u) {
+                                if (a + k + u < e) s = __dadd_rn(s, __dmul_rn(v[u], xv[u]));
+                                if (a2 + k + u < e2) s2 = __dadd_rn(s2, __dmul_rn(v2[u], xv2[u]));
+                            }
                         }
                         const uint64_t r = r0 + lr;
                         if (MODE == 1) s = __dsub_rn(__ldg(b + r), s);
                         y[r] = s;
                         if (with_norm) acc = __dadd_rn(acc, __dmul_rn(s, s));
+                        if (two) {
+                            const uint64_t rr = r0 + lr2;
+                            if (MODE == 1) s2 = __dsub_rn(__ldg(b + rr), s2);
+                            y[rr] = s2;
+                            if (with_norm) acc = __dadd_rn(acc, __dmul_rn(s2, s2));
+                        }
                     }
                 } else {
                     // long rows: products entry-parallel (in place), then
@@ -620,7 +644,7 @@ uint32_t plan_spmv_tiles(const cbgx_csr& A, cudaStream_t st) {
     CBGX_CUDA(cudaFreeAsync(d, st));
     CBGX_CUDA(cudaStreamSynchronize(st));
     for (int i = 3; i >= 0; --i)
-        if ((32 << i) <= kGroupThreads && h[i] <= static_cast<unsigned long long>(kTileEntries)) return 32u << i;
+        if ((32 << i) <= kTileRowsMax && h[i] <= static_cast<unsigned long long>(kTileEntries)) return 32u << i;
     return 0;
 }
 
@@ -723,7 +747,7 @@ int cbgx_csr_spmv_staged(const cbgx_csr* A, uint32_t tile_rows, const double* d_
                          double* d_y, double* d_ynorm2, int reduction, cbgx_workspace* ws, void* stream) {
     return guard([&] {
         check_csr(A);
-        if (tile_rows < 32 || tile_rows > static_cast<uint32_t>(kGroupThreads) || (tile_rows & (tile_rows - 1)))
+        if (tile_rows < 32 || tile_rows > static_cast<uint32_t>(kTileRowsMax) || (tile_rows & (tile_rows - 1)))
             throw Error(CBGX_EINVAL, "spmv: tile_rows must be a power of two in [32, 256]");
         if (d_ynorm2 && !ws) throw Error(CBGX_EINVAL, "spmv: fused norm needs a workspace");
         if (A->n_rows == 0) return;
