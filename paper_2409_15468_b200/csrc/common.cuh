@@ -100,6 +100,27 @@ __device__ __forceinline__ double decode_any(uint64_t code, uint32_t e_max, uint
     return __longlong_as_double(static_cast<long long>((neg << 63) | (static_cast<uint64_t>(e) << 52) | f52));
 }
 
+// 256-bit global accesses (sm_100: LDG/STG.E.ENL2.256): four doubles per
+// lane per instruction halve the LSU instructions of the streaming kernels.
+// The address must be 32-B aligned.
+__device__ __forceinline__ void ld4_cs(const double* p, double v[4]) {
+    asm volatile("ld.global.cs.v4.f64 {%0,%1,%2,%3}, [%4];"
+                 : "=d"(v[0]), "=d"(v[1]), "=d"(v[2]), "=d"(v[3]) : "l"(p));
+}
+__device__ __forceinline__ void ld4_nc(const double* p, double v[4]) {
+    asm volatile("ld.global.nc.v4.f64 {%0,%1,%2,%3}, [%4];"
+                 : "=d"(v[0]), "=d"(v[1]), "=d"(v[2]), "=d"(v[3]) : "l"(p));
+}
+__device__ __forceinline__ void st4(double* p, const double v[4]) {
+    asm volatile("st.global.v4.f64 [%0], {%1,%2,%3,%4};" ::"l"(p), "d"(v[0]), "d"(v[1]), "d"(v[2]), "d"(v[3])
+                 : "memory");
+}
+__device__ __forceinline__ void st4_cs(double* p, const double v[4]) {
+    asm volatile("st.global.cs.v4.f64 [%0], {%1,%2,%3,%4};" ::"l"(p), "d"(v[0]), "d"(v[1]), "d"(v[2]), "d"(v[3])
+                 : "memory");
+}
+__device__ __forceinline__ bool aligned32(const void* p) { return (reinterpret_cast<uintptr_t>(p) & 31u) == 0; }
+
 // Exact u32 -> double on the FP64 pipe: (2^52 + m) - 2^52. The conversion
 // instruction (I2F.F64.U32) issues on the XU pipe, 16 lanes/clk/SM, which
 // the FRSZ2 decode saturated (ncu: XU pipe 74% in the fused CGS kernel);
