@@ -120,12 +120,8 @@ __device__ __forceinline__ void step_lds<kF16>(Step<kF16>& st, const unsigned ch
 }
 
 __device__ __forceinline__ void load_w(const double* __restrict__ w, uint64_t n, uint64_t r, double out[4]) {
-    if (r + 3 < n && aligned32(w)) {
-        ld4_nc(w + r, out);
-    } else if (r + 3 < n) {
-        const double2 a = __ldg(reinterpret_cast<const double2*>(w + r));
-        const double2 b = __ldg(reinterpret_cast<const double2*>(w + r + 2));
-        out[0] = a.x; out[1] = a.y; out[2] = b.x; out[3] = b.y;
+    if (r + 3 < n) {
+        load4(w + r, out);
     } else {
 #pragma unroll
         for (int k = 0; k < 4; ++k) out[k] = r + k < n ? w[r + k] : 0.0;
@@ -320,11 +316,8 @@ cgs_update_kernel(BasisView B, uint64_t first, uint32_t cols, const double* __re
             for (int s = 0; s < Geo<F>::sub; ++s) {
                 if (s >= steps) break;
                 const uint64_t r = (sb + s) * kStepRows + 4u * threadIdx.x;
-                if (r + 3 < B.n && aligned32(w)) {
-                    st4(w + r, wv[s]);
-                } else if (r + 3 < B.n) {
-                    reinterpret_cast<double2*>(w + r)[0] = make_double2(wv[s][0], wv[s][1]);
-                    reinterpret_cast<double2*>(w + r)[1] = make_double2(wv[s][2], wv[s][3]);
+                if (r + 3 < B.n) {
+                    store4(w + r, wv[s]);
                 } else {
 #pragma unroll
                     for (int k = 0; k < 4; ++k)
@@ -714,11 +707,8 @@ __device__ __forceinline__ void fused_write(const FusedArgs& a, uint64_t r0, uin
         double v[4];
 #pragma unroll
         for (int k = 0; k < 4; ++k) v[k] = r + k < a.B.n ? __dmul_rn(wv[s][k], scale) : 0.0;
-        if (r + 3 < a.B.n && aligned32(a.v_out)) {
-            st4(a.v_out + r, v);
-        } else if (r + 3 < a.B.n) {
-            reinterpret_cast<double2*>(a.v_out + r)[0] = make_double2(v[0], v[1]);
-            reinterpret_cast<double2*>(a.v_out + r)[1] = make_double2(v[2], v[3]);
+        if (r + 3 < a.B.n) {
+            store4(a.v_out + r, v);
         } else {
 #pragma unroll
             for (int k = 0; k < 4; ++k)

@@ -42,7 +42,6 @@ compress4_kernel(const double* __restrict__ x, uint64_t n, uint64_t nb_write,
     const int lane = threadIdx.x & 31;
     uint32_t* wbuf = wbuf_all[threadIdx.x >> 5];
     const double s = kScale ? scale.value() : 1.0;
-    const bool a32 = aligned32(x), a32v = aligned32(v_out);
     const uint64_t nsteps = (nb_write + 3) / 4;
     const uint64_t warp = (static_cast<uint64_t>(blockIdx.x) * kWarps) + (threadIdx.x >> 5);
     const uint64_t nwarps = static_cast<uint64_t>(gridDim.x) * kWarps;
@@ -52,13 +51,7 @@ compress4_kernel(const double* __restrict__ x, uint64_t n, uint64_t nb_write,
         for (int u = 0; u < kSteps; ++u) {
             const uint64_t r = (s0 + u) * 128 + 4u * lane;
             if (s0 + u < nsteps && r + 3 < n) {
-                if (a32) {
-                    ld4_cs(x + r, v[u]);
-                } else {
-                    const double2 a = __ldcs(reinterpret_cast<const double2*>(x + r));
-                    const double2 b = __ldcs(reinterpret_cast<const double2*>(x + r + 2));
-                    v[u][0] = a.x; v[u][1] = a.y; v[u][2] = b.x; v[u][3] = b.y;
-                }
+                load4_cs(x + r, v[u]);
             } else {
 #pragma unroll
                 for (int k = 0; k < 4; ++k) v[u][k] = (s0 + u < nsteps && r + k < n) ? x[r + k] : 0.0;
@@ -79,11 +72,8 @@ compress4_kernel(const double* __restrict__ x, uint64_t n, uint64_t nb_write,
                 e = max(e, ek);
             }
             if (kScale && v_out) {
-                if (r + 3 < n && a32v) {
-                    st4(v_out + r, v[u]);
-                } else if (r + 3 < n) {
-                    reinterpret_cast<double2*>(v_out + r)[0] = make_double2(v[u][0], v[u][1]);
-                    reinterpret_cast<double2*>(v_out + r)[1] = make_double2(v[u][2], v[u][3]);
+                if (r + 3 < n) {
+                    store4(v_out + r, v[u]);
                 } else {
 #pragma unroll
                     for (int k = 0; k < 4; ++k)
@@ -130,7 +120,6 @@ decompress4_kernel(const uint32_t* __restrict__ exps, const uint32_t* __restrict
     __shared__ uint32_t wbuf_all[kWarps][84 + 4];
     const int lane = threadIdx.x & 31;
     uint32_t* wbuf = wbuf_all[threadIdx.x >> 5];
-    const bool a32 = aligned32(out);
     const uint64_t nb = (n + 31) / 32;
     const uint64_t nsteps = (nb + 3) / 4;
     const uint64_t warp = (static_cast<uint64_t>(blockIdx.x) * kWarps) + (threadIdx.x >> 5);
@@ -186,11 +175,8 @@ decompress4_kernel(const uint32_t* __restrict__ exps, const uint32_t* __restrict
             double v[4];
 #pragma unroll
             for (int k = 0; k < 4; ++k) v[k] = dec(code[k]);
-            if (r + 3 < n && a32) {
-                st4_cs(out + r, v);
-            } else if (r + 3 < n) {
-                __stcs(reinterpret_cast<double2*>(out + r), make_double2(v[0], v[1]));
-                __stcs(reinterpret_cast<double2*>(out + r) + 1, make_double2(v[2], v[3]));
+            if (r + 3 < n) {
+                store4(out + r, v, true);
             } else {
 #pragma unroll
                 for (int k = 0; k < 4; ++k)

@@ -120,6 +120,46 @@ __device__ __forceinline__ void st4_cs(double* p, const double v[4]) {
                  : "memory");
 }
 __device__ __forceinline__ bool aligned32(const void* p) { return (reinterpret_cast<uintptr_t>(p) & 31u) == 0; }
+__device__ __forceinline__ bool aligned16(const void* p) { return (reinterpret_cast<uintptr_t>(p) & 15u) == 0; }
+
+// Four consecutive doubles at an 8-B aligned address: one 256-bit access,
+// two 128-bit accesses or four scalar ones, by the address's alignment.
+__device__ __forceinline__ void load4(const double* p, double v[4]) {
+    if (aligned32(p)) {
+        ld4_nc(p, v);
+    } else if (aligned16(p)) {
+        const double2 a = __ldg(reinterpret_cast<const double2*>(p));
+        const double2 b = __ldg(reinterpret_cast<const double2*>(p) + 1);
+        v[0] = a.x; v[1] = a.y; v[2] = b.x; v[3] = b.y;
+    } else {
+#pragma unroll
+        for (int k = 0; k < 4; ++k) v[k] = __ldg(p + k);
+    }
+}
+__device__ __forceinline__ void load4_cs(const double* p, double v[4]) {
+    if (aligned32(p)) {
+        ld4_cs(p, v);
+    } else if (aligned16(p)) {
+        const double2 a = __ldcs(reinterpret_cast<const double2*>(p));
+        const double2 b = __ldcs(reinterpret_cast<const double2*>(p) + 1);
+        v[0] = a.x; v[1] = a.y; v[2] = b.x; v[3] = b.y;
+    } else {
+#pragma unroll
+        for (int k = 0; k < 4; ++k) v[k] = __ldcs(p + k);
+    }
+}
+__device__ __forceinline__ void store4(double* p, const double v[4], bool streaming = false) {
+    if (aligned32(p)) {
+        if (streaming) st4_cs(p, v);
+        else st4(p, v);
+    } else if (aligned16(p)) {
+        reinterpret_cast<double2*>(p)[0] = make_double2(v[0], v[1]);
+        reinterpret_cast<double2*>(p)[1] = make_double2(v[2], v[3]);
+    } else {
+#pragma unroll
+        for (int k = 0; k < 4; ++k) p[k] = v[k];
+    }
+}
 
 // Exact u32 -> double on the FP64 pipe: (2^52 + m) - 2^52. The conversion
 // instruction (I2F.F64.U32) issues on the XU pipe, 16 lanes/clk/SM, which

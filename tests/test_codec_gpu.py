@@ -167,3 +167,30 @@ def test_error_bound_and_truncation_oracle(cbg, port):
         assert np.all(np.abs(back) <= np.abs(v))
         for i in range(0, v.size, 4099):
             assert bits(back[i]) == bits(port.truncate_exact(v[i], int(e[i // 32]), l)[1])
+
+
+@pytest.mark.parametrize("l", [16, 21, 32])
+@pytest.mark.parametrize("offset", [1, 2, 3])
+def test_unaligned_vectors(cbg, port, l, offset):
+    """The fast codec uses 256-bit accesses when the fp64 vector is 32-B
+    aligned and 16-B/scalar accesses otherwise: compress from / decompress
+    into vectors offset by 8..24 bytes give the same bits."""
+    import torch
+    n = 4099
+    v = port_mixed(port, n)
+    big = torch.zeros(n + 8, dtype=torch.float64, device="cuda")
+    big[offset:offset + n] = torch.from_numpy(v).cuda()
+    src = big[offset:offset + n]
+    cv = cbg.compress(src, cbg.Frsz2Params(32, l))
+    e, p = port.compress(v, l)
+    assert np.array_equal(cv.exponents(), e) and np.array_equal(cv.payload_words(), p)
+    out_big = torch.full((n + 8,), 7.0, dtype=torch.float64, device="cuda")
+    dst = out_big[offset:offset + n]
+    cbg.decompress(cv, out=dst)
+    assert dst.cpu().numpy().tobytes() == port.decompress(e, p, n, l).tobytes()
+    assert (out_big[:offset] == 7.0).all() and (out_big[offset + n:] == 7.0).all()
+
+
+def port_mixed(port, n):
+    from oracle import pyoracle as po
+    return po.mixed_values(n, 7)

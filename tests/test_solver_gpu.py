@@ -261,3 +261,39 @@ def test_staged_and_csr_solves_agree(cbg, port):
     r2 = solve(cbg, rp, ci, va, b, "frsz2-32", 30, reduction=0, tma_spmv=False)
     assert hist(r1) == hist(r2)
     assert np.asarray(r1.solution).tobytes() == np.asarray(r2.solution).tobytes()
+
+
+def test_host_drop_in_reuses_state_across_calls(cbg, port):
+    """cbgx_gmres_solve_host keeps its buffers and solver between calls:
+    consecutive solves of different matrices of the same shape, a changed
+    configuration, a bigger and again a smaller problem all give the results
+    of fresh solves (reference order: bit-identical histories)."""
+    cases = []
+    for pe in (1.0, 0.5, 2.0):
+        rp, ci, va = port.convdiff(14, 14, pe)
+        b, _ = port.generate_problem(rp, ci, va)
+        cases.append((rp, ci, va, b))
+    rp2, ci2, va2 = port.stencil(0, 12, 12, 12)
+    b2, _ = port.generate_problem(rp2, ci2, va2)
+    seq = [(cases[0], "frsz2-32"), (cases[1], "frsz2-32"), (cases[2], "f64"), ((rp2, ci2, va2, b2), "frsz2-32"),
+           (cases[0], "frsz2-32")]
+    for (rp, ci, va, b), fmt in seq:
+        r = solve(cbg, rp, ci, va, b, fmt, 30, reduction=1)
+        o = port.gmres(rp, ci, va, b, fmt=fmt, restart=30)
+        assert r.total_iterations == o["iterations"]
+        assert [(h.iteration, h.rrn, h.is_explicit) for h in r.residual_history] == o["history"]
+
+
+def test_gmres_solve_out_parameter(cbg, port):
+    import torch
+    rp, ci, va = port.convdiff(10, 10, 1.0)
+    b, _ = port.generate_problem(rp, ci, va)
+    n = rp.size - 1
+    cfg = cbg.GmresConfig(restart=20, storage_format=cbg.StorageFormat.frsz2_format(32))
+    out = torch.empty(n, dtype=torch.float64).pin_memory().numpy()
+    r1 = cbg.gmres_solve(cbg.CsrMatrix(n, n, rp, ci, va), b, np.zeros(n), cfg, out=out)
+    r2 = cbg.gmres_solve(cbg.CsrMatrix(n, n, rp, ci, va), b, np.zeros(n), cfg)
+    assert out.tobytes() == np.asarray(r2.solution).tobytes()
+    assert r1.solution is out or np.shares_memory(np.asarray(r1.solution), out)
+    with pytest.raises(ValueError):
+        cbg.gmres_solve(cbg.CsrMatrix(n, n, rp, ci, va), b, np.zeros(n), cfg, out=np.zeros(n - 1))
