@@ -67,8 +67,10 @@ def test_basis_layout(L):
     db, eb = ctypes.c_uint64(), ctypes.c_uint64()
     assert L.cbgx_basis_layout(3, 21, 100, 5, ctypes.byref(B), ctypes.byref(db), ctypes.byref(eb)) == 0
     assert B.n_pad % 8192 == 0 and B.n_pad >= 100
-    assert B.col_stride_bytes == B.n_pad // 32 * 21 * 4
-    assert B.exp_col_stride == B.n_pad // 32
+    # each column: n_pad rows + a 2048-row zero tail (whole fused steps)
+    assert B.col_stride_bytes == (B.n_pad + 2048) // 32 * 21 * 4
+    assert B.exp_col_stride == (B.n_pad + 2048) // 32
+    assert db.value == B.col_stride_bytes * 5 + 64 and eb.value == B.exp_col_stride * 5 * 4
     assert L.cbgx_basis_layout(3, 24, 100, 5, ctypes.byref(B), None, None) == 1
     assert "bit length" in L.cbgx_last_error().decode()
 
