@@ -292,6 +292,13 @@ int cbgx_solver_solve(cbgx_solver* s, const double* d_b, const double* d_x0, dou
  * CBGX_SOLVER_PHASE_TIMING_DEFERRED since the last call; resets. */
 int cbgx_solver_phase_times(cbgx_solver* s, double* ms, uint64_t count);
 
+/* Streaming read benchmark (run_read_benchmark, bench.cpp:55-152; paper
+ * Fig. 3): decode the first n values (n % 32 == 0) of basis column `col`,
+ * apply `intensity` multiply-adds per value (v = v * mul + add, two
+ * roundings) and sum everything into *d_checksum (fixed-shape tree). */
+int cbgx_read_sweep(const cbgx_basis* V, uint64_t col, uint64_t n, int intensity, double mul, double add,
+                    double* d_checksum, cbgx_workspace* ws, void* stream);
+
 /* Host-buffer drop-in for gmres_solve(const CsrMatrix&, span b, span x0,
  * cfg) (gmres.hpp:113-115): size_t CSR as in CsrMatrix, uploads, solves on
  * the current device, downloads the solution. */

@@ -486,6 +486,71 @@ def spmv(a: DeviceCsr, x, y=None, want_norm=False, reduction=_lib.REDUCE_TREE):
     return (y[:a.desc.n_rows], nrm) if want_norm else y[:a.desc.n_rows]
 
 
+@dataclasses.dataclass
+class BenchResult:
+    """bench.hpp:15-24."""
+    format: str
+    intensity: int
+    elements: int
+    stored_bytes: int
+    seconds: float       # minimum over trials (CUDA events)
+    stored_gbps: float   # stored bytes / time
+    logical_gbps: float  # 8 * elements / time
+
+
+def _read_sweep_launch(basis, col, n, intensity, mul, add, out):
+    import ctypes
+    check(lib().cbgx_read_sweep(ctypes.byref(basis.desc), col, n, intensity, mul, add, _ptr(out), _ws(), _stream()))
+
+
+def read_sweep(basis: "KrylovBasis", col: int, n: int, intensity: int, mul: float, add: float) -> float:
+    """One device sweep (cbgx_read_sweep): checksum of decode + intensity FMAs."""
+    torch = _torch()
+    out = torch.empty(1, dtype=torch.float64, device="cuda")
+    _read_sweep_launch(basis, col, n, intensity, mul, add, out)
+    return float(out.item())
+
+
+def read_benchmark(elements: int, formats, intensities, trials: int = 10, seed: int = 0) -> List[BenchResult]:
+    """run_read_benchmark (bench.hpp:28-30, bench.cpp:100-152) on the device:
+    uniform[-1, 1) data of `elements` (rounded down to whole 32-blocks),
+    stored in each format, decoded and swept with `intensity` multiply-adds
+    per value; the minimum kernel time over `trials` runs (after a warm-up
+    run) per (format, intensity)."""
+    torch = _torch()
+    if elements < 32:
+        raise ValueError("bench: need at least one block")
+    if trials < 1:
+        raise ValueError("bench: trials must be >= 1")
+    if any(i < 1 for i in intensities):
+        raise ValueError("bench: intensity must be >= 1")
+    n = elements // 32 * 32
+    g = torch.Generator(device="cuda").manual_seed(seed)
+    data = torch.rand(n, dtype=torch.float64, device="cuda", generator=g) * 2 - 1
+    u = (torch.rand(2, dtype=torch.float64, device="cuda", generator=g) * 2 - 1).tolist()
+    mul, add = 1.0 + u[0] * 1e-7, u[1] * 1e-9
+    out = []
+    for f in formats:
+        fmt = StorageFormat.parse(f) if isinstance(f, str) else f
+        basis = KrylovBasis(n, 1, fmt)
+        basis.write_vector(0, data)
+        stored = fmt.column_bytes(n)
+        chk = torch.empty(1, dtype=torch.float64, device="cuda")
+        for inten in intensities:
+            _read_sweep_launch(basis, 0, n, inten, mul, add, chk)  # warm-up
+            best = float("inf")
+            for _ in range(trials):
+                e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+                e0.record()
+                _read_sweep_launch(basis, 0, n, inten, mul, add, chk)
+                e1.record()
+                torch.cuda.synchronize()
+                best = min(best, e0.elapsed_time(e1) * 1e-3)
+            out.append(BenchResult(fmt.name(), inten, n, stored, best, stored / best / 1e9, 8.0 * n / best / 1e9))
+        del basis
+    return out
+
+
 def spmv_plan(a: DeviceCsr) -> int:
     """Tile height of the staged SpMV for this matrix (0: not stageable)."""
     import ctypes

@@ -194,6 +194,18 @@ __device__ __forceinline__ double frsz_dot(const Codes4& c, uint32_t e, const do
     return s;
 }
 
+// The 4 decoded values (warp-uniform fast/exact split like frsz_dot).
+template <int L>
+__device__ __forceinline__ void frsz_decode(const Codes4& c, uint32_t e, double v[4]) {
+    if (__builtin_expect(__all_sync(0xFFFFFFFFu, e > L - 2), 1)) {
+        const double sc = __hiloint2double(static_cast<int>((e - (L - 2)) << 20), 0);
+#pragma unroll
+        for (int k = 0; k < 4; ++k) v[k] = __dmul_rn(signed_i2f(c.mag[k], c.sgn[k]), sc);
+        return;
+    }
+    slow_decode<L>(c, e, v);
+}
+
 // h_exp: biased exponent field of h (hoisted per column by the caller).
 template <int L>
 __device__ __forceinline__ void frsz_update(const Codes4& c, uint32_t e, double h, int h_exp, double w[4]) {
@@ -239,6 +251,7 @@ template <> struct Step<kZ32> {
         return k;
     }
     __device__ __forceinline__ double dot(const double w[4]) const { return frsz_dot<32>(codes(), e, w); }
+    __device__ __forceinline__ void decode(double v[4]) const { frsz_decode<32>(codes(), e, v); }
     __device__ __forceinline__ void update(double h, int he, double w[4]) const { frsz_update<32>(codes(), e, h, he, w); }
 };
 
@@ -258,6 +271,7 @@ template <> struct Step<kZ16> {
         return k;
     }
     __device__ __forceinline__ double dot(const double w[4]) const { return frsz_dot<16>(codes(), e, w); }
+    __device__ __forceinline__ void decode(double v[4]) const { frsz_decode<16>(codes(), e, v); }
     __device__ __forceinline__ void update(double h, int he, double w[4]) const { frsz_update<16>(codes(), e, h, he, w); }
 };
 
@@ -289,6 +303,7 @@ template <> struct Step<kZ21> {
         return k;
     }
     __device__ __forceinline__ double dot(const double w[4]) const { return frsz_dot<21>(codes(), e, w); }
+    __device__ __forceinline__ void decode(double v[4]) const { frsz_decode<21>(codes(), e, v); }
     __device__ __forceinline__ void update(double h, int he, double w[4]) const { frsz_update<21>(codes(), e, h, he, w); }
 };
 
@@ -300,6 +315,7 @@ template <> struct Step<kF64> {
         b = __ldg(p + 1);
     }
     __device__ __forceinline__ void values(double v[4]) const { v[0] = a.x; v[1] = a.y; v[2] = b.x; v[3] = b.y; }
+    __device__ __forceinline__ void decode(double v[4]) const { values(v); }
     __device__ __forceinline__ double dot(const double w[4]) const {
         double v[4];
         values(v);
@@ -322,6 +338,7 @@ template <> struct Step<kF32> {
         c = __ldg(reinterpret_cast<const float4*>(B.data + col * B.col_stride_bytes) + r / 4);
     }
     __device__ __forceinline__ void values(double v[4]) const { v[0] = c.x; v[1] = c.y; v[2] = c.z; v[3] = c.w; }
+    __device__ __forceinline__ void decode(double v[4]) const { values(v); }
     __device__ __forceinline__ double dot(const double w[4]) const {
         double v[4];
         values(v);
@@ -344,9 +361,29 @@ template <> struct Step<kF16> {
         c = __ldg(reinterpret_cast<const uint2*>(B.data + col * B.col_stride_bytes) + r / 4);
     }
     __device__ __forceinline__ void values(double v[4]) const {
-        v[0] = half_bits_to_double(c.x & 0xFFFFu); v[1] = half_bits_to_double(c.x >> 16);
-        v[2] = half_bits_to_double(c.y & 0xFFFFu); v[3] = half_bits_to_double(c.y >> 16);
+        const uint32_t h[4] = {c.x & 0xFFFFu, c.x >> 16, c.y & 0xFFFFu, c.y >> 16};
+        // warp-uniform fast path: normal halves and signed zeros widen by
+        // re-biasing the exponent (exact); subnormal / inf / nan take the
+        // general conversion (half.cpp:62-81)
+        bool fast = true;
+#pragma unroll
+        for (int k = 0; k < 4; ++k) {
+            const uint32_t e = (h[k] >> 10) & 31u;
+            fast = fast && e != 31u && (e != 0u || (h[k] & 1023u) == 0u);
+        }
+        if (__builtin_expect(__all_sync(0xFFFFFFFFu, fast), 1)) {
+#pragma unroll
+            for (int k = 0; k < 4; ++k) {
+                const uint32_t e = (h[k] >> 10) & 31u;
+                const uint32_t hi = ((h[k] & 0x8000u) << 16) | (e ? ((e + 1008u) << 20) | ((h[k] & 1023u) << 10) : 0u);
+                v[k] = __hiloint2double(static_cast<int>(hi), 0);
+            }
+            return;
+        }
+#pragma unroll
+        for (int k = 0; k < 4; ++k) v[k] = half_bits_to_double(h[k]);
     }
+    __device__ __forceinline__ void decode(double v[4]) const { values(v); }
     __device__ __forceinline__ double dot(const double w[4]) const {
         double v[4];
         values(v);

@@ -152,3 +152,37 @@ def test_fused_scale_write(cbg):
     assert v.cpu().numpy().tobytes() == want.tobytes()
     B.write_vector(1, want)
     assert B.read_column(0).cpu().numpy().tobytes() == B.read_column(1).cpu().numpy().tobytes()
+
+
+@pytest.mark.parametrize("fmt", ["f64", "f32", "f16", "frsz2-16", "frsz2-21", "frsz2-32"])
+def test_read_sweep_checksum(cbg, port, fmt):
+    """Read benchmark sweep (bench.cpp:55-96): decoded values after
+    `intensity` two-rounding multiply-adds, summed; vs the oracle decode +
+    numpy's identical arithmetic (summation order differs: 1e-12 rel.)."""
+    import torch
+    n = 32 * 1000
+    v = np.random.default_rng(5).uniform(-1, 1, n)
+    B = cbg.KrylovBasis(n, 2, cbg.StorageFormat.parse(fmt))
+    B.write_vector(0, -v)  # columns are written in order (basis.cpp:85-115)
+    B.write_vector(1, v)
+    dec = port.basis_roundtrip(fmt, v)
+    mul, add = 1.0 + 3e-8, -2e-10
+    for inten in (1, 3):
+        buf = dec.copy()
+        for _ in range(inten):
+            buf = buf * mul + add
+        want = float(np.sum(buf, dtype=np.float64))
+        got = cbg.read_sweep(B, 1, n, inten, mul, add)
+        assert abs(got - want) <= 1e-12 * np.sum(np.abs(buf)), (fmt, inten, got, want)
+    # partial length (multiple of 32) and argument checks
+    got = cbg.read_sweep(B, 1, 64, 1, 1.0, 0.0)
+    assert abs(got - float(np.sum(dec[:64]))) <= 1e-14
+    with pytest.raises(Exception):
+        cbg.read_sweep(B, 1, 33, 1, 1.0, 0.0)
+
+
+def test_read_benchmark_api(cbg):
+    res = cbg.read_benchmark(1 << 16, ["f64", "frsz2-32"], [1, 4], trials=2, seed=3)
+    assert [(r.format, r.intensity) for r in res] == [("f64", 1), ("f64", 4), ("frsz2-32", 1), ("frsz2-32", 4)]
+    assert res[0].stored_bytes == 8 * 65536 and res[2].stored_bytes == 2048 * 4 * 33
+    assert all(r.seconds > 0 and r.logical_gbps > 0 for r in res)
