@@ -314,6 +314,8 @@ int cbgx_host_cache_release(void);
 /* Debug: globaltimer stamps of CTA 0 in the last fused orthogonalisation
  * launch (requires CBGX_TRACE_FUSED=1 in the environment). */
 int cbgx_debug_fused_trace(uint64_t* out, int count);
+/* diagnostic: rotate the fused kernel's CTA -> row-range map by `rot` (0 = production) */
+int cbgx_debug_fused_rotation(uint32_t rot);
 
 /* ---------------------------------------------- multi-GPU row partition
  * One process per GPU; each rank owns rows [row_begin, row_end) (multiples

@@ -69,6 +69,7 @@ def lib():
             "cbgx_sin_solution": ([u64, u64, u64, vp, C.c_int], C.c_int),
             "cbgx_halo_exchange": ([vp, vp, vp], C.c_int),
             "cbgx_debug_fused_trace": ([vp, C.c_int], C.c_int),
+            "cbgx_debug_fused_rotation": ([u32], C.c_int),
             "cbgx_device_info": ([P(C.c_int), P(C.c_int), P(i64)], C.c_int),
             "cbgx_frsz2_num_blocks": ([u64, u32], u64),
             "cbgx_frsz2_words_per_block": ([u32, u32], u64),

@@ -587,6 +587,7 @@ struct FusedArgs {
     double eta;
     double* partials;          // kRegions regions of (cols + 1) x gs doubles (value-major)
     uint32_t gs;               // gridDim.x rounded up to even
+    uint32_t rot;              // diagnostic rotation of the row ranges (cbgx_debug_fused_rotation)
     unsigned* bar;             // this launch's arrival counter (zero at launch)
     unsigned* bar_next;        // the next launch's counter: zeroed here (CTA 0)
     unsigned* gate_hist;       // previous launch's gate: 0 open (speculate), 1 closed
@@ -620,10 +621,11 @@ __device__ __forceinline__ unsigned ld_acquire(const unsigned* p) {
 }
 
 // This CTA's rows: [r0, r1) in 128-row units, balanced over the grid.
-__device__ __forceinline__ void fused_rows(uint64_t n, uint64_t& r0, uint64_t& r1) {
+__device__ __forceinline__ void fused_rows(uint64_t n, uint32_t rot, uint64_t& r0, uint64_t& r1) {
     const uint64_t units = (n + kUnitRows - 1) / kUnitRows;
-    r0 = units * blockIdx.x / gridDim.x * kUnitRows;
-    r1 = units * (blockIdx.x + 1) / gridDim.x * kUnitRows;
+    const uint64_t slot = (blockIdx.x + rot) % gridDim.x;  // rot: diagnostic only (0 in production)
+    r0 = units * slot / gridDim.x * kUnitRows;
+    r1 = units * (slot + 1) / gridDim.x * kUnitRows;
 }
 
 // Grid all-reduce among the consumer warps of all (co-resident) CTAs, one
@@ -872,7 +874,7 @@ __global__ void __launch_bounds__(kFThreads, kFCtasPerSM) arnoldi_fused_kernel(F
     if (blockIdx.x == 0 && threadIdx.x == 0) *a.bar_next = 0u;
     __syncthreads();
     uint64_t r0, r1;
-    fused_rows(a.B.n, r0, r1);
+    fused_rows(a.B.n, a.rot, r0, r1);
     const uint32_t lim = static_cast<uint32_t>(r1 - r0);
     const uint32_t steps = (lim + kFStepRows - 1) / kFStepRows;
     constexpr int kChunkSteps = FGeo<F>::chunk;
@@ -1010,6 +1012,10 @@ __global__ void __launch_bounds__(kFThreads, kFCtasPerSM) arnoldi_fused_kernel(F
     FTRACE(10);
 }
 
+// Diagnostic: rotate the CTA -> row-range map (are slow CTAs slow because of
+// their SM or their rows?). 0 in production.
+uint32_t g_fused_rot = 0;
+
 // Debug timeline of the fused kernel (CTA 0): enabled by CBGX_TRACE_FUSED=1,
 // read back with cbgx_debug_fused_trace.
 unsigned long long* g_trace = nullptr;
@@ -1096,6 +1102,7 @@ template <int F> struct FusedLaunch {
         a.gate_hist = c + Workspace::kFusedGate;
         a.trace = fused_trace_buffer();
         a.host_slot = host_slot;
+        a.rot = g_fused_rot;
         cudaLaunchConfig_t lc = {};
         lc.gridDim = dim3(grid);
         lc.blockDim = dim3(kFThreads);
@@ -1254,6 +1261,10 @@ int cbgx_cgs_update(const cbgx_basis* V, uint64_t first, uint32_t cols, const do
         launch_cgs_update(*V, first, cols, d_h, h_sign < 0 ? -1.0 : 1.0, d_w, d_wnorm2, reduction,
                           ws_of(ws), as_stream(stream));
     });
+}
+
+int cbgx_debug_fused_rotation(uint32_t rot) {
+    return guard([&] { g_fused_rot = rot; });
 }
 
 int cbgx_debug_fused_trace(uint64_t* out, int count) {

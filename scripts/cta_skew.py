@@ -13,6 +13,9 @@ from paper_2409_15468_b200 import _lib  # noqa: E402
 
 A = cbg.stencil(0, 128)
 b = cbg.spmv(A, torch.from_numpy(cbg.sin_problem_host(128 ** 3)).cuda())
+rot = int(sys.argv[1]) if len(sys.argv) > 1 else 0
+_lib.check(_lib.lib().cbgx_debug_fused_rotation(rot))
+print("rotation", rot)
 runs = []
 for its in (20, 21, 22, 20, 21):
     S = cbg.Solver(A, cbg.GmresConfig(storage_format=cbg.StorageFormat.parse("frsz2-32"), max_total_iterations=its))
@@ -32,6 +35,12 @@ a = runs[0][0]
 print("dot1 per-CTA us: min %.1f med %.1f max %.1f" % (a.min(), np.median(a), a.max()))
 order = np.argsort(-a)
 print("slowest CTAs", order[:12].tolist(), "fastest", order[-8:].tolist())
+G = len(a)
+slots = [(int(c) + rot) % G for c in order[:12]]
+print("slowest slots (row ranges)", slots)
+u = runs[0][1]
+ou = np.argsort(-u)
+print("upd1 slowest CTAs", ou[:12].tolist(), "slots", [(int(c) + rot) % G for c in ou[:12]])
 # by SM pair (c, c+148) and by index parity
 G = len(a)
 print("mean dot1 by CTA half: first %.2f second %.2f" % (a[:G // 2].mean(), a[G // 2:].mean()))
