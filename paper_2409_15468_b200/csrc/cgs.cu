@@ -562,10 +562,16 @@ template <int F> struct FBytes {
 
 // Ring stage = one column's segment of `chunk` steps (~32 KB), `stages` deep
 // (~100 KB of shared memory per CTA at two CTAs per SM).
+#ifndef FUSED_CHUNK_BYTES
+#define FUSED_CHUNK_BYTES 32768
+#endif
+#ifndef FUSED_RING_BYTES
+#define FUSED_RING_BYTES 100000
+#endif
 template <int F> struct FGeo {
-    static constexpr int chunk_raw = static_cast<int>(32768 / (FBytes<F>::pay + FBytes<F>::ex));
+    static constexpr int chunk_raw = static_cast<int>(FUSED_CHUNK_BYTES / (FBytes<F>::pay + FBytes<F>::ex));
     static constexpr int chunk = chunk_raw < 1 ? 1 : (chunk_raw > kFusedMaxSteps ? kFusedMaxSteps : chunk_raw);
-    static constexpr int stages_raw = static_cast<int>((kFCtasPerSM == 1 ? 170000 : 100000) /
+    static constexpr int stages_raw = static_cast<int>((kFCtasPerSM == 1 ? 170000 : FUSED_RING_BYTES) /
                                                        (chunk * (FBytes<F>::pay + FBytes<F>::ex) + 32));
     static constexpr int stages = stages_raw < 2 ? 2 : stages_raw;
 };

@@ -165,8 +165,15 @@ __device__ __forceinline__ void store4(double* p, const double v[4], bool stream
 // instruction (I2F.F64.U32) issues on the XU pipe, 16 lanes/clk/SM, which
 // the FRSZ2 decode saturated (ncu: XU pipe 74% in the fused CGS kernel);
 // DADD runs at the FP64 rate.
+#ifndef FRSZ_CONV_I2F
+#define FRSZ_CONV_I2F 0
+#endif
 __device__ __forceinline__ double u32_to_f64(uint32_t m) {
+#if FRSZ_CONV_I2F
+    return __uint2double_rn(m);  // XU pipe (A/B builds)
+#else
     return __dsub_rn(__hiloint2double(0x43300000, static_cast<int>(m)), 0x1p52);
+#endif
 }
 
 // Per-block decode context for the fixed-rate formats (L <= 32).

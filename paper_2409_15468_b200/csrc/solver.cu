@@ -178,7 +178,7 @@ void Solver::setup_matrix(bool before_basis, cudaStream_t st) {
     if (A_.max_row_nnz == 0) A_.max_row_nnz = csr_max_row_nnz(A_, st);
     uint32_t plan = 0;
     if (!(cfg_.flags & CBGX_SOLVER_NO_TMA_SPMV)) plan = plan_spmv_tiles(A_, st);
-    if (plan == 256) tile_rows_ = plan;
+    if (plan >= 128 && A_.max_row_nnz < 16) tile_rows_ = plan;
     if (!tile_rows_ && !(cfg_.flags & CBGX_SOLVER_NO_SELL) && A_.max_row_nnz >= 16) {
         uint64_t db = 0, eb = 0;
         if (before_basis) {

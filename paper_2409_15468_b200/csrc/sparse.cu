@@ -165,8 +165,14 @@ sell_spmv_kernel(uint64_t n_rows, const RP* __restrict__ rp, const uint64_t* __r
 // That is exactly the reference's mul-then-add sequence (sparse.cpp:50-52),
 // so y is bit-identical to spmv(). The last <16 B of an array that a bulk
 // copy cannot cover (end of allocation) is read directly from global.
-constexpr int kTileEntries = 2048;
-constexpr int kSpmvStages = 4;
+#ifndef SPMV_TILE_ENTRIES
+#define SPMV_TILE_ENTRIES 2048
+#endif
+#ifndef SPMV_STAGES
+#define SPMV_STAGES 4
+#endif
+constexpr int kTileEntries = SPMV_TILE_ENTRIES;
+constexpr int kSpmvStages = SPMV_STAGES;
 constexpr int kSpmvConsumers = 256;
 // Consumer groups take alternate tiles (measured on B200: one group of 8
 // warps with 256-row tiles beats two groups with 128-row tiles -- the
