@@ -43,6 +43,19 @@ WORKLOADS = {
 FMT_BYTES = {"f64": 8.0, "f32": 4.0, "f16": 2.0, "frsz2-16": 17 / 8, "frsz2-21": 22 / 8, "frsz2-32": 33 / 8}
 
 
+def traffic_for(kernel):
+    """Measured DRAM bytes per launch of `kernel` from the committed ncu
+    launch list of one solve (profiles/traffic.json, scripts/
+    traffic_from_launches.py); None when absent."""
+    p = os.path.join(ROOT, "profiles", "traffic.json")
+    if not os.path.exists(p):
+        return None, None
+    with open(p) as f:
+        d = json.load(f)
+    e = d.get(kernel)
+    return (e["bytes_per_launch"], d.get("_source")) if e else (None, None)
+
+
 def peaks():
     p = os.path.join(ROOT, "MEASURED_PEAKS.json")
     if os.path.exists(p):
@@ -348,7 +361,11 @@ def run_ours(args):
                 "peak_source": peak_kind,
                 "unit": "GB/s",
                 "frac": round(achieved / peak, 4) if achieved else None,
-                "traffic": None,
+                "traffic": traffic_for(kernel_name)[0],
+                "traffic_source": "ncu dram__bytes_read.sum + dram__bytes_write.sum per launch, averaged over one "
+                                  "solve's launches of this kernel (%s); compare with algorithmic_bytes_per_launch"
+                                  % traffic_for(kernel_name)[1],
+                "algorithmic_bytes_per_launch": round(ph_bytes[dominant] / max(1, ph_launch[dominant])),
                 "algorithmic_bytes_per_solve": ph_bytes[dominant],
                 "launches_per_solve": ph_launch[dominant],
                 "note": "achieved = algorithmic bytes of the %s phase (sum over its launches in a solve; basis "
