@@ -81,6 +81,10 @@ void launch_spmv_sell(const cbgx_csr& A, const Sell& S, const double* x, const d
 // Staged (TMA) CSR SpMV: plan_spmv_tiles returns the tile height (32..256
 // rows, 0 when some tile would exceed the stage capacity).
 uint32_t plan_spmv_tiles(const cbgx_csr& A, cudaStream_t st);
+// Stream-ordered CSR statistics [max_row, max 32/64/128/256-row tile nnz]
+// into d_out[5] (no sync), and the tile plan they imply.
+void launch_csr_stats(const cbgx_csr& A, unsigned long long* d_out, cudaStream_t st);
+uint32_t plan_from_stats(const unsigned long long* h);
 void launch_spmv_tma(const cbgx_csr& A, uint32_t tile_rows, const double* x, const double* b, double* y,
                      double* norm, int reduction, Workspace* ws, cudaStream_t st, bool pdl = false);
 

@@ -15,6 +15,8 @@
 #include <algorithm>
 #include <chrono>
 #include <cmath>
+#include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <memory>
 #include <mutex>
@@ -172,12 +174,13 @@ Solver::Solver(const cbgx_csr& A, const cbgx_gmres_config& cfg, Comm* comm, Halo
 // 93% vs 81% of HBM peak); for long rows a SELL-32 copy when memory allows
 // (27-pt 128^3: 4.8 vs 5.4 ms/solve of SpMV), else staged with smaller
 // tiles, else the plain CSR kernel.
-void Solver::setup_matrix(bool before_basis, cudaStream_t st) {
+void Solver::setup_matrix(bool before_basis, cudaStream_t st, const unsigned long long* stats) {
     sell_.reset();
     tile_rows_ = 0;
+    if (stats) A_.max_row_nnz = static_cast<uint32_t>(stats[0]);
     if (A_.max_row_nnz == 0) A_.max_row_nnz = csr_max_row_nnz(A_, st);
     uint32_t plan = 0;
-    if (!(cfg_.flags & CBGX_SOLVER_NO_TMA_SPMV)) plan = plan_spmv_tiles(A_, st);
+    if (!(cfg_.flags & CBGX_SOLVER_NO_TMA_SPMV)) plan = stats ? plan_from_stats(stats) : plan_spmv_tiles(A_, st);
     if (plan >= 128 && A_.max_row_nnz < 16) tile_rows_ = plan;
     if (!tile_rows_ && !(cfg_.flags & CBGX_SOLVER_NO_SELL) && A_.max_row_nnz >= 16) {
         uint64_t db = 0, eb = 0;
@@ -193,10 +196,10 @@ void Solver::setup_matrix(bool before_basis, cudaStream_t st) {
     if (!tile_rows_ && !sell_) tile_rows_ = plan;  // no SELL copy (memory): staged if any tile fits
 }
 
-void Solver::rebind(const cbgx_csr& A, cudaStream_t st) {
+void Solver::rebind(const cbgx_csr& A, cudaStream_t st, const unsigned long long* stats) {
     if (A.n_rows != n_ || A.n_cols != A_.n_cols) throw Error(CBGX_EINVAL, "solver: rebind needs the same shape");
     A_ = A;
-    setup_matrix(false, st);
+    setup_matrix(false, st, stats);
 }
 
 void Solver::collect_phases(double* ms, size_t count) {
@@ -546,7 +549,7 @@ struct HostSolveCache {
     void ensure(uint64_t n, uint64_t nnz, bool wide) {
         (void)wide;
         if (!st) CBGX_CUDA(cudaStreamCreateWithFlags(&st, cudaStreamNonBlocking));
-        if (!h_bad) CBGX_CUDA(cudaMallocHost(&h_bad, sizeof(uint64_t)));
+        if (!h_bad) CBGX_CUDA(cudaMallocHost(&h_bad, 6 * sizeof(uint64_t)));
         if (n <= cap_n && nnz <= cap_nnz && d_bad) return;
         solver.reset();  // it points into the buffers
         free_buffers();
@@ -559,7 +562,7 @@ struct HostSolveCache {
         CBGX_CUDA(cudaMalloc(&d_x, N * 8));
         CBGX_CUDA(cudaMalloc(&d_ci, Z * 4));
         CBGX_CUDA(cudaMalloc(&d_rp32, (N + 1) * 4));
-        CBGX_CUDA(cudaMalloc(&d_bad, 8));
+        CBGX_CUDA(cudaMalloc(&d_bad, 6 * 8));  // [bad index flag, csr stats x5]
         cap_n = n;
         cap_nnz = nnz;
     }
@@ -628,6 +631,13 @@ int cbgx_gmres_solve_host(uint64_t n, const uint64_t* row_ptrs, const uint64_t* 
         const bool wide = nnz > 0x7FFFFFFFull;
         HostSolveCache& H = host_cache();
         std::lock_guard<std::mutex> lock(H.mu);
+        static const bool prof = [] {
+            const char* e = getenv("CBGX_PROFILE_HOST_SOLVE");
+            return e && e[0] == '1';
+        }();
+        auto tnow = [] { return std::chrono::steady_clock::now(); };
+        auto ms = [](auto a, auto b) { return std::chrono::duration<double, std::milli>(b - a).count(); };
+        const auto t0 = tnow();
         H.ensure(n, nnz, wide);
         cudaStream_t st = H.st;
         // Stream-ordered staging: the size_t CSR of the reference
@@ -639,24 +649,36 @@ int cbgx_gmres_solve_host(uint64_t n, const uint64_t* row_ptrs, const uint64_t* 
         CBGX_CUDA(cudaMemcpyAsync(H.d_va, values, nnz * 8, cudaMemcpyHostToDevice, st));
         CBGX_CUDA(cudaMemcpyAsync(H.d_b, b, n * 8, cudaMemcpyHostToDevice, st));
         CBGX_CUDA(cudaMemcpyAsync(H.d_x0, x0, n * 8, cudaMemcpyHostToDevice, st));
+        if (prof) CBGX_CUDA(cudaStreamSynchronize(st));
+        const auto t1 = tnow();
         void* d_rp = wide ? static_cast<void*>(H.d_rp64) : static_cast<void*>(H.d_rp32);
         narrow_csr(H.d_rp64, n, wide ? nullptr : H.d_rp32, H.d_ci64, nnz, H.d_ci, H.d_bad, st);
-        CBGX_CUDA(cudaMemcpyAsync(H.h_bad, H.d_bad, 8, cudaMemcpyDeviceToHost, st));
+        cbgx_csr A{n, n, nnz, d_rp, wide ? 64u : 32u, H.d_ci, H.d_va};
+        // the SpMV set-up statistics ride along with the range check: one sync
+        launch_csr_stats(A, reinterpret_cast<unsigned long long*>(H.d_bad + 1), st);
+        CBGX_CUDA(cudaMemcpyAsync(H.h_bad, H.d_bad, 6 * 8, cudaMemcpyDeviceToHost, st));
         CBGX_CUDA(cudaStreamSynchronize(st));
         if (*H.h_bad) throw Error(CBGX_EINVAL, "csr: column index out of range");
-        cbgx_csr A{n, n, nnz, d_rp, wide ? 64u : 32u, H.d_ci, H.d_va};
+        const unsigned long long* csr_stats = reinterpret_cast<const unsigned long long*>(H.h_bad + 1);
+        const auto t2 = tnow();
         // One solver per configuration and shape, kept between calls (its
         // basis, vectors and workspaces); only the matrix-dependent SpMV
         // state is recomputed for the new contents.
         if (H.solver && H.solver->rows() == n && same_config(H.solver->config(), c)) {
-            H.solver->rebind(A, st);
+            H.solver->rebind(A, st, csr_stats);
         } else {
             H.solver.reset();
             H.solver = std::make_unique<Solver>(A, c, nullptr, nullptr);
         }
+        const auto t3 = tnow();
         H.solver->solve(H.d_b, H.d_x0, H.d_x, hist, stats, st);
+        const auto t4 = tnow();
         CBGX_CUDA(cudaMemcpyAsync(x_out, H.d_x, n * 8, cudaMemcpyDeviceToHost, st));
         CBGX_CUDA(cudaStreamSynchronize(st));
+        if (prof)
+            fprintf(stderr, "cbgx host solve: h2d %.3f ms (%.1f GB/s) narrow %.3f setup %.3f solve %.3f d2h %.3f\n",
+                    ms(t0, t1), ((n + 1) * 8.0 + nnz * 16.0 + n * 16.0) / ms(t0, t1) / 1e6, ms(t1, t2), ms(t2, t3),
+                    ms(t3, t4), ms(t4, tnow()));
     });
 }
 

@@ -62,7 +62,7 @@ public:
     void collect_phases(double* ms, size_t count);
     // Same shape, new matrix contents/pointers: recompute the SpMV state,
     // keep every allocation (basis, vectors, workspaces).
-    void rebind(const cbgx_csr& A, cudaStream_t st);
+    void rebind(const cbgx_csr& A, cudaStream_t st, const unsigned long long* stats = nullptr);
     uint64_t rows() const { return n_; }
     const cbgx_gmres_config& config() const { return cfg_; }
 
@@ -72,7 +72,7 @@ private:
     void reduce(double* d_vals, size_t count, cudaStream_t st);
     void spmv(const double* x, const double* b, double* y, double* norm, cudaStream_t st, bool pdl = false);
     double fetch_scalar(const double* d, cudaStream_t st);
-    void setup_matrix(bool before_basis, cudaStream_t st);
+    void setup_matrix(bool before_basis, cudaStream_t st, const unsigned long long* stats = nullptr);
 
     cbgx_csr A_;
     cbgx_gmres_config cfg_;

@@ -409,34 +409,7 @@ spmv_tma_kernel(uint64_t n_rows, uint64_t nnz, uint32_t tile_rows, const RP* __r
     block_finalize(red, kSpmvConsumers / 32, 1, partials, ticket, norm_out);
 }
 
-// Largest entry count over row tiles of 32/64/128/256 rows.
-template <typename RP>
-__global__ void tile_nnz_kernel(const RP* __restrict__ rp, uint64_t n, unsigned long long* __restrict__ out) {
-    unsigned long long m[4] = {0, 0, 0, 0};
-    for (uint64_t t = blockIdx.x * static_cast<uint64_t>(blockDim.x) + threadIdx.x; t * 256 < n;
-         t += static_cast<uint64_t>(gridDim.x) * blockDim.x) {
-        unsigned long long c[8];
-        for (int g = 0; g < 8; ++g) {
-            const uint64_t a = min(n, t * 256 + g * 32), e = min(n, t * 256 + g * 32 + 32);
-            c[g] = static_cast<unsigned long long>(rp[e] - rp[a]);
-        }
-        for (int g = 0; g < 8; ++g) m[0] = max(m[0], c[g]);
-        for (int g = 0; g < 8; g += 2) m[1] = max(m[1], c[g] + c[g + 1]);
-        for (int g = 0; g < 8; g += 4) m[2] = max(m[2], c[g] + c[g + 1] + c[g + 2] + c[g + 3]);
-        m[3] = max(m[3], c[0] + c[1] + c[2] + c[3] + c[4] + c[5] + c[6] + c[7]);
-    }
-    for (int i = 0; i < 4; ++i) atomicMax(out + i, m[i]);
-}
 
-template <typename RP>
-__global__ void max_row_kernel(const RP* __restrict__ rp, uint64_t n, unsigned* __restrict__ out) {
-    unsigned m = 0;
-    for (uint64_t r = blockIdx.x * static_cast<uint64_t>(blockDim.x) + threadIdx.x; r < n;
-         r += static_cast<uint64_t>(gridDim.x) * blockDim.x)
-        m = max(m, static_cast<unsigned>(rp[r + 1] - rp[r]));
-    m = __reduce_max_sync(0xFFFFFFFFu, m);
-    if ((threadIdx.x & 31) == 0) atomicMax(out, m);
-}
 
 __global__ void __launch_bounds__(kThreads)
 dot_kernel(const double* __restrict__ x, const double* __restrict__ y, uint64_t n,
@@ -635,23 +608,71 @@ void launch_spmv_sell(const cbgx_csr& A, const Sell& S, const double* x, const d
 }
 
 
-uint32_t plan_spmv_tiles(const cbgx_csr& A, cudaStream_t st) {
-    if (A.n_rows == 0) return 0;
-    unsigned long long* d = nullptr;
-    CBGX_CUDA(cudaMallocAsync(reinterpret_cast<void**>(&d), 4 * sizeof(unsigned long long), st));
-    CBGX_CUDA(cudaMemsetAsync(d, 0, 4 * sizeof(unsigned long long), st));
+// One pass over the row offsets: longest row and the largest entry count of
+// any 32/64/128/256-row tile (blocks of 256 threads own aligned 256-row
+// tiles). out: [max_row, t32, t64, t128, t256], zeroed by the caller.
+template <typename RP>
+__global__ void __launch_bounds__(256) csr_stats_kernel(const RP* __restrict__ rp, uint64_t n,
+                                                        unsigned long long* __restrict__ out) {
+    __shared__ unsigned long long t32[8];
+    unsigned long long mrow = 0, m[4] = {0, 0, 0, 0};
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    for (uint64_t base = blockIdx.x * 256ull; base < n; base += 256ull * gridDim.x) {
+        const uint64_t r = base + threadIdx.x;
+        const uint64_t a = r < n ? static_cast<uint64_t>(rp[r]) : 0, e = r < n ? static_cast<uint64_t>(rp[r + 1]) : 0;
+        mrow = max(mrow, static_cast<unsigned long long>(e - a));
+        if (lane == 0) {
+            const uint64_t r0 = min(n, base + static_cast<uint64_t>(32 * warp)), r1 = min(n, base + static_cast<uint64_t>(32 * warp + 32));
+            t32[warp] = static_cast<unsigned long long>(rp[r1] - rp[r0]);
+        }
+        __syncthreads();
+        if (threadIdx.x == 0) {
+            unsigned long long c[8];
+            for (int g = 0; g < 8; ++g) c[g] = t32[g];
+            for (int g = 0; g < 8; ++g) m[0] = max(m[0], c[g]);
+            for (int g = 0; g < 8; g += 2) m[1] = max(m[1], c[g] + c[g + 1]);
+            for (int g = 0; g < 8; g += 4) m[2] = max(m[2], c[g] + c[g + 1] + c[g + 2] + c[g + 3]);
+            m[3] = max(m[3], c[0] + c[1] + c[2] + c[3] + c[4] + c[5] + c[6] + c[7]);
+        }
+        __syncthreads();
+    }
+    for (int o = 16; o > 0; o >>= 1) mrow = max(mrow, __shfl_xor_sync(0xFFFFFFFFu, mrow, o));
+    if (lane == 0) atomicMax(out, mrow);
+    if (threadIdx.x == 0)
+        for (int i = 0; i < 4; ++i) atomicMax(out + 1 + i, m[i]);
+}
+
+void launch_csr_stats(const cbgx_csr& A, unsigned long long* d_out, cudaStream_t st) {
+    CBGX_CUDA(cudaMemsetAsync(d_out, 0, 5 * sizeof(unsigned long long), st));
+    if (A.n_rows == 0) return;
     const int grid = rows_grid((A.n_rows + 255) / 256);
     if (A.row_ptr_bits == 32)
-        CBGX_K(tile_nnz_kernel<int32_t><<<grid, kThreads, 0, st>>>(static_cast<const int32_t*>(A.d_row_ptr), A.n_rows, d));
+        CBGX_K(csr_stats_kernel<int32_t><<<grid, 256, 0, st>>>(static_cast<const int32_t*>(A.d_row_ptr), A.n_rows, d_out));
     else
-        CBGX_K(tile_nnz_kernel<int64_t><<<grid, kThreads, 0, st>>>(static_cast<const int64_t*>(A.d_row_ptr), A.n_rows, d));
-    unsigned long long h[4] = {0, 0, 0, 0};
-    CBGX_CUDA(cudaMemcpyAsync(h, d, sizeof(h), cudaMemcpyDeviceToHost, st));
+        CBGX_K(csr_stats_kernel<int64_t><<<grid, 256, 0, st>>>(static_cast<const int64_t*>(A.d_row_ptr), A.n_rows, d_out));
+    CBGX_CUDA(cudaGetLastError());
+}
+
+uint32_t plan_from_stats(const unsigned long long* h) {
+    for (int i = 3; i >= 0; --i)
+        if ((32 << i) <= kTileRowsMax && h[1 + i] <= static_cast<unsigned long long>(kTileEntries)) return 32u << i;
+    return 0;
+}
+
+static void csr_stats_sync(const cbgx_csr& A, unsigned long long h[5], cudaStream_t st) {
+    unsigned long long* d = nullptr;
+    CBGX_CUDA(cudaMallocAsync(reinterpret_cast<void**>(&d), 5 * sizeof(unsigned long long), st));
+    launch_csr_stats(A, d, st);
+    CBGX_CUDA(cudaMemcpyAsync(h, d, 5 * sizeof(unsigned long long), cudaMemcpyDeviceToHost, st));
     CBGX_CUDA(cudaFreeAsync(d, st));
     CBGX_CUDA(cudaStreamSynchronize(st));
-    for (int i = 3; i >= 0; --i)
-        if ((32 << i) <= kTileRowsMax && h[i] <= static_cast<unsigned long long>(kTileEntries)) return 32u << i;
-    return 0;
+}
+
+uint32_t plan_spmv_tiles(const cbgx_csr& A, cudaStream_t st) {
+    if (A.n_rows == 0) return 0;
+    unsigned long long h[5];
+    csr_stats_sync(A, h, st);
+    return plan_from_stats(h);
 }
 
 template <typename RP, int MODE>
@@ -700,19 +721,10 @@ void launch_spmv_tma(const cbgx_csr& A, uint32_t tile_rows, const double* x, con
 }
 
 uint32_t csr_max_row_nnz(const cbgx_csr& A, cudaStream_t st) {
-    unsigned* d = nullptr;
-    CBGX_CUDA(cudaMallocAsync(reinterpret_cast<void**>(&d), sizeof(unsigned), st));
-    CBGX_CUDA(cudaMemsetAsync(d, 0, sizeof(unsigned), st));
-    const int grid = rows_grid(A.n_rows);
-    if (A.row_ptr_bits == 32)
-        CBGX_K(max_row_kernel<int32_t><<<grid, kThreads, 0, st>>>(static_cast<const int32_t*>(A.d_row_ptr), A.n_rows, d));
-    else
-        CBGX_K(max_row_kernel<int64_t><<<grid, kThreads, 0, st>>>(static_cast<const int64_t*>(A.d_row_ptr), A.n_rows, d));
-    unsigned h = 0;
-    CBGX_CUDA(cudaMemcpyAsync(&h, d, sizeof(unsigned), cudaMemcpyDeviceToHost, st));
-    CBGX_CUDA(cudaFreeAsync(d, st));
-    CBGX_CUDA(cudaStreamSynchronize(st));
-    return h;
+    if (A.n_rows == 0) return 0;
+    unsigned long long h[5];
+    csr_stats_sync(A, h, st);
+    return static_cast<uint32_t>(h[0]);
 }
 
 void launch_dot(const double* x, const double* y, uint64_t n, int reduction, double* out,
