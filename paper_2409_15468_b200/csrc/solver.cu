@@ -515,7 +515,8 @@ cbgx_gmres_config checked(const cbgx_gmres_config* cfg) {
 // cbgx_host_cache_release.
 struct HostSolveCache {
     std::mutex mu;
-    cudaStream_t st = nullptr;
+    cudaStream_t st = nullptr, st2 = nullptr;
+    cudaEvent_t ev_idx = nullptr, ev_narrow = nullptr;
     uint64_t cap_n = 0, cap_nnz = 0;
     uint64_t* d_rp64 = nullptr;
     uint64_t* d_ci64 = nullptr;
@@ -544,11 +545,18 @@ struct HostSolveCache {
         if (h_bad) cudaFreeHost(h_bad);
         h_bad = nullptr;
         if (st) cudaStreamDestroy(st);
-        st = nullptr;
+        if (st2) cudaStreamDestroy(st2);
+        if (ev_idx) cudaEventDestroy(ev_idx);
+        if (ev_narrow) cudaEventDestroy(ev_narrow);
+        st = st2 = nullptr;
+        ev_idx = ev_narrow = nullptr;
     }
     void ensure(uint64_t n, uint64_t nnz, bool wide) {
         (void)wide;
         if (!st) CBGX_CUDA(cudaStreamCreateWithFlags(&st, cudaStreamNonBlocking));
+        if (!st2) CBGX_CUDA(cudaStreamCreateWithFlags(&st2, cudaStreamNonBlocking));
+        if (!ev_idx) CBGX_CUDA(cudaEventCreateWithFlags(&ev_idx, cudaEventDisableTiming));
+        if (!ev_narrow) CBGX_CUDA(cudaEventCreateWithFlags(&ev_narrow, cudaEventDisableTiming));
         if (!h_bad) CBGX_CUDA(cudaMallocHost(&h_bad, 6 * sizeof(uint64_t)));
         if (n <= cap_n && nnz <= cap_nnz && d_bad) return;
         solver.reset();  // it points into the buffers
@@ -646,16 +654,22 @@ int cbgx_gmres_solve_host(uint64_t n, const uint64_t* row_ptrs, const uint64_t* 
         CBGX_CUDA(cudaMemsetAsync(H.d_bad, 0, 8, st));
         CBGX_CUDA(cudaMemcpyAsync(H.d_rp64, row_ptrs, (n + 1) * 8, cudaMemcpyHostToDevice, st));
         CBGX_CUDA(cudaMemcpyAsync(H.d_ci64, col_idx, nnz * 8, cudaMemcpyHostToDevice, st));
+        // narrowing + CSR statistics on a second stream, overlapped with the
+        // remaining uploads (values, b, x0)
+        CBGX_CUDA(cudaEventRecord(H.ev_idx, st));
+        CBGX_CUDA(cudaStreamWaitEvent(H.st2, H.ev_idx, 0));
+        void* d_rp = wide ? static_cast<void*>(H.d_rp64) : static_cast<void*>(H.d_rp32);
+        narrow_csr(H.d_rp64, n, wide ? nullptr : H.d_rp32, H.d_ci64, nnz, H.d_ci, H.d_bad, H.st2);
+        cbgx_csr A{n, n, nnz, d_rp, wide ? 64u : 32u, H.d_ci, H.d_va};
+        // the SpMV set-up statistics ride along with the range check: one sync
+        launch_csr_stats(A, reinterpret_cast<unsigned long long*>(H.d_bad + 1), H.st2);
+        CBGX_CUDA(cudaEventRecord(H.ev_narrow, H.st2));
         CBGX_CUDA(cudaMemcpyAsync(H.d_va, values, nnz * 8, cudaMemcpyHostToDevice, st));
         CBGX_CUDA(cudaMemcpyAsync(H.d_b, b, n * 8, cudaMemcpyHostToDevice, st));
         CBGX_CUDA(cudaMemcpyAsync(H.d_x0, x0, n * 8, cudaMemcpyHostToDevice, st));
         if (prof) CBGX_CUDA(cudaStreamSynchronize(st));
         const auto t1 = tnow();
-        void* d_rp = wide ? static_cast<void*>(H.d_rp64) : static_cast<void*>(H.d_rp32);
-        narrow_csr(H.d_rp64, n, wide ? nullptr : H.d_rp32, H.d_ci64, nnz, H.d_ci, H.d_bad, st);
-        cbgx_csr A{n, n, nnz, d_rp, wide ? 64u : 32u, H.d_ci, H.d_va};
-        // the SpMV set-up statistics ride along with the range check: one sync
-        launch_csr_stats(A, reinterpret_cast<unsigned long long*>(H.d_bad + 1), st);
+        CBGX_CUDA(cudaStreamWaitEvent(st, H.ev_narrow, 0));
         CBGX_CUDA(cudaMemcpyAsync(H.h_bad, H.d_bad, 6 * 8, cudaMemcpyDeviceToHost, st));
         CBGX_CUDA(cudaStreamSynchronize(st));
         if (*H.h_bad) throw Error(CBGX_EINVAL, "csr: column index out of range");
