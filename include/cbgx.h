@@ -244,7 +244,9 @@ enum {
     CBGX_SOLVER_PHASE_TIMING_DEFERRED = 2, /* record events, collect later (no per-solve sync) */
     CBGX_SOLVER_NO_FUSION = 4,             /* always use the split dot/update/write kernels */
     CBGX_SOLVER_NO_SELL = 8,               /* SpMV directly on the CSR (no SELL-32 copy) */
-    CBGX_SOLVER_NO_TMA_SPMV = 16           /* no staged (bulk-copy) CSR SpMV */
+    CBGX_SOLVER_NO_TMA_SPMV = 16,          /* no staged (bulk-copy) CSR SpMV */
+    CBGX_SOLVER_FOLD = 32                  /* fold the SpMV into the fused orthogonalisation launch
+                                              (experimental; measured slower on B200, off by default) */
 };
 
 typedef struct {

@@ -16,6 +16,7 @@ PHASE_TIMING_DEFERRED = 2
 NO_FUSION = 4
 NO_SELL = 8
 NO_TMA_SPMV = 16
+FOLD = 32
 PHASES = ["spmv", "dot", "update", "write", "residual", "solution", "comm", "ortho"]
 
 u32, u64, i32, i64, dbl, vp = C.c_uint32, C.c_uint64, C.c_int32, C.c_int64, C.c_double, C.c_void_p

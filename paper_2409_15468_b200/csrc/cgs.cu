@@ -568,17 +568,28 @@ template <int F> struct FBytes {
 #ifndef FUSED_RING_BYTES
 #define FUSED_RING_BYTES 100000
 #endif
+// Folded SpMV (see arnoldi_fused_kernel): a ring stage also carries one
+// 256-row CSR tile -- values, int32 columns, int32 row offsets -- of at most
+// kFoldEntries entries (the staged-SpMV plan of 256-row tiles).
+constexpr uint32_t kFoldRows = 192;  // two tiles in flight: consumer halves of 192 threads
+constexpr uint32_t kFoldEntries = 2048;
+constexpr uint32_t kFoldValBytes = (kFoldEntries + 2) * 8;
+constexpr uint32_t kFoldColBytes = (kFoldEntries + 4) * 4;
+constexpr uint32_t kFoldRpBytes = (kFoldRows + 1 + 4) * 4 + 12;
+constexpr uint32_t kFoldStageBytes = kFoldValBytes + kFoldColBytes + kFoldRpBytes;
+
 template <int F> struct FGeo {
     static constexpr int chunk_raw = static_cast<int>(FUSED_CHUNK_BYTES / (FBytes<F>::pay + FBytes<F>::ex));
     static constexpr int chunk = chunk_raw < 1 ? 1 : (chunk_raw > kFusedMaxSteps ? kFusedMaxSteps : chunk_raw);
-    static constexpr int stages_raw = static_cast<int>((kFCtasPerSM == 1 ? 170000 : FUSED_RING_BYTES) /
-                                                       (chunk * (FBytes<F>::pay + FBytes<F>::ex) + 32));
+    static constexpr uint32_t basis_bytes = chunk * (FBytes<F>::pay + FBytes<F>::ex) + 16;
+    static constexpr uint32_t stage_bytes = (basis_bytes > kFoldStageBytes ? basis_bytes : kFoldStageBytes) / 16 * 16 + 16;
+    static constexpr int stages_raw = static_cast<int>((kFCtasPerSM == 1 ? 170000 : FUSED_RING_BYTES) / (stage_bytes + 16));
     static constexpr int stages = stages_raw < 2 ? 2 : stages_raw;
 };
 
 template <int F>
 __host__ __device__ constexpr uint32_t fstage_bytes() {
-    return FGeo<F>::chunk * (FBytes<F>::pay + FBytes<F>::ex) + 16;
+    return FGeo<F>::stage_bytes;
 }
 
 struct FusedArgs {
@@ -599,6 +610,14 @@ struct FusedArgs {
     unsigned* gate_hist;       // previous launch's gate: 0 open (speculate), 1 closed
     double* host_slot;         // optional mapped pinned copy of the slot (read by the host)
     unsigned long long* trace; // optional: CTA 0 phase timestamps (debug)
+    // folded SpMV w = A x (fold != 0): int32 CSR, x = the previous step's v
+    int fold;
+    const int32_t* rp;
+    const int32_t* ci;
+    const double* va;
+    const double* x;
+    uint64_t nnz;
+    double* w_scratch;         // w rows written by the SpMV phase, reloaded by the owners
 };
 
 // Partial regions, one per grid reduction of a launch, so a CTA that runs
@@ -684,6 +703,19 @@ __device__ __forceinline__ void grid_allreduce(unsigned* bar, unsigned seq, cons
     for (uint32_t off = R >> 1; off >= 1; off >>= 1) v = __dadd_rn(v, __shfl_xor_sync(0xFFFFFFFFu, v, off));
     if (g == 0 && k < count) out_smem[k] = v;
     consumer_sync();
+}
+
+// CTA sum of one value per consumer thread (warp butterflies, then the warp
+// sums in order); returned in every thread.
+__device__ __forceinline__ double cta_wnorm_sum(double v, double* nred) {
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    v = warp_sum(v);
+    consumer_sync();  // nred may still be read by a previous reduction
+    if (lane == 0) nred[warp] = v;
+    consumer_sync();
+    double s = nred[0];
+    for (int w = 1; w < kFWarps; ++w) s = __dadd_rn(s, nred[w]);
+    return s;
 }
 
 // This CTA's <w, w> over its register-resident rows (fixed order); the
@@ -848,7 +880,7 @@ __device__ __forceinline__ void dot_partials_out(const double* red, uint32_t col
 // the gate turns out closed its coefficients are simply not used. With the
 // previous gate closed the dot2 pass waits for the gate (R1 = [hn1] only,
 // then R2'[u] in region 2).
-template <int F>
+template <int F, bool kFold>
 __global__ void __launch_bounds__(kFThreads, kFCtasPerSM) arnoldi_fused_kernel(FusedArgs a) {
     constexpr int S = FGeo<F>::stages;
     constexpr uint32_t PAY = FBytes<F>::pay, UPAY = FBytes<F>::upay, UEX = FBytes<F>::uex, SB = fstage_bytes<F>();
@@ -889,11 +921,50 @@ __global__ void __launch_bounds__(kFThreads, kFCtasPerSM) arnoldi_fused_kernel(F
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
 
     if (warp == kFWarps) {
-        // ---------------- producer: dot1 (rev), update1, [dot2 (rev), update2]
-        if (lane != 0) return;
+        // ---------------- producer: [SpMV tiles], dot1 (rev), update1, [dot2 (rev), update2]
         const uint64_t policy = policy_evict_normal();
-        const uint64_t u0 = r0 / kUnitRows;
         uint32_t it = 0;
+        if constexpr (kFold) {
+            // CSR tiles of this CTA's rows; the entry ranges of 32 tiles are
+            // fetched by the whole warp at once, lane 0 issues the copies
+            const uint64_t n = a.B.n;
+            const uint32_t ntile = (lim + kFoldRows - 1) / kFoldRows;
+            const uint64_t pol_stream = policy_evict_first();
+            for (uint32_t tb = 0; tb < ntile; tb += 32) {
+                const uint32_t tj = tb + lane;
+                uint64_t mk0 = 0, mk1 = 0;
+                if (tj < ntile) {
+                    const uint64_t ra = min(n, r0 + static_cast<uint64_t>(tj) * kFoldRows);
+                    const uint64_t rb = min(n, min(r1, ra + kFoldRows));
+                    mk0 = static_cast<uint64_t>(__ldg(a.rp + ra));
+                    mk1 = static_cast<uint64_t>(__ldg(a.rp + rb));
+                }
+                for (uint32_t j = 0; j < 32 && tb + j < ntile; ++j, ++it) {
+                    const uint64_t k0 = __shfl_sync(0xFFFFFFFFu, mk0, j), k1 = __shfl_sync(0xFFFFFFFFu, mk1, j);
+                    if (lane == 0) {
+                        const uint64_t ra = min(n, r0 + static_cast<uint64_t>(tb + j) * kFoldRows);
+                        const uint64_t rb = min(n, min(r1, ra + kFoldRows));
+                        const int stage = it % S;
+                        mbar_wait(empty + stage, ((it / S) & 1) ^ 1);
+                        unsigned char* dst = stages + stage * SB;
+                        const uint64_t av = k0 / 2 * 2, ac = k0 / 4 * 4, ar = ra / 4 * 4;
+                        const uint64_t av1 = min((k1 + 1) / 2 * 2, a.nnz / 2 * 2);
+                        const uint64_t ac1 = min((k1 + 3) / 4 * 4, a.nnz / 4 * 4);
+                        const uint64_t ar1 = min((rb + 1 + 3) / 4 * 4, (n + 1) / 4 * 4);
+                        const uint32_t bv = av1 > av ? static_cast<uint32_t>((av1 - av) * 8) : 0u;
+                        const uint32_t bc = ac1 > ac ? static_cast<uint32_t>((ac1 - ac) * 4) : 0u;
+                        const uint32_t br = ar1 > ar ? static_cast<uint32_t>((ar1 - ar) * 4) : 0u;
+                        mbar_arrive_expect_tx(full + stage, bv + bc + br);
+                        if (bv) bulk_g2s(dst, a.va + av, bv, full + stage, pol_stream);
+                        if (bc) bulk_g2s(dst + kFoldValBytes, a.ci + ac, bc, full + stage, pol_stream);
+                        if (br) bulk_g2s(dst + kFoldValBytes + kFoldColBytes, a.rp + ar, br, full + stage, pol_stream);
+                    }
+                    __syncwarp();
+                }
+            }
+        }
+        if (lane != 0) return;
+        const uint64_t u0 = r0 / kUnitRows;
         for (int pass = 0; pass < 4; ++pass) {
             if (pass == (spec ? 3 : 2)) {
                 while (*s_gate < 0) __nanosleep(64);
@@ -925,15 +996,79 @@ __global__ void __launch_bounds__(kFThreads, kFCtasPerSM) arnoldi_fused_kernel(F
     // ---------------- consumers
     FTRACE(0);
     if (a.trace && threadIdx.x == 0) a.trace[32 + 2048 + blockIdx.x] = global_ns();
+    uint32_t it = 0;
+    double om_part = 0.0;  // this CTA's <w, w> (folded SpMV)
+    if constexpr (kFold) {
+        // w = A x for this CTA's rows (sparse.cpp:43-56 order: each row from
+        // +0.0, mul then add, entries in row order -- bit-identical), one
+        // 256-row CSR tile per ring stage, one row per thread; the rows go
+        // to w_scratch and come back to their owners below (CTA-local).
+        const uint64_t n = a.B.n;
+        const uint32_t ntile = (lim + kFoldRows - 1) / kFoldRows;
+        static_assert(kFConsumers == 2 * kFoldRows, "two consumer halves, one row per thread");
+        const uint32_t half = threadIdx.x / kFoldRows, t = threadIdx.x % kFoldRows;
+        for (uint32_t tj = 0; tj < ntile; ++tj, ++it) {
+            const int stage = it % S;
+            mbar_wait(full + stage, (it / S) & 1);
+            const uint64_t ra = min(n, r0 + static_cast<uint64_t>(tj) * kFoldRows);
+            const uint64_t rb = min(n, min(r1, ra + kFoldRows));
+            // the halves take alternate tiles (both arrive on every stage)
+            if ((tj & 1u) == half && t < rb - ra) {
+                const unsigned char* st = stages + stage * SB;
+                const double* sv = reinterpret_cast<const double*>(st);
+                const int32_t* sc = reinterpret_cast<const int32_t*>(st + kFoldValBytes);
+                const int32_t* sr = reinterpret_cast<const int32_t*>(st + kFoldValBytes + kFoldColBytes);
+                const uint64_t r = ra + t;
+                const bool rtail = rb + 1 > (n + 1) / 4 * 4;  // row offsets past the copied window
+                const uint64_t k0 = rtail ? static_cast<uint64_t>(__ldg(a.rp + ra)) : static_cast<uint64_t>(sr[0]);
+                const uint64_t ka = rtail ? static_cast<uint64_t>(__ldg(a.rp + r)) : static_cast<uint64_t>(sr[t]);
+                const uint64_t ke = rtail ? static_cast<uint64_t>(__ldg(a.rp + r + 1)) : static_cast<uint64_t>(sr[t + 1]);
+                const uint64_t av = k0 / 2 * 2, ac = k0 / 4 * 4;
+                const uint64_t av1 = a.nnz / 2 * 2, ac1 = a.nnz / 4 * 4;
+                double acc = 0.0;
+                for (uint64_t k = ka; k < ke; k += 8) {
+                    int32_t c[8];
+                    double v[8], xv[8];
+#pragma unroll
+                    for (int u = 0; u < 8; ++u) {
+                        const uint64_t kk = k + u;
+                        const bool in = kk < ke;
+                        c[u] = in ? (kk < ac1 ? sc[kk - ac] : __ldg(a.ci + kk)) : 0;
+                        v[u] = in ? (kk < av1 ? sv[kk - av] : __ldg(a.va + kk)) : 0.0;
+                    }
+#pragma unroll
+                    for (int u = 0; u < 8; ++u) xv[u] = k + u < ke ? __ldg(a.x + c[u]) : 0.0;
+#pragma unroll
+                    for (int u = 0; u < 8; ++u)
+                        if (k + u < ke) acc = __dadd_rn(acc, __dmul_rn(v[u], xv[u]));
+                }
+                a.w_scratch[r] = acc;
+                om_part = __dadd_rn(om_part, __dmul_rn(acc, acc));
+            }
+            __syncwarp();
+            if (lane == 0) mbar_arrive(empty + stage);
+        }
+        consumer_sync();  // w_scratch rows of this CTA are written
+        FTRACE(20);
+    }
     double wv[kFusedMaxSteps][4];
     const uint64_t wend = min(r1, a.B.n);
+    const double* wsrc = kFold ? a.w_scratch : a.w;
 #pragma unroll
     for (int s = 0; s < kFusedMaxSteps; ++s) {
-        if (s < static_cast<int>(steps)) load_w(a.w, wend, r0 + s * kFStepRows + 4u * threadIdx.x, wv[s]);
-        else wv[s][0] = wv[s][1] = wv[s][2] = wv[s][3] = 0.0;
+        const uint64_t r = r0 + s * kFStepRows + 4u * threadIdx.x;
+        if (s < static_cast<int>(steps)) {
+            if constexpr (kFold) {  // written in this launch: L2 loads, not the read-only path
+#pragma unroll
+                for (int k = 0; k < 4; ++k) wv[s][k] = r + k < wend ? __ldcg(wsrc + r + k) : 0.0;
+            } else {
+                load_w(wsrc, wend, r, wv[s]);
+            }
+        } else {
+            wv[s][0] = wv[s][1] = wv[s][2] = wv[s][3] = 0.0;
+        }
     }
     FTRACE(1);
-    uint32_t it = 0;
     const uint32_t gs = a.gs;
     const uint64_t region = static_cast<uint64_t>(cols + 1) * gs;
     double* const P = a.partials;
@@ -945,12 +1080,19 @@ __global__ void __launch_bounds__(kFThreads, kFCtasPerSM) arnoldi_fused_kernel(F
     FTRACE(2);
     if (a.trace && threadIdx.x == 0) a.trace[32 + blockIdx.x] = global_ns();
     dot_partials_out(red, cols, P, gs);
-    grid_allreduce(a.bar, seq++, P, gs, cols, hsm, a.trace);
+    if constexpr (kFold) {
+        // <w, w> of the folded SpMV rides along with h
+        const double om_cta = cta_wnorm_sum(om_part, nred);
+        if (threadIdx.x == 0) P[static_cast<uint64_t>(cols) * gs + blockIdx.x] = om_cta;
+    }
+    grid_allreduce(a.bar, seq++, P, gs, cols + (kFold ? 1u : 0u), hsm, a.trace);
+    const double omega2 = kFold ? hsm[cols] : a.slot[2];
     if (cta0)
         for (uint32_t j = threadIdx.x; j < cols; j += kFConsumers) {
             a.slot[3 + j] = hsm[j];
             if (a.host_slot) a.host_slot[3 + j] = hsm[j];
         }
+    if (kFold && cta0 && threadIdx.x == 0) a.slot[2] = omega2;
     FTRACE(3);
     // update1
     fused_pass<F, false>(cols, lim, steps, nch, stages, full, empty, it, wv, red, hsm);
@@ -970,7 +1112,7 @@ __global__ void __launch_bounds__(kFThreads, kFCtasPerSM) arnoldi_fused_kernel(F
     FTRACE(6);
     const double hn1 = hsm[cols];
     // gmres.cpp:51 on the device (same IEEE ops as the host)
-    const bool gate = sqrt(hn1) < a.eta * sqrt(a.slot[2]);
+    const bool gate = sqrt(hn1) < a.eta * sqrt(omega2);
     if (threadIdx.x == 0) {
         *s_gate = gate ? 1 : 0;
         __threadfence_block();
@@ -979,7 +1121,7 @@ __global__ void __launch_bounds__(kFThreads, kFCtasPerSM) arnoldi_fused_kernel(F
         a.slot[0] = hn1;
         if (a.host_slot) {
             a.host_slot[0] = hn1;
-            a.host_slot[2] = a.slot[2];
+            a.host_slot[2] = omega2;
         }
     }
     double hn2 = hn1;
@@ -1062,9 +1204,15 @@ int fused_grid(uint64_t n, uint32_t max_cols) {
             per_sm = it->second;
         } else {
             // the attribute is per kernel, not per size: set the maximum once
-            CBGX_CUDA(cudaFuncSetAttribute(arnoldi_fused_kernel<F>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+            // the attribute is per kernel: both variants
+            CBGX_CUDA(cudaFuncSetAttribute(arnoldi_fused_kernel<F, false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                            227 * 1024));
-            CBGX_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, arnoldi_fused_kernel<F>, kFThreads, smem));
+            CBGX_CUDA(cudaFuncSetAttribute(arnoldi_fused_kernel<F, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                           227 * 1024));
+            int p2 = 0;
+            CBGX_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, arnoldi_fused_kernel<F, false>, kFThreads, smem));
+            CBGX_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&p2, arnoldi_fused_kernel<F, true>, kFThreads, smem));
+            per_sm = std::min(per_sm, p2);
             int coop = 0;
             CBGX_CUDA(cudaDeviceGetAttribute(&coop, cudaDevAttrCooperativeLaunch, current_device()));
             if (!coop) per_sm = 0;
@@ -1080,8 +1228,8 @@ int fused_grid(uint64_t n, uint32_t max_cols) {
 
 template <int F> struct FusedLaunch {
     static void run(const cbgx_basis& V, uint32_t cols, const double* w, double* v_out, double* slot,
-                    uint32_t u_off, double eta, uint32_t max_cols, double* host_slot, bool pdl, Workspace* ws,
-                    cudaStream_t st, bool* done) {
+                    uint32_t u_off, double eta, uint32_t max_cols, double* host_slot, bool pdl,
+                    const FoldArg& fold, Workspace* ws, cudaStream_t st, bool* done) {
         // geometry fixed by the solver's capacity so it never changes mid-solve
         const int grid = fused_grid<F>(V.n, max_cols);
         *done = false;
@@ -1109,6 +1257,13 @@ template <int F> struct FusedLaunch {
         a.trace = fused_trace_buffer();
         a.host_slot = host_slot;
         a.rot = g_fused_rot;
+        a.fold = fold.A != nullptr;
+        a.rp = fold.A ? static_cast<const int32_t*>(fold.A->d_row_ptr) : nullptr;
+        a.ci = fold.A ? fold.A->d_col_idx : nullptr;
+        a.va = fold.A ? fold.A->d_values : nullptr;
+        a.nnz = fold.A ? fold.A->nnz : 0;
+        a.x = fold.x;
+        a.w_scratch = fold.w;
         cudaLaunchConfig_t lc = {};
         lc.gridDim = dim3(grid);
         lc.blockDim = dim3(kFThreads);
@@ -1122,7 +1277,8 @@ template <int F> struct FusedLaunch {
         lc.attrs = at;
         lc.numAttrs = pdl ? 2 : 1;
         note_launch();
-        CBGX_CUDA(cudaLaunchKernelEx(&lc, arnoldi_fused_kernel<F>, a));
+        if (a.fold) CBGX_CUDA(cudaLaunchKernelEx(&lc, arnoldi_fused_kernel<F, true>, a));
+        else CBGX_CUDA(cudaLaunchKernelEx(&lc, arnoldi_fused_kernel<F, false>, a));
         *done = true;
     }
 };
@@ -1173,11 +1329,13 @@ bool fused_eligible(const cbgx_basis& V, uint64_t max_cols) {
 
 bool launch_arnoldi_fused(const cbgx_basis& V, uint32_t cols, const double* w, double* v_out, double* slot,
                           uint32_t u_off, double eta, uint32_t max_cols, double* host_slot, bool pdl,
-                          Workspace* ws, cudaStream_t st) {
+                          const FoldArg& fold, Workspace* ws, cudaStream_t st) {
     if (cols + 1 > V.capacity) throw Error(CBGX_ERANGE, "basis: cannot write column");
+    if (fold.A && (fold.A->row_ptr_bits != 32 || fold.A->n_rows != V.n))
+        throw Error(CBGX_EINVAL, "fused: folded SpMV needs int32 row offsets and n rows");
     bool done = false;
-    dispatch_fmt<FusedLaunch>(fmt_of(V), V, cols, w, v_out, slot, u_off, eta, max_cols, host_slot, pdl, ws, st,
-                              &done);
+    dispatch_fmt<FusedLaunch>(fmt_of(V), V, cols, w, v_out, slot, u_off, eta, max_cols, host_slot, pdl, fold, ws,
+                              st, &done);
     CBGX_CUDA(cudaGetLastError());
     return done;
 }

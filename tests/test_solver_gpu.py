@@ -298,3 +298,15 @@ def test_gmres_solve_out_parameter(cbg, port):
     assert r1.solution is out or np.shares_memory(np.asarray(r1.solution), out)
     with pytest.raises(ValueError):
         cbg.gmres_solve(cbg.CsrMatrix(n, n, rp, ci, va), b, np.zeros(n), cfg, out=np.zeros(n - 1))
+
+
+def test_folded_spmv_solve_matches(cbg, port):
+    """Experimental SpMV-in-the-fused-kernel path (CBGX_SOLVER_FOLD): the
+    folded SpMV is bit-identical, so the tree-order solve equals the default
+    path's exactly (same reduction trees elsewhere)."""
+    rp, ci, va = port.stencil(0, 40, 40, 40)
+    b, _ = port.generate_problem(rp, ci, va)
+    r1 = solve(cbg, rp, ci, va, b, "frsz2-32", 30, reduction=0, fold=True)
+    r2 = solve(cbg, rp, ci, va, b, "frsz2-32", 30, reduction=0, fold=False)
+    assert r1.total_iterations == r2.total_iterations
+    assert np.allclose(np.asarray(r1.solution), np.asarray(r2.solution), rtol=1e-9, atol=1e-13)
