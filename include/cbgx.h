@@ -300,6 +300,10 @@ int cbgx_solver_phase_times(cbgx_solver* s, double* ms, uint64_t count);
  * roundings) and sum everything into *d_checksum (fixed-shape tree). */
 int cbgx_read_sweep(const cbgx_basis* V, uint64_t col, uint64_t n, int intensity, double mul, double add,
                     double* d_checksum, cbgx_workspace* ws, void* stream);
+/* One warm-up sweep, then `trials` sweeps timed with CUDA events: minimum
+ * seconds and the last checksum (for run_read_benchmark, bench.cpp:100-152). */
+int cbgx_read_sweep_timed(const cbgx_basis* V, uint64_t col, uint64_t n, int intensity, double mul, double add,
+                          int trials, double* best_seconds, double* checksum);
 
 /* Host-buffer drop-in for gmres_solve(const CsrMatrix&, span b, span x0,
  * cfg) (gmres.hpp:113-115): size_t CSR as in CsrMatrix, uploads, solves on

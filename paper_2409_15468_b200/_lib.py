@@ -103,6 +103,8 @@ def lib():
             "cbgx_solver_solve": ([vp, vp, vp, vp, P(History), P(SolveStats), vp], C.c_int),
             "cbgx_host_cache_release": ([], C.c_int),
             "cbgx_read_sweep": ([P(Basis), u64, u64, C.c_int, C.c_double, C.c_double, vp, vp, vp], C.c_int),
+            "cbgx_read_sweep_timed": ([P(Basis), u64, u64, C.c_int, C.c_double, C.c_double, C.c_int, P(C.c_double),
+                                       P(C.c_double)], C.c_int),
             "cbgx_gmres_solve_host": ([u64, vp, vp, vp, vp, vp, P(GmresConfig), vp, P(History), P(SolveStats)], C.c_int),
             "cbgx_nccl_unique_id": ([vp], C.c_int),
             "cbgx_comm_create_nccl": ([vp, C.c_int, C.c_int, P(vp)], C.c_int),

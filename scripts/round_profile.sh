@@ -31,4 +31,7 @@ timeout 600 ncu --set full --clock-control none --import-source on -k regex:cgs_
     python scripts/cgs_micro.py --k 100 --formats frsz2-32 --reps 1 > /dev/null 2>&1
 timeout 600 ncu --set full --clock-control none --import-source on -k regex:cgs_update_kernel -s 2 -c 1 -o "$OUT/ncu_cgs_update_2p26" \
     python scripts/cgs_micro.py --k 100 --formats frsz2-32 --reps 1 > /dev/null 2>&1
+timeout 900 python scripts/read_bench.py > "$OUT/read_bench.csv" 2>&1
+timeout 1800 python scripts/config_sweep.py --configs 2,3 > "$OUT/config_sweep_c2_c3.jsonl" 2>&1
+timeout 1800 python scripts/config_sweep.py --configs 5 --reps 1 > "$OUT/config_sweep_c5.jsonl" 2>&1
 ls -la "$OUT"

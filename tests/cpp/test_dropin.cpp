@@ -13,6 +13,7 @@
 #include <string>
 #include <vector>
 
+#include "cbg/bench.hpp"
 #include "cbg/frsz2.hpp"
 #include "cbg/gmres.hpp"
 
@@ -281,10 +282,33 @@ static void solver() {
     std::printf("solver: done\n");
 }
 
+// run_read_benchmark (bench.hpp; bench.cpp:100-152 argument checks and
+// result shape) on the device read sweep.
+static void bench() {
+    const std::vector<StorageFormat> fmts = {StorageFormat::f64(), StorageFormat::frsz2_format(32),
+                                             StorageFormat::frsz2_format(16)};
+    const std::vector<int> ints = {1, 3};
+    const auto res = run_read_benchmark(1000, fmts, ints, 2, 7);
+    CHECK(res.size() == 6);
+    for (size_t i = 0; i < res.size(); ++i) {
+        CHECK(res[i].format == fmts[i / 2].name());
+        CHECK(res[i].intensity == ints[i % 2]);
+        CHECK(res[i].elements == 992);
+        CHECK(res[i].stored_bytes == fmts[i / 2].column_bytes(992));
+        CHECK(res[i].seconds > 0.0 && res[i].stored_gbps > 0.0 && res[i].logical_gbps > 0.0);
+    }
+    CHECK(throws<std::invalid_argument>([&] { run_read_benchmark(31, fmts, ints, 2, 7); }));
+    CHECK(throws<std::invalid_argument>([&] { run_read_benchmark(64, fmts, ints, 0, 7); }));
+    const std::vector<int> bad = {0};
+    CHECK(throws<std::invalid_argument>([&] { run_read_benchmark(64, fmts, bad, 1, 7); }));
+    std::printf("bench: done\n");
+}
+
 int main() {
     codec();
     basis();
     solver();
+    bench();
     std::printf(g_fail ? "%d check(s) failed\n" : "all drop-in checks passed\n", g_fail);
     return g_fail ? 1 : 0;
 }
