@@ -282,6 +282,51 @@ static void solver() {
     std::printf("solver: done\n");
 }
 
+// MatrixMarket I/O (test_sparsela.cpp:136-208 restated).
+static void matrix_market() {
+    {
+        std::istringstream mm("%%MatrixMarket matrix coordinate real general\n% a comment\n2 2 3\n1 1 2.0\n2 1 1.0\n2 2 3.0\n");
+        const CsrMatrix a = parse_matrix_market(mm);
+        a.validate();
+        CHECK(a.n_rows == 2 && a.nnz() == 3);
+        const auto y = spmv(a, std::vector<double>{1.0, 1.0});
+        CHECK(y[0] == 2.0 && y[1] == 4.0);
+    }
+    {
+        std::istringstream mm("%%MatrixMarket matrix coordinate real symmetric\n2 2 2\n2 1 5.0\n2 2 1.0\n");
+        const CsrMatrix a = parse_matrix_market(mm);
+        a.validate();
+        CHECK(a.nnz() == 3);
+        CHECK(a.col_idx[0] == 1 && a.values[0] == 5.0 && a.col_idx[1] == 0 && a.values[1] == 5.0);
+        std::istringstream dup("%%MatrixMarket matrix coordinate real general\n1 1 2\n1 1 2.0\n1 1 0.5\n");
+        const CsrMatrix b = parse_matrix_market(dup);
+        CHECK(b.nnz() == 1 && b.values[0] == 2.5);
+    }
+    {
+        std::istringstream h("%%MatrixMarket matrix array real general\n");
+        CHECK(throws<std::runtime_error>([&] { parse_matrix_market(h); },
+                                         "matrix market: line 1: only 'matrix coordinate' files are supported"));
+        std::istringstream pat("%%MatrixMarket matrix coordinate pattern general\n2 2 1\n1 1\n");
+        CHECK(throws<std::runtime_error>([&] { parse_matrix_market(pat); }));
+        std::istringstream cx("%%MatrixMarket matrix coordinate complex general\n2 2 1\n1 1 1 0\n");
+        CHECK(throws<std::runtime_error>([&] { parse_matrix_market(cx); }));
+        std::istringstream oob("%%MatrixMarket matrix coordinate real general\n2 2 1\n3 1 1.0\n");
+        CHECK(throws<std::runtime_error>([&] { parse_matrix_market(oob); }, "matrix market: line 3: index out of bounds"));
+        std::istringstream bad("%%MatrixMarket matrix coordinate real general\n2 2 1\n1 1 abc\n");
+        CHECK(throws<std::runtime_error>([&] { parse_matrix_market(bad); }));
+    }
+    {
+        const CsrMatrix a = gen_convdiff(7, 6, 1.0);
+        std::stringstream ss;
+        write_matrix_market(ss, a);
+        const CsrMatrix b = parse_matrix_market(ss);
+        CHECK(a.n_rows == b.n_rows && a.n_cols == b.n_cols && a.nnz() == b.nnz());
+        CHECK(a.row_ptrs == b.row_ptrs && a.col_idx == b.col_idx);
+        for (size_t k = 0; k < a.nnz() && k < b.nnz(); ++k) CHECK(same(a.values[k], b.values[k]));
+    }
+    std::printf("matrix market: done\n");
+}
+
 // run_read_benchmark (bench.hpp; bench.cpp:100-152 argument checks and
 // result shape) on the device read sweep.
 static void bench() {
@@ -308,6 +353,7 @@ int main() {
     codec();
     basis();
     solver();
+    matrix_market();
     bench();
     std::printf(g_fail ? "%d check(s) failed\n" : "all drop-in checks passed\n", g_fail);
     return g_fail ? 1 : 0;
