@@ -541,6 +541,9 @@ template <int F> struct ReadLaunch {
 #ifndef FUSED_WARPS
 #define FUSED_WARPS 12
 #endif
+#ifndef FUSED_DOT_ACC4
+#define FUSED_DOT_ACC4 0
+#endif
 #ifndef FUSED_STEPS
 #define FUSED_STEPS 5
 #endif
@@ -816,7 +819,7 @@ __device__ __forceinline__ void fused_pass(uint32_t cols, uint32_t lim, uint32_t
         const uint32_t j = kDot ? cols - 1 - jj : jj;
         const double hj = kDot ? 0.0 : hsm[j];
         const int he = static_cast<int>(exp_field(hj));
-        double acc = 0.0, acc2 = 0.0;
+        double acc = 0.0, acc2 = 0.0, acc3 = 0.0, acc4 = 0.0;
 #pragma unroll
         for (int ch = 0; ch < kChunks; ++ch) {
             if (ch >= static_cast<int>(nch)) break;
@@ -834,8 +837,15 @@ __device__ __forceinline__ void fused_pass(uint32_t cols, uint32_t lim, uint32_t
                     Step<F> st;
                     step_lds<F>(st, pay, ex, lr);
                     if constexpr (kDot) {
+#if FUSED_DOT_ACC4
+                        if ((s & 3) == 0) acc = __dadd_rn(acc, st.dot(wv[gs]));
+                        else if ((s & 3) == 1) acc2 = __dadd_rn(acc2, st.dot(wv[gs]));
+                        else if ((s & 3) == 2) acc3 = __dadd_rn(acc3, st.dot(wv[gs]));
+                        else acc4 = __dadd_rn(acc4, st.dot(wv[gs]));
+#else
                         if (s & 1) acc2 = __dadd_rn(acc2, st.dot(wv[gs]));
                         else acc = __dadd_rn(acc, st.dot(wv[gs]));
+#endif
                     } else {
                         st.update(hj, he, wv[gs]);
                     }
@@ -846,7 +856,7 @@ __device__ __forceinline__ void fused_pass(uint32_t cols, uint32_t lim, uint32_t
             ++it;
         }
         if constexpr (kDot) {
-            acc = warp_sum(__dadd_rn(acc, acc2));
+            acc = warp_sum(__dadd_rn(__dadd_rn(acc, acc2), __dadd_rn(acc3, acc4)));
             if (lane == 0) red[warp * cols + j] = acc;
         }
     }
