@@ -56,8 +56,11 @@ constexpr uint32_t kStepRows = 4 * kConsumers;  // 1024
 // and ring depth. A ring stage holds one column's segment of a sub-tile.
 template <int F> struct Geo;
 template <> struct Geo<kZ32> { static constexpr uint32_t pay = 4096, ex = 128; static constexpr int sub = 4, stages = 4; };
-template <> struct Geo<kZ16> { static constexpr uint32_t pay = 2048, ex = 128; static constexpr int sub = 4, stages = 6; };
-template <> struct Geo<kZ21> { static constexpr uint32_t pay = 2688, ex = 128; static constexpr int sub = 4, stages = 5; };
+#ifndef SPLIT_SUB_SMALL
+#define SPLIT_SUB_SMALL 4
+#endif
+template <> struct Geo<kZ16> { static constexpr uint32_t pay = 2048, ex = 128; static constexpr int sub = SPLIT_SUB_SMALL, stages = 6; };
+template <> struct Geo<kZ21> { static constexpr uint32_t pay = 2688, ex = 128; static constexpr int sub = SPLIT_SUB_SMALL, stages = 5; };
 template <> struct Geo<kF64> { static constexpr uint32_t pay = 8192, ex = 0; static constexpr int sub = 4, stages = 3; };
 template <> struct Geo<kF32> { static constexpr uint32_t pay = 4096, ex = 0; static constexpr int sub = 4, stages = 4; };
 template <> struct Geo<kF16> { static constexpr uint32_t pay = 2048, ex = 0; static constexpr int sub = 4, stages = 6; };
@@ -190,8 +193,13 @@ __device__ __forceinline__ void produce(const Ring& R, const BasisView& B, uint6
 }
 
 // ------------------------------------------------------------------ dot
+// Resident CTAs per SM the split kernels are register-budgeted for (w of a
+// sub-tile lives in registers: sub * 4 doubles per thread).
 template <int F>
-__global__ void __launch_bounds__(kThreads, 3)
+constexpr int split_min_blocks() { return Geo<F>::sub > 4 ? 2 : 3; }
+
+template <int F>
+__global__ void __launch_bounds__(kThreads, split_min_blocks<F>())
 cgs_dot_kernel(BasisView B, uint64_t first, uint32_t cols, const double* __restrict__ w,
                int with_wnorm, double* __restrict__ partials, unsigned* __restrict__ ticket,
                double* __restrict__ h_out, GateArg gate) {
@@ -261,7 +269,7 @@ cgs_dot_kernel(BasisView B, uint64_t first, uint32_t cols, const double* __restr
 
 // --------------------------------------------------------------- update
 template <int F>
-__global__ void __launch_bounds__(kThreads, 3)
+__global__ void __launch_bounds__(kThreads, split_min_blocks<F>())
 cgs_update_kernel(BasisView B, uint64_t first, uint32_t cols, const double* __restrict__ h,
                   double h_sign, double* __restrict__ w, int with_norm,
                   double* __restrict__ partials, unsigned* __restrict__ ticket,
