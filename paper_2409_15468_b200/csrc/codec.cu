@@ -263,9 +263,12 @@ __global__ void encode_block_kernel(const double* __restrict__ v, uint32_t count
     for (uint32_t j = 0; j < count; ++j) codes[j] = encode_any(v[j], e_max, l);
 }
 
+#ifndef CODEC_CTAS_PER_SM
+#define CODEC_CTAS_PER_SM 16  // measured (scripts/ab_codec.sh): 16 > 8 ~ 32 for the 2^24 round trip
+#endif
 int grid_for(uint64_t units, int per_cta) {
     const uint64_t want = (units + per_cta - 1) / per_cta;
-    const uint64_t cap = static_cast<uint64_t>(sm_count()) * 8;
+    const uint64_t cap = static_cast<uint64_t>(sm_count()) * CODEC_CTAS_PER_SM;
     return static_cast<int>(want < 1 ? 1 : (want > cap ? cap : want));
 }
 
