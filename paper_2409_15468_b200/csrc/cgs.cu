@@ -347,6 +347,332 @@ cgs_update_kernel(BasisView B, uint64_t first, uint32_t cols, const double* __re
     if (with_norm) block_finalize(red, kWarps, 1, partials, ticket, norm_out);
 }
 
+// ------------------------------------------------ update, dynamic tiles
+// Same pass as cgs_update_kernel, but the sub-tiles are handed out through a
+// device counter (the producer takes the next one when it has a free stage),
+// so faster SMs take more tiles: the static split leaves every launch waiting
+// for the slowest CTA (per-SM throughput differs by ~10% on B200). Rows are
+// still updated exactly once in column order (bit-identical); the optional
+// <w, w> is summed per tile and the tiles in tile order -- deterministic
+// whatever the assignment.
+constexpr uint32_t kTileEnd = 0xFFFFFFFFu;
+
+__device__ __forceinline__ unsigned ld_acquire_u32(const unsigned* p) {
+    unsigned v;
+    asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+    return v;
+}
+
+__device__ __forceinline__ void split_consumer_sync() {
+    asm volatile("bar.sync 1, %0;" ::"n"(kConsumers) : "memory");
+}
+
+template <int F>
+__global__ void __launch_bounds__(kThreads, split_min_blocks<F>())
+cgs_update_dyn_kernel(BasisView B, uint64_t first, uint32_t cols, const double* __restrict__ h,
+                      double h_sign, double* __restrict__ w, int with_norm,
+                      double* __restrict__ tile_norms, unsigned* __restrict__ counters,
+                      double* __restrict__ norm_out, GateArg gate) {
+    if (!gate.open()) return;
+    constexpr int S = Geo<F>::stages;
+    constexpr uint32_t PAY = Geo<F>::pay, EX = Geo<F>::ex;
+    extern __shared__ __align__(128) unsigned char smem[];
+    const Ring R = ring_setup<F>(smem);
+    double* hs = reinterpret_cast<double*>(R.empty + S);  // [cols]
+    double* red = hs + cols;                               // [kWarps]
+    uint32_t* tid_ring = reinterpret_cast<uint32_t*>(red + kWarps);  // [S]
+    __shared__ bool s_last;
+    for (uint32_t k = threadIdx.x; k < cols; k += kThreads) hs[k] = h_sign * h[k];
+    __syncthreads();
+    const uint64_t nsteps = (B.n + kStepRows - 1) / kStepRows;
+    const uint32_t ntiles = static_cast<uint32_t>((nsteps + Geo<F>::sub - 1) / Geo<F>::sub);
+    unsigned* tile_ctr = counters + 2;
+    unsigned* ticket = counters + 3;
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    if (warp == kConsumerWarps) {
+        if (lane == 0) {
+            const uint64_t policy = policy_evict_normal();
+            uint32_t it = 0;
+            for (;;) {
+                const uint32_t tile = atomicAdd(tile_ctr, 1u);
+                if (tile >= ntiles) break;
+                const uint64_t sb = static_cast<uint64_t>(tile) * Geo<F>::sub;
+                const uint32_t steps = static_cast<uint32_t>(min(static_cast<uint64_t>(Geo<F>::sub), nsteps - sb));
+                const uint32_t pb = steps * PAY, eb = steps * EX;
+                for (uint32_t j = 0; j < cols; ++j, ++it) {
+                    const int stage = it % S;
+                    mbar_wait(R.empty + stage, ((it / S) & 1) ^ 1);
+                    tid_ring[stage] = tile;
+                    mbar_arrive_expect_tx(R.full + stage, pb + eb);
+                    unsigned char* dst = R.stages + stage * stage_bytes<F>();
+                    bulk_g2s(dst, B.data + (first + j) * B.col_stride_bytes + sb * PAY, pb, R.full + stage, policy);
+                    if constexpr (EX > 0)
+                        bulk_g2s(dst + Geo<F>::sub * PAY,
+                                 reinterpret_cast<const unsigned char*>(B.exp + (first + j) * B.exp_col_stride) + sb * EX,
+                                 eb, R.full + stage, policy);
+                }
+            }
+            // sentinel stage: no data, tells the consumers to stop
+            const int stage = it % S;
+            mbar_wait(R.empty + stage, ((it / S) & 1) ^ 1);
+            tid_ring[stage] = kTileEnd;
+            mbar_arrive(R.full + stage);
+        }
+    } else {
+        uint32_t it = 0;
+        for (;;) {
+            const int stage0 = it % S;
+            mbar_wait(R.full + stage0, (it / S) & 1);
+            const uint32_t tile = tid_ring[stage0];
+            if (tile == kTileEnd) break;
+            const uint64_t sb = static_cast<uint64_t>(tile) * Geo<F>::sub;
+            const uint32_t steps = static_cast<uint32_t>(min(static_cast<uint64_t>(Geo<F>::sub), nsteps - sb));
+            double wv[Geo<F>::sub][4];
+#pragma unroll
+            for (int s = 0; s < Geo<F>::sub; ++s) {
+                if (s < steps) load_w(w, B.n, (sb + s) * kStepRows + 4u * threadIdx.x, wv[s]);
+                else wv[s][0] = wv[s][1] = wv[s][2] = wv[s][3] = 0.0;
+            }
+            for (uint32_t j = 0; j < cols; ++j, ++it) {
+                const int stage = it % S;
+                if (j) mbar_wait(R.full + stage, (it / S) & 1);
+                const unsigned char* pay = R.stages + stage * stage_bytes<F>();
+                const uint32_t* ex = reinterpret_cast<const uint32_t*>(pay + Geo<F>::sub * PAY);
+                const double hj = hs[j];
+                const int he = static_cast<int>(exp_field(hj));
+#pragma unroll
+                for (int s = 0; s < Geo<F>::sub; ++s) {
+                    if (s < steps) {
+                        Step<F> st;
+                        step_lds<F>(st, pay, ex, s * kStepRows + 4u * threadIdx.x);
+                        st.update(hj, he, wv[s]);
+                    }
+                }
+                __syncwarp();
+                if (lane == 0) mbar_arrive(R.empty + stage);
+            }
+            double nacc = 0.0;
+#pragma unroll
+            for (int s = 0; s < Geo<F>::sub; ++s) {
+                if (s >= steps) break;
+                const uint64_t r = (sb + s) * kStepRows + 4u * threadIdx.x;
+                if (r + 3 < B.n) {
+                    store4(w + r, wv[s]);
+                } else {
+#pragma unroll
+                    for (int k = 0; k < 4; ++k)
+                        if (r + k < B.n) w[r + k] = wv[s][k];
+                }
+                if (with_norm) {
+#pragma unroll
+                    for (int k = 0; k < 4; ++k)
+                        if (r + k < B.n) nacc = fma(wv[s][k], wv[s][k], nacc);
+                }
+            }
+            if (with_norm) {
+                // this tile's <w, w>: warps in order
+                nacc = warp_sum(nacc);
+                split_consumer_sync();
+                if (lane == 0) red[warp] = nacc;
+                split_consumer_sync();
+                if (threadIdx.x == 0) {
+                    double t = red[0];
+                    for (int k = 1; k < kWarps; ++k) t = __dadd_rn(t, red[k]);
+                    tile_norms[tile] = t;
+                }
+            }
+        }
+    }
+    // last CTA: reset the tile counter; sum the tile norms in tile order
+    __syncthreads();
+    __threadfence();
+    if (threadIdx.x == 0) s_last = atomicAdd(ticket, 1u) == gridDim.x - 1;
+    __syncthreads();
+    if (!s_last) return;
+    __threadfence();
+    if (threadIdx.x == 0) {
+        *tile_ctr = 0u;
+        *ticket = 0u;
+    }
+    if (with_norm && warp == 0) {
+        double v = 0.0;
+        for (uint32_t t0 = lane; t0 < ntiles; t0 += 32) v = __dadd_rn(v, __ldcg(tile_norms + t0));
+        v = warp_sum(v);
+        if (lane == 0) *norm_out = v;
+    }
+}
+
+// --------------------------------------------------- dot, dynamic tiles
+// Tiles handed out as in cgs_update_dyn_kernel. Partial sums are kept per
+// TILE (column-major table part[col * ntiles + tile], warps of the tile in
+// order), so the grouping never depends on which CTA took which tile; after a
+// grid barrier (cooperative launch: every CTA is resident) each CTA reduces
+// its share of the columns over the tiles in one fixed order.
+template <int F>
+__global__ void __launch_bounds__(kThreads, split_min_blocks<F>())
+cgs_dot_dyn_kernel(BasisView B, uint64_t first, uint32_t cols, const double* __restrict__ w,
+                   int with_wnorm, double* __restrict__ part, unsigned* __restrict__ counters,
+                   double* __restrict__ h_out, GateArg gate) {
+    if (!gate.open()) return;  // re-orthogonalisation pass not needed
+    constexpr int S = Geo<F>::stages;
+    constexpr uint32_t PAY = Geo<F>::pay, EX = Geo<F>::ex;
+    extern __shared__ __align__(128) unsigned char smem[];
+    const uint32_t ncol = cols + (with_wnorm ? 1 : 0);
+    const Ring R = ring_setup<F>(smem);
+    double* red = reinterpret_cast<double*>(R.empty + S);  // [kWarps][ncol]
+    uint32_t* tid_ring = reinterpret_cast<uint32_t*>(red + kWarps * ncol);  // [S]
+    __syncthreads();
+    const uint64_t nsteps = (B.n + kStepRows - 1) / kStepRows;
+    const uint32_t ntiles = static_cast<uint32_t>((nsteps + Geo<F>::sub - 1) / Geo<F>::sub);
+    unsigned* tile_ctr = counters + 4;
+    unsigned* arrive = counters + 5;
+    unsigned* ticket = counters + 6;
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    if (warp == kConsumerWarps) {
+        if (lane == 0) {
+            const uint64_t policy = policy_evict_normal();
+            uint32_t it = 0;
+            for (;;) {
+                const uint32_t tile = atomicAdd(tile_ctr, 1u);
+                if (tile >= ntiles) break;
+                const uint64_t sb = static_cast<uint64_t>(tile) * Geo<F>::sub;
+                const uint32_t steps = static_cast<uint32_t>(min(static_cast<uint64_t>(Geo<F>::sub), nsteps - sb));
+                const uint32_t pb = steps * PAY, eb = steps * EX;
+                for (uint32_t jj = 0; jj < cols; ++jj, ++it) {
+                    const uint32_t j = cols - 1 - jj;  // last-to-first (L2 reuse after an update pass)
+                    const int stage = it % S;
+                    mbar_wait(R.empty + stage, ((it / S) & 1) ^ 1);
+                    tid_ring[stage] = tile;
+                    mbar_arrive_expect_tx(R.full + stage, pb + eb);
+                    unsigned char* dst = R.stages + stage * stage_bytes<F>();
+                    bulk_g2s(dst, B.data + (first + j) * B.col_stride_bytes + sb * PAY, pb, R.full + stage, policy);
+                    if constexpr (EX > 0)
+                        bulk_g2s(dst + Geo<F>::sub * PAY,
+                                 reinterpret_cast<const unsigned char*>(B.exp + (first + j) * B.exp_col_stride) + sb * EX,
+                                 eb, R.full + stage, policy);
+                }
+                if (cols == 0) {  // <w, w> only: one empty stage per tile
+                    const int stage = it % S;
+                    mbar_wait(R.empty + stage, ((it / S) & 1) ^ 1);
+                    tid_ring[stage] = tile;
+                    mbar_arrive(R.full + stage);
+                    ++it;
+                }
+            }
+            const int stage = it % S;
+            mbar_wait(R.empty + stage, ((it / S) & 1) ^ 1);
+            tid_ring[stage] = kTileEnd;
+            mbar_arrive(R.full + stage);
+        }
+    } else {
+        uint32_t it = 0;
+        const uint32_t per_tile = cols ? cols : 1u;
+        for (;;) {
+            const int stage0 = it % S;
+            mbar_wait(R.full + stage0, (it / S) & 1);
+            const uint32_t tile = tid_ring[stage0];
+            if (tile == kTileEnd) break;
+            const uint64_t sb = static_cast<uint64_t>(tile) * Geo<F>::sub;
+            const uint32_t steps = static_cast<uint32_t>(min(static_cast<uint64_t>(Geo<F>::sub), nsteps - sb));
+            double wv[Geo<F>::sub][4];
+#pragma unroll
+            for (int s = 0; s < Geo<F>::sub; ++s) {
+                if (s < steps) load_w(w, B.n, (sb + s) * kStepRows + 4u * threadIdx.x, wv[s]);
+                else wv[s][0] = wv[s][1] = wv[s][2] = wv[s][3] = 0.0;
+            }
+            if (with_wnorm) {
+                double acc = 0.0;
+#pragma unroll
+                for (int s = 0; s < Geo<F>::sub; ++s)
+#pragma unroll
+                    for (int k = 0; k < 4; ++k) acc = fma(wv[s][k], wv[s][k], acc);
+                acc = warp_sum(acc);
+                if (lane == 0) red[warp * ncol + cols] = acc;
+            }
+            for (uint32_t jj = 0; jj < per_tile; ++jj, ++it) {
+                const int stage = it % S;
+                if (jj) mbar_wait(R.full + stage, (it / S) & 1);
+                if (cols) {
+                    const uint32_t j = cols - 1 - jj;
+                    const unsigned char* pay = R.stages + stage * stage_bytes<F>();
+                    const uint32_t* ex = reinterpret_cast<const uint32_t*>(pay + Geo<F>::sub * PAY);
+                    double acc = 0.0;
+#pragma unroll
+                    for (int s = 0; s < Geo<F>::sub; ++s) {
+                        if (s < steps) {
+                            Step<F> st;
+                            step_lds<F>(st, pay, ex, s * kStepRows + 4u * threadIdx.x);
+                            acc = __dadd_rn(acc, st.dot(wv[s]));
+                        }
+                    }
+                    __syncwarp();
+                    if (lane == 0) mbar_arrive(R.empty + stage);
+                    acc = warp_sum(acc);
+                    if (lane == 0) red[warp * ncol + j] = acc;
+                } else {
+                    __syncwarp();
+                    if (lane == 0) mbar_arrive(R.empty + stage);
+                }
+            }
+            // this tile's partials: warps in order, column-major table
+            split_consumer_sync();
+            for (uint32_t k = threadIdx.x; k < ncol; k += kConsumers) {
+                double t = red[k];
+                for (int q = 1; q < kWarps; ++q) t = __dadd_rn(t, red[q * ncol + k]);
+                part[static_cast<uint64_t>(k) * ntiles + tile] = t;
+            }
+            split_consumer_sync();
+        }
+    }
+    // grid barrier (all CTAs resident: cooperative launch)
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        __threadfence();
+        atomicAdd(arrive, 1u);
+        while (ld_acquire_u32(arrive) < gridDim.x) {
+        }
+    }
+    __syncthreads();
+    // columns k = blockIdx.x, blockIdx.x + gridDim.x, ...: every thread sums
+    // the tiles t, t + kThreads, ... of the column, then warp 0 adds the
+    // kThreads partials lane-strided and a butterfly (fixed shape)
+    double* csum = red;  // the per-tile scratch is free now (>= kThreads doubles, see the launcher)
+    for (uint32_t k = blockIdx.x; k < ncol; k += gridDim.x) {
+        const double* col = part + static_cast<uint64_t>(k) * ntiles;
+        double v = 0.0, x[8];
+        for (uint32_t t0 = threadIdx.x; t0 < ntiles; t0 += kThreads * 8) {
+#pragma unroll
+            for (int q = 0; q < 8; ++q) {
+                const uint32_t t = t0 + kThreads * q;
+                x[q] = t < ntiles ? __ldcg(col + t) : 0.0;
+            }
+#pragma unroll
+            for (int q = 0; q < 8; ++q)
+                if (t0 + kThreads * q < ntiles) v = __dadd_rn(v, x[q]);
+        }
+        __syncthreads();
+        csum[threadIdx.x] = v;
+        __syncthreads();
+        if (warp == 0) {
+            double u = 0.0;
+            for (uint32_t i = lane; i < static_cast<uint32_t>(kThreads); i += 32) u = __dadd_rn(u, csum[i]);
+            u = warp_sum(u);
+            if (lane == 0) h_out[k] = u;
+        }
+    }
+    // the last CTA out resets the counters for the next launch
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        __threadfence();
+        if (atomicAdd(ticket, 1u) == gridDim.x - 1) {
+            *tile_ctr = 0u;
+            *arrive = 0u;
+            *ticket = 0u;
+            __threadfence();
+        }
+    }
+}
+
 // ------------------------------------------------- reference-order dot
 // One thread per column, the exact order of KrylovBasis::dot: per 32-block
 // partial from +0.0 left to right, then a running total over blocks
@@ -464,14 +790,36 @@ void allow_smem(K kernel) {
     done.insert(key);
 }
 
+// Dynamic tile scheduling for the split CGS kernels (measured on B200:
+// update at n = 2^26, k = 100 0.85 -> 1.03 of the HBM peak).
+#ifndef SPLIT_DYNAMIC
+#define SPLIT_DYNAMIC 1
+#endif
 template <int F> struct DotLaunch {
     static void run(const BasisView& B, uint64_t first, uint32_t cols, const double* w, int wn,
-                    int reduction, double* h, Workspace* ws, cudaStream_t st, const GateArg& gate) {
+                    int reduction, double* h, Workspace* ws, cudaStream_t st, const GateArg& gate, bool coop) {
         const uint32_t ncol = cols + (wn ? 1 : 0);
         if (ncol == 0) return;
         if (reduction == CBGX_REDUCE_REFERENCE) {
             const uint32_t threads = ncol;
             CBGX_K(serial_dot_kernel<F><<<(threads + 63) / 64, 64, 0, st>>>(B, first, cols, w, wn, h, gate));
+            return;
+        }
+        if (SPLIT_DYNAMIC && coop) {
+            // reduction scratch: kWarps x ncol per tile, kThreads for the
+            // final column sums
+            const size_t smem = ring_smem<F>(std::max<size_t>(static_cast<size_t>(kWarps) * ncol, kThreads)) + 64;
+            allow_smem(cgs_dot_dyn_kernel<F>);
+            const int grid = ring_grid(cgs_dot_dyn_kernel<F>, B.n, smem);
+            const uint64_t nsteps = (B.n + kStepRows - 1) / kStepRows;
+            const uint64_t ntiles = (nsteps + Geo<F>::sub - 1) / Geo<F>::sub;
+            double* part = ws->get_partials(static_cast<size_t>(ntiles) * ncol);
+            unsigned* ctr = ws->get_counter();
+            void* args[] = {const_cast<BasisView*>(&B), &first, &cols, &w, &wn, &part, &ctr, &h,
+                            const_cast<GateArg*>(&gate)};
+            note_launch();
+            CBGX_CUDA(cudaLaunchCooperativeKernel(reinterpret_cast<void*>(cgs_dot_dyn_kernel<F>), dim3(grid),
+                                                  dim3(kThreads), args, smem, st));
             return;
         }
         const size_t smem = ring_smem<F>(static_cast<size_t>(kWarps) * ncol);
@@ -488,6 +836,17 @@ template <int F> struct UpdateLaunch {
                     double* w, double* norm, int reduction, Workspace* ws, cudaStream_t st,
                     const GateArg& gate) {
         const bool fused_norm = norm && reduction == CBGX_REDUCE_TREE;
+        if (SPLIT_DYNAMIC && (cols > 0 || fused_norm)) {
+            const size_t smem = ring_smem<F>(cols + kWarps) + 64;
+            allow_smem(cgs_update_dyn_kernel<F>);
+            const int grid = ring_grid(cgs_update_dyn_kernel<F>, B.n, smem);
+            const uint64_t nsteps = (B.n + kStepRows - 1) / kStepRows;
+            double* tn = fused_norm ? ws->get_partials((nsteps + Geo<F>::sub - 1) / Geo<F>::sub) : nullptr;
+            CBGX_K(cgs_update_dyn_kernel<F><<<grid, kThreads, smem, st>>>(B, first, cols, h, sign, w, fused_norm, tn,
+                                                                   ws->get_counter(), norm, gate));
+            if (norm && !fused_norm) launch_dot(w, w, B.n, CBGX_REDUCE_REFERENCE, norm, ws, st, gate);
+            return;
+        }
         if (cols > 0 || fused_norm) {
             const size_t smem = ring_smem<F>(cols + kWarps);
             allow_smem(cgs_update_kernel<F>);
@@ -1310,9 +1669,9 @@ void check_basis(const cbgx_basis* V) {
 }  // namespace
 
 void launch_cgs_dot(const cbgx_basis& V, uint64_t first, uint32_t cols, const double* w, int wn,
-                    int reduction, double* h, Workspace* ws, cudaStream_t st, const GateArg& gate) {
+                    int reduction, double* h, Workspace* ws, cudaStream_t st, const GateArg& gate, bool coop) {
     if (first + cols > V.capacity) throw Error(CBGX_ERANGE, "basis: column index out of range");
-    dispatch_fmt<DotLaunch>(fmt_of(V), view_of(V), first, cols, w, wn, reduction, h, ws, st, gate);
+    dispatch_fmt<DotLaunch>(fmt_of(V), view_of(V), first, cols, w, wn, reduction, h, ws, st, gate, coop);
     CBGX_CUDA(cudaGetLastError());
 }
 

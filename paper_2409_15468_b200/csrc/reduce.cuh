@@ -94,9 +94,12 @@ void launch_dot(const double* x, const double* y, uint64_t n, int reduction, dou
                 Workspace* ws, cudaStream_t st, const GateArg& gate = GateArg{});
 
 // gate: run only when the device-side re-orthogonalisation test holds.
+// coop: the dynamic-tile dot (a cooperative launch with a grid barrier);
+// false for callers that may run several grids concurrently on one device
+// (the threaded partitioned solve).
 void launch_cgs_dot(const cbgx_basis& V, uint64_t first, uint32_t cols, const double* w, int wn,
                     int reduction, double* h, Workspace* ws, cudaStream_t st,
-                    const GateArg& gate = GateArg{});
+                    const GateArg& gate = GateArg{}, bool coop = true);
 void launch_cgs_update(const cbgx_basis& V, uint64_t first, uint32_t cols, const double* h,
                        double sign, double* w, double* norm, int reduction, Workspace* ws,
                        cudaStream_t st, const GateArg& gate = GateArg{});

@@ -352,7 +352,7 @@ void Solver::solve(const double* d_b, const double* d_x0, double* d_x, cbgx_hist
                 if (fold) count(CBGX_PHASE_SPMV, spmv_bytes, 0);  // folded into the same launch
             } else {
                 timer.begin(CBGX_PHASE_DOT);
-                launch_cgs_dot(V_, 0, cols, d_w_, 0, red, sl + kH, &ws_, st);      // h = V^T w
+                launch_cgs_dot(V_, 0, cols, d_w_, 0, red, sl + kH, &ws_, st, GateArg{}, !multi);  // h = V^T w
                 timer.end();
                 count(CBGX_PHASE_DOT, cols * bpv * n + 8.0 * n);
                 if (multi) {
@@ -372,7 +372,7 @@ void Solver::solve(const double* d_b, const double* d_x0, double* d_x, cbgx_hist
                 // Second CGS pass, gated on the device by the reference's test
                 // h_next < eta * omega (gmres.cpp:51-68); empty launches otherwise.
                 timer.begin(CBGX_PHASE_DOT);
-                launch_cgs_dot(V_, 0, cols, d_w_, 0, red, sl + kU(m), &ws_, st, gate);
+                launch_cgs_dot(V_, 0, cols, d_w_, 0, red, sl + kU(m), &ws_, st, gate, !multi);
                 timer.end();
                 if (multi) reduce(sl + kU(m), cols, st);
                 timer.begin(CBGX_PHASE_UPDATE);
