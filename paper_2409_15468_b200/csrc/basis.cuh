@@ -217,22 +217,34 @@ __device__ __forceinline__ void frsz_decode(const Codes4& c, uint32_t e, double 
 }
 
 // h_exp: biased exponent field of h (hoisted per column by the caller).
+// The FMA update below is exact-equivalent when the block scale is normal and
+// h * scale stays in range.
 template <int L>
-__device__ __forceinline__ void frsz_update(const Codes4& c, uint32_t e, double h, int h_exp, double w[4]) {
+__device__ __forceinline__ bool frsz_upd_ok(uint32_t e, double h, int h_exp) {
     const int es = static_cast<int>(e) - (L - 2);          // scale's biased exponent
     const int hse = h_exp + es - 1023;                      // exponent of h*scale
     // hse <= 1994: 2^52 * hs stays finite, so c0 below is exact
-    const bool ok = es > 0 && (h == 0.0 || (h_exp != 0 && hse >= 1 && hse <= 1994));
-    if (__builtin_expect(__all_sync(0xFFFFFFFFu, ok), 1)) {
-        const double hs = __dmul_rn(h, __hiloint2double(es << 20, 0));
-        const double c0 = __dmul_rn(hs, -0x1p52);
+    return es > 0 && (h == 0.0 || (h_exp != 0 && hse >= 1 && hse <= 1994));
+}
+
+template <int L>
+__device__ __forceinline__ void frsz_update_fast(const Codes4& c, uint32_t e, double h, double w[4]) {
+    const int es = static_cast<int>(e) - (L - 2);
+    const double hs = __dmul_rn(h, __hiloint2double(es << 20, 0));
+    const double c0 = __dmul_rn(hs, -0x1p52);
 #pragma unroll
-        for (int k = 0; k < 4; ++k) {
-            // RN(mag * hs) as one FMA on the FP64 pipe: (2^52 + mag) * hs
-            // - 2^52 * hs is exactly mag * hs before the single rounding
-            const double p = fma(__hiloint2double(0x43300000, static_cast<int>(c.mag[k])), hs, c0);
-            w[k] = __dsub_rn(w[k], __hiloint2double(__double2hiint(p) ^ static_cast<int>(c.sgn[k]), __double2loint(p)));
-        }
+    for (int k = 0; k < 4; ++k) {
+        // RN(mag * hs) as one FMA on the FP64 pipe: (2^52 + mag) * hs
+        // - 2^52 * hs is exactly mag * hs before the single rounding
+        const double p = fma(__hiloint2double(0x43300000, static_cast<int>(c.mag[k])), hs, c0);
+        w[k] = __dsub_rn(w[k], __hiloint2double(__double2hiint(p) ^ static_cast<int>(c.sgn[k]), __double2loint(p)));
+    }
+}
+
+template <int L>
+__device__ __forceinline__ void frsz_update(const Codes4& c, uint32_t e, double h, int h_exp, double w[4]) {
+    if (__builtin_expect(__all_sync(0xFFFFFFFFu, frsz_upd_ok<L>(e, h, h_exp)), 1)) {
+        frsz_update_fast<L>(c, e, h, w);
         return;
     }
     double v[4];
@@ -263,6 +275,11 @@ template <> struct Step<kZ32> {
     __device__ __forceinline__ double dot(const double w[4]) const { return frsz_dot<32>(codes(), e, w); }
     __device__ __forceinline__ void decode(double v[4]) const { frsz_decode<32>(codes(), e, v); }
     __device__ __forceinline__ void update(double h, int he, double w[4]) const { frsz_update<32>(codes(), e, h, he, w); }
+    // stage-level fast path (the caller votes once over all steps of a stage)
+    __device__ __forceinline__ bool fast() const { return e > 32 - 2; }
+    __device__ __forceinline__ double dot_fast(const double w[4]) const { return fast_dot<32>(codes(), e, w); }
+    __device__ __forceinline__ bool upd_ok(double h, int he) const { return frsz_upd_ok<32>(e, h, he); }
+    __device__ __forceinline__ void update_fast(double h, int, double w[4]) const { frsz_update_fast<32>(codes(), e, h, w); }
 };
 
 template <> struct Step<kZ16> {
@@ -283,6 +300,11 @@ template <> struct Step<kZ16> {
     __device__ __forceinline__ double dot(const double w[4]) const { return frsz_dot<16>(codes(), e, w); }
     __device__ __forceinline__ void decode(double v[4]) const { frsz_decode<16>(codes(), e, v); }
     __device__ __forceinline__ void update(double h, int he, double w[4]) const { frsz_update<16>(codes(), e, h, he, w); }
+    // stage-level fast path (the caller votes once over all steps of a stage)
+    __device__ __forceinline__ bool fast() const { return e > 16 - 2; }
+    __device__ __forceinline__ double dot_fast(const double w[4]) const { return fast_dot<16>(codes(), e, w); }
+    __device__ __forceinline__ bool upd_ok(double h, int he) const { return frsz_upd_ok<16>(e, h, he); }
+    __device__ __forceinline__ void update_fast(double h, int, double w[4]) const { frsz_update_fast<16>(codes(), e, h, w); }
 };
 
 template <> struct Step<kZ21> {
@@ -315,6 +337,11 @@ template <> struct Step<kZ21> {
     __device__ __forceinline__ double dot(const double w[4]) const { return frsz_dot<21>(codes(), e, w); }
     __device__ __forceinline__ void decode(double v[4]) const { frsz_decode<21>(codes(), e, v); }
     __device__ __forceinline__ void update(double h, int he, double w[4]) const { frsz_update<21>(codes(), e, h, he, w); }
+    // stage-level fast path (the caller votes once over all steps of a stage)
+    __device__ __forceinline__ bool fast() const { return e > 21 - 2; }
+    __device__ __forceinline__ double dot_fast(const double w[4]) const { return fast_dot<21>(codes(), e, w); }
+    __device__ __forceinline__ bool upd_ok(double h, int he) const { return frsz_upd_ok<21>(e, h, he); }
+    __device__ __forceinline__ void update_fast(double h, int, double w[4]) const { frsz_update_fast<21>(codes(), e, h, w); }
 };
 
 template <> struct Step<kF64> {

@@ -107,6 +107,24 @@ __device__ __forceinline__ void step_lds<kZ21>(Step<kZ21>& st, const unsigned ch
     st.w0 = p[q]; st.w1 = p[q + 1]; st.w2 = p[q + 2]; st.w3 = p[q + 3];
     st.e = ex[r / 32];
 }
+// Payload only (the exponent was read by the caller for the stage vote).
+template <int F>
+__device__ __forceinline__ void step_lds_pay(Step<F>& st, const unsigned char* pay, uint32_t r) {
+    if constexpr (F == kZ32) {
+        st.c = *reinterpret_cast<const uint4*>(pay + 4u * r);
+    } else if constexpr (F == kZ16) {
+        st.c = *reinterpret_cast<const uint2*>(pay + 2u * r);
+    } else if constexpr (F == kZ21) {
+        const uint32_t* p = reinterpret_cast<const uint32_t*>(pay);
+        const uint32_t bit = (r & 31u) * 21u;
+        const uint32_t q = (r / 32) * 21 + (bit >> 5);
+        st.sh = bit & 31u;
+        st.w0 = p[q]; st.w1 = p[q + 1]; st.w2 = p[q + 2]; st.w3 = p[q + 3];
+    } else {
+        step_lds<F>(st, pay, nullptr, r);
+    }
+}
+
 template <>
 __device__ __forceinline__ void step_lds<kF64>(Step<kF64>& st, const unsigned char* pay, const uint32_t*, uint32_t r) {
     const double2* p = reinterpret_cast<const double2*>(pay + 8u * r);
@@ -120,6 +138,130 @@ __device__ __forceinline__ void step_lds<kF32>(Step<kF32>& st, const unsigned ch
 template <>
 __device__ __forceinline__ void step_lds<kF16>(Step<kF16>& st, const unsigned char* pay, const uint32_t*, uint32_t r) {
     st.c = *reinterpret_cast<const uint2*>(pay + 2u * r);
+}
+
+// Per-thread offsets into a ring stage, constant for the whole launch: step s
+// of the stage sits at + s * PAY bytes (payload) and + 32 s words (exponents),
+// so the per-step addresses fold into immediates.
+template <int F> struct StageOff {
+    uint32_t pay;  // bytes
+    uint32_t ex;   // words
+    uint32_t sh;   // l=21: bit offset of the thread's first code in its window
+    __device__ __forceinline__ StageOff() {
+        const uint32_t t = threadIdx.x;
+        if constexpr (F == kZ21) {
+            const uint32_t bit = (t & 7u) * 84u;  // rows 4t..4t+3 of block t/8
+            pay = ((t >> 3) * 21u + (bit >> 5)) * 4u;
+            sh = bit & 31u;
+        } else {
+            pay = t * (Geo<F>::pay / kConsumers);  // 4 rows per thread
+            sh = 0;
+        }
+        ex = t >> 3;
+    }
+};
+
+template <int F>
+__device__ __forceinline__ void step_lds_at(Step<F>& st, const unsigned char* pay, const uint32_t* ex, const StageOff<F>& o,
+                                            int s, bool with_exp = true) {
+    const unsigned char* p = pay + s * Geo<F>::pay;
+    if constexpr (FmtInfo<F>::frsz) {
+        if (with_exp) st.e = ex[32 * s];
+    }
+    if constexpr (F == kZ32) {
+        st.c = *reinterpret_cast<const uint4*>(p);
+    } else if constexpr (F == kZ16) {
+        st.c = *reinterpret_cast<const uint2*>(p);
+    } else if constexpr (F == kZ21) {
+        const uint32_t* q = reinterpret_cast<const uint32_t*>(p);
+        st.sh = o.sh;
+        st.w0 = q[0]; st.w1 = q[1]; st.w2 = q[2]; st.w3 = q[3];
+    } else if constexpr (F == kF64) {
+        st.a = reinterpret_cast<const double2*>(p)[0];
+        st.b = reinterpret_cast<const double2*>(p)[1];
+    } else if constexpr (F == kF32) {
+        st.c = *reinterpret_cast<const float4*>(p);
+    } else {
+        st.c = *reinterpret_cast<const uint2*>(p);
+    }
+}
+
+// One column's stage of a sub-tile. The exponents of all steps are read
+// first and ONE warp vote decides the fast decode for the whole stage (the
+// exact per-step path only when some block of the stage needs it); payloads
+// are read step by step (kPreload: all up front -- more loads in flight, but
+// the register pressure spills at 3 CTAs/SM: slower for every format on B200,
+// scripts/ab_split.sh). kFull: all Geo<F>::sub steps are present (every tile but the
+// last), no per-step bounds checks.
+#ifndef SPLIT_PRELOAD_MASK
+#define SPLIT_PRELOAD_MASK 0
+#endif
+template <int F> constexpr bool kPreload = (SPLIT_PRELOAD_MASK >> F) & 1;
+
+template <int F, bool kFull>
+__device__ __forceinline__ double stage_dot(const unsigned char* pay, const uint32_t* ex, const StageOff<F>& o,
+                                            uint32_t steps, const double (&wv)[Geo<F>::sub][4]) {
+    constexpr int SUB = Geo<F>::sub;
+    Step<F> st[SUB];
+    double acc = 0.0;
+    if constexpr (FmtInfo<F>::frsz) {
+        bool ok = true;
+#pragma unroll
+        for (int s = 0; s < SUB; ++s)
+            if (kFull || s < steps) {
+                st[s].e = ex[32 * s];
+                ok &= st[s].fast();
+                if constexpr (kPreload<F>) step_lds_at<F>(st[s], pay, ex, o, s, false);
+            }
+        if (__builtin_expect(__all_sync(0xFFFFFFFFu, ok), 1)) {
+#pragma unroll
+            for (int s = 0; s < SUB; ++s)
+                if (kFull || s < steps) {
+                    if constexpr (!kPreload<F>) step_lds_at<F>(st[s], pay, ex, o, s, false);
+                    acc = __dadd_rn(acc, st[s].dot_fast(wv[s]));
+                }
+            return acc;
+        }
+    }
+#pragma unroll
+    for (int s = 0; s < SUB; ++s)
+        if (kFull || s < steps) {
+            step_lds_at<F>(st[s], pay, ex, o, s);
+            acc = __dadd_rn(acc, st[s].dot(wv[s]));
+        }
+    return acc;
+}
+
+template <int F, bool kFull>
+__device__ __forceinline__ void stage_update(const unsigned char* pay, const uint32_t* ex, const StageOff<F>& o,
+                                             uint32_t steps, double hj, int he, double (&wv)[Geo<F>::sub][4]) {
+    constexpr int SUB = Geo<F>::sub;
+    Step<F> st[SUB];
+    if constexpr (FmtInfo<F>::frsz) {
+        bool ok = true;
+#pragma unroll
+        for (int s = 0; s < SUB; ++s)
+            if (kFull || s < steps) {
+                st[s].e = ex[32 * s];
+                ok &= st[s].upd_ok(hj, he);
+                if constexpr (kPreload<F>) step_lds_at<F>(st[s], pay, ex, o, s, false);
+            }
+        if (__builtin_expect(__all_sync(0xFFFFFFFFu, ok), 1)) {
+#pragma unroll
+            for (int s = 0; s < SUB; ++s)
+                if (kFull || s < steps) {
+                    if constexpr (!kPreload<F>) step_lds_at<F>(st[s], pay, ex, o, s, false);
+                    st[s].update_fast(hj, he, wv[s]);
+                }
+            return;
+        }
+    }
+#pragma unroll
+    for (int s = 0; s < SUB; ++s)
+        if (kFull || s < steps) {
+            step_lds_at<F>(st[s], pay, ex, o, s);
+            st[s].update(hj, he, wv[s]);
+        }
 }
 
 __device__ __forceinline__ void load_w(const double* __restrict__ w, uint64_t n, uint64_t r, double out[4]) {
@@ -218,6 +360,7 @@ cgs_dot_kernel(BasisView B, uint64_t first, uint32_t cols, const double* __restr
     if (warp == kConsumerWarps) {
         if (lane == 0) produce<F>(R, B, first, cols, s0, s1, true);
     } else {
+        const StageOff<F> off;
         uint32_t it = 0;
         const SubTiles T = sub_tiles<F>(s0, s1);
         for (uint64_t t = 0; t < T.count; ++t) {
@@ -247,15 +390,8 @@ cgs_dot_kernel(BasisView B, uint64_t first, uint32_t cols, const double* __restr
                 mbar_wait(R.full + stage, (it / S) & 1);
                 const unsigned char* pay = R.stages + stage * stage_bytes<F>();
                 const uint32_t* ex = reinterpret_cast<const uint32_t*>(pay + Geo<F>::sub * PAY);
-                double acc = 0.0;
-#pragma unroll
-                for (int s = 0; s < Geo<F>::sub; ++s) {
-                    if (s < steps) {
-                        Step<F> st;
-                        step_lds<F>(st, pay, ex, s * kStepRows + 4u * threadIdx.x);
-                        acc = __dadd_rn(acc, st.dot(wv[s]));
-                    }
-                }
+                double acc = steps == Geo<F>::sub ? stage_dot<F, true>(pay + off.pay, ex + off.ex, off, steps, wv)
+                                                  : stage_dot<F, false>(pay + off.pay, ex + off.ex, off, steps, wv);
                 __syncwarp();
                 if (lane == 0) mbar_arrive(R.empty + stage);
                 acc = warp_sum(acc);
@@ -290,6 +426,7 @@ cgs_update_kernel(BasisView B, uint64_t first, uint32_t cols, const double* __re
     if (warp == kConsumerWarps) {
         if (lane == 0) produce<F>(R, B, first, cols, s0, s1, false);
     } else {
+        const StageOff<F> off;
         uint32_t it = 0;
         double nacc = 0.0;
         const SubTiles T = sub_tiles<F>(s0, s1);
@@ -309,14 +446,8 @@ cgs_update_kernel(BasisView B, uint64_t first, uint32_t cols, const double* __re
                 const uint32_t* ex = reinterpret_cast<const uint32_t*>(pay + Geo<F>::sub * PAY);
                 const double hj = hs[j];
                 const int he = static_cast<int>(exp_field(hj));
-#pragma unroll
-                for (int s = 0; s < Geo<F>::sub; ++s) {
-                    if (s < steps) {
-                        Step<F> st;
-                        step_lds<F>(st, pay, ex, s * kStepRows + 4u * threadIdx.x);
-                        st.update(hj, he, wv[s]);
-                    }
-                }
+                if (steps == Geo<F>::sub) stage_update<F, true>(pay + off.pay, ex + off.ex, off, steps, hj, he, wv);
+                else stage_update<F, false>(pay + off.pay, ex + off.ex, off, steps, hj, he, wv);
                 __syncwarp();
                 if (lane == 0) mbar_arrive(R.empty + stage);
             }
@@ -356,6 +487,9 @@ cgs_update_kernel(BasisView B, uint64_t first, uint32_t cols, const double* __re
 // <w, w> is summed per tile and the tiles in tile order -- deterministic
 // whatever the assignment.
 constexpr uint32_t kTileEnd = 0xFFFFFFFFu;
+#ifndef SPLIT_PAIR_REDUCE
+#define SPLIT_PAIR_REDUCE 0  // neutral on B200 (scripts/ab_split.sh): the column passes are not reduction-bound
+#endif
 
 __device__ __forceinline__ unsigned ld_acquire_u32(const unsigned* p) {
     unsigned v;
@@ -419,6 +553,7 @@ cgs_update_dyn_kernel(BasisView B, uint64_t first, uint32_t cols, const double* 
             mbar_arrive(R.full + stage);
         }
     } else {
+        const StageOff<F> off;
         uint32_t it = 0;
         for (;;) {
             const int stage0 = it % S;
@@ -440,14 +575,8 @@ cgs_update_dyn_kernel(BasisView B, uint64_t first, uint32_t cols, const double* 
                 const uint32_t* ex = reinterpret_cast<const uint32_t*>(pay + Geo<F>::sub * PAY);
                 const double hj = hs[j];
                 const int he = static_cast<int>(exp_field(hj));
-#pragma unroll
-                for (int s = 0; s < Geo<F>::sub; ++s) {
-                    if (s < steps) {
-                        Step<F> st;
-                        step_lds<F>(st, pay, ex, s * kStepRows + 4u * threadIdx.x);
-                        st.update(hj, he, wv[s]);
-                    }
-                }
+                if (steps == Geo<F>::sub) stage_update<F, true>(pay + off.pay, ex + off.ex, off, steps, hj, he, wv);
+                else stage_update<F, false>(pay + off.pay, ex + off.ex, off, steps, hj, he, wv);
                 __syncwarp();
                 if (lane == 0) mbar_arrive(R.empty + stage);
             }
@@ -565,6 +694,7 @@ cgs_dot_dyn_kernel(BasisView B, uint64_t first, uint32_t cols, const double* __r
             mbar_arrive(R.full + stage);
         }
     } else {
+        const StageOff<F> off;
         uint32_t it = 0;
         const uint32_t per_tile = cols ? cols : 1u;
         for (;;) {
@@ -589,30 +719,42 @@ cgs_dot_dyn_kernel(BasisView B, uint64_t first, uint32_t cols, const double* __r
                 acc = warp_sum(acc);
                 if (lane == 0) red[warp * ncol + cols] = acc;
             }
-            for (uint32_t jj = 0; jj < per_tile; ++jj, ++it) {
+            // one column's stage: wait (the tile's first stage was waited on
+            // above), the lane's partial, release the stage
+            auto column = [&](uint32_t jj) -> double {
                 const int stage = it % S;
                 if (jj) mbar_wait(R.full + stage, (it / S) & 1);
-                if (cols) {
-                    const uint32_t j = cols - 1 - jj;
-                    const unsigned char* pay = R.stages + stage * stage_bytes<F>();
-                    const uint32_t* ex = reinterpret_cast<const uint32_t*>(pay + Geo<F>::sub * PAY);
-                    double acc = 0.0;
-#pragma unroll
-                    for (int s = 0; s < Geo<F>::sub; ++s) {
-                        if (s < steps) {
-                            Step<F> st;
-                            step_lds<F>(st, pay, ex, s * kStepRows + 4u * threadIdx.x);
-                            acc = __dadd_rn(acc, st.dot(wv[s]));
-                        }
-                    }
-                    __syncwarp();
-                    if (lane == 0) mbar_arrive(R.empty + stage);
-                    acc = warp_sum(acc);
-                    if (lane == 0) red[warp * ncol + j] = acc;
-                } else {
-                    __syncwarp();
-                    if (lane == 0) mbar_arrive(R.empty + stage);
+                const unsigned char* pay = R.stages + stage * stage_bytes<F>();
+                const uint32_t* ex = reinterpret_cast<const uint32_t*>(pay + Geo<F>::sub * PAY);
+                const double acc = steps == Geo<F>::sub
+                                       ? stage_dot<F, true>(pay + off.pay, ex + off.ex, off, steps, wv)
+                                       : stage_dot<F, false>(pay + off.pay, ex + off.ex, off, steps, wv);
+                __syncwarp();
+                if (lane == 0) mbar_arrive(R.empty + stage);
+                ++it;
+                return acc;
+            };
+            if (cols) {
+                uint32_t jj = 0;
+#if SPLIT_PAIR_REDUCE
+                // columns in pairs: one butterfly for two sums
+                for (; jj + 1 < cols; jj += 2) {
+                    const double a = column(jj);
+                    const double b = column(jj + 1);
+                    const double v = warp_sum2(a, b);
+                    if (lane == 0) red[warp * ncol + cols - 1 - jj] = v;
+                    if (lane == 16) red[warp * ncol + cols - 2 - jj] = v;
                 }
+#endif
+                for (; jj < cols; ++jj) {
+                    const double v = warp_sum(column(jj));
+                    if (lane == 0) red[warp * ncol + cols - 1 - jj] = v;
+                }
+            } else {
+                const int stage = it % S;
+                __syncwarp();
+                if (lane == 0) mbar_arrive(R.empty + stage);
+                ++it;
             }
             // this tile's partials: warps in order, column-major table
             split_consumer_sync();
@@ -914,6 +1056,9 @@ template <int F> struct ReadLaunch {
 #ifndef FUSED_STEPS
 #define FUSED_STEPS 5
 #endif
+#ifndef FUSED_STAGE_VOTE
+#define FUSED_STAGE_VOTE 0  // 9.04 vs 8.02 ms on the bench solve (register pressure at 72 regs)
+#endif
 constexpr int kFusedMaxSteps = FUSED_STEPS;
 constexpr int kFCtasPerSM = FUSED_CTAS_PER_SM;
 constexpr int kFWarps = FUSED_WARPS;            // consumer warps
@@ -1194,6 +1339,48 @@ __device__ __forceinline__ void fused_pass(uint32_t cols, uint32_t lim, uint32_t
             mbar_wait(full + stage, (it / S) & 1);
             const unsigned char* pay = stages + stage * SB;
             const uint32_t* ex = reinterpret_cast<const uint32_t*>(pay + kChunkSteps * PAY);
+#if FUSED_STAGE_VOTE
+            if constexpr (FmtInfo<F>::frsz) {
+                // exponents of the chunk first, ONE warp vote for its fast path
+                Step<F> st[kChunkSteps];
+                bool ok = true;
+#pragma unroll
+                for (int s = 0; s < kChunkSteps; ++s) {
+                    const int gs = ch * kChunkSteps + s;
+                    if (gs < kFusedMaxSteps && static_cast<uint32_t>(gs) < steps) {
+                        st[s].e = ex[(s * kFStepRows + 4u * threadIdx.x) / 32];
+                        if constexpr (kDot) ok &= st[s].fast();
+                        else ok &= st[s].upd_ok(hj, he);
+                    }
+                }
+                if (__builtin_expect(__all_sync(0xFFFFFFFFu, ok), 1)) {
+#pragma unroll
+                    for (int s = 0; s < kChunkSteps; ++s) {
+                        const int gs = ch * kChunkSteps + s;
+                        if (gs < kFusedMaxSteps && static_cast<uint32_t>(gs) < steps) {
+                            step_lds_pay<F>(st[s], pay, s * kFStepRows + 4u * threadIdx.x);
+                            if constexpr (kDot) {
+#if FUSED_DOT_ACC4
+                                if ((s & 3) == 0) acc = __dadd_rn(acc, st[s].dot_fast(wv[gs]));
+                                else if ((s & 3) == 1) acc2 = __dadd_rn(acc2, st[s].dot_fast(wv[gs]));
+                                else if ((s & 3) == 2) acc3 = __dadd_rn(acc3, st[s].dot_fast(wv[gs]));
+                                else acc4 = __dadd_rn(acc4, st[s].dot_fast(wv[gs]));
+#else
+                                if (s & 1) acc2 = __dadd_rn(acc2, st[s].dot_fast(wv[gs]));
+                                else acc = __dadd_rn(acc, st[s].dot_fast(wv[gs]));
+#endif
+                            } else {
+                                st[s].update_fast(hj, he, wv[gs]);
+                            }
+                        }
+                    }
+                    __syncwarp();
+                    if (lane == 0) mbar_arrive(empty + stage);
+                    ++it;
+                    continue;
+                }
+            }
+#endif
 #pragma unroll
             for (int s = 0; s < kChunkSteps; ++s) {
                 const int gs = ch * kChunkSteps + s;

@@ -248,6 +248,19 @@ __device__ __forceinline__ double warp_sum(double v) {
     return v;
 }
 
+// Two warp sums in one butterfly: the first level exchanges a for b between
+// the half-warps, then each half reduces one of them. Returns a's sum in lane
+// 0 and b's in lane 16 -- bit-identical to warp_sum (a butterfly's additions
+// are the same pairs, and x + y == y + x).
+__device__ __forceinline__ double warp_sum2(double a, double b) {
+    const bool hi = (threadIdx.x & 16) != 0;
+    double v = hi ? b : a;
+    v = __dadd_rn(v, __shfl_xor_sync(0xFFFFFFFFu, hi ? a : b, 16));
+#pragma unroll
+    for (int o = 8; o > 0; o >>= 1) v = __dadd_rn(v, __shfl_xor_sync(0xFFFFFFFFu, v, o));
+    return v;
+}
+
 }  // namespace cbgx
 
 namespace cbgx {
