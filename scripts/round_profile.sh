@@ -27,10 +27,15 @@ timeout 600 ncu --set full --clock-control none --import-source on -k regex:deco
     python scripts/quick_perf.py > /dev/null 2>&1
 timeout 600 ncu --set full --clock-control none --import-source on -k regex:compress4 -s 3 -c 1 -o "$OUT/ncu_compress" \
     python scripts/quick_perf.py > /dev/null 2>&1
-timeout 600 ncu --set full --clock-control none --import-source on -k regex:cgs_dot_kernel -s 2 -c 1 -o "$OUT/ncu_cgs_dot_2p26" \
-    python scripts/cgs_micro.py --k 100 --formats frsz2-32 --reps 1 > /dev/null 2>&1
-timeout 600 ncu --set full --clock-control none --import-source on -k regex:cgs_update_kernel -s 2 -c 1 -o "$OUT/ncu_cgs_update_2p26" \
-    python scripts/cgs_micro.py --k 100 --formats frsz2-32 --reps 1 > /dev/null 2>&1
+# split CGS kernels (dynamic tiles) at n = 2^26, k = 100, per FRSZ2 format: the
+# reports stay on the box (size), their raw metric pages come back as CSV
+for f in frsz2-32 frsz2-21 frsz2-16; do
+  for kk in dot update; do
+    timeout 300 ncu --set full --clock-control none --import-source on -k regex:cgs_${kk}_dyn -s 1 -c 1 -o /tmp/ncu_cgs_${kk}_$f \
+        python scripts/cgs_micro.py --k 100 --formats $f --reps 2 > /dev/null 2>&1
+    ncu -i /tmp/ncu_cgs_${kk}_$f.ncu-rep --page raw --csv > "$OUT/ncu_cgs_${kk}_${f}_raw.csv" 2>&1
+  done
+done
 timeout 900 python scripts/read_bench.py > "$OUT/read_bench.csv" 2>&1
 timeout 1800 python scripts/config_sweep.py --configs 2,3 > "$OUT/config_sweep_c2_c3.jsonl" 2>&1
 timeout 1800 python scripts/config_sweep.py --configs 5 --reps 1 > "$OUT/config_sweep_c5.jsonl" 2>&1
