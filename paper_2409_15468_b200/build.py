@@ -20,6 +20,7 @@ INCLUDE = os.path.join(ROOT, "include")
 BUILD = os.path.join(PKG, "_build")
 LIB = os.path.join(PKG, "libcbgx.so")
 DROPIN_LIB = os.path.join(PKG, "libcbg_b200.so")
+CLI_BIN = os.path.join(PKG, "cbgmres")
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
@@ -90,6 +91,22 @@ def _build_dropin(force: bool) -> None:
     r = subprocess.run(cmd, capture_output=True, text=True)
     if r.returncode != 0:
         raise RuntimeError("drop-in build failed:\n" + r.stderr)
+    _build_cli(True)
+
+
+def _build_cli(force: bool) -> None:
+    """The `cbgmres` tool (the reference's tools/cbgmres_main.cpp) over libcbg_b200.so."""
+    src = os.path.join(CSRC, "tools", "cbgmres.cpp")
+    if not os.path.exists(src):
+        return
+    if not force and os.path.exists(CLI_BIN) and os.path.getmtime(CLI_BIN) >= max(
+            os.path.getmtime(src), os.path.getmtime(DROPIN_LIB)):
+        return
+    cmd = ["g++", "-std=gnu++20", "-O2", "-I" + INCLUDE, "-o", CLI_BIN, src,
+           "-L" + PKG, "-lcbg_b200", "-lcbgx", "-Wl,-rpath,$ORIGIN"]
+    r = subprocess.run(cmd, capture_output=True, text=True)
+    if r.returncode != 0:
+        raise RuntimeError("cbgmres build failed:\n" + r.stderr)
 
 
 if __name__ == "__main__":
