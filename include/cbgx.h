@@ -190,6 +190,17 @@ int cbgx_csr_spmv(const cbgx_csr* A, const double* d_x, double* d_y, double* d_y
 int cbgx_csr_spmv_plan(const cbgx_csr* A, uint32_t* tile_rows, void* stream);
 int cbgx_csr_spmv_staged(const cbgx_csr* A, uint32_t tile_rows, const double* d_x, const double* d_b,
                          double* d_y, double* d_ynorm2, int reduction, cbgx_workspace* ws, void* stream);
+/* Dictionary-coded SELL-32 copy of A (dsell.cu): entries become 2-byte codes
+ * into <= 255 distinct values and <= 255 distinct column offsets (col - row)
+ * -- the structured-grid matrices of the paper's configurations -- 6x fewer
+ * matrix bytes per SpMV, y bit-identical to cbgx_csr_spmv. create fails with
+ * CBGX_EINVAL for matrices outside the pattern. d_b != NULL: r = b - A x. */
+typedef struct cbgx_dict_csr cbgx_dict_csr;
+int cbgx_csr_dict_create(const cbgx_csr* A, cbgx_dict_csr** out, void* stream);
+int cbgx_csr_dict_info(const cbgx_dict_csr* D, uint32_t* n_offsets, uint32_t* n_values, uint64_t* entries);
+int cbgx_csr_dict_spmv(const cbgx_csr* A, const cbgx_dict_csr* D, const double* d_x, const double* d_b, double* d_y,
+                       double* d_ynorm2, int reduction, cbgx_workspace* ws, void* stream);
+void cbgx_csr_dict_destroy(cbgx_dict_csr* D);
 /* r = b - A x (gmres.cpp:181-184); if d_rnorm2, also <r, r>. */
 int cbgx_csr_residual(const cbgx_csr* A, const double* d_x, const double* d_b, double* d_r,
                       double* d_rnorm2, int reduction, cbgx_workspace* ws, void* stream);
@@ -245,8 +256,9 @@ enum {
     CBGX_SOLVER_NO_FUSION = 4,             /* always use the split dot/update/write kernels */
     CBGX_SOLVER_NO_SELL = 8,               /* SpMV directly on the CSR (no SELL-32 copy) */
     CBGX_SOLVER_NO_TMA_SPMV = 16,          /* no staged (bulk-copy) CSR SpMV */
-    CBGX_SOLVER_FOLD = 32                  /* fold the SpMV into the fused orthogonalisation launch
+    CBGX_SOLVER_FOLD = 32,                 /* fold the SpMV into the fused orthogonalisation launch
                                               (experimental; measured slower on B200, off by default) */
+    CBGX_SOLVER_NO_DICT_SPMV = 64          /* no dictionary-coded SELL-32 copy (cbgx_csr_dict_*) */
 };
 
 typedef struct {

@@ -572,6 +572,44 @@ def spmv_staged(a: DeviceCsr, x, tile_rows: int, b=None, want_norm=False, reduct
     return (y[:a.desc.n_rows], nrm) if want_norm else y[:a.desc.n_rows]
 
 
+class DictCsr:
+    """Dictionary-coded SELL-32 copy of a device CSR matrix (cbgx_csr_dict_*):
+    2-byte codes into <= 255 distinct values and column offsets. Raises
+    CbgxError for matrices outside that pattern."""
+
+    def __init__(self, a: DeviceCsr):
+        import ctypes
+        self.a = a
+        self.h = ctypes.c_void_p()
+        check(lib().cbgx_csr_dict_create(ctypes.byref(a.desc), ctypes.byref(self.h), _stream()))
+
+    def info(self):
+        import ctypes
+        no, nv, ne = ctypes.c_uint32(), ctypes.c_uint32(), ctypes.c_uint64()
+        check(lib().cbgx_csr_dict_info(self.h, ctypes.byref(no), ctypes.byref(nv), ctypes.byref(ne)))
+        return no.value, nv.value, ne.value
+
+    def spmv(self, x, b=None, want_norm=False, reduction=_lib.REDUCE_TREE):
+        """y = A x, or r = b - A x when b is given."""
+        import ctypes
+        torch = _torch()
+        x = _dev(x)
+        bb = _dev(b) if b is not None else None
+        y = torch.empty(max(self.a.desc.n_rows, 1), dtype=torch.float64, device="cuda")
+        nrm = torch.empty(1, dtype=torch.float64, device="cuda") if want_norm else None
+        check(lib().cbgx_csr_dict_spmv(ctypes.byref(self.a.desc), self.h, _ptr(x), _ptr(bb), _ptr(y), _ptr(nrm),
+                                       reduction, _ws(), _stream()))
+        return (y[:self.a.desc.n_rows], nrm) if want_norm else y[:self.a.desc.n_rows]
+
+    def __del__(self):
+        try:
+            if self.h:
+                lib().cbgx_csr_dict_destroy(self.h)
+                self.h = None
+        except Exception:
+            pass
+
+
 def dot(x, y, reduction=_lib.REDUCE_TREE) -> float:
     torch = _torch()
     x, y = _dev(x), _dev(y)
@@ -613,12 +651,14 @@ class GmresConfig:
     sell: bool = True     # SELL-32 copy of A for the SpMV when memory allows
     tma_spmv: bool = True  # staged (bulk-copy) CSR SpMV when every row tile fits
     fold: bool = False     # SpMV folded into the fused orthogonalisation launch (experimental)
+    dict_spmv: bool = True  # dictionary-coded SELL-32 SpMV when A has <= 255 distinct values/offsets
 
     def c(self):
         flags = (_lib.PHASE_TIMING if self.phase_timing else 0) | \
             (_lib.PHASE_TIMING_DEFERRED if self.phase_timing_deferred else 0) | \
             (0 if self.fusion else _lib.NO_FUSION) | (0 if self.sell else _lib.NO_SELL) | \
-            (0 if self.tma_spmv else _lib.NO_TMA_SPMV) | (_lib.FOLD if self.fold else 0)
+            (0 if self.tma_spmv else _lib.NO_TMA_SPMV) | (_lib.FOLD if self.fold else 0) | \
+            (0 if self.dict_spmv else _lib.NO_DICT_SPMV)
         return _lib.GmresConfig(self.restart, self.target_rrn, self.max_total_iterations, self.eta,
                                 self.storage_format.kind, self.storage_format.bit_length,
                                 self.reduction, flags)

@@ -17,6 +17,7 @@ NO_FUSION = 4
 NO_SELL = 8
 NO_TMA_SPMV = 16
 FOLD = 32
+NO_DICT_SPMV = 64
 PHASES = ["spmv", "dot", "update", "write", "residual", "solution", "comm", "ortho"]
 
 u32, u64, i32, i64, dbl, vp = C.c_uint32, C.c_uint64, C.c_int32, C.c_int64, C.c_double, C.c_void_p
@@ -92,6 +93,10 @@ def lib():
             "cbgx_csr_residual": ([P(Csr), vp, vp, vp, vp, C.c_int, vp, vp], C.c_int),
             "cbgx_csr_spmv_plan": ([P(Csr), P(C.c_uint32), vp], C.c_int),
             "cbgx_csr_spmv_staged": ([P(Csr), C.c_uint32, vp, vp, vp, vp, C.c_int, vp, vp], C.c_int),
+            "cbgx_csr_dict_create": ([P(Csr), P(vp), vp], C.c_int),
+            "cbgx_csr_dict_info": ([vp, P(C.c_uint32), P(C.c_uint32), P(C.c_uint64)], C.c_int),
+            "cbgx_csr_dict_spmv": ([P(Csr), vp, vp, vp, vp, vp, C.c_int, vp, vp], C.c_int),
+            "cbgx_csr_dict_destroy": ([vp], None),
             "cbgx_dot": ([vp, vp, u64, C.c_int, vp, vp, vp], C.c_int),
             "cbgx_scale": ([dbl, vp, u64, vp], C.c_int),
             "cbgx_axpy": ([dbl, vp, vp, u64, vp], C.c_int),

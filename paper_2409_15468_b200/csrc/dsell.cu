@@ -1,0 +1,512 @@
+// dsell.cu -- dictionary-coded SELL-32 SpMV ("DSELL").
+//
+// The SpMV of the reference (sparse.cpp:43-56) streams 12 B per entry (8 B
+// value + 4 B column) on the device -- for the structured-grid systems of
+// the paper's configurations (7/27-point stencils, 5-point convection-
+// diffusion) that is all the solver reads besides the basis. Those matrices
+// hold a handful of distinct values and a handful of distinct column offsets
+// (col - row). At setup the solver detects that (at most 255 of each) and
+// builds a SELL-32 copy whose entries are 2-byte codes
+//     code = value_index << 8 | offset_index      (0xFFFF = slice padding)
+// into two tiny dictionaries kept in shared memory, so an entry costs 2 B of
+// HBM instead of 12 (6x fewer matrix bytes). Entry k of row 32s + lane sits
+// at soff[s] + 32 k + lane (coalesced 64-B warp loads), entries keep their
+// in-row order, and the decoded (value, column) pairs are exactly the CSR's,
+// so y is bit-identical to spmv() (products and sums in row order, separate
+// roundings). Matrices outside the pattern (more distinct values/offsets,
+// halo-remapped columns) keep the CSR paths.
+#include <cub/device/device_scan.cuh>
+
+#include <algorithm>
+#include <cstring>
+#include <vector>
+
+#include "common.cuh"
+#include "pipeline.cuh"
+#include "reduce.cuh"
+#include "runtime.h"
+
+namespace cbgx {
+
+namespace {
+
+constexpr int kDThreads = 256;
+constexpr int kDWarps = kDThreads / 32;
+constexpr uint32_t kSlots = 1024;         // open-addressing hash tables (keys are u64)
+constexpr uint32_t kDictMax = 255;        // entries per dictionary (index 255 unused)
+constexpr uint16_t kPad = 0xFFFF;
+constexpr unsigned long long kEmpty = ~0ull;
+
+__device__ __forceinline__ uint32_t hslot(unsigned long long key) {
+    return static_cast<uint32_t>((key * 0x9E3779B97F4A7C15ull) >> 54);  // 10 bits
+}
+// column offsets are stored biased by 2^32 (never equal to kEmpty)
+__device__ __forceinline__ unsigned long long off_key(int64_t off) {
+    return static_cast<unsigned long long>(off + (1ll << 32));
+}
+
+// Insert `key` (idempotent). false: the table already holds kDictMax keys.
+__device__ bool table_insert(unsigned long long* tab, unsigned long long key, unsigned* count) {
+    uint32_t h = hslot(key);
+    for (uint32_t p = 0; p < kSlots; ++p) {
+        unsigned long long cur = *reinterpret_cast<volatile unsigned long long*>(tab + h);
+        if (cur == key) return true;
+        if (cur == kEmpty) {
+            cur = atomicCAS(tab + h, kEmpty, key);
+            if (cur == kEmpty) return atomicAdd(count, 1u) < kDictMax;
+            if (cur == key) return true;
+        }
+        h = (h + 1) & (kSlots - 1);
+    }
+    return false;
+}
+
+__device__ __forceinline__ uint32_t table_find(const unsigned long long* tab, unsigned long long key) {
+    uint32_t h = hslot(key);
+    while (tab[h] != key) h = (h + 1) & (kSlots - 1);
+    return h;
+}
+
+// Pass 1: the distinct column offsets and values. Every CTA dedups into its
+// own shared tables (warp-level match first), then merges them into the
+// global ones; any overflow (or an offset outside int32, or a value whose
+// bits equal the empty marker) sets *bad and the matrix keeps CSR.
+template <typename RP>
+__global__ void __launch_bounds__(kDThreads)
+dict_scan_kernel(const RP* __restrict__ rp, const int32_t* __restrict__ ci, const double* __restrict__ va,
+                 uint64_t n_rows, unsigned long long* __restrict__ g_off, unsigned long long* __restrict__ g_val,
+                 unsigned* __restrict__ g_cnt, unsigned* __restrict__ bad) {
+    __shared__ unsigned long long s_off[kSlots], s_val[kSlots];
+    __shared__ unsigned s_cnt[2];
+    for (uint32_t i = threadIdx.x; i < kSlots; i += kDThreads) s_off[i] = s_val[i] = kEmpty;
+    if (threadIdx.x < 2) s_cnt[threadIdx.x] = 0;
+    __syncthreads();
+    bool ok = true;
+    for (uint64_t r = blockIdx.x * static_cast<uint64_t>(kDThreads) + threadIdx.x; r < n_rows && ok;
+         r += static_cast<uint64_t>(gridDim.x) * kDThreads) {
+        if (*reinterpret_cast<volatile unsigned*>(bad)) break;
+        const uint64_t k0 = static_cast<uint64_t>(rp[r]), k1 = static_cast<uint64_t>(rp[r + 1]);
+        for (uint64_t k = k0; k < k1 && ok; ++k) {
+            const int64_t off = static_cast<int64_t>(ci[k]) - static_cast<int64_t>(r);
+            const unsigned long long ko = off_key(off);
+            const unsigned long long kv = static_cast<unsigned long long>(__double_as_longlong(va[k]));
+            if (off < INT32_MIN || off > INT32_MAX || kv == kEmpty) {
+                ok = false;
+                break;
+            }
+            const unsigned act = __activemask();
+            const unsigned mo = __match_any_sync(act, ko), mv = __match_any_sync(act, kv);
+            const int lane = threadIdx.x & 31;
+            if (__ffs(mo) - 1 == lane) ok = ok && table_insert(s_off, ko, &s_cnt[0]);
+            if (__ffs(mv) - 1 == lane) ok = ok && table_insert(s_val, kv, &s_cnt[1]);
+        }
+    }
+    if (!ok) atomicExch(bad, 1u);
+    __syncthreads();
+    if (*reinterpret_cast<volatile unsigned*>(bad)) return;
+    for (uint32_t i = threadIdx.x; i < kSlots; i += kDThreads) {
+        bool fine = true;
+        if (s_off[i] != kEmpty) fine = table_insert(g_off, s_off[i], &g_cnt[0]);
+        if (s_val[i] != kEmpty) fine = fine && table_insert(g_val, s_val[i], &g_cnt[1]);
+        if (!fine) atomicExch(bad, 1u);
+    }
+}
+
+// Per-slice width (longest row of the 32) in entries * 32.
+template <typename RP>
+__global__ void dict_slice_kernel(const RP* __restrict__ rp, uint64_t n, uint64_t nslices, uint64_t* __restrict__ slen,
+                                  unsigned* __restrict__ max_w) {
+    for (uint64_t sl = (blockIdx.x * static_cast<uint64_t>(blockDim.x) + threadIdx.x) / 32; sl < nslices + 1;
+         sl += static_cast<uint64_t>(gridDim.x) * blockDim.x / 32) {
+        const int lane = threadIdx.x & 31;
+        const uint64_t r = sl * 32 + lane;
+        const unsigned len = (sl < nslices && r < n) ? static_cast<unsigned>(rp[r + 1] - rp[r]) : 0u;
+        const unsigned m = __reduce_max_sync(0xFFFFFFFFu, len);
+        if (lane == 0) {
+            slen[sl] = static_cast<uint64_t>(m) * 32;
+            atomicMax(max_w, m);
+        }
+    }
+}
+
+// Pass 2: the codes, slice-major (entry k of row 32s+lane at soff[s]+32k+lane).
+template <typename RP>
+__global__ void __launch_bounds__(kDThreads)
+dict_fill_kernel(const RP* __restrict__ rp, const int32_t* __restrict__ ci, const double* __restrict__ va,
+                 uint64_t n_rows, const uint64_t* __restrict__ soff, const unsigned long long* __restrict__ g_off,
+                 const unsigned long long* __restrict__ g_val, const uint8_t* __restrict__ off_idx,
+                 const uint8_t* __restrict__ val_idx, uint32_t ell4, uint16_t* __restrict__ codes) {
+    __shared__ unsigned long long s_off[kSlots], s_val[kSlots];
+    __shared__ uint8_t s_oi[kSlots], s_vi[kSlots];
+    for (uint32_t i = threadIdx.x; i < kSlots; i += kDThreads) {
+        s_off[i] = g_off[i];
+        s_val[i] = g_val[i];
+        s_oi[i] = off_idx[i];
+        s_vi[i] = val_idx[i];
+    }
+    __syncthreads();
+    const uint64_t padded = (n_rows + 31) / 32 * 32;
+    for (uint64_t r = blockIdx.x * static_cast<uint64_t>(kDThreads) + threadIdx.x; r < padded;
+         r += static_cast<uint64_t>(gridDim.x) * kDThreads) {
+        const uint64_t sl = r / 32, lane = r % 32;
+        const uint64_t base = soff[sl], width = ell4 ? 4ull * ell4 : (soff[sl + 1] - base) / 32;
+        const uint64_t k0 = r < n_rows ? static_cast<uint64_t>(rp[r]) : 0;
+        const uint64_t len = r < n_rows ? static_cast<uint64_t>(rp[r + 1]) - k0 : 0;
+        for (uint64_t k = 0; k < width; ++k) {
+            uint16_t code = kPad;
+            if (k < len) {
+                const int64_t off = static_cast<int64_t>(ci[k0 + k]) - static_cast<int64_t>(r);
+                const uint32_t oi = s_oi[table_find(s_off, off_key(off))];
+                const uint32_t vi = s_vi[table_find(s_val, static_cast<unsigned long long>(__double_as_longlong(va[k0 + k])))];
+                code = static_cast<uint16_t>(vi << 8 | oi);
+            }
+            // SELL: entry k at base + 32 k + lane; ELL4: groups of 4 entries
+            // of a row contiguous (one 8-byte load per group), group g at
+            // ((s * ell4 + g) * 32 + lane) * 4
+            codes[ell4 ? ((sl * ell4 + k / 4) * 32 + lane) * 4 + (k & 3) : base + k * 32 + lane] = code;
+        }
+    }
+}
+
+// MODE 0: y = A x.  MODE 1: y = b - A x. One warp per slice (persistent
+// grid, one wave); kEll: every slice has the same width W (no offset table
+// to read before the codes). The first 8 codes of a warp's NEXT slice are
+// loaded before the current slice's x gathers, so the code stream of one
+// slice overlaps the gathers of the previous one. Per batch of 8 entries:
+// dictionary lookups (shared), x gathers, then the in-order multiply-adds
+// (sparse.cpp:50-52: separate roundings from +0.0).
+// SELL layout (ragged slices): one warp per slice, the first 8 codes of
+// the warp's NEXT slice are requested before the current slice's x gathers.
+__device__ __forceinline__ void sell_head(uint64_t sl, const uint64_t* __restrict__ soff,
+                                          const uint16_t* __restrict__ codes, int lane, uint64_t& base,
+                                          uint32_t& width, uint16_t (&cc)[8]) {
+    base = __ldg(soff + sl);
+    width = static_cast<uint32_t>((__ldg(soff + sl + 1) - base) / 32);
+#pragma unroll
+    for (int i = 0; i < 8; ++i) cc[i] = i < static_cast<int>(width) ? __ldcs(codes + base + 32 * i + lane) : kPad;
+}
+
+// Per batch of 8 entries: dictionary lookups (shared), x gathers, then the
+// in-order multiply-adds (sparse.cpp:50-52: separate roundings from +0.0).
+__device__ __forceinline__ double batch8(const uint16_t (&c)[8], int32_t r, const int32_t* s_o, const double* s_v,
+                                         const double* __restrict__ x, double s) {
+    double xv[8];
+#pragma unroll
+    for (int i = 0; i < 8; ++i) xv[i] = c[i] != kPad ? __ldg(x + (r + s_o[c[i] & 0xFF])) : 0.0;
+#pragma unroll
+    for (int i = 0; i < 8; ++i)
+        if (c[i] != kPad) s = __dadd_rn(s, __dmul_rn(s_v[c[i] >> 8], xv[i]));
+    return s;
+}
+
+__device__ __forceinline__ void unpack8(uint2 a, uint2 b, uint16_t (&c)[8]) {
+    c[0] = a.x & 0xFFFF; c[1] = a.x >> 16; c[2] = a.y & 0xFFFF; c[3] = a.y >> 16;
+    c[4] = b.x & 0xFFFF; c[5] = b.x >> 16; c[6] = b.y & 0xFFFF; c[7] = b.y >> 16;
+}
+
+// MODE 0: y = A x.  MODE 1: y = b - A x. Persistent grid (one wave), one
+// warp per 32-row slice. kEll: ELL4 layout (uniform width, 8-byte groups of
+// 4 codes, no offset table).
+#ifndef DSELL_MIN_BLOCKS
+#define DSELL_MIN_BLOCKS 0  // plain bounds (40 regs): 167 vs 221 us at 7-pt 256^3 (scripts/ab_spmv.sh)
+#endif
+#if DSELL_MIN_BLOCKS
+#define DSELL_BOUNDS __launch_bounds__(kDThreads, DSELL_MIN_BLOCKS)
+#else
+#define DSELL_BOUNDS __launch_bounds__(kDThreads)
+#endif
+template <int MODE, bool kEll>
+__global__ void DSELL_BOUNDS
+dsell_spmv_kernel(uint64_t n_rows, const uint64_t* __restrict__ soff, uint32_t ell_w, const uint16_t* __restrict__ codes,
+                  const int32_t* __restrict__ d_off, const double* __restrict__ d_val, const double* __restrict__ x,
+                  const double* __restrict__ b, double* __restrict__ y, int with_norm,
+                  double* __restrict__ partials, unsigned* __restrict__ ticket, double* __restrict__ norm_out) {
+    __shared__ int32_t s_o[256];
+    __shared__ double s_v[256];
+    __shared__ double red[kDWarps];
+    s_o[threadIdx.x] = d_off[threadIdx.x];
+    s_v[threadIdx.x] = d_val[threadIdx.x];
+    __syncthreads();
+    pdl_trigger();
+    const int lane = threadIdx.x & 31;
+    const uint64_t nsl = (n_rows + 31) / 32;
+    const uint64_t nw = static_cast<uint64_t>(gridDim.x) * kDWarps;
+    uint64_t sl = (blockIdx.x * static_cast<uint64_t>(kDThreads) + threadIdx.x) / 32;
+    double acc = 0.0;
+    if constexpr (kEll) {
+        const uint32_t g4 = ell_w / 4;  // 8-byte groups per row
+        const uint2* c4 = reinterpret_cast<const uint2*>(codes);
+        uint2 n0 = make_uint2(0xFFFFFFFFu, 0xFFFFFFFFu), n1 = n0;
+        // the codes do not depend on the predecessor grid
+        if (sl < nsl) {
+            n0 = __ldcs(c4 + sl * g4 * 32 + lane);
+            if (g4 > 1) n1 = __ldcs(c4 + (sl * g4 + 1) * 32 + lane);
+        }
+        pdl_wait();
+        for (; sl < nsl; sl += nw) {
+            const int32_t r = static_cast<int32_t>(sl * 32 + lane);
+            uint2 a0 = n0, a1 = n1;
+            const uint64_t nx = sl + nw;
+            if (nx < nsl) {
+                n0 = __ldcs(c4 + nx * g4 * 32 + lane);
+                if (g4 > 1) n1 = __ldcs(c4 + (nx * g4 + 1) * 32 + lane);
+            }
+            double s = 0.0;
+            for (uint32_t g = 0; g < g4; g += 2) {
+                if (g) {
+                    a0 = __ldcs(c4 + (sl * g4 + g) * 32 + lane);
+                    a1 = g + 1 < g4 ? __ldcs(c4 + (sl * g4 + g + 1) * 32 + lane) : make_uint2(0xFFFFFFFFu, 0xFFFFFFFFu);
+                } else if (g4 == 1) {
+                    a1 = make_uint2(0xFFFFFFFFu, 0xFFFFFFFFu);
+                }
+                uint16_t c[8];
+                unpack8(a0, a1, c);
+                s = batch8(c, r, s_o, s_v, x, s);
+            }
+            if (static_cast<uint64_t>(r) < n_rows) {
+                if (MODE == 1) s = __dsub_rn(__ldg(b + r), s);
+                y[r] = s;
+                if (with_norm) acc = __dadd_rn(acc, __dmul_rn(s, s));
+            }
+        }
+    } else {
+        uint16_t cc[8];
+        uint64_t base = 0;
+        uint32_t width = 0;
+        if (sl < nsl) sell_head(sl, soff, codes, lane, base, width, cc);
+        pdl_wait();
+        for (; sl < nsl; sl += nw) {
+            const int64_t r = static_cast<int64_t>(sl * 32 + lane);
+            uint16_t cur[8];
+#pragma unroll
+            for (int i = 0; i < 8; ++i) cur[i] = cc[i];
+            const uint64_t cbase = base;
+            const uint32_t cw = width;
+            if (sl + nw < nsl) sell_head(sl + nw, soff, codes, lane, base, width, cc);
+            double s = 0.0;
+            for (uint32_t k = 0; k < cw; k += 8) {
+                if (k) {
+#pragma unroll
+                    for (int i = 0; i < 8; ++i) cur[i] = k + i < cw ? __ldcs(codes + cbase + 32 * (k + i) + lane) : kPad;
+                }
+                double xv[8];
+#pragma unroll
+                for (int i = 0; i < 8; ++i) xv[i] = cur[i] != kPad ? __ldg(x + (r + s_o[cur[i] & 0xFF])) : 0.0;
+#pragma unroll
+                for (int i = 0; i < 8; ++i)
+                    if (cur[i] != kPad) s = __dadd_rn(s, __dmul_rn(s_v[cur[i] >> 8], xv[i]));
+            }
+            if (static_cast<uint64_t>(r) < n_rows) {
+                if (MODE == 1) s = __dsub_rn(__ldg(b + r), s);
+                y[r] = s;
+                if (with_norm) acc = __dadd_rn(acc, __dmul_rn(s, s));
+            }
+        }
+    }
+    if (!with_norm) return;
+    acc = warp_sum(acc);
+    if (lane == 0) red[threadIdx.x >> 5] = acc;
+    __syncthreads();
+    block_finalize(red, kDWarps, 1, partials, ticket, norm_out);
+}
+
+int dict_grid(uint64_t rows) {
+    const uint64_t want = (rows + kDThreads - 1) / kDThreads;
+    const uint64_t cap = static_cast<uint64_t>(sm_count()) * 8;
+    return static_cast<int>(std::max<uint64_t>(1, std::min(want, cap)));
+}
+
+template <typename RP>
+std::unique_ptr<DictSell> dict_build(const cbgx_csr& A, double max_fraction_of_free, cudaStream_t st) {
+    const RP* rp = static_cast<const RP*>(A.d_row_ptr);
+    // pass 1: dictionaries
+    unsigned long long* tabs = nullptr;  // [2][kSlots]
+    unsigned* flags = nullptr;           // [cnt_off, cnt_val, bad]
+    CBGX_CUDA(cudaMallocAsync(reinterpret_cast<void**>(&tabs), 2 * kSlots * sizeof(unsigned long long), st));
+    CBGX_CUDA(cudaMallocAsync(reinterpret_cast<void**>(&flags), 4 * sizeof(unsigned), st));
+    CBGX_CUDA(cudaMemsetAsync(tabs, 0xFF, 2 * kSlots * sizeof(unsigned long long), st));
+    CBGX_CUDA(cudaMemsetAsync(flags, 0, 4 * sizeof(unsigned), st));
+    CBGX_K(dict_scan_kernel<RP><<<dict_grid(A.n_rows), kDThreads, 0, st>>>(rp, A.d_col_idx, A.d_values, A.n_rows, tabs,
+                                                                            tabs + kSlots, flags, flags + 2));
+    CBGX_CUDA(cudaGetLastError());
+    std::vector<unsigned long long> h_tabs(2 * kSlots);
+    unsigned h_flags[4];
+    CBGX_CUDA(cudaMemcpyAsync(h_tabs.data(), tabs, h_tabs.size() * sizeof(unsigned long long), cudaMemcpyDeviceToHost, st));
+    CBGX_CUDA(cudaMemcpyAsync(h_flags, flags, sizeof h_flags, cudaMemcpyDeviceToHost, st));
+    CBGX_CUDA(cudaStreamSynchronize(st));
+    auto release = [&] {
+        cudaFreeAsync(tabs, st);
+        cudaFreeAsync(flags, st);
+    };
+    if (h_flags[2] || h_flags[0] > kDictMax || h_flags[1] > kDictMax) {
+        release();
+        return nullptr;
+    }
+    // dense dictionaries + slot -> index maps
+    std::vector<int32_t> d_off(256, 0);
+    std::vector<double> d_val(256, 0.0);
+    std::vector<uint8_t> idx(2 * kSlots, 0);
+    uint32_t no = 0, nv = 0;
+    for (uint32_t i = 0; i < kSlots; ++i) {
+        if (h_tabs[i] != kEmpty) {
+            d_off[no] = static_cast<int32_t>(static_cast<int64_t>(h_tabs[i]) - (1ll << 32));
+            idx[i] = static_cast<uint8_t>(no++);
+        }
+        if (h_tabs[kSlots + i] != kEmpty) {
+            const unsigned long long bits = h_tabs[kSlots + i];
+            std::memcpy(&d_val[nv], &bits, 8);
+            idx[kSlots + i] = static_cast<uint8_t>(nv++);
+        }
+    }
+    // slice widths -> offsets
+    auto D = std::make_unique<DictSell>();
+    D->nslices = (A.n_rows + 31) / 32;
+    D->n_off = no;
+    D->n_val = nv;
+    CBGX_CUDA(cudaMalloc(&D->soff, (D->nslices + 1) * sizeof(uint64_t)));
+    const int g1 = static_cast<int>(std::min<uint64_t>((D->nslices + 1 + 7) / 8 + 1, sm_count() * 16ull));
+    CBGX_K(dict_slice_kernel<RP><<<g1, 256, 0, st>>>(rp, A.n_rows, D->nslices, D->soff, flags + 3));
+    size_t tmp_bytes = 0;
+    CBGX_CUDA(cub::DeviceScan::ExclusiveSum(nullptr, tmp_bytes, D->soff, D->soff, D->nslices + 1, st));
+    void* tmp = nullptr;
+    CBGX_CUDA(cudaMallocAsync(&tmp, tmp_bytes, st));
+    CBGX_CUDA(cub::DeviceScan::ExclusiveSum(tmp, tmp_bytes, D->soff, D->soff, D->nslices + 1, st));
+    CBGX_CUDA(cudaFreeAsync(tmp, st));
+    uint64_t total = 0;
+    unsigned max_w = 0;
+    CBGX_CUDA(cudaMemcpyAsync(&total, D->soff + D->nslices, sizeof(uint64_t), cudaMemcpyDeviceToHost, st));
+    CBGX_CUDA(cudaMemcpyAsync(&max_w, flags + 3, sizeof(unsigned), cudaMemcpyDeviceToHost, st));
+    CBGX_CUDA(cudaStreamSynchronize(st));
+    // uniform slice width (ELL) when it pads by <= 1/8: no offset table read
+    // per slice in the SpMV
+    // Uniform width padded to groups of 4 (ELL4) when that pads by <= 1/4
+    // (7-point rows: 8, 27-point: 28): no offset table read per slice and
+    // one 8-byte code load per 4 entries in the SpMV.
+    const uint32_t w4 = (max_w + 3) / 4;
+    const uint64_t ell_total = D->nslices * 32 * 4 * static_cast<uint64_t>(w4);
+    if (max_w > 0 && ell_total <= total + total / 4 && A.n_rows < (1ull << 31) - (1ull << 30)) {
+        D->ell_w = 4 * w4;
+        total = ell_total;
+    }
+    D->entries = total;
+    size_t free_b = 0, total_b = 0;
+    CBGX_CUDA(cudaMemGetInfo(&free_b, &total_b));
+    if (static_cast<double>(total) * 2.0 > max_fraction_of_free * static_cast<double>(free_b)) {
+        release();
+        return nullptr;
+    }
+    CBGX_CUDA(cudaMalloc(&D->codes, std::max<uint64_t>(total, 1) * sizeof(uint16_t)));
+    CBGX_CUDA(cudaMalloc(&D->off, 256 * sizeof(int32_t)));
+    CBGX_CUDA(cudaMalloc(&D->val, 256 * sizeof(double)));
+    uint8_t* d_idx = nullptr;
+    CBGX_CUDA(cudaMallocAsync(reinterpret_cast<void**>(&d_idx), idx.size(), st));
+    CBGX_CUDA(cudaMemcpyAsync(d_idx, idx.data(), idx.size(), cudaMemcpyHostToDevice, st));
+    CBGX_CUDA(cudaMemcpyAsync(D->off, d_off.data(), 256 * sizeof(int32_t), cudaMemcpyHostToDevice, st));
+    CBGX_CUDA(cudaMemcpyAsync(D->val, d_val.data(), 256 * sizeof(double), cudaMemcpyHostToDevice, st));
+    CBGX_K(dict_fill_kernel<RP><<<dict_grid(D->nslices * 32), kDThreads, 0, st>>>(
+        rp, A.d_col_idx, A.d_values, A.n_rows, D->soff, tabs, tabs + kSlots, d_idx, d_idx + kSlots, D->ell_w / 4,
+        D->codes));
+    CBGX_CUDA(cudaGetLastError());
+    CBGX_CUDA(cudaFreeAsync(d_idx, st));
+    release();
+    CBGX_CUDA(cudaStreamSynchronize(st));
+    return D;
+}
+
+}  // namespace
+
+DictSell::~DictSell() {
+    if (codes) cudaFree(codes);
+    if (soff) cudaFree(soff);
+    if (off) cudaFree(off);
+    if (val) cudaFree(val);
+}
+
+std::unique_ptr<DictSell> build_dict_sell(const cbgx_csr& A, double max_fraction_of_free, cudaStream_t st) {
+    if (A.n_rows == 0 || A.nnz == 0) return nullptr;
+    return A.row_ptr_bits == 32 ? dict_build<int32_t>(A, max_fraction_of_free, st)
+                                : dict_build<int64_t>(A, max_fraction_of_free, st);
+}
+
+template <int MODE, bool kEll>
+static void dict_launch(const cbgx_csr& A, const DictSell& D, const double* x, const double* b, double* y, int fused,
+                        double* norm, Workspace* ws, cudaStream_t st, bool pdl) {
+    static int per_sm = -1;  // per instantiation; one device geometry
+    if (per_sm < 0) {
+        CBGX_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, dsell_spmv_kernel<MODE, kEll>, kDThreads, 0));
+        per_sm = std::max(per_sm, 1);
+    }
+    const uint64_t want = (D.nslices + kDWarps - 1) / kDWarps;
+    const int grid = static_cast<int>(std::max<uint64_t>(1, std::min<uint64_t>(want, static_cast<uint64_t>(sm_count()) * per_sm)));
+    double* partials = fused ? ws->get_partials(grid) : nullptr;
+    unsigned* ticket = fused ? ws->get_counter() : nullptr;
+    cudaLaunchConfig_t lc = {};
+    lc.gridDim = dim3(grid);
+    lc.blockDim = dim3(kDThreads);
+    lc.stream = st;
+    cudaLaunchAttribute at[1];
+    at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    at[0].val.programmaticStreamSerializationAllowed = 1;
+    lc.attrs = at;
+    lc.numAttrs = pdl ? 1 : 0;
+    note_launch();
+    CBGX_CUDA(cudaLaunchKernelEx(&lc, dsell_spmv_kernel<MODE, kEll>, A.n_rows, static_cast<const uint64_t*>(D.soff),
+                                 D.ell_w, static_cast<const uint16_t*>(D.codes), static_cast<const int32_t*>(D.off),
+                                 static_cast<const double*>(D.val), x, b, y, fused, partials, ticket, norm));
+}
+
+void launch_spmv_dict(const cbgx_csr& A, const DictSell& D, const double* x, const double* b, double* y, double* norm,
+                      int reduction, Workspace* ws, cudaStream_t st, bool pdl) {
+    const int fused = norm && reduction == CBGX_REDUCE_TREE;
+    if (D.ell_w) {
+        if (b) dict_launch<1, true>(A, D, x, b, y, fused, norm, ws, st, pdl);
+        else dict_launch<0, true>(A, D, x, b, y, fused, norm, ws, st, pdl);
+    } else {
+        if (b) dict_launch<1, false>(A, D, x, b, y, fused, norm, ws, st, pdl);
+        else dict_launch<0, false>(A, D, x, b, y, fused, norm, ws, st, pdl);
+    }
+    if (norm && !fused) launch_dot(y, y, A.n_rows, CBGX_REDUCE_REFERENCE, norm, ws, st);
+}
+
+}  // namespace cbgx
+
+using namespace cbgx;
+
+struct cbgx_dict_csr {
+    std::unique_ptr<DictSell> d;
+};
+
+extern "C" {
+
+int cbgx_csr_dict_create(const cbgx_csr* A, cbgx_dict_csr** out, void* stream) {
+    return guard([&] {
+        if (!A || !out) throw Error(CBGX_EINVAL, "dict: null argument");
+        if (A->row_ptr_bits != 32 && A->row_ptr_bits != 64) throw Error(CBGX_EINVAL, "csr: row_ptr_bits must be 32 or 64");
+        *out = nullptr;
+        auto D = build_dict_sell(*A, 0.8, as_stream(stream));
+        if (!D) throw Error(CBGX_EINVAL, "dict: matrix has more than 255 distinct values or column offsets");
+        *out = new cbgx_dict_csr{std::move(D)};
+    });
+}
+
+int cbgx_csr_dict_info(const cbgx_dict_csr* D, uint32_t* n_offsets, uint32_t* n_values, uint64_t* entries) {
+    return guard([&] {
+        if (!D) throw Error(CBGX_EINVAL, "dict: null handle");
+        if (n_offsets) *n_offsets = D->d->n_off;
+        if (n_values) *n_values = D->d->n_val;
+        if (entries) *entries = D->d->entries;
+    });
+}
+
+int cbgx_csr_dict_spmv(const cbgx_csr* A, const cbgx_dict_csr* D, const double* d_x, const double* d_b, double* d_y,
+                       double* d_ynorm2, int reduction, cbgx_workspace* ws, void* stream) {
+    return guard([&] {
+        if (!A || !D) throw Error(CBGX_EINVAL, "dict: null argument");
+        if (d_ynorm2 && !ws) throw Error(CBGX_EINVAL, "spmv: fused norm needs a workspace");
+        launch_spmv_dict(*A, *D->d, d_x, d_b, d_y, d_ynorm2, reduction, ws_of(ws), as_stream(stream), false);
+    });
+}
+
+void cbgx_csr_dict_destroy(cbgx_dict_csr* D) { delete D; }
+
+}  // extern "C"

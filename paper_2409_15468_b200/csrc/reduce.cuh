@@ -78,6 +78,25 @@ std::unique_ptr<Sell> build_sell(const cbgx_csr& A, double max_fraction_of_free,
 void launch_spmv_sell(const cbgx_csr& A, const Sell& S, const double* x, const double* b, double* y, double* norm,
                       int reduction, Workspace* ws, cudaStream_t st);
 
+// Dictionary-coded SELL-32 copy (see dsell.cu): 2-byte codes into <= 255
+// distinct values and <= 255 distinct column offsets.
+struct DictSell {
+    uint16_t* codes = nullptr;
+    uint64_t* soff = nullptr;
+    int32_t* off = nullptr;  // [256]
+    double* val = nullptr;   // [256]
+    uint64_t nslices = 0;
+    uint64_t entries = 0;
+    uint32_t n_off = 0, n_val = 0;
+    uint32_t ell_w = 0;  // > 0: every slice has this width (soff[s] = 32 s ell_w)
+    ~DictSell();
+};
+// nullptr when the matrix does not fit the dictionaries or the copy would
+// take more than max_fraction_of_free of free memory.
+std::unique_ptr<DictSell> build_dict_sell(const cbgx_csr& A, double max_fraction_of_free, cudaStream_t st);
+void launch_spmv_dict(const cbgx_csr& A, const DictSell& D, const double* x, const double* b, double* y, double* norm,
+                      int reduction, Workspace* ws, cudaStream_t st, bool pdl = false);
+
 // Staged (TMA) CSR SpMV: plan_spmv_tiles returns the tile height (32..256
 // rows, 0 when some tile would exceed the stage capacity).
 uint32_t plan_spmv_tiles(const cbgx_csr& A, cudaStream_t st);

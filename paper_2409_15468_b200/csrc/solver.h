@@ -91,6 +91,7 @@ private:
     cudaEvent_t step_ev_[2] = {nullptr, nullptr};
     int fused_state_ = 0;
     std::unique_ptr<Sell> sell_;
+    std::unique_ptr<DictSell> dict_;  // dictionary-coded SELL-32 (preferred when it applies)
     uint32_t tile_rows_ = 0;      // staged SpMV tile height (0: not used)
     Workspace ws_;
 };

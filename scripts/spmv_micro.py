@@ -1,4 +1,5 @@
-"""SpMV micro-bench: plain CSR kernel vs staged (bulk-copy) kernel, CUDA events."""
+"""SpMV micro-bench: plain CSR kernel vs staged (bulk-copy) kernel vs the dictionary-coded
+SELL-32 copy, CUDA events. *_frac: own bytes / time / HBM peak; dict_speedup: staged time / dict time."""
 import json
 import sys
 
@@ -21,6 +22,12 @@ for kind, nx in ((0, 128), (2, 128), (1, 192), (0, 256)):
     if t:
         assert torch.equal(cbg.spmv_staged(A, x, t), ref)
         variants["staged"] = lambda: cbg.spmv_staged(A, x, t, want_norm=True)
+    D = cbg.DictCsr(A)
+    no, nv, ne = D.info()
+    assert torch.equal(D.spmv(x), ref)
+    variants["dict"] = lambda: D.spmv(x, want_norm=True)
+    own = {"dict": ne * 2 + ((n + 31) // 32 + 1) * 8 + 16 * n}
+    res["dict_entries"] = ne
     for name, fn in variants.items():
         for _ in range(3):
             fn()
@@ -34,6 +41,9 @@ for kind, nx in ((0, 128), (2, 128), (1, 192), (0, 256)):
             ts.append(e0.elapsed_time(e1))
         ms = sorted(ts)[len(ts) // 2]
         res[name + "_us"] = round(ms * 1e3, 1)
-        res[name + "_gbs"] = round(byt / ms / 1e6, 1)
-        res[name + "_frac"] = round(byt / ms / 1e6 / peak, 3)
+        bb = own.get(name, byt)
+        res[name + "_gbs"] = round(bb / ms / 1e6, 1)
+        res[name + "_frac"] = round(bb / ms / 1e6 / peak, 3)
+    if "staged_us" in res:
+        res["dict_speedup"] = round(res["staged_us"] / res["dict_us"], 2)
     print(json.dumps(res), flush=True)

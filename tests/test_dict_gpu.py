@@ -1,0 +1,140 @@
+"""Dictionary-coded SELL-32 SpMV (csrc/dsell.cu): y = A x and r = b - A x
+bit-identical to the reference spmv (sparse.cpp:43-56, restated in the
+oracle) on stencils, convection-diffusion, ragged rows, empty rows and
+row counts off the 32-row slices; matrices outside the dictionary limits
+are refused; solves through it equal the CSR-path solves."""
+import numpy as np
+import pytest
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.fixture(scope="module")
+def cbg():
+    import torch
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    import paper_2409_15468_b200 as m
+    return m
+
+
+def few_valued(rng, n, max_len, offsets, values, empty_frac=0.1):
+    """Ragged rows whose entries draw (col - row) from `offsets` (in-row
+    order kept sorted) and values from `values`."""
+    rows_c, lens = [], []
+    for r in range(n):
+        L = 0 if rng.random() < empty_frac else int(rng.integers(0, max_len + 1))
+        cand = sorted({int(r + o) for o in rng.choice(offsets, size=L)} & set(range(n)))
+        rows_c.append(cand)
+        lens.append(len(cand))
+    rp = np.zeros(n + 1, dtype=np.uint64)
+    rp[1:] = np.cumsum(lens)
+    ci = np.array([c for cs in rows_c for c in cs], dtype=np.uint64)
+    va = rng.choice(values, size=ci.size).astype(np.float64)
+    return rp, ci, va
+
+
+def check_paths(cbg, port, rp, ci, va, seed):
+    n = rp.size - 1
+    A = cbg.DeviceCsr.from_host(cbg.CsrMatrix(n, n, rp, ci, va))
+    D = cbg.DictCsr(A)
+    rng = np.random.default_rng(seed)
+    x = rng.standard_normal(n)
+    ref = port.spmv(rp, ci, va, x)
+    y, nrm = D.spmv(x, want_norm=True)
+    assert y.cpu().numpy().tobytes() == ref.tobytes()
+    assert abs(nrm.item() - float(ref @ ref)) <= 1e-12 * max(1.0, float(ref @ ref))
+    _, nrm_ref = D.spmv(x, want_norm=True, reduction=1)
+    assert nrm_ref.item() == port.dot(ref, ref)
+    b = rng.standard_normal(n)
+    r = D.spmv(x, b=b)
+    assert r.cpu().numpy().tobytes() == (b - ref).tobytes()
+    return D
+
+
+@pytest.mark.parametrize("kind,dims,pe", [(0, (9, 7, 5), 0.0), (1, (6, 6, 6), 1.0), (2, (5, 4, 6), 0.0),
+                                          (0, (33, 17, 9), 0.0), (2, (21, 19, 11), 0.0)])
+def test_stencils_bit_exact(cbg, port, kind, dims, pe):
+    rp, ci, va = port.stencil(kind, *dims, pe=pe)
+    D = check_paths(cbg, port, rp, ci, va, kind)
+    no, nv, ne = D.info()
+    assert no == {0: 7, 1: 7, 2: 27}[kind] and nv <= 7
+    assert ne >= ci.size and ne % 32 == 0
+
+
+@pytest.mark.parametrize("nx,ny,pe,dec", [(10, 10, 1.0, 0.0), (37, 29, 3.0, 0.0), (8, 8, 1.0, 12.0)])
+def test_convdiff_bit_exact(cbg, port, nx, ny, pe, dec):
+    rp, ci, va = port.convdiff(nx, ny, pe, decades=dec)
+    if dec:  # geometric row scaling: one value set per row, beyond the dictionary
+        n = rp.size - 1
+        A = cbg.DeviceCsr.from_host(cbg.CsrMatrix(n, n, rp, ci, va))
+        if len(np.unique(va)) > 255:
+            with pytest.raises(Exception):
+                cbg.DictCsr(A)
+            return
+    check_paths(cbg, port, rp, ci, va, nx)
+
+
+@pytest.mark.parametrize("n,max_len,nvals", [(1, 3, 2), (31, 5, 3), (33, 9, 200), (1000, 27, 255), (4099, 40, 17)])
+def test_ragged_rows_bit_exact(cbg, port, n, max_len, nvals):
+    rng = np.random.default_rng(n)
+    offsets = np.unique(rng.integers(-3 * n, 3 * n + 1, size=60))
+    values = rng.standard_normal(nvals)
+    rp, ci, va = few_valued(rng, n, max_len, offsets, values)
+    if ci.size == 0:
+        pytest.skip("empty matrix")
+    check_paths(cbg, port, rp, ci, va, n)
+
+
+def test_refuses_outside_dictionary_limits(cbg):
+    rng = np.random.default_rng(5)
+    n = 2000
+    # 256 distinct values
+    rp = np.arange(n + 1, dtype=np.uint64)
+    ci = np.arange(n, dtype=np.uint64)
+    va = np.arange(n, dtype=np.float64) % 256 + 1.0
+    A = cbg.DeviceCsr.from_host(cbg.CsrMatrix(n, n, rp, ci, va))
+    with pytest.raises(Exception, match="255 distinct"):
+        cbg.DictCsr(A)
+    # 255 distinct values: accepted
+    va2 = np.arange(n, dtype=np.float64) % 255 + 1.0
+    D = cbg.DictCsr(cbg.DeviceCsr.from_host(cbg.CsrMatrix(n, n, rp, ci, va2)))
+    assert D.info()[:2] == (1, 255)
+    # 300 distinct column offsets
+    ci3 = ((np.arange(n) + np.arange(n) % 300) % n).astype(np.uint64)
+    A3 = cbg.DeviceCsr.from_host(cbg.CsrMatrix(n, n, rp, ci3, np.ones(n)))
+    with pytest.raises(Exception, match="255 distinct"):
+        cbg.DictCsr(A3)
+    # random sparse matrix (many offsets): refused, solver keeps CSR
+    rng = np.random.default_rng(1)
+    lens = rng.integers(1, 8, size=n)
+    rp4 = np.zeros(n + 1, dtype=np.uint64)
+    rp4[1:] = np.cumsum(lens)
+    ci4 = np.concatenate([np.sort(rng.choice(n, size=int(L), replace=False)) for L in lens]).astype(np.uint64)
+    A4 = cbg.DeviceCsr.from_host(cbg.CsrMatrix(n, n, rp4, ci4, np.ones(ci4.size)))
+    with pytest.raises(Exception):
+        cbg.DictCsr(A4)
+
+
+@pytest.mark.parametrize("fmt", ["frsz2-32", "frsz2-16", "f64"])
+def test_solves_through_dictionary_match_csr(cbg, port, fmt):
+    """Reference order: the dictionary path reproduces the oracle's history
+    byte for byte; tree order: the same solve as the CSR paths (the SpMV is
+    bit-identical; only the fused norm's reduction tree differs)."""
+    rp, ci, va = port.stencil(1, 14, 13, 12, pe=1.0)
+    b, _ = port.generate_problem(rp, ci, va)
+    n = rp.size - 1
+
+    def run(red, dict_spmv):
+        cfg = cbg.GmresConfig(restart=30, storage_format=cbg.StorageFormat.parse(fmt), reduction=red,
+                              dict_spmv=dict_spmv)
+        return cbg.gmres_solve(cbg.CsrMatrix(n, n, rp, ci, va), b, np.zeros(n), cfg)
+
+    o = port.gmres(rp, ci, va, b, fmt=fmt, restart=30)
+    r = run(1, True)
+    assert [(h.iteration, h.rrn, h.is_explicit) for h in r.residual_history] == o["history"]
+    assert np.asarray(r.solution).tobytes() == o["x"].tobytes()
+    t1, t0 = run(0, True), run(0, False)
+    assert abs(t1.total_iterations - t0.total_iterations) <= 2
+    assert t1.converged and t1.final_rrn <= 1e-10
+    assert np.allclose(np.asarray(t1.solution), np.asarray(t0.solution), rtol=1e-7, atol=1e-12)

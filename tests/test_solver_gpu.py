@@ -166,8 +166,8 @@ def test_sell_and_csr_spmv_paths_agree(cbg, port):
     exactly (same reduction trees elsewhere)."""
     rp, ci, va = port.stencil(2, 13, 11, 9)
     b, _ = port.generate_problem(rp, ci, va)
-    r1 = solve(cbg, rp, ci, va, b, "frsz2-32", 30, reduction=0, sell=True)
-    r2 = solve(cbg, rp, ci, va, b, "frsz2-32", 30, reduction=0, sell=False)
+    r1 = solve(cbg, rp, ci, va, b, "frsz2-32", 30, reduction=0, sell=True, dict_spmv=False)
+    r2 = solve(cbg, rp, ci, va, b, "frsz2-32", 30, reduction=0, sell=False, dict_spmv=False)
     assert hist(r1) == hist(r2)
     assert np.asarray(r1.solution).tobytes() == np.asarray(r2.solution).tobytes()
 
@@ -258,8 +258,8 @@ def test_staged_spmv_plan_limits(cbg):
 def test_staged_and_csr_solves_agree(cbg, port):
     rp, ci, va = port.stencil(0, 14, 13, 11)
     b, _ = port.generate_problem(rp, ci, va)
-    r1 = solve(cbg, rp, ci, va, b, "frsz2-32", 30, reduction=0, tma_spmv=True)
-    r2 = solve(cbg, rp, ci, va, b, "frsz2-32", 30, reduction=0, tma_spmv=False)
+    r1 = solve(cbg, rp, ci, va, b, "frsz2-32", 30, reduction=0, tma_spmv=True, dict_spmv=False)
+    r2 = solve(cbg, rp, ci, va, b, "frsz2-32", 30, reduction=0, tma_spmv=False, dict_spmv=False)
     assert hist(r1) == hist(r2)
     assert np.asarray(r1.solution).tobytes() == np.asarray(r2.solution).tobytes()
 
@@ -306,7 +306,7 @@ def test_folded_spmv_solve_matches(cbg, port):
     path's exactly (same reduction trees elsewhere)."""
     rp, ci, va = port.stencil(0, 40, 40, 40)
     b, _ = port.generate_problem(rp, ci, va)
-    r1 = solve(cbg, rp, ci, va, b, "frsz2-32", 30, reduction=0, fold=True)
-    r2 = solve(cbg, rp, ci, va, b, "frsz2-32", 30, reduction=0, fold=False)
+    r1 = solve(cbg, rp, ci, va, b, "frsz2-32", 30, reduction=0, fold=True, dict_spmv=False)
+    r2 = solve(cbg, rp, ci, va, b, "frsz2-32", 30, reduction=0, fold=False, dict_spmv=False)
     assert r1.total_iterations == r2.total_iterations
     assert np.allclose(np.asarray(r1.solution), np.asarray(r2.solution), rtol=1e-9, atol=1e-13)
