@@ -149,7 +149,7 @@ dict_fill_kernel(const RP* __restrict__ rp, const int32_t* __restrict__ ci, cons
     for (uint64_t r = blockIdx.x * static_cast<uint64_t>(kDThreads) + threadIdx.x; r < padded;
          r += static_cast<uint64_t>(gridDim.x) * kDThreads) {
         const uint64_t sl = r / 32, lane = r % 32;
-        const uint64_t base = soff[sl], width = ell4 ? 4ull * ell4 : (soff[sl + 1] - base) / 32;
+        const uint64_t base = ell4 ? 0 : soff[sl], width = ell4 ? 4ull * ell4 : (soff[sl + 1] - base) / 32;
         const uint64_t k0 = r < n_rows ? static_cast<uint64_t>(rp[r]) : 0;
         const uint64_t len = r < n_rows ? static_cast<uint64_t>(rp[r + 1]) - k0 : 0;
         for (uint64_t k = 0; k < width; ++k) {
@@ -316,32 +316,42 @@ int dict_grid(uint64_t rows) {
     return static_cast<int>(std::max<uint64_t>(1, std::min(want, cap)));
 }
 
+template <typename T>
+void ensure(T*& p, uint64_t& cap, uint64_t need) {
+    if (p && cap >= need) return;
+    if (p) CBGX_CUDA(cudaFree(p));
+    p = nullptr;
+    CBGX_CUDA(cudaMalloc(reinterpret_cast<void**>(&p), std::max<uint64_t>(need, 1) * sizeof(T)));
+    cap = need;
+}
+
+// Builds (or rebuilds, reusing D's buffers) the dictionary copy of A. One
+// host round trip (the dictionaries); a second only for ragged matrices that
+// need the per-slice offset table. Stream-ordered otherwise.
 template <typename RP>
-std::unique_ptr<DictSell> dict_build(const cbgx_csr& A, double max_fraction_of_free, cudaStream_t st) {
+bool dict_build(const cbgx_csr& A, double reserve_bytes, cudaStream_t st, DictSell& D) {
+    D.ready = false;
     const RP* rp = static_cast<const RP*>(A.d_row_ptr);
+    uint64_t cap = 0;
+    if (!D.tabs) {
+        ensure(D.tabs, cap, 2ull * kSlots);
+        ensure(D.flags, cap, 4);
+        ensure(D.idx, cap, 2ull * kSlots);
+        ensure(D.off, cap, 256);
+        ensure(D.val, cap, 256);
+    }
     // pass 1: dictionaries
-    unsigned long long* tabs = nullptr;  // [2][kSlots]
-    unsigned* flags = nullptr;           // [cnt_off, cnt_val, bad]
-    CBGX_CUDA(cudaMallocAsync(reinterpret_cast<void**>(&tabs), 2 * kSlots * sizeof(unsigned long long), st));
-    CBGX_CUDA(cudaMallocAsync(reinterpret_cast<void**>(&flags), 4 * sizeof(unsigned), st));
-    CBGX_CUDA(cudaMemsetAsync(tabs, 0xFF, 2 * kSlots * sizeof(unsigned long long), st));
-    CBGX_CUDA(cudaMemsetAsync(flags, 0, 4 * sizeof(unsigned), st));
-    CBGX_K(dict_scan_kernel<RP><<<dict_grid(A.n_rows), kDThreads, 0, st>>>(rp, A.d_col_idx, A.d_values, A.n_rows, tabs,
-                                                                            tabs + kSlots, flags, flags + 2));
+    CBGX_CUDA(cudaMemsetAsync(D.tabs, 0xFF, 2 * kSlots * sizeof(unsigned long long), st));
+    CBGX_CUDA(cudaMemsetAsync(D.flags, 0, 4 * sizeof(unsigned), st));
+    CBGX_K(dict_scan_kernel<RP><<<dict_grid(A.n_rows), kDThreads, 0, st>>>(rp, A.d_col_idx, A.d_values, A.n_rows, D.tabs,
+                                                                            D.tabs + kSlots, D.flags, D.flags + 2));
     CBGX_CUDA(cudaGetLastError());
     std::vector<unsigned long long> h_tabs(2 * kSlots);
     unsigned h_flags[4];
-    CBGX_CUDA(cudaMemcpyAsync(h_tabs.data(), tabs, h_tabs.size() * sizeof(unsigned long long), cudaMemcpyDeviceToHost, st));
-    CBGX_CUDA(cudaMemcpyAsync(h_flags, flags, sizeof h_flags, cudaMemcpyDeviceToHost, st));
+    CBGX_CUDA(cudaMemcpyAsync(h_tabs.data(), D.tabs, h_tabs.size() * sizeof(unsigned long long), cudaMemcpyDeviceToHost, st));
+    CBGX_CUDA(cudaMemcpyAsync(h_flags, D.flags, sizeof h_flags, cudaMemcpyDeviceToHost, st));
     CBGX_CUDA(cudaStreamSynchronize(st));
-    auto release = [&] {
-        cudaFreeAsync(tabs, st);
-        cudaFreeAsync(flags, st);
-    };
-    if (h_flags[2] || h_flags[0] > kDictMax || h_flags[1] > kDictMax) {
-        release();
-        return nullptr;
-    }
+    if (h_flags[2] || h_flags[0] > kDictMax || h_flags[1] > kDictMax) return false;
     // dense dictionaries + slot -> index maps
     std::vector<int32_t> d_off(256, 0);
     std::vector<double> d_val(256, 0.0);
@@ -358,74 +368,77 @@ std::unique_ptr<DictSell> dict_build(const cbgx_csr& A, double max_fraction_of_f
             idx[kSlots + i] = static_cast<uint8_t>(nv++);
         }
     }
-    // slice widths -> offsets
-    auto D = std::make_unique<DictSell>();
-    D->nslices = (A.n_rows + 31) / 32;
-    D->n_off = no;
-    D->n_val = nv;
-    CBGX_CUDA(cudaMalloc(&D->soff, (D->nslices + 1) * sizeof(uint64_t)));
-    const int g1 = static_cast<int>(std::min<uint64_t>((D->nslices + 1 + 7) / 8 + 1, sm_count() * 16ull));
-    CBGX_K(dict_slice_kernel<RP><<<g1, 256, 0, st>>>(rp, A.n_rows, D->nslices, D->soff, flags + 3));
-    size_t tmp_bytes = 0;
-    CBGX_CUDA(cub::DeviceScan::ExclusiveSum(nullptr, tmp_bytes, D->soff, D->soff, D->nslices + 1, st));
-    void* tmp = nullptr;
-    CBGX_CUDA(cudaMallocAsync(&tmp, tmp_bytes, st));
-    CBGX_CUDA(cub::DeviceScan::ExclusiveSum(tmp, tmp_bytes, D->soff, D->soff, D->nslices + 1, st));
-    CBGX_CUDA(cudaFreeAsync(tmp, st));
-    uint64_t total = 0;
-    unsigned max_w = 0;
-    CBGX_CUDA(cudaMemcpyAsync(&total, D->soff + D->nslices, sizeof(uint64_t), cudaMemcpyDeviceToHost, st));
-    CBGX_CUDA(cudaMemcpyAsync(&max_w, flags + 3, sizeof(unsigned), cudaMemcpyDeviceToHost, st));
-    CBGX_CUDA(cudaStreamSynchronize(st));
-    // uniform slice width (ELL) when it pads by <= 1/8: no offset table read
-    // per slice in the SpMV
+    D.nslices = (A.n_rows + 31) / 32;
+    D.n_off = no;
+    D.n_val = nv;
+    D.ell_w = 0;
     // Uniform width padded to groups of 4 (ELL4) when that pads by <= 1/4
-    // (7-point rows: 8, 27-point: 28): no offset table read per slice and
-    // one 8-byte code load per 4 entries in the SpMV.
-    const uint32_t w4 = (max_w + 3) / 4;
-    const uint64_t ell_total = D->nslices * 32 * 4 * static_cast<uint64_t>(w4);
-    if (max_w > 0 && ell_total <= total + total / 4 && A.n_rows < (1ull << 31) - (1ull << 30)) {
-        D->ell_w = 4 * w4;
-        total = ell_total;
+    // (7-point rows: 8, 27-point: 28): no offset table and one 8-byte code
+    // load per 4 entries in the SpMV. Decided from the known longest row and
+    // nnz when available (no pass over the row offsets).
+    uint64_t total = 0;
+    uint32_t max_w = A.max_row_nnz;
+    const bool small = A.n_rows < (1ull << 31) - (1ull << 30);  // 32-bit row indices in the ELL4 kernel
+    auto ell_fits = [&](uint32_t w, uint64_t entries) {
+        const uint64_t t = D.nslices * 128 * static_cast<uint64_t>((w + 3) / 4);
+        return w > 0 && small && t <= entries + entries / 4;
+    };
+    if (max_w > 0 && ell_fits(max_w, A.nnz)) {
+        D.ell_w = 4 * ((max_w + 3) / 4);
+        total = D.nslices * 32 * static_cast<uint64_t>(D.ell_w);
+    } else {
+        ensure(D.soff, D.soff_cap, D.nslices + 1);
+        const int g1 = static_cast<int>(std::min<uint64_t>((D.nslices + 1 + 7) / 8 + 1, sm_count() * 16ull));
+        CBGX_K(dict_slice_kernel<RP><<<g1, 256, 0, st>>>(rp, A.n_rows, D.nslices, D.soff, D.flags + 3));
+        size_t tmp_bytes = 0;
+        CBGX_CUDA(cub::DeviceScan::ExclusiveSum(nullptr, tmp_bytes, D.soff, D.soff, D.nslices + 1, st));
+        void* tmp = nullptr;
+        CBGX_CUDA(cudaMallocAsync(&tmp, tmp_bytes, st));
+        CBGX_CUDA(cub::DeviceScan::ExclusiveSum(tmp, tmp_bytes, D.soff, D.soff, D.nslices + 1, st));
+        CBGX_CUDA(cudaFreeAsync(tmp, st));
+        unsigned mw = 0;
+        CBGX_CUDA(cudaMemcpyAsync(&total, D.soff + D.nslices, sizeof(uint64_t), cudaMemcpyDeviceToHost, st));
+        CBGX_CUDA(cudaMemcpyAsync(&mw, D.flags + 3, sizeof(unsigned), cudaMemcpyDeviceToHost, st));
+        CBGX_CUDA(cudaStreamSynchronize(st));
+        if (ell_fits(mw, total)) {
+            D.ell_w = 4 * ((mw + 3) / 4);
+            total = D.nslices * 32 * static_cast<uint64_t>(D.ell_w);
+        }
     }
-    D->entries = total;
-    size_t free_b = 0, total_b = 0;
-    CBGX_CUDA(cudaMemGetInfo(&free_b, &total_b));
-    if (static_cast<double>(total) * 2.0 > max_fraction_of_free * static_cast<double>(free_b)) {
-        release();
-        return nullptr;
+    if (total > D.codes_cap) {
+        if (D.codes) CBGX_CUDA(cudaFree(D.codes));
+        D.codes = nullptr;
+        D.codes_cap = 0;
+        size_t free_b = 0, total_b = 0;
+        CBGX_CUDA(cudaMemGetInfo(&free_b, &total_b));
+        if (static_cast<double>(total) * 2.0 > 0.8 * (static_cast<double>(free_b) - reserve_bytes)) return false;
+        ensure(D.codes, D.codes_cap, total);
     }
-    CBGX_CUDA(cudaMalloc(&D->codes, std::max<uint64_t>(total, 1) * sizeof(uint16_t)));
-    CBGX_CUDA(cudaMalloc(&D->off, 256 * sizeof(int32_t)));
-    CBGX_CUDA(cudaMalloc(&D->val, 256 * sizeof(double)));
-    uint8_t* d_idx = nullptr;
-    CBGX_CUDA(cudaMallocAsync(reinterpret_cast<void**>(&d_idx), idx.size(), st));
-    CBGX_CUDA(cudaMemcpyAsync(d_idx, idx.data(), idx.size(), cudaMemcpyHostToDevice, st));
-    CBGX_CUDA(cudaMemcpyAsync(D->off, d_off.data(), 256 * sizeof(int32_t), cudaMemcpyHostToDevice, st));
-    CBGX_CUDA(cudaMemcpyAsync(D->val, d_val.data(), 256 * sizeof(double), cudaMemcpyHostToDevice, st));
-    CBGX_K(dict_fill_kernel<RP><<<dict_grid(D->nslices * 32), kDThreads, 0, st>>>(
-        rp, A.d_col_idx, A.d_values, A.n_rows, D->soff, tabs, tabs + kSlots, d_idx, d_idx + kSlots, D->ell_w / 4,
-        D->codes));
+    D.entries = total;
+    CBGX_CUDA(cudaMemcpyAsync(D.idx, idx.data(), idx.size(), cudaMemcpyHostToDevice, st));
+    CBGX_CUDA(cudaMemcpyAsync(D.off, d_off.data(), 256 * sizeof(int32_t), cudaMemcpyHostToDevice, st));
+    CBGX_CUDA(cudaMemcpyAsync(D.val, d_val.data(), 256 * sizeof(double), cudaMemcpyHostToDevice, st));
+    CBGX_K(dict_fill_kernel<RP><<<dict_grid(D.nslices * 32), kDThreads, 0, st>>>(
+        rp, A.d_col_idx, A.d_values, A.n_rows, D.soff, D.tabs, D.tabs + kSlots, D.idx, D.idx + kSlots, D.ell_w / 4,
+        D.codes));
     CBGX_CUDA(cudaGetLastError());
-    CBGX_CUDA(cudaFreeAsync(d_idx, st));
-    release();
-    CBGX_CUDA(cudaStreamSynchronize(st));
-    return D;
+    D.ready = true;
+    return true;
 }
 
 }  // namespace
 
 DictSell::~DictSell() {
-    if (codes) cudaFree(codes);
-    if (soff) cudaFree(soff);
-    if (off) cudaFree(off);
-    if (val) cudaFree(val);
+    for (void* p : {static_cast<void*>(codes), static_cast<void*>(soff), static_cast<void*>(off), static_cast<void*>(val),
+                    static_cast<void*>(tabs), static_cast<void*>(flags), static_cast<void*>(idx)})
+        if (p) cudaFree(p);
 }
 
-std::unique_ptr<DictSell> build_dict_sell(const cbgx_csr& A, double max_fraction_of_free, cudaStream_t st) {
-    if (A.n_rows == 0 || A.nnz == 0) return nullptr;
-    return A.row_ptr_bits == 32 ? dict_build<int32_t>(A, max_fraction_of_free, st)
-                                : dict_build<int64_t>(A, max_fraction_of_free, st);
+bool build_dict_sell(const cbgx_csr& A, double reserve_bytes, cudaStream_t st, DictSell& D) {
+    D.ready = false;
+    if (A.n_rows == 0 || A.nnz == 0) return false;
+    return A.row_ptr_bits == 32 ? dict_build<int32_t>(A, reserve_bytes, st, D)
+                                : dict_build<int64_t>(A, reserve_bytes, st, D);
 }
 
 template <int MODE, bool kEll>
@@ -483,8 +496,10 @@ int cbgx_csr_dict_create(const cbgx_csr* A, cbgx_dict_csr** out, void* stream) {
         if (!A || !out) throw Error(CBGX_EINVAL, "dict: null argument");
         if (A->row_ptr_bits != 32 && A->row_ptr_bits != 64) throw Error(CBGX_EINVAL, "csr: row_ptr_bits must be 32 or 64");
         *out = nullptr;
-        auto D = build_dict_sell(*A, 0.8, as_stream(stream));
-        if (!D) throw Error(CBGX_EINVAL, "dict: matrix has more than 255 distinct values or column offsets");
+        auto D = std::make_unique<DictSell>();
+        if (!build_dict_sell(*A, 0.0, as_stream(stream), *D))
+            throw Error(CBGX_EINVAL, "dict: matrix has more than 255 distinct values or column offsets");
+        CBGX_CUDA(cudaStreamSynchronize(as_stream(stream)));
         *out = new cbgx_dict_csr{std::move(D)};
     });
 }

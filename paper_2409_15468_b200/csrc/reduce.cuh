@@ -82,18 +82,26 @@ void launch_spmv_sell(const cbgx_csr& A, const Sell& S, const double* x, const d
 // distinct values and <= 255 distinct column offsets.
 struct DictSell {
     uint16_t* codes = nullptr;
-    uint64_t* soff = nullptr;
-    int32_t* off = nullptr;  // [256]
-    double* val = nullptr;   // [256]
+    uint64_t* soff = nullptr;  // SELL layout only
+    int32_t* off = nullptr;    // [256]
+    double* val = nullptr;     // [256]
     uint64_t nslices = 0;
     uint64_t entries = 0;
     uint32_t n_off = 0, n_val = 0;
-    uint32_t ell_w = 0;  // > 0: every slice has this width (soff[s] = 32 s ell_w)
+    uint32_t ell_w = 0;  // > 0: ELL4 layout, every row padded to this width
+    bool ready = false;
+    // build scratch and capacities (kept across rebuilds)
+    unsigned long long* tabs = nullptr;
+    unsigned* flags = nullptr;
+    uint8_t* idx = nullptr;
+    uint64_t codes_cap = 0, soff_cap = 0;
     ~DictSell();
 };
-// nullptr when the matrix does not fit the dictionaries or the copy would
-// take more than max_fraction_of_free of free memory.
-std::unique_ptr<DictSell> build_dict_sell(const cbgx_csr& A, double max_fraction_of_free, cudaStream_t st);
+// (Re)builds D for A, reusing its buffers; false when A does not fit the
+// dictionaries or a (re)allocated copy would take more than 80% of the free
+// memory less reserve_bytes (kept for later allocations, e.g. the basis).
+// Stream-ordered on return (no trailing synchronisation).
+bool build_dict_sell(const cbgx_csr& A, double reserve_bytes, cudaStream_t st, DictSell& D);
 void launch_spmv_dict(const cbgx_csr& A, const DictSell& D, const double* x, const double* b, double* y, double* norm,
                       int reduction, Workspace* ws, cudaStream_t st, bool pdl = false);
 

@@ -176,7 +176,7 @@ Solver::Solver(const cbgx_csr& A, const cbgx_gmres_config& cfg, Comm* comm, Halo
 // tiles, else the plain CSR kernel.
 void Solver::setup_matrix(bool before_basis, cudaStream_t st, const unsigned long long* stats) {
     sell_.reset();
-    dict_.reset();
+    if (dict_) dict_->ready = false;
     tile_rows_ = 0;
     if (stats) A_.max_row_nnz = static_cast<uint32_t>(stats[0]);
     if (A_.max_row_nnz == 0) A_.max_row_nnz = csr_max_row_nnz(A_, st);
@@ -189,11 +189,8 @@ void Solver::setup_matrix(bool before_basis, cudaStream_t st, const unsigned lon
             cbgx_basis tmp{};
             cbgx_basis_layout(cfg_.format_kind, cfg_.bit_length, n_, cfg_.restart + 1, &tmp, &db, &eb);
         }
-        size_t free_b = 0, total_b = 0;
-        CBGX_CUDA(cudaMemGetInfo(&free_b, &total_b));
-        const double after_basis = static_cast<double>(free_b) - static_cast<double>(db + eb) - 64.0 * n_ * 8;
-        if (after_basis > 0) dict_ = build_dict_sell(A_, 0.8 * after_basis / static_cast<double>(free_b), st);
-        if (dict_) return;
+        if (!dict_) dict_ = std::make_unique<DictSell>();
+        if (build_dict_sell(A_, static_cast<double>(db + eb) + 64.0 * n_ * 8, st, *dict_)) return;
     }
     uint32_t plan = 0;
     if (!(cfg_.flags & CBGX_SOLVER_NO_TMA_SPMV)) plan = stats ? plan_from_stats(stats) : plan_spmv_tiles(A_, st);
@@ -238,7 +235,7 @@ Solver::~Solver() {
 }
 
 void Solver::spmv(const double* x, const double* b, double* y, double* norm, cudaStream_t st, bool pdl) {
-    if (dict_) launch_spmv_dict(A_, *dict_, x, b, y, norm, static_cast<int>(cfg_.reduction), &ws_, st, pdl);
+    if (dict_ && dict_->ready) launch_spmv_dict(A_, *dict_, x, b, y, norm, static_cast<int>(cfg_.reduction), &ws_, st, pdl);
     else if (tile_rows_) launch_spmv_tma(A_, tile_rows_, x, b, y, norm, static_cast<int>(cfg_.reduction), &ws_, st, pdl);
     else if (sell_) launch_spmv_sell(A_, *sell_, x, b, y, norm, static_cast<int>(cfg_.reduction), &ws_, st);
     else launch_spmv(A_, x, b, y, norm, static_cast<int>(cfg_.reduction), &ws_, st);
@@ -268,7 +265,7 @@ void Solver::solve(const double* d_b, const double* d_x0, double* d_x, cbgx_hist
     const int fmt = fmt_from_cfg(cfg_);
     const double bpv = stored_bytes_per_value(fmt);
     const double rp_bytes = A_.row_ptr_bits / 8.0;
-    const double spmv_bytes = dict_ ? dict_->entries * 2.0 + (dict_->nslices + 1) * 8.0 + 16.0 * n
+    const double spmv_bytes = dict_ && dict_->ready ? dict_->entries * 2.0 + (dict_->nslices + 1) * 8.0 + 16.0 * n
                                     : A_.nnz * 12.0 + (n + 1) * rp_bytes + 16.0 * n;
     const bool multi = comm_ && comm_->size() > 1;
     uint64_t hist_len = 0;
