@@ -190,7 +190,8 @@ void Solver::setup_matrix(bool before_basis, cudaStream_t st, const unsigned lon
             cbgx_basis_layout(cfg_.format_kind, cfg_.bit_length, n_, cfg_.restart + 1, &tmp, &db, &eb);
         }
         if (!dict_) dict_ = std::make_unique<DictSell>();
-        if (build_dict_sell(A_, static_cast<double>(db + eb) + 64.0 * n_ * 8, st, *dict_)) return;
+        // reserve: the basis (when not allocated yet) + the solver vectors
+        if (build_dict_sell(A_, static_cast<double>(db + eb) + 8.0 * n_ * 8, st, *dict_)) return;
     }
     uint32_t plan = 0;
     if (!(cfg_.flags & CBGX_SOLVER_NO_TMA_SPMV)) plan = stats ? plan_from_stats(stats) : plan_spmv_tiles(A_, st);
