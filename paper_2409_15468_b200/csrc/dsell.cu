@@ -207,13 +207,26 @@ __device__ __forceinline__ void unpack8(uint2 a, uint2 b, uint16_t (&c)[8]) {
 // MODE 0: y = A x.  MODE 1: y = b - A x. Persistent grid (one wave), one
 // warp per 32-row slice. kEll: ELL4 layout (uniform width, 8-byte groups of
 // 4 codes, no offset table).
+#ifndef DSELL_SPMV_THREADS
+#define DSELL_SPMV_THREADS 256
+#endif
+#ifndef DSELL_CODES_LDG
+#define DSELL_CODES_LDG 0  // 0: streaming (evict-first) code loads
+#endif
+#if DSELL_CODES_LDG
+#define CLD(p) __ldg(p)
+#else
+#define CLD(p) __ldcs(p)
+#endif
+constexpr int kST = DSELL_SPMV_THREADS;
+constexpr int kSW = kST / 32;
 #ifndef DSELL_MIN_BLOCKS
 #define DSELL_MIN_BLOCKS 0  // plain bounds (40 regs): 167 vs 221 us at 7-pt 256^3 (scripts/ab_spmv.sh)
 #endif
 #if DSELL_MIN_BLOCKS
-#define DSELL_BOUNDS __launch_bounds__(kDThreads, DSELL_MIN_BLOCKS)
+#define DSELL_BOUNDS __launch_bounds__(kST, DSELL_MIN_BLOCKS)
 #else
-#define DSELL_BOUNDS __launch_bounds__(kDThreads)
+#define DSELL_BOUNDS __launch_bounds__(kST)
 #endif
 template <int MODE, bool kEll>
 __global__ void DSELL_BOUNDS
@@ -223,15 +236,17 @@ dsell_spmv_kernel(uint64_t n_rows, const uint64_t* __restrict__ soff, uint32_t e
                   double* __restrict__ partials, unsigned* __restrict__ ticket, double* __restrict__ norm_out) {
     __shared__ int32_t s_o[256];
     __shared__ double s_v[256];
-    __shared__ double red[kDWarps];
-    s_o[threadIdx.x] = d_off[threadIdx.x];
-    s_v[threadIdx.x] = d_val[threadIdx.x];
+    __shared__ double red[kSW];
+    for (uint32_t i = threadIdx.x; i < 256; i += kST) {
+        s_o[i] = d_off[i];
+        s_v[i] = d_val[i];
+    }
     __syncthreads();
     pdl_trigger();
     const int lane = threadIdx.x & 31;
     const uint64_t nsl = (n_rows + 31) / 32;
-    const uint64_t nw = static_cast<uint64_t>(gridDim.x) * kDWarps;
-    uint64_t sl = (blockIdx.x * static_cast<uint64_t>(kDThreads) + threadIdx.x) / 32;
+    const uint64_t nw = static_cast<uint64_t>(gridDim.x) * kSW;
+    uint64_t sl = (blockIdx.x * static_cast<uint64_t>(kST) + threadIdx.x) / 32;
     double acc = 0.0;
     if constexpr (kEll) {
         const uint32_t g4 = ell_w / 4;  // 8-byte groups per row
@@ -239,8 +254,8 @@ dsell_spmv_kernel(uint64_t n_rows, const uint64_t* __restrict__ soff, uint32_t e
         uint2 n0 = make_uint2(0xFFFFFFFFu, 0xFFFFFFFFu), n1 = n0;
         // the codes do not depend on the predecessor grid
         if (sl < nsl) {
-            n0 = __ldcs(c4 + sl * g4 * 32 + lane);
-            if (g4 > 1) n1 = __ldcs(c4 + (sl * g4 + 1) * 32 + lane);
+            n0 = CLD(c4 + sl * g4 * 32 + lane);
+            if (g4 > 1) n1 = CLD(c4 + (sl * g4 + 1) * 32 + lane);
         }
         pdl_wait();
         for (; sl < nsl; sl += nw) {
@@ -248,14 +263,14 @@ dsell_spmv_kernel(uint64_t n_rows, const uint64_t* __restrict__ soff, uint32_t e
             uint2 a0 = n0, a1 = n1;
             const uint64_t nx = sl + nw;
             if (nx < nsl) {
-                n0 = __ldcs(c4 + nx * g4 * 32 + lane);
-                if (g4 > 1) n1 = __ldcs(c4 + (nx * g4 + 1) * 32 + lane);
+                n0 = CLD(c4 + nx * g4 * 32 + lane);
+                if (g4 > 1) n1 = CLD(c4 + (nx * g4 + 1) * 32 + lane);
             }
             double s = 0.0;
             for (uint32_t g = 0; g < g4; g += 2) {
                 if (g) {
-                    a0 = __ldcs(c4 + (sl * g4 + g) * 32 + lane);
-                    a1 = g + 1 < g4 ? __ldcs(c4 + (sl * g4 + g + 1) * 32 + lane) : make_uint2(0xFFFFFFFFu, 0xFFFFFFFFu);
+                    a0 = CLD(c4 + (sl * g4 + g) * 32 + lane);
+                    a1 = g + 1 < g4 ? CLD(c4 + (sl * g4 + g + 1) * 32 + lane) : make_uint2(0xFFFFFFFFu, 0xFFFFFFFFu);
                 } else if (g4 == 1) {
                     a1 = make_uint2(0xFFFFFFFFu, 0xFFFFFFFFu);
                 }
@@ -307,7 +322,7 @@ dsell_spmv_kernel(uint64_t n_rows, const uint64_t* __restrict__ soff, uint32_t e
     acc = warp_sum(acc);
     if (lane == 0) red[threadIdx.x >> 5] = acc;
     __syncthreads();
-    block_finalize(red, kDWarps, 1, partials, ticket, norm_out);
+    block_finalize(red, kSW, 1, partials, ticket, norm_out);
 }
 
 int dict_grid(uint64_t rows) {
@@ -446,16 +461,16 @@ static void dict_launch(const cbgx_csr& A, const DictSell& D, const double* x, c
                         double* norm, Workspace* ws, cudaStream_t st, bool pdl) {
     static int per_sm = -1;  // per instantiation; one device geometry
     if (per_sm < 0) {
-        CBGX_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, dsell_spmv_kernel<MODE, kEll>, kDThreads, 0));
+        CBGX_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, dsell_spmv_kernel<MODE, kEll>, kST, 0));
         per_sm = std::max(per_sm, 1);
     }
-    const uint64_t want = (D.nslices + kDWarps - 1) / kDWarps;
+    const uint64_t want = (D.nslices + kSW - 1) / kSW;
     const int grid = static_cast<int>(std::max<uint64_t>(1, std::min<uint64_t>(want, static_cast<uint64_t>(sm_count()) * per_sm)));
     double* partials = fused ? ws->get_partials(grid) : nullptr;
     unsigned* ticket = fused ? ws->get_counter() : nullptr;
     cudaLaunchConfig_t lc = {};
     lc.gridDim = dim3(grid);
-    lc.blockDim = dim3(kDThreads);
+    lc.blockDim = dim3(kST);
     lc.stream = st;
     cudaLaunchAttribute at[1];
     at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
