@@ -18,10 +18,10 @@ timeout 300 python scripts/spmv_micro.py > "$OUT/spmv_micro.txt" 2>&1
 timeout 900 ncu --metrics gpu__time_duration.sum,dram__bytes_read.sum,dram__bytes_write.sum --clock-control none --csv \
     --log-file "$OUT/ncu_launches.csv" python scripts/one_solve.py poisson128 frsz2-32 > /dev/null 2>&1
 python scripts/traffic_from_launches.py "$OUT/ncu_launches.csv" "$OUT/traffic.json" > /dev/null 2>&1
-# full captures: fused orthogonalisation (mid-cycle launch), staged SpMV, codec, CGS micro at n = 2^26
+# full captures: fused orthogonalisation (mid-cycle launch), dictionary SpMV, codec, CGS micro at n = 2^26
 timeout 600 ncu --set full --clock-control none --import-source on -k regex:arnoldi_fused -s 63 -c 1 -o "$OUT/ncu_fused" \
     python scripts/one_solve.py poisson128 frsz2-32 > /dev/null 2>&1
-timeout 600 ncu --set full --clock-control none --import-source on -k regex:spmv_tma -s 66 -c 1 -o "$OUT/ncu_spmv" \
+timeout 600 ncu --set full --clock-control none --import-source on -k regex:dsell_spmv -s 30 -c 1 -o "$OUT/ncu_spmv" \
     python scripts/one_solve.py poisson128 frsz2-32 > /dev/null 2>&1
 timeout 600 ncu --set full --clock-control none --import-source on -k regex:decompress4 -s 3 -c 1 -o "$OUT/ncu_decompress" \
     python scripts/quick_perf.py > /dev/null 2>&1
