@@ -1,7 +1,8 @@
 """Small end-to-end exercise of every kernel family for compute-sanitizer:
 codec (3 fast formats + generic), basis write/read, split CGS, fused
-orthogonalisation (+ folded SpMV variant), staged / plain / SELL SpMV, read
-sweep, host drop-in solve."""
+orthogonalisation (+ folded SpMV variant), staged / plain / SELL /
+dictionary SpMV (ELL4 and ragged SELL layouts, build + apply), read sweep,
+host drop-in solve."""
 import sys
 
 import numpy as np
@@ -33,11 +34,14 @@ for kind, nx in ((0, 20), (2, 14), (1, 18)):
     t = cbg.spmv_plan(A)
     if t:
         cbg.spmv_staged(A, x, t, want_norm=True)
+    D = cbg.DictCsr(A)
+    D.spmv(x, want_norm=True)
+    D.spmv(x, b=x)
     b = cbg.spmv(A, torch.from_numpy(cbg.sin_problem_host(n)).cuda())
     for fmt in ("frsz2-32", "f64"):
-        for fold in (False, True):
+        for fold, dic in ((False, True), (False, False), (True, False)):
             S = cbg.Solver(A, cbg.GmresConfig(restart=20, storage_format=cbg.StorageFormat.parse(fmt), fold=fold,
-                                              max_total_iterations=60))
+                                              dict_spmv=dic, max_total_iterations=60))
             r = S.solve(b)
             print(kind, fmt, fold, r.total_iterations, r.final_rrn, flush=True)
     rp = A.row_ptr.cpu().numpy().astype(np.uint64)
@@ -47,5 +51,22 @@ for kind, nx in ((0, 20), (2, 14), (1, 18)):
                         cbg.GmresConfig(restart=20, storage_format=cbg.StorageFormat.parse("frsz2-32"),
                                         max_total_iterations=60))
     print("host", kind, r.total_iterations, flush=True)
+# ragged few-valued matrix: dictionary SELL layout (per-slice offsets)
+nr = 3001
+lens = rng.integers(0, 12, size=nr)
+lens[rng.random(nr) < 0.1] = 0
+rp = np.zeros(nr + 1, dtype=np.uint64)
+rp[1:] = np.cumsum(lens)
+rows = [sorted({min(nr - 1, max(0, r + int(o))) for o in rng.choice(np.arange(-40, 41), size=int(L))}) for r, L in
+        enumerate(lens)]
+rp[1:] = np.cumsum([len(c) for c in rows])
+ci = np.array([c for cs in rows for c in cs], dtype=np.uint64)
+va = rng.choice([1.0, -2.0, 0.5], size=ci.size)
+Ar = cbg.DeviceCsr.from_host(cbg.CsrMatrix(nr, nr, rp, ci, va))
+try:
+    Dr = cbg.DictCsr(Ar)
+    Dr.spmv(torch.from_numpy(rng.standard_normal(nr)).cuda(), want_norm=True)
+except Exception as e:  # many distinct offsets: refused (still exercises the scan kernel)
+    print("dict refused:", e)
 torch.cuda.synchronize()
 print("sanitize_small done")
