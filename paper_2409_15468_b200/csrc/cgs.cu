@@ -161,12 +161,15 @@ template <int F> struct StageOff {
     }
 };
 
-template <int F>
+// pay / ex: the stage base plus the thread's StageOff; step s at + s * PAY
+// bytes and + s * EXW exponent words (defaults: the split kernels' 1024-row
+// steps).
+template <int F, uint32_t PAY = Geo<F>::pay, uint32_t EXW = 32>
 __device__ __forceinline__ void step_lds_at(Step<F>& st, const unsigned char* pay, const uint32_t* ex, const StageOff<F>& o,
                                             int s, bool with_exp = true) {
-    const unsigned char* p = pay + s * Geo<F>::pay;
+    const unsigned char* p = pay + s * PAY;
     if constexpr (FmtInfo<F>::frsz) {
-        if (with_exp) st.e = ex[32 * s];
+        if (with_exp) st.e = ex[EXW * s];
     }
     if constexpr (F == kZ32) {
         st.c = *reinterpret_cast<const uint4*>(p);
@@ -1056,6 +1059,9 @@ template <int F> struct ReadLaunch {
 #ifndef FUSED_STEPS
 #define FUSED_STEPS 5
 #endif
+#ifndef FUSED_HOIST_OFF
+#define FUSED_HOIST_OFF 1
+#endif
 #ifndef FUSED_STAGE_VOTE
 #define FUSED_STAGE_VOTE 0  // 9.04 vs 8.02 ms on the bench solve (register pressure at 72 regs)
 #endif
@@ -1381,15 +1387,23 @@ __device__ __forceinline__ void fused_pass(uint32_t cols, uint32_t lim, uint32_t
                 }
             }
 #endif
+#if FUSED_HOIST_OFF
+            const StageOff<F> off;
+            const unsigned char* pay_t = pay + off.pay;
+            const uint32_t* ex_t = ex + off.ex;
+#endif
 #pragma unroll
             for (int s = 0; s < kChunkSteps; ++s) {
                 const int gs = ch * kChunkSteps + s;
-                const uint32_t lr = s * kFStepRows + 4u * threadIdx.x;
                 // whole steps (warp-uniform): rows past the CTA's range hold
                 // valid FRSZ2 data of the next range and w = 0 there
                 if (gs < kFusedMaxSteps && static_cast<uint32_t>(gs) < steps) {
                     Step<F> st;
-                    step_lds<F>(st, pay, ex, lr);
+#if FUSED_HOIST_OFF
+                    step_lds_at<F, FBytes<F>::pay, FBytes<F>::ex / 4>(st, pay_t, ex_t, off, s);
+#else
+                    step_lds<F>(st, pay, ex, s * kFStepRows + 4u * threadIdx.x);
+#endif
                     if constexpr (kDot) {
 #if FUSED_DOT_ACC4
                         if ((s & 3) == 0) acc = __dadd_rn(acc, st.dot(wv[gs]));
