@@ -1059,6 +1059,9 @@ template <int F> struct ReadLaunch {
 #ifndef FUSED_STEPS
 #define FUSED_STEPS 5
 #endif
+#ifndef FUSED_STAGE_CTR
+#define FUSED_STAGE_CTR 0  // incremental ring position: 6.04 vs 5.84 ms ortho (register allocation), off
+#endif
 #ifndef FUSED_HOIST_OFF
 #define FUSED_HOIST_OFF 1
 #endif
@@ -1333,6 +1336,12 @@ __device__ __forceinline__ void fused_pass(uint32_t cols, uint32_t lim, uint32_t
     constexpr uint32_t PAY = FBytes<F>::pay, SB = fstage_bytes<F>();
     constexpr int kChunkSteps = FGeo<F>::chunk, kChunks = (kFusedMaxSteps + kChunkSteps - 1) / kChunkSteps;
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+#if FUSED_STAGE_CTR
+    // ring position tracked incrementally (no division by the stage count
+    // per stage); `it` advanced once at the end
+    uint32_t rs = it % S, rph = (it / S) & 1;
+    const uint32_t it0 = it;
+#endif
     for (uint32_t jj = 0; jj < cols; ++jj) {
         const uint32_t j = kDot ? cols - 1 - jj : jj;
         const double hj = kDot ? 0.0 : hsm[j];
@@ -1341,8 +1350,13 @@ __device__ __forceinline__ void fused_pass(uint32_t cols, uint32_t lim, uint32_t
 #pragma unroll
         for (int ch = 0; ch < kChunks; ++ch) {
             if (ch >= static_cast<int>(nch)) break;
+#if FUSED_STAGE_CTR
+            const int stage = static_cast<int>(rs);
+            mbar_wait(full + stage, rph);
+#else
             const int stage = it % S;
             mbar_wait(full + stage, (it / S) & 1);
+#endif
             const unsigned char* pay = stages + stage * SB;
             const uint32_t* ex = reinterpret_cast<const uint32_t*>(pay + kChunkSteps * PAY);
 #if FUSED_STAGE_VOTE
@@ -1382,7 +1396,14 @@ __device__ __forceinline__ void fused_pass(uint32_t cols, uint32_t lim, uint32_t
                     }
                     __syncwarp();
                     if (lane == 0) mbar_arrive(empty + stage);
+#if FUSED_STAGE_CTR
+                    if (++rs == S) {
+                        rs = 0;
+                        rph ^= 1;
+                    }
+#else
                     ++it;
+#endif
                     continue;
                 }
             }
@@ -1421,13 +1442,23 @@ __device__ __forceinline__ void fused_pass(uint32_t cols, uint32_t lim, uint32_t
             }
             __syncwarp();
             if (lane == 0) mbar_arrive(empty + stage);
+#if FUSED_STAGE_CTR
+            if (++rs == S) {
+                rs = 0;
+                rph ^= 1;
+            }
+#else
             ++it;
+#endif
         }
         if constexpr (kDot) {
             acc = warp_sum(__dadd_rn(__dadd_rn(acc, acc2), __dadd_rn(acc3, acc4)));
             if (lane == 0) red[warp * cols + j] = acc;
         }
     }
+#if FUSED_STAGE_CTR
+    it = it0 + cols * min(nch, static_cast<uint32_t>(kChunks));
+#endif
     if constexpr (!kDot) {
         // the update also touched the rows past the CTA's range: w = 0 there
 #pragma unroll
