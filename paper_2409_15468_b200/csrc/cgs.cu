@@ -1169,12 +1169,46 @@ __device__ __forceinline__ unsigned ld_acquire(const unsigned* p) {
     return v;
 }
 
-// This CTA's rows: [r0, r1) in 128-row units, balanced over the grid.
+// Row shares of the fused grid. Measured on B200 (scripts/cta_buckets.py):
+// CTAs of the second half of the cooperative grid (the second CTA on each
+// SM) stream ~10% slower than the first half, and the slowest CTA sets the
+// pace of every grid all-reduce. Slot weights (integers, so the partition is
+// a fixed function of n and the grid -- deterministic):
+//   w(i) = G * 1e6 - FUSED_W2 * 1000 * G * [i >= G/2] - FUSED_WG * 1000 * i
+// (FUSED_W2: per-mille less for the second half; FUSED_WG: per-mille linear
+// decrease across the grid); slot s owns units [U C(s) / C(G), U C(s+1) / C(G)).
+#ifndef FUSED_W2
+#define FUSED_W2 0
+#endif
+#ifndef FUSED_WG
+#define FUSED_WG 0
+#endif
+__host__ __device__ __forceinline__ uint64_t fused_cum_weight(uint64_t s, uint64_t G) {
+    const uint64_t h = G / 2;
+    return s * G * 1000000ull - static_cast<uint64_t>(FUSED_W2) * 1000ull * G * (s > h ? s - h : 0) -
+           static_cast<uint64_t>(FUSED_WG) * 1000ull * (s * (s ? s - 1 : 0) / 2);
+}
+__host__ __device__ __forceinline__ void fused_unit_range(uint64_t units, uint64_t G, uint64_t slot, uint64_t& u0,
+                                                          uint64_t& u1) {
+    if (FUSED_W2 == 0 && FUSED_WG == 0) {
+        u0 = units * slot / G;
+        u1 = units * (slot + 1) / G;
+        return;
+    }
+    const uint64_t tot = fused_cum_weight(G, G);
+    // units * C(s) can exceed 64 bits only for units >= 2^64 / tot (> 2^26 at G = 296)
+    u0 = static_cast<uint64_t>((static_cast<unsigned __int128>(units) * fused_cum_weight(slot, G)) / tot);
+    u1 = static_cast<uint64_t>((static_cast<unsigned __int128>(units) * fused_cum_weight(slot + 1, G)) / tot);
+}
+
+// This CTA's rows: [r0, r1) in 128-row units, weighted over the grid.
 __device__ __forceinline__ void fused_rows(uint64_t n, uint32_t rot, uint64_t& r0, uint64_t& r1) {
     const uint64_t units = (n + kUnitRows - 1) / kUnitRows;
     const uint64_t slot = (blockIdx.x + rot) % gridDim.x;  // rot: diagnostic only (0 in production)
-    r0 = units * slot / gridDim.x * kUnitRows;
-    r1 = units * (slot + 1) / gridDim.x * kUnitRows;
+    uint64_t u0, u1;
+    fused_unit_range(units, gridDim.x, slot, u0, u1);
+    r0 = u0 * kUnitRows;
+    r1 = u1 * kUnitRows;
 }
 
 // Grid all-reduce among the consumer warps of all (co-resident) CTAs, one
@@ -1831,7 +1865,13 @@ int fused_grid(uint64_t n, uint32_t max_cols) {
     if (per_sm < 1) return 0;
     const uint64_t units = (n + kUnitRows - 1) / kUnitRows;
     const uint64_t G = std::min<uint64_t>(static_cast<uint64_t>(sm_count()) * std::min(per_sm, kFCtasPerSM), std::max<uint64_t>(units, 1));
-    if ((units + G - 1) / G * kUnitRows > static_cast<uint64_t>(kFusedMaxSteps) * kFStepRows) return 0;
+    uint64_t umax = 0;
+    for (uint64_t sl = 0; sl < G; ++sl) {
+        uint64_t u0, u1;
+        fused_unit_range(units, G, sl, u0, u1);
+        umax = std::max(umax, u1 - u0);
+    }
+    if (umax * kUnitRows > static_cast<uint64_t>(kFusedMaxSteps) * kFStepRows) return 0;
     return static_cast<int>(G);
 }
 
