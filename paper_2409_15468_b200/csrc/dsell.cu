@@ -207,6 +207,9 @@ __device__ __forceinline__ void unpack8(uint2 a, uint2 b, uint16_t (&c)[8]) {
 // MODE 0: y = A x.  MODE 1: y = b - A x. Persistent grid (one wave), one
 // warp per 32-row slice. kEll: ELL4 layout (uniform width, 8-byte groups of
 // 4 codes, no offset table).
+#ifndef DSELL_PADFREE
+#define DSELL_PADFREE 1
+#endif
 #ifndef DSELL_SPMV_THREADS
 #define DSELL_SPMV_THREADS 256
 #endif
@@ -238,8 +241,10 @@ dsell_spmv_kernel(uint64_t n_rows, const uint64_t* __restrict__ soff, uint32_t e
     __shared__ double s_v[256];
     __shared__ double red[kSW];
     for (uint32_t i = threadIdx.x; i < 256; i += kST) {
-        s_o[i] = d_off[i];
-        s_v[i] = d_val[i];
+        // index 255 never occurs in a real code: the padding code 0xFFFF
+        // decodes to offset 0, value +0.0
+        s_o[i] = i == 255 ? 0 : d_off[i];
+        s_v[i] = i == 255 ? 0.0 : d_val[i];
     }
     __syncthreads();
     pdl_trigger();
@@ -267,6 +272,15 @@ dsell_spmv_kernel(uint64_t n_rows, const uint64_t* __restrict__ soff, uint32_t e
                 if (g4 > 1) n1 = CLD(c4 + (nx * g4 + 1) * 32 + lane);
             }
             double s = 0.0;
+#if DSELL_PADFREE
+            // Padding codes decode to (offset 0, value +0.0): the gather reads
+            // x[r] (clamped into range for the rows past n) and adds 0 * x[r]
+            // = +-0, which leaves s unchanged (s starts at +0.0 and is never
+            // -0.0), so the batches need no per-entry predicates. A NaN sum
+            // (which a non-finite x[r] under a padding code could cause) is
+            // recomputed exactly below.
+            const int32_t rc = static_cast<uint64_t>(r) < n_rows ? r : static_cast<int32_t>(n_rows - 1);
+#endif
             for (uint32_t g = 0; g < g4; g += 2) {
                 if (g) {
                     a0 = CLD(c4 + (sl * g4 + g) * 32 + lane);
@@ -276,8 +290,29 @@ dsell_spmv_kernel(uint64_t n_rows, const uint64_t* __restrict__ soff, uint32_t e
                 }
                 uint16_t c[8];
                 unpack8(a0, a1, c);
+#if DSELL_PADFREE
+                double xv[8];
+#pragma unroll
+                for (int i = 0; i < 8; ++i) xv[i] = __ldg(x + (rc + s_o[c[i] & 0xFF]));
+#pragma unroll
+                for (int i = 0; i < 8; ++i) s = __dadd_rn(s, __dmul_rn(s_v[c[i] >> 8], xv[i]));
+#else
                 s = batch8(c, r, s_o, s_v, x, s);
+#endif
             }
+#if DSELL_PADFREE
+            if (isnan(s) && static_cast<uint64_t>(r) < n_rows) {
+                s = 0.0;
+                for (uint32_t g = 0; g < g4; g += 2) {
+                    const uint2 e0 = CLD(c4 + (sl * g4 + g) * 32 + lane);
+                    const uint2 e1 = g + 1 < g4 ? CLD(c4 + (sl * g4 + g + 1) * 32 + lane)
+                                                : make_uint2(0xFFFFFFFFu, 0xFFFFFFFFu);
+                    uint16_t c[8];
+                    unpack8(e0, e1, c);
+                    s = batch8(c, r, s_o, s_v, x, s);
+                }
+            }
+#endif
             if (static_cast<uint64_t>(r) < n_rows) {
                 if (MODE == 1) s = __dsub_rn(__ldg(b + r), s);
                 y[r] = s;

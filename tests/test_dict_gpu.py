@@ -138,3 +138,21 @@ def test_solves_through_dictionary_match_csr(cbg, port, fmt):
     assert abs(t1.total_iterations - t0.total_iterations) <= 2
     assert t1.converged and t1.final_rrn <= 1e-10
     assert np.allclose(np.asarray(t1.solution), np.asarray(t0.solution), rtol=1e-7, atol=1e-12)
+
+
+@pytest.mark.parametrize("special", [np.inf, -np.inf, np.nan])
+def test_nonfinite_x_matches_reference(cbg, port, special):
+    """Padding codes gather x[r] * 0.0: a non-finite x[r] must not leak into
+    rows whose real entries do not produce it (exact recompute path); rows
+    that do reference it give the reference's result."""
+    rp, ci, va = port.stencil(0, 9, 7, 5)
+    n = rp.size - 1
+    A = cbg.DeviceCsr.from_host(cbg.CsrMatrix(n, n, rp, ci, va))
+    D = cbg.DictCsr(A)
+    x = np.random.default_rng(3).standard_normal(n)
+    x[[0, 17, n - 1]] = special  # boundary rows (padded) and an interior row
+    ref = port.spmv(rp, ci, va, x)
+    y = D.spmv(x).cpu().numpy()
+    np.testing.assert_array_equal(np.isnan(y), np.isnan(ref))
+    fin = ~np.isnan(ref)
+    assert y[fin].tobytes() == ref[fin].tobytes()
