@@ -224,13 +224,10 @@ __device__ __forceinline__ void unpack8(uint2 a, uint2 b, uint16_t (&c)[8]) {
 constexpr int kST = DSELL_SPMV_THREADS;
 constexpr int kSW = kST / 32;
 #ifndef DSELL_MIN_BLOCKS
-#define DSELL_MIN_BLOCKS 0  // plain bounds (40 regs): 167 vs 221 us at 7-pt 256^3 (scripts/ab_spmv.sh)
+#define DSELL_MIN_BLOCKS 5  // with the pad-free batches: 160 vs 192 us at 7-pt 256^3, 82 vs 96 convdiff 192^3 (scripts/ab_spmv.sh)
 #endif
-#if DSELL_MIN_BLOCKS
-#define DSELL_BOUNDS __launch_bounds__(kST, DSELL_MIN_BLOCKS)
-#else
-#define DSELL_BOUNDS __launch_bounds__(kST)
-#endif
+// (ELL4 instantiations; the ragged SELL path: 4 CTAs, its former 64-register budget)
+#define DSELL_BOUNDS __launch_bounds__(kST, kEll && DSELL_MIN_BLOCKS ? DSELL_MIN_BLOCKS : 4)
 template <int MODE, bool kEll>
 __global__ void DSELL_BOUNDS
 dsell_spmv_kernel(uint64_t n_rows, const uint64_t* __restrict__ soff, uint32_t ell_w, const uint16_t* __restrict__ codes,
