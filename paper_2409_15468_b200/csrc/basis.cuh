@@ -180,9 +180,18 @@ __device__ __forceinline__ double fast_dot(const Codes4& c, uint32_t e, const do
 #endif
 }
 
-// Exact per-step decode (rare path), kept out of line.
+// Exact per-step decode (rare path). FRSZ_SLOW_NOINLINE: a real call, so the
+// hot loops carry no copy of the BlockDecoder code (smaller kernels).
+#ifndef FRSZ_SLOW_NOINLINE
+#define FRSZ_SLOW_NOINLINE 0
+#endif
+#if FRSZ_SLOW_NOINLINE
+#define FRSZ_SLOW_ATTR __noinline__
+#else
+#define FRSZ_SLOW_ATTR __forceinline__
+#endif
 template <int L>
-__device__ __forceinline__ void slow_decode(const Codes4& c, uint32_t e, double v[4]) {
+__device__ FRSZ_SLOW_ATTR void slow_decode(const Codes4& c, uint32_t e, double v[4]) {
     const BlockDecoder<L> d(e);
 #pragma unroll
     for (int k = 0; k < 4; ++k) {
