@@ -1059,6 +1059,9 @@ template <int F> struct ReadLaunch {
 #ifndef FUSED_STEPS
 #define FUSED_STEPS 5
 #endif
+#ifndef FUSED_FULL_SPEC
+#define FUSED_FULL_SPEC 1
+#endif
 #ifndef FUSED_STAGE_CTR
 #define FUSED_STAGE_CTR 0  // incremental ring position: 6.04 vs 5.84 ms ortho (register allocation), off
 #endif
@@ -1362,7 +1365,7 @@ __device__ __forceinline__ void fused_write(const FusedArgs& a, uint64_t r0, uin
 // One column pass over the CTA's rows: dot (partials into red[warp][j]) or
 // update (w -= h_j v_j) for columns in the given order. `lim` = number of
 // the CTA's rows; a thread's 4 rows are skipped past it (its w stays 0).
-template <int F, bool kDot>
+template <int F, bool kDot, bool kFull>
 __device__ __forceinline__ void fused_pass(uint32_t cols, uint32_t lim, uint32_t steps, uint32_t nch, unsigned char* stages,
                                            uint64_t* full, uint64_t* empty, uint32_t& it, double wv[][4],
                                            double* red, const double* hsm) {
@@ -1383,7 +1386,7 @@ __device__ __forceinline__ void fused_pass(uint32_t cols, uint32_t lim, uint32_t
         double acc = 0.0, acc2 = 0.0, acc3 = 0.0, acc4 = 0.0;
 #pragma unroll
         for (int ch = 0; ch < kChunks; ++ch) {
-            if (ch >= static_cast<int>(nch)) break;
+            if (!kFull && ch >= static_cast<int>(nch)) break;
 #if FUSED_STAGE_CTR
             const int stage = static_cast<int>(rs);
             mbar_wait(full + stage, rph);
@@ -1401,7 +1404,7 @@ __device__ __forceinline__ void fused_pass(uint32_t cols, uint32_t lim, uint32_t
 #pragma unroll
                 for (int s = 0; s < kChunkSteps; ++s) {
                     const int gs = ch * kChunkSteps + s;
-                    if (gs < kFusedMaxSteps && static_cast<uint32_t>(gs) < steps) {
+                    if (gs < kFusedMaxSteps && (kFull || static_cast<uint32_t>(gs) < steps)) {
                         st[s].e = ex[(s * kFStepRows + 4u * threadIdx.x) / 32];
                         if constexpr (kDot) ok &= st[s].fast();
                         else ok &= st[s].upd_ok(hj, he);
@@ -1411,7 +1414,7 @@ __device__ __forceinline__ void fused_pass(uint32_t cols, uint32_t lim, uint32_t
 #pragma unroll
                     for (int s = 0; s < kChunkSteps; ++s) {
                         const int gs = ch * kChunkSteps + s;
-                        if (gs < kFusedMaxSteps && static_cast<uint32_t>(gs) < steps) {
+                        if (gs < kFusedMaxSteps && (kFull || static_cast<uint32_t>(gs) < steps)) {
                             step_lds_pay<F>(st[s], pay, s * kFStepRows + 4u * threadIdx.x);
                             if constexpr (kDot) {
 #if FUSED_DOT_ACC4
@@ -1452,7 +1455,7 @@ __device__ __forceinline__ void fused_pass(uint32_t cols, uint32_t lim, uint32_t
                 const int gs = ch * kChunkSteps + s;
                 // whole steps (warp-uniform): rows past the CTA's range hold
                 // valid FRSZ2 data of the next range and w = 0 there
-                if (gs < kFusedMaxSteps && static_cast<uint32_t>(gs) < steps) {
+                if (gs < kFusedMaxSteps && (kFull || static_cast<uint32_t>(gs) < steps)) {
                     Step<F> st;
 #if FUSED_HOIST_OFF
                     step_lds_at<F, FBytes<F>::pay, FBytes<F>::ex / 4>(st, pay_t, ex_t, off, s);
@@ -1500,6 +1503,20 @@ __device__ __forceinline__ void fused_pass(uint32_t cols, uint32_t lim, uint32_t
             if (static_cast<uint32_t>(s) * kFStepRows + 4u * threadIdx.x >= lim)
                 wv[s][0] = wv[s][1] = wv[s][2] = wv[s][3] = 0.0;
     }
+}
+
+// Every CTA but the last few holds kFusedMaxSteps steps: a specialisation
+// without the per-step bounds checks (FUSED_FULL_SPEC).
+template <int F, bool kDot>
+__device__ __forceinline__ void fused_pass_any(uint32_t cols, uint32_t lim, uint32_t steps, uint32_t nch,
+                                               unsigned char* stages, uint64_t* full, uint64_t* empty, uint32_t& it,
+                                               double wv[][4], double* red, const double* hsm) {
+#if FUSED_FULL_SPEC
+    if (steps == static_cast<uint32_t>(kFusedMaxSteps))
+        fused_pass<F, kDot, true>(cols, lim, steps, nch, stages, full, empty, it, wv, red, hsm);
+    else
+#endif
+        fused_pass<F, kDot, false>(cols, lim, steps, nch, stages, full, empty, it, wv, red, hsm);
 }
 
 // This CTA's dot-pass partials (red[warp][j] summed over warps in order)
@@ -1719,7 +1736,7 @@ __global__ void __launch_bounds__(kFThreads, kFCtasPerSM) arnoldi_fused_kernel(F
     unsigned seq = 0;
 
     // dot1 -> h
-    fused_pass<F, true>(cols, lim, steps, nch, stages, full, empty, it, wv, red, hsm);
+    fused_pass_any<F, true>(cols, lim, steps, nch, stages, full, empty, it, wv, red, hsm);
     FTRACE(2);
     if (a.trace && threadIdx.x == 0) a.trace[32 + blockIdx.x] = global_ns();
     dot_partials_out(red, cols, P, gs);
@@ -1738,14 +1755,14 @@ __global__ void __launch_bounds__(kFThreads, kFCtasPerSM) arnoldi_fused_kernel(F
     if (kFold && cta0 && threadIdx.x == 0) a.slot[2] = omega2;
     FTRACE(3);
     // update1
-    fused_pass<F, false>(cols, lim, steps, nch, stages, full, empty, it, wv, red, hsm);
+    fused_pass_any<F, false>(cols, lim, steps, nch, stages, full, empty, it, wv, red, hsm);
     FTRACE(4);
     if (a.trace && threadIdx.x == 0) a.trace[32 + 1024 + blockIdx.x] = global_ns();
     const double hn1_part = cta_wnorm2(wv, nred);
     double* const P1 = P + region;
     if (spec) {
         // speculative dot2 -> u, reduced together with hn1
-        fused_pass<F, true>(cols, lim, steps, nch, stages, full, empty, it, wv, red, hsm);
+        fused_pass_any<F, true>(cols, lim, steps, nch, stages, full, empty, it, wv, red, hsm);
         FTRACE(5);
         dot_partials_out(red, cols, P1, gs);
     }
@@ -1770,7 +1787,7 @@ __global__ void __launch_bounds__(kFThreads, kFCtasPerSM) arnoldi_fused_kernel(F
     double hn2 = hn1;
     if (gate) {
         if (!spec) {
-            fused_pass<F, true>(cols, lim, steps, nch, stages, full, empty, it, wv, red, hsm);
+            fused_pass_any<F, true>(cols, lim, steps, nch, stages, full, empty, it, wv, red, hsm);
             FTRACE(5);
             dot_partials_out(red, cols, P + 2 * region, gs);
             grid_allreduce(a.bar, seq++, P + 2 * region, gs, cols, hsm);
@@ -1782,7 +1799,7 @@ __global__ void __launch_bounds__(kFThreads, kFCtasPerSM) arnoldi_fused_kernel(F
             }
         FTRACE(7);
         // update2 (u in hsm)
-        fused_pass<F, false>(cols, lim, steps, nch, stages, full, empty, it, wv, red, hsm);
+        fused_pass_any<F, false>(cols, lim, steps, nch, stages, full, empty, it, wv, red, hsm);
         FTRACE(8);
         const double p = cta_wnorm2(wv, nred);
         double* const P3 = P + 3 * region;
