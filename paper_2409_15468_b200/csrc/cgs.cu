@@ -59,8 +59,14 @@ template <> struct Geo<kZ32> { static constexpr uint32_t pay = 4096, ex = 128; s
 #ifndef SPLIT_SUB_SMALL
 #define SPLIT_SUB_SMALL 4
 #endif
-template <> struct Geo<kZ16> { static constexpr uint32_t pay = 2048, ex = 128; static constexpr int sub = SPLIT_SUB_SMALL, stages = 6; };
-template <> struct Geo<kZ21> { static constexpr uint32_t pay = 2688, ex = 128; static constexpr int sub = SPLIT_SUB_SMALL, stages = 5; };
+#ifndef SPLIT_STAGES_Z16
+#define SPLIT_STAGES_Z16 6
+#endif
+#ifndef SPLIT_STAGES_Z21
+#define SPLIT_STAGES_Z21 5
+#endif
+template <> struct Geo<kZ16> { static constexpr uint32_t pay = 2048, ex = 128; static constexpr int sub = SPLIT_SUB_SMALL, stages = SPLIT_STAGES_Z16; };
+template <> struct Geo<kZ21> { static constexpr uint32_t pay = 2688, ex = 128; static constexpr int sub = SPLIT_SUB_SMALL, stages = SPLIT_STAGES_Z21; };
 template <> struct Geo<kF64> { static constexpr uint32_t pay = 8192, ex = 0; static constexpr int sub = 4, stages = 3; };
 template <> struct Geo<kF32> { static constexpr uint32_t pay = 4096, ex = 0; static constexpr int sub = 4, stages = 4; };
 template <> struct Geo<kF16> { static constexpr uint32_t pay = 2048, ex = 0; static constexpr int sub = 4, stages = 6; };
