@@ -164,6 +164,26 @@ int cbgx_cgs_update(const cbgx_basis* V, uint64_t first, uint32_t cols, const do
                     int h_sign, double* d_w, double* d_wnorm2, int reduction,
                     cbgx_workspace* ws, void* stream);
 
+/* One complete Arnoldi orthogonalisation step -- arnoldi_orthogonalize
+ * (gmres.cpp:36-71: h = V^T w, w -= V h, gated second pass with
+ * h_next < eta * omega) followed by the scaled write of the next basis
+ * column (gmres.cpp:230-234: v = w * (1/h_next), write_vector(cols, v)) --
+ * as ONE cooperative launch of the fused kernel the solver uses on a single
+ * GPU (tree reductions). Columns 0..cols-1 are read, column `cols` is
+ * written, d_w is read only (the updated w lives in registers), d_v_out
+ * receives v. d_slot (3 + 2 * (max_cols + 1) doubles) =
+ * [hn1, hn2, omega2, h[0..max_cols], u[0..max_cols]]: slot[2] = <w, w> is
+ * an INPUT (the solver's SpMV epilogue writes it); the kernel writes h,
+ * hn1 = ||w - V h||^2 and, when the gate closes (sqrt(hn1) < eta *
+ * sqrt(omega2)), u and hn2; v is scaled by the last pass's norm.
+ * speculate = 1: the second dot pass runs before the gate is known (the
+ * solver's choice after an open gate); its u is discarded when the gate
+ * stays open. CBGX_EINVAL when the fused kernel is not eligible (n too
+ * large for register-resident rows, capacity, device). Synchronous. */
+int cbgx_arnoldi_fused_step(const cbgx_basis* V, uint32_t cols, uint32_t max_cols, const double* d_w,
+                            double* d_v_out, double* d_slot, double eta, int speculate,
+                            cbgx_workspace* ws, void* stream);
+
 /* ------------------------------------------------ CSR SpMV and BLAS-1
  * Reference: sparse.hpp:17-26, sparse.cpp:43-84. Per-row left-to-right
  * accumulation from +0.0 with separate multiply and add roundings, so SpMV

@@ -251,6 +251,15 @@ class Port:
         assert self.lib.orc_basis_roundtrip(kind, l, col.size, col, out) == 0
         return out
 
+    def basis_subtract_scaled(self, fmt, col, alpha, y):
+        """y -= alpha * column (through the storage format), in place
+        (basis.cpp:189-205)."""
+        kind, l = FORMATS[fmt]
+        assert y.dtype == np.float64 and y.flags.c_contiguous
+        assert self.lib.orc_basis_subtract_scaled(kind, l, y.size, np.ascontiguousarray(col, np.float64),
+                                                  float(alpha), y) == 0
+        return y
+
     def basis_dot(self, fmt, col, w):
         kind, l = FORMATS[fmt]
         out = C.c_double()

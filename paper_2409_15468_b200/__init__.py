@@ -403,6 +403,27 @@ class KrylovBasis:
                                     _ptr(norm_out) if want_norm else None, reduction, _ws(), _stream()))
         return norm_out
 
+    def arnoldi_fused_step(self, cols: int, w, omega2, max_cols: int, eta=0.70710678118654752,
+                           speculate=True):
+        """One fused Arnoldi step (cbgx_arnoldi_fused_step: gmres.cpp:36-71
+        + the scaled write of column `cols`, :230-234). Returns (slot, v):
+        slot = [hn1, hn2, omega2, h[0..max_cols], u[0..max_cols]] (CUDA
+        float64), v = the written column's fp64 values."""
+        import ctypes
+        torch = _torch()
+        if cols > self.count_ or cols + 1 > self.capacity_:
+            raise IndexError("basis: column index out of range")
+        w = _dev(w)
+        if w.numel() != self.n:
+            raise ValueError("basis: length mismatch")
+        slot = torch.zeros(3 + 2 * (max_cols + 1), dtype=torch.float64, device="cuda")
+        slot[2] = omega2
+        v = torch.empty(max(self.n, 1), dtype=torch.float64, device="cuda")
+        check(lib().cbgx_arnoldi_fused_step(ctypes.byref(self.desc), cols, max_cols, _ptr(w), _ptr(v), _ptr(slot),
+                                            eta, int(bool(speculate)), _ws(), _stream()))
+        self.count_ = max(self.count_, cols + 1)
+        return slot, v[:self.n]
+
     def dot(self, j: int, w) -> float:
         """basis.cpp:168-187 (single column; syncs)."""
         self._check(j)

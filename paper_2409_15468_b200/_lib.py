@@ -89,6 +89,7 @@ def lib():
             "cbgx_basis_read": ([P(Basis), u64, u64, u64, vp, vp], C.c_int),
             "cbgx_cgs_dot": ([P(Basis), u64, u32, vp, C.c_int, C.c_int, vp, vp, vp], C.c_int),
             "cbgx_cgs_update": ([P(Basis), u64, u32, vp, C.c_int, vp, vp, C.c_int, vp, vp], C.c_int),
+            "cbgx_arnoldi_fused_step": ([P(Basis), u32, u32, vp, vp, vp, dbl, C.c_int, vp, vp], C.c_int),
             "cbgx_csr_spmv": ([P(Csr), vp, vp, vp, C.c_int, vp, vp], C.c_int),
             "cbgx_csr_residual": ([P(Csr), vp, vp, vp, vp, C.c_int, vp, vp], C.c_int),
             "cbgx_csr_spmv_plan": ([P(Csr), P(C.c_uint32), vp], C.c_int),

@@ -1922,7 +1922,9 @@ template <int F> struct FusedLaunch {
         // two arrival counters used by alternate launches: each launch
         // zeroes the other one (the previous launch has completed)
         unsigned* c = ws->get_counter();
-        const uint64_t seq = ws->fused_launches++;
+        // the launch sequence advances only once the launch succeeded: each
+        // launch zeroes the counter the next one uses
+        const uint64_t seq = ws->fused_launches;
         a.bar = c + Workspace::kFusedBar + (seq & 1) * 32;
         a.bar_next = c + Workspace::kFusedBar + ((seq + 1) & 1) * 32;
         a.gate_hist = c + Workspace::kFusedGate;
@@ -1951,6 +1953,7 @@ template <int F> struct FusedLaunch {
         note_launch();
         if (a.fold) CBGX_CUDA(cudaLaunchKernelEx(&lc, arnoldi_fused_kernel<F, true>, a));
         else CBGX_CUDA(cudaLaunchKernelEx(&lc, arnoldi_fused_kernel<F, false>, a));
+        ws->fused_launches = seq + 1;
         *done = true;
     }
 };
@@ -2096,6 +2099,29 @@ int cbgx_cgs_update(const cbgx_basis* V, uint64_t first, uint32_t cols, const do
         if (!ws) throw Error(CBGX_EINVAL, "cgs: null workspace");
         launch_cgs_update(*V, first, cols, d_h, h_sign < 0 ? -1.0 : 1.0, d_w, d_wnorm2, reduction,
                           ws_of(ws), as_stream(stream));
+    });
+}
+
+int cbgx_arnoldi_fused_step(const cbgx_basis* V, uint32_t cols, uint32_t max_cols, const double* d_w,
+                            double* d_v_out, double* d_slot, double eta, int speculate, cbgx_workspace* ws,
+                            void* stream) {
+    return guard([&] {
+        check_basis(V);
+        if (!ws) throw Error(CBGX_EINVAL, "fused: null workspace");
+        if (cols < 1 || cols > max_cols || max_cols + 1 > V->capacity)
+            throw Error(CBGX_ERANGE, "fused: need 1 <= cols <= max_cols < capacity");
+        cudaStream_t st = as_stream(stream);
+        Workspace* w = ws_of(ws);
+        // the gate history the kernel reads: 0 = previous gate open (the
+        // second dot pass runs speculatively), 1 = closed
+        unsigned* c = w->get_counter();
+        const unsigned hist = speculate ? 0u : 1u;
+        CBGX_CUDA(cudaMemcpyAsync(c + Workspace::kFusedGate, &hist, sizeof(unsigned), cudaMemcpyHostToDevice, st));
+        const uint32_t u_off = 3 + max_cols + 1;
+        if (!launch_arnoldi_fused(*V, cols, d_w, d_v_out, d_slot, u_off, eta, max_cols, nullptr, false, FoldArg{}, w,
+                                  st))
+            throw Error(CBGX_EINVAL, "fused: not eligible for this basis (n, capacity, format or device)");
+        CBGX_CUDA(cudaStreamSynchronize(st));  // `hist` is a host stack value
     });
 }
 

@@ -81,24 +81,41 @@ dict_scan_kernel(const RP* __restrict__ rp, const int32_t* __restrict__ ci, cons
     for (uint32_t i = threadIdx.x; i < kSlots; i += kDThreads) s_off[i] = s_val[i] = kEmpty;
     if (threadIdx.x < 2) s_cnt[threadIdx.x] = 0;
     __syncthreads();
+    // Warp-uniform loops (the lanes of a warp share the row base; rows past
+    // n and entries past a row's end take part as inactive lanes), so every
+    // __match_any_sync below is reached by all 32 lanes together.
     bool ok = true;
-    for (uint64_t r = blockIdx.x * static_cast<uint64_t>(kDThreads) + threadIdx.x; r < n_rows && ok;
-         r += static_cast<uint64_t>(gridDim.x) * kDThreads) {
-        if (*reinterpret_cast<volatile unsigned*>(bad)) break;
-        const uint64_t k0 = static_cast<uint64_t>(rp[r]), k1 = static_cast<uint64_t>(rp[r + 1]);
-        for (uint64_t k = k0; k < k1 && ok; ++k) {
-            const int64_t off = static_cast<int64_t>(ci[k]) - static_cast<int64_t>(r);
-            const unsigned long long ko = off_key(off);
-            const unsigned long long kv = static_cast<unsigned long long>(__double_as_longlong(va[k]));
-            if (off < INT32_MIN || off > INT32_MAX || kv == kEmpty) {
-                ok = false;
-                break;
+    const uint64_t stride = static_cast<uint64_t>(gridDim.x) * kDThreads;
+    const int lane = threadIdx.x & 31;
+    for (uint64_t r0 = blockIdx.x * static_cast<uint64_t>(kDThreads) + (threadIdx.x & ~31u); r0 < n_rows;
+         r0 += stride) {
+        if (!__all_sync(0xFFFFFFFFu, ok) || *reinterpret_cast<volatile unsigned*>(bad)) {
+            ok = false;
+            break;
+        }
+        const uint64_t r = r0 + lane;
+        const bool row = r < n_rows;
+        const uint64_t k0 = row ? static_cast<uint64_t>(rp[r]) : 0, k1 = row ? static_cast<uint64_t>(rp[r + 1]) : 0;
+        const unsigned len = static_cast<unsigned>(k1 - k0);
+        const unsigned wlen = __reduce_max_sync(0xFFFFFFFFu, len);
+        for (unsigned k = 0; k < wlen; ++k) {
+            bool act = k < len;
+            unsigned long long ko = kEmpty, kv = kEmpty;
+            if (act) {
+                const int64_t off = static_cast<int64_t>(ci[k0 + k]) - static_cast<int64_t>(r);
+                ko = off_key(off);
+                kv = static_cast<unsigned long long>(__double_as_longlong(va[k0 + k]));
+                if (off < INT32_MIN || off > INT32_MAX || kv == kEmpty) {
+                    ok = false;
+                    act = false;
+                    ko = kv = kEmpty;
+                }
             }
-            const unsigned act = __activemask();
-            const unsigned mo = __match_any_sync(act, ko), mv = __match_any_sync(act, kv);
-            const int lane = threadIdx.x & 31;
-            if (__ffs(mo) - 1 == lane) ok = ok && table_insert(s_off, ko, &s_cnt[0]);
-            if (__ffs(mv) - 1 == lane) ok = ok && table_insert(s_val, kv, &s_cnt[1]);
+            // inactive lanes carry the empty key: they group together and
+            // never insert
+            const unsigned mo = __match_any_sync(0xFFFFFFFFu, ko), mv = __match_any_sync(0xFFFFFFFFu, kv);
+            if (act && __ffs(mo) - 1 == lane) ok = table_insert(s_off, ko, &s_cnt[0]) && ok;
+            if (act && __ffs(mv) - 1 == lane) ok = table_insert(s_val, kv, &s_cnt[1]) && ok;
         }
     }
     if (!ok) atomicExch(bad, 1u);
@@ -135,7 +152,8 @@ __global__ void __launch_bounds__(kDThreads)
 dict_fill_kernel(const RP* __restrict__ rp, const int32_t* __restrict__ ci, const double* __restrict__ va,
                  uint64_t n_rows, const uint64_t* __restrict__ soff, const unsigned long long* __restrict__ g_off,
                  const unsigned long long* __restrict__ g_val, const uint8_t* __restrict__ off_idx,
-                 const uint8_t* __restrict__ val_idx, uint32_t ell4, uint16_t* __restrict__ codes) {
+                 const uint8_t* __restrict__ val_idx, uint32_t ell4, uint16_t* __restrict__ codes,
+                 unsigned* __restrict__ too_long) {
     __shared__ unsigned long long s_off[kSlots], s_val[kSlots];
     __shared__ uint8_t s_oi[kSlots], s_vi[kSlots];
     for (uint32_t i = threadIdx.x; i < kSlots; i += kDThreads) {
@@ -152,6 +170,9 @@ dict_fill_kernel(const RP* __restrict__ rp, const int32_t* __restrict__ ci, cons
         const uint64_t base = ell4 ? 0 : soff[sl], width = ell4 ? 4ull * ell4 : (soff[sl + 1] - base) / 32;
         const uint64_t k0 = r < n_rows ? static_cast<uint64_t>(rp[r]) : 0;
         const uint64_t len = r < n_rows ? static_cast<uint64_t>(rp[r + 1]) - k0 : 0;
+        // a row longer than the slice width (an understated max_row_nnz
+        // hint) would be cut short: the build is refused instead
+        if (len > width) atomicExch(too_long, 1u);
         for (uint64_t k = 0; k < width; ++k) {
             uint16_t code = kPad;
             if (k < len) {
@@ -467,8 +488,16 @@ bool dict_build(const cbgx_csr& A, double reserve_bytes, cudaStream_t st, DictSe
     CBGX_CUDA(cudaMemcpyAsync(D.val, d_val.data(), 256 * sizeof(double), cudaMemcpyHostToDevice, st));
     CBGX_K(dict_fill_kernel<RP><<<dict_grid(D.nslices * 32), kDThreads, 0, st>>>(
         rp, A.d_col_idx, A.d_values, A.n_rows, D.soff, D.tabs, D.tabs + kSlots, D.idx, D.idx + kSlots, D.ell_w / 4,
-        D.codes));
+        D.codes, D.flags + 2));  // flags[2] (scan failure) is 0 here
     CBGX_CUDA(cudaGetLastError());
+    if (max_w == A.max_row_nnz && max_w > 0) {
+        // the ELL width came from the caller's max_row_nnz hint (cbgx.h:
+        // "0 = unknown"), not from a pass over the row offsets: verify it
+        unsigned long_rows = 0;
+        CBGX_CUDA(cudaMemcpyAsync(&long_rows, D.flags + 2, sizeof(unsigned), cudaMemcpyDeviceToHost, st));
+        CBGX_CUDA(cudaStreamSynchronize(st));
+        if (long_rows) return false;
+    }
     D.ready = true;
     return true;
 }
@@ -484,6 +513,8 @@ DictSell::~DictSell() {
 bool build_dict_sell(const cbgx_csr& A, double reserve_bytes, cudaStream_t st, DictSell& D) {
     D.ready = false;
     if (A.n_rows == 0 || A.nnz == 0) return false;
+    // padding codes gather x[min(r, n_rows - 1)]: x must hold n_rows values
+    if (A.n_cols < A.n_rows) return false;
     return A.row_ptr_bits == 32 ? dict_build<int32_t>(A, reserve_bytes, st, D)
                                 : dict_build<int64_t>(A, reserve_bytes, st, D);
 }
@@ -543,9 +574,10 @@ int cbgx_csr_dict_create(const cbgx_csr* A, cbgx_dict_csr** out, void* stream) {
         if (!A || !out) throw Error(CBGX_EINVAL, "dict: null argument");
         if (A->row_ptr_bits != 32 && A->row_ptr_bits != 64) throw Error(CBGX_EINVAL, "csr: row_ptr_bits must be 32 or 64");
         *out = nullptr;
+        if (A->n_cols < A->n_rows) throw Error(CBGX_EINVAL, "dict: needs n_cols >= n_rows");
         auto D = std::make_unique<DictSell>();
         if (!build_dict_sell(*A, 0.0, as_stream(stream), *D))
-            throw Error(CBGX_EINVAL, "dict: matrix has more than 255 distinct values or column offsets");
+            throw Error(CBGX_EINVAL, "dict: matrix does not fit the dictionary format (more than 255 distinct values or column offsets, or a row longer than max_row_nnz)");
         CBGX_CUDA(cudaStreamSynchronize(as_stream(stream)));
         *out = new cbgx_dict_csr{std::move(D)};
     });

@@ -156,3 +156,31 @@ def test_nonfinite_x_matches_reference(cbg, port, special):
     np.testing.assert_array_equal(np.isnan(y), np.isnan(ref))
     fin = ~np.isnan(ref)
     assert y[fin].tobytes() == ref[fin].tobytes()
+
+
+def test_understated_row_length_hint_refused_or_exact(cbg, port):
+    """cbgx.h documents max_row_nnz as a hint (0 = unknown): a hint below
+    the longest row must not cut rows short (dsell.cu:427)."""
+    rp, ci, va = port.stencil(0, 12, 11, 10)
+    n = rp.size - 1
+    A = cbg.DeviceCsr.from_host(cbg.CsrMatrix(n, n, rp, ci, va))
+    A.desc.max_row_nnz = 2  # the real longest row has 7 entries
+    try:
+        D = cbg.DictCsr(A)
+    except Exception as e:  # refused: the caller keeps CSR
+        assert "max_row_nnz" in str(e)
+        return
+    x = np.random.default_rng(3).standard_normal(n)
+    assert D.spmv(x).cpu().numpy().tobytes() == port.spmv(rp, ci, va, x).tobytes()
+
+
+def test_tall_matrix_refused(cbg):
+    """Padding codes gather x[r]: x must hold n_rows values (ADVICE r01:
+    dsell.cu:293), so a matrix with n_cols < n_rows is refused."""
+    n_rows, n_cols = 64, 40
+    rp = np.arange(n_rows + 1, dtype=np.uint64)
+    ci = (np.arange(n_rows) % n_cols).astype(np.uint64)
+    va = np.ones(n_rows)
+    A = cbg.DeviceCsr.from_host(cbg.CsrMatrix(n_rows, n_cols, rp, ci, va))
+    with pytest.raises(Exception, match="n_cols >= n_rows"):
+        cbg.DictCsr(A)
