@@ -276,8 +276,7 @@ enum {
     CBGX_SOLVER_NO_FUSION = 4,             /* always use the split dot/update/write kernels */
     CBGX_SOLVER_NO_SELL = 8,               /* SpMV directly on the CSR (no SELL-32 copy) */
     CBGX_SOLVER_NO_TMA_SPMV = 16,          /* no staged (bulk-copy) CSR SpMV */
-    CBGX_SOLVER_FOLD = 32,                 /* fold the SpMV into the fused orthogonalisation launch
-                                              (experimental; measured slower on B200, off by default) */
+    /* 32: reserved (was an experimental folded-SpMV variant, measured slower; removed) */
     CBGX_SOLVER_NO_DICT_SPMV = 64          /* no dictionary-coded SELL-32 copy (cbgx_csr_dict_*) */
 };
 

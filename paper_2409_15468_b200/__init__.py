@@ -671,14 +671,13 @@ class GmresConfig:
     fusion: bool = True   # fused single-GPU orthogonalisation kernel when eligible
     sell: bool = True     # SELL-32 copy of A for the SpMV when memory allows
     tma_spmv: bool = True  # staged (bulk-copy) CSR SpMV when every row tile fits
-    fold: bool = False     # SpMV folded into the fused orthogonalisation launch (experimental)
     dict_spmv: bool = True  # dictionary-coded SELL-32 SpMV when A has <= 255 distinct values/offsets
 
     def c(self):
         flags = (_lib.PHASE_TIMING if self.phase_timing else 0) | \
             (_lib.PHASE_TIMING_DEFERRED if self.phase_timing_deferred else 0) | \
             (0 if self.fusion else _lib.NO_FUSION) | (0 if self.sell else _lib.NO_SELL) | \
-            (0 if self.tma_spmv else _lib.NO_TMA_SPMV) | (_lib.FOLD if self.fold else 0) | \
+            (0 if self.tma_spmv else _lib.NO_TMA_SPMV) | \
             (0 if self.dict_spmv else _lib.NO_DICT_SPMV)
         return _lib.GmresConfig(self.restart, self.target_rrn, self.max_total_iterations, self.eta,
                                 self.storage_format.kind, self.storage_format.bit_length,

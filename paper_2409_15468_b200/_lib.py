@@ -16,7 +16,6 @@ PHASE_TIMING_DEFERRED = 2
 NO_FUSION = 4
 NO_SELL = 8
 NO_TMA_SPMV = 16
-FOLD = 32
 NO_DICT_SPMV = 64
 PHASES = ["spmv", "dot", "update", "write", "residual", "solution", "comm", "ortho"]
 

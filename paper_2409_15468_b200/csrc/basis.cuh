@@ -162,36 +162,18 @@ __device__ __forceinline__ double signed_i2f(uint32_t mag, uint32_t sgn) {
     return __hiloint2double(__double2hiint(d) ^ static_cast<int>(sgn), __double2loint(d));
 }
 
-#ifndef FRSZ_DOT_PAIRS
-#define FRSZ_DOT_PAIRS 1
-#endif
 template <int L>
 __device__ __forceinline__ double fast_dot(const Codes4& c, uint32_t e, const double w[4]) {
-#if FRSZ_DOT_PAIRS
     // two independent FMA chains (depth 3 instead of 4 dependent FP64 ops)
     const double a = fma(signed_i2f(c.mag[1], c.sgn[1]), w[1], __dmul_rn(signed_i2f(c.mag[0], c.sgn[0]), w[0]));
     const double b = fma(signed_i2f(c.mag[3], c.sgn[3]), w[3], __dmul_rn(signed_i2f(c.mag[2], c.sgn[2]), w[2]));
     return __dmul_rn(__dadd_rn(a, b), __hiloint2double(static_cast<int>((e - (L - 2)) << 20), 0));
-#else
-    double s = __dmul_rn(signed_i2f(c.mag[0], c.sgn[0]), w[0]);
-#pragma unroll
-    for (int k = 1; k < 4; ++k) s = fma(signed_i2f(c.mag[k], c.sgn[k]), w[k], s);
-    return __dmul_rn(s, __hiloint2double(static_cast<int>((e - (L - 2)) << 20), 0));
-#endif
 }
 
-// Exact per-step decode (rare path). FRSZ_SLOW_NOINLINE: a real call, so the
-// hot loops carry no copy of the BlockDecoder code (smaller kernels).
-#ifndef FRSZ_SLOW_NOINLINE
-#define FRSZ_SLOW_NOINLINE 0
-#endif
-#if FRSZ_SLOW_NOINLINE
-#define FRSZ_SLOW_ATTR __noinline__
-#else
-#define FRSZ_SLOW_ATTR __forceinline__
-#endif
+// Exact per-step decode (rare path), inlined: as a real call it forces w
+// out of registers (2.4x slower fused passes on B200).
 template <int L>
-__device__ FRSZ_SLOW_ATTR void slow_decode(const Codes4& c, uint32_t e, double v[4]) {
+__device__ __forceinline__ void slow_decode(const Codes4& c, uint32_t e, double v[4]) {
     const BlockDecoder<L> d(e);
 #pragma unroll
     for (int k = 0; k < 4; ++k) {

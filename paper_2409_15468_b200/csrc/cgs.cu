@@ -198,14 +198,9 @@ __device__ __forceinline__ void step_lds_at(Step<F>& st, const unsigned char* pa
 // One column's stage of a sub-tile. The exponents of all steps are read
 // first and ONE warp vote decides the fast decode for the whole stage (the
 // exact per-step path only when some block of the stage needs it); payloads
-// are read step by step (kPreload: all up front -- more loads in flight, but
-// the register pressure spills at 3 CTAs/SM: slower for every format on B200,
-// scripts/ab_split.sh). kFull: all Geo<F>::sub steps are present (every tile but the
-// last), no per-step bounds checks.
-#ifndef SPLIT_PRELOAD_MASK
-#define SPLIT_PRELOAD_MASK 0
-#endif
-template <int F> constexpr bool kPreload = (SPLIT_PRELOAD_MASK >> F) & 1;
+// are read step by step (reading them all up front spills at 3 CTAs/SM:
+// slower for every format on B200). kFull: all Geo<F>::sub steps are present
+// (every tile but the last), no per-step bounds checks.
 
 template <int F, bool kFull>
 __device__ __forceinline__ double stage_dot(const unsigned char* pay, const uint32_t* ex, const StageOff<F>& o,
@@ -220,13 +215,12 @@ __device__ __forceinline__ double stage_dot(const unsigned char* pay, const uint
             if (kFull || s < steps) {
                 st[s].e = ex[32 * s];
                 ok &= st[s].fast();
-                if constexpr (kPreload<F>) step_lds_at<F>(st[s], pay, ex, o, s, false);
             }
         if (__builtin_expect(__all_sync(0xFFFFFFFFu, ok), 1)) {
 #pragma unroll
             for (int s = 0; s < SUB; ++s)
                 if (kFull || s < steps) {
-                    if constexpr (!kPreload<F>) step_lds_at<F>(st[s], pay, ex, o, s, false);
+                    step_lds_at<F>(st[s], pay, ex, o, s, false);
                     acc = __dadd_rn(acc, st[s].dot_fast(wv[s]));
                 }
             return acc;
@@ -253,13 +247,12 @@ __device__ __forceinline__ void stage_update(const unsigned char* pay, const uin
             if (kFull || s < steps) {
                 st[s].e = ex[32 * s];
                 ok &= st[s].upd_ok(hj, he);
-                if constexpr (kPreload<F>) step_lds_at<F>(st[s], pay, ex, o, s, false);
             }
         if (__builtin_expect(__all_sync(0xFFFFFFFFu, ok), 1)) {
 #pragma unroll
             for (int s = 0; s < SUB; ++s)
                 if (kFull || s < steps) {
-                    if constexpr (!kPreload<F>) step_lds_at<F>(st[s], pay, ex, o, s, false);
+                    step_lds_at<F>(st[s], pay, ex, o, s, false);
                     st[s].update_fast(hj, he, wv[s]);
                 }
             return;
@@ -496,10 +489,6 @@ cgs_update_kernel(BasisView B, uint64_t first, uint32_t cols, const double* __re
 // <w, w> is summed per tile and the tiles in tile order -- deterministic
 // whatever the assignment.
 constexpr uint32_t kTileEnd = 0xFFFFFFFFu;
-#ifndef SPLIT_PAIR_REDUCE
-#define SPLIT_PAIR_REDUCE 0  // neutral on B200 (scripts/ab_split.sh): the column passes are not reduction-bound
-#endif
-
 __device__ __forceinline__ unsigned ld_acquire_u32(const unsigned* p) {
     unsigned v;
     asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
@@ -745,16 +734,6 @@ cgs_dot_dyn_kernel(BasisView B, uint64_t first, uint32_t cols, const double* __r
             };
             if (cols) {
                 uint32_t jj = 0;
-#if SPLIT_PAIR_REDUCE
-                // columns in pairs: one butterfly for two sums
-                for (; jj + 1 < cols; jj += 2) {
-                    const double a = column(jj);
-                    const double b = column(jj + 1);
-                    const double v = warp_sum2(a, b);
-                    if (lane == 0) red[warp * ncol + cols - 1 - jj] = v;
-                    if (lane == 16) red[warp * ncol + cols - 2 - jj] = v;
-                }
-#endif
                 for (; jj < cols; ++jj) {
                     const double v = warp_sum(column(jj));
                     if (lane == 0) red[warp * ncol + cols - 1 - jj] = v;
@@ -943,9 +922,6 @@ void allow_smem(K kernel) {
 
 // Dynamic tile scheduling for the split CGS kernels (measured on B200:
 // update at n = 2^26, k = 100 0.85 -> 1.03 of the HBM peak).
-#ifndef SPLIT_DYNAMIC
-#define SPLIT_DYNAMIC 1
-#endif
 template <int F> struct DotLaunch {
     static void run(const BasisView& B, uint64_t first, uint32_t cols, const double* w, int wn,
                     int reduction, double* h, Workspace* ws, cudaStream_t st, const GateArg& gate, bool coop) {
@@ -956,7 +932,7 @@ template <int F> struct DotLaunch {
             CBGX_K(serial_dot_kernel<F><<<(threads + 63) / 64, 64, 0, st>>>(B, first, cols, w, wn, h, gate));
             return;
         }
-        if (SPLIT_DYNAMIC && coop) {
+        if (coop) {
             // reduction scratch: kWarps x ncol per tile, kThreads for the
             // final column sums
             const size_t smem = ring_smem<F>(std::max<size_t>(static_cast<size_t>(kWarps) * ncol, kThreads)) + 64;
@@ -987,7 +963,7 @@ template <int F> struct UpdateLaunch {
                     double* w, double* norm, int reduction, Workspace* ws, cudaStream_t st,
                     const GateArg& gate) {
         const bool fused_norm = norm && reduction == CBGX_REDUCE_TREE;
-        if (SPLIT_DYNAMIC && (cols > 0 || fused_norm)) {
+        if (cols > 0 || fused_norm) {
             const size_t smem = ring_smem<F>(cols + kWarps) + 64;
             allow_smem(cgs_update_dyn_kernel<F>);
             const int grid = ring_grid(cgs_update_dyn_kernel<F>, B.n, smem);
@@ -1059,23 +1035,8 @@ template <int F> struct ReadLaunch {
 #ifndef FUSED_WARPS
 #define FUSED_WARPS 12
 #endif
-#ifndef FUSED_DOT_ACC4
-#define FUSED_DOT_ACC4 0
-#endif
 #ifndef FUSED_STEPS
 #define FUSED_STEPS 5
-#endif
-#ifndef FUSED_FULL_SPEC
-#define FUSED_FULL_SPEC 1
-#endif
-#ifndef FUSED_STAGE_CTR
-#define FUSED_STAGE_CTR 0  // incremental ring position: 6.04 vs 5.84 ms ortho (register allocation), off
-#endif
-#ifndef FUSED_HOIST_OFF
-#define FUSED_HOIST_OFF 1
-#endif
-#ifndef FUSED_STAGE_VOTE
-#define FUSED_STAGE_VOTE 0  // 9.04 vs 8.02 ms on the bench solve (register pressure at 72 regs)
 #endif
 constexpr int kFusedMaxSteps = FUSED_STEPS;
 constexpr int kFCtasPerSM = FUSED_CTAS_PER_SM;
@@ -1101,21 +1062,12 @@ template <int F> struct FBytes {
 #ifndef FUSED_RING_BYTES
 #define FUSED_RING_BYTES 100000
 #endif
-// Folded SpMV (see arnoldi_fused_kernel): a ring stage also carries one
-// 256-row CSR tile -- values, int32 columns, int32 row offsets -- of at most
-// kFoldEntries entries (the staged-SpMV plan of 256-row tiles).
-constexpr uint32_t kFoldRows = 192;  // two tiles in flight: consumer halves of 192 threads
-constexpr uint32_t kFoldEntries = 2048;
-constexpr uint32_t kFoldValBytes = (kFoldEntries + 2) * 8;
-constexpr uint32_t kFoldColBytes = (kFoldEntries + 4) * 4;
-constexpr uint32_t kFoldRpBytes = (kFoldRows + 1 + 4) * 4 + 12;
-constexpr uint32_t kFoldStageBytes = kFoldValBytes + kFoldColBytes + kFoldRpBytes;
 
 template <int F> struct FGeo {
     static constexpr int chunk_raw = static_cast<int>(FUSED_CHUNK_BYTES / (FBytes<F>::pay + FBytes<F>::ex));
     static constexpr int chunk = chunk_raw < 1 ? 1 : (chunk_raw > kFusedMaxSteps ? kFusedMaxSteps : chunk_raw);
     static constexpr uint32_t basis_bytes = chunk * (FBytes<F>::pay + FBytes<F>::ex) + 16;
-    static constexpr uint32_t stage_bytes = (basis_bytes > kFoldStageBytes ? basis_bytes : kFoldStageBytes) / 16 * 16 + 16;
+    static constexpr uint32_t stage_bytes = basis_bytes / 16 * 16 + 16;
     static constexpr int stages_raw = static_cast<int>((kFCtasPerSM == 1 ? 170000 : FUSED_RING_BYTES) / (stage_bytes + 16));
     static constexpr int stages = stages_raw < 2 ? 2 : stages_raw;
 };
@@ -1143,14 +1095,6 @@ struct FusedArgs {
     unsigned* gate_hist;       // previous launch's gate: 0 open (speculate), 1 closed
     double* host_slot;         // optional mapped pinned copy of the slot (read by the host)
     unsigned long long* trace; // optional: CTA 0 phase timestamps (debug)
-    // folded SpMV w = A x (fold != 0): int32 CSR, x = the previous step's v
-    int fold;
-    const int32_t* rp;
-    const int32_t* ci;
-    const double* va;
-    const double* x;
-    uint64_t nnz;
-    double* w_scratch;         // w rows written by the SpMV phase, reloaded by the owners
 };
 
 // Partial regions, one per grid reduction of a launch, so a CTA that runs
@@ -1162,7 +1106,9 @@ __device__ __forceinline__ unsigned long long global_ns() {
     asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
     return t;
 }
-#define FTRACE(i) do { if (a.trace && blockIdx.x == 0 && threadIdx.x == 0) a.trace[i] = global_ns(); } while (0)
+// phase timestamps of every CTA: trace[kTraceBase + phase * 1024 + cta]
+constexpr int kTraceBase = 32, kTracePhases = 24;
+#define FTRACE(i) do { if (a.trace && threadIdx.x == 0) a.trace[kTraceBase + (i) * 1024 + blockIdx.x] = global_ns(); } while (0)
 
 __device__ __forceinline__ void consumer_sync() {
     asm volatile("bar.sync 1, %0;" ::"n"(kFConsumers) : "memory");
@@ -1178,36 +1124,14 @@ __device__ __forceinline__ unsigned ld_acquire(const unsigned* p) {
     return v;
 }
 
-// Row shares of the fused grid. Measured on B200 (scripts/cta_buckets.py):
-// CTAs of the second half of the cooperative grid (the second CTA on each
-// SM) stream ~10% slower than the first half, and the slowest CTA sets the
-// pace of every grid all-reduce. Slot weights (integers, so the partition is
-// a fixed function of n and the grid -- deterministic):
-//   w(i) = G * 1e6 - FUSED_W2 * 1000 * G * [i >= G/2] - FUSED_WG * 1000 * i
-// (FUSED_W2: per-mille less for the second half; FUSED_WG: per-mille linear
-// decrease across the grid); slot s owns units [U C(s) / C(G), U C(s+1) / C(G)).
-#ifndef FUSED_W2
-#define FUSED_W2 0
-#endif
-#ifndef FUSED_WG
-#define FUSED_WG 0
-#endif
-__host__ __device__ __forceinline__ uint64_t fused_cum_weight(uint64_t s, uint64_t G) {
-    const uint64_t h = G / 2;
-    return s * G * 1000000ull - static_cast<uint64_t>(FUSED_W2) * 1000ull * G * (s > h ? s - h : 0) -
-           static_cast<uint64_t>(FUSED_WG) * 1000ull * (s * (s ? s - 1 : 0) / 2);
-}
+// Row shares of the fused grid: equal shares of 128-row units. (Weighted
+// shares -- fewer rows for the second CTA of an SM, which streams ~10%
+// slower -- measured 0.5-0.7% slower: the two CTAs share the SM's
+// throughput.)
 __host__ __device__ __forceinline__ void fused_unit_range(uint64_t units, uint64_t G, uint64_t slot, uint64_t& u0,
                                                           uint64_t& u1) {
-    if (FUSED_W2 == 0 && FUSED_WG == 0) {
-        u0 = units * slot / G;
-        u1 = units * (slot + 1) / G;
-        return;
-    }
-    const uint64_t tot = fused_cum_weight(G, G);
-    // units * C(s) can exceed 64 bits only for units >= 2^64 / tot (> 2^26 at G = 296)
-    u0 = static_cast<uint64_t>((static_cast<unsigned __int128>(units) * fused_cum_weight(slot, G)) / tot);
-    u1 = static_cast<uint64_t>((static_cast<unsigned __int128>(units) * fused_cum_weight(slot + 1, G)) / tot);
+    u0 = units * slot / G;
+    u1 = units * (slot + 1) / G;
 }
 
 // This CTA's rows: [r0, r1) in 128-row units, weighted over the grid.
@@ -1368,9 +1292,26 @@ __device__ __forceinline__ void fused_write(const FusedArgs& a, uint64_t r0, uin
     }
 }
 
+// Significant bits of a stored basis value (|V^T V - I| <~ 2^-p for the
+// decoded columns): FRSZ2-l keeps l - 2 magnitude bits below the block
+// maximum; f16 10, f32 22; f64 bounded by the orthogonality of the computed
+// basis, taken as 2^-40.
+template <int F>
+constexpr int kOrthBits = FmtInfo<F>::frsz ? FmtInfo<F>::L - 2 : (F == kF64 ? 40 : (F == kF32 ? 22 : 10));
+__host__ __device__ constexpr double pow2(int e) {
+    double r = 1.0;
+    for (; e > 0; --e) r *= 2.0;
+    for (; e < 0; ++e) r *= 0.5;
+    return r;
+}
+
 // One column pass over the CTA's rows: dot (partials into red[warp][j]) or
 // update (w -= h_j v_j) for columns in the given order. `lim` = number of
 // the CTA's rows; a thread's 4 rows are skipped past it (its w stays 0).
+// kFull: the CTA holds kFusedMaxSteps steps (every CTA but the last few),
+// no per-step bounds checks. Per ring stage the shared-memory step loads
+// use a per-thread stage base (StageOff), so the per-step offsets are
+// immediates.
 template <int F, bool kDot, bool kFull>
 __device__ __forceinline__ void fused_pass(uint32_t cols, uint32_t lim, uint32_t steps, uint32_t nch, unsigned char* stages,
                                            uint64_t* full, uint64_t* empty, uint32_t& it, double wv[][4],
@@ -1379,83 +1320,21 @@ __device__ __forceinline__ void fused_pass(uint32_t cols, uint32_t lim, uint32_t
     constexpr uint32_t PAY = FBytes<F>::pay, SB = fstage_bytes<F>();
     constexpr int kChunkSteps = FGeo<F>::chunk, kChunks = (kFusedMaxSteps + kChunkSteps - 1) / kChunkSteps;
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-#if FUSED_STAGE_CTR
-    // ring position tracked incrementally (no division by the stage count
-    // per stage); `it` advanced once at the end
-    uint32_t rs = it % S, rph = (it / S) & 1;
-    const uint32_t it0 = it;
-#endif
     for (uint32_t jj = 0; jj < cols; ++jj) {
         const uint32_t j = kDot ? cols - 1 - jj : jj;
         const double hj = kDot ? 0.0 : hsm[j];
         const int he = static_cast<int>(exp_field(hj));
-        double acc = 0.0, acc2 = 0.0, acc3 = 0.0, acc4 = 0.0;
+        double acc = 0.0, acc2 = 0.0;
 #pragma unroll
         for (int ch = 0; ch < kChunks; ++ch) {
             if (!kFull && ch >= static_cast<int>(nch)) break;
-#if FUSED_STAGE_CTR
-            const int stage = static_cast<int>(rs);
-            mbar_wait(full + stage, rph);
-#else
             const int stage = it % S;
             mbar_wait(full + stage, (it / S) & 1);
-#endif
             const unsigned char* pay = stages + stage * SB;
             const uint32_t* ex = reinterpret_cast<const uint32_t*>(pay + kChunkSteps * PAY);
-#if FUSED_STAGE_VOTE
-            if constexpr (FmtInfo<F>::frsz) {
-                // exponents of the chunk first, ONE warp vote for its fast path
-                Step<F> st[kChunkSteps];
-                bool ok = true;
-#pragma unroll
-                for (int s = 0; s < kChunkSteps; ++s) {
-                    const int gs = ch * kChunkSteps + s;
-                    if (gs < kFusedMaxSteps && (kFull || static_cast<uint32_t>(gs) < steps)) {
-                        st[s].e = ex[(s * kFStepRows + 4u * threadIdx.x) / 32];
-                        if constexpr (kDot) ok &= st[s].fast();
-                        else ok &= st[s].upd_ok(hj, he);
-                    }
-                }
-                if (__builtin_expect(__all_sync(0xFFFFFFFFu, ok), 1)) {
-#pragma unroll
-                    for (int s = 0; s < kChunkSteps; ++s) {
-                        const int gs = ch * kChunkSteps + s;
-                        if (gs < kFusedMaxSteps && (kFull || static_cast<uint32_t>(gs) < steps)) {
-                            step_lds_pay<F>(st[s], pay, s * kFStepRows + 4u * threadIdx.x);
-                            if constexpr (kDot) {
-#if FUSED_DOT_ACC4
-                                if ((s & 3) == 0) acc = __dadd_rn(acc, st[s].dot_fast(wv[gs]));
-                                else if ((s & 3) == 1) acc2 = __dadd_rn(acc2, st[s].dot_fast(wv[gs]));
-                                else if ((s & 3) == 2) acc3 = __dadd_rn(acc3, st[s].dot_fast(wv[gs]));
-                                else acc4 = __dadd_rn(acc4, st[s].dot_fast(wv[gs]));
-#else
-                                if (s & 1) acc2 = __dadd_rn(acc2, st[s].dot_fast(wv[gs]));
-                                else acc = __dadd_rn(acc, st[s].dot_fast(wv[gs]));
-#endif
-                            } else {
-                                st[s].update_fast(hj, he, wv[gs]);
-                            }
-                        }
-                    }
-                    __syncwarp();
-                    if (lane == 0) mbar_arrive(empty + stage);
-#if FUSED_STAGE_CTR
-                    if (++rs == S) {
-                        rs = 0;
-                        rph ^= 1;
-                    }
-#else
-                    ++it;
-#endif
-                    continue;
-                }
-            }
-#endif
-#if FUSED_HOIST_OFF
             const StageOff<F> off;
             const unsigned char* pay_t = pay + off.pay;
             const uint32_t* ex_t = ex + off.ex;
-#endif
 #pragma unroll
             for (int s = 0; s < kChunkSteps; ++s) {
                 const int gs = ch * kChunkSteps + s;
@@ -1463,21 +1342,10 @@ __device__ __forceinline__ void fused_pass(uint32_t cols, uint32_t lim, uint32_t
                 // valid FRSZ2 data of the next range and w = 0 there
                 if (gs < kFusedMaxSteps && (kFull || static_cast<uint32_t>(gs) < steps)) {
                     Step<F> st;
-#if FUSED_HOIST_OFF
                     step_lds_at<F, FBytes<F>::pay, FBytes<F>::ex / 4>(st, pay_t, ex_t, off, s);
-#else
-                    step_lds<F>(st, pay, ex, s * kFStepRows + 4u * threadIdx.x);
-#endif
                     if constexpr (kDot) {
-#if FUSED_DOT_ACC4
-                        if ((s & 3) == 0) acc = __dadd_rn(acc, st.dot(wv[gs]));
-                        else if ((s & 3) == 1) acc2 = __dadd_rn(acc2, st.dot(wv[gs]));
-                        else if ((s & 3) == 2) acc3 = __dadd_rn(acc3, st.dot(wv[gs]));
-                        else acc4 = __dadd_rn(acc4, st.dot(wv[gs]));
-#else
                         if (s & 1) acc2 = __dadd_rn(acc2, st.dot(wv[gs]));
                         else acc = __dadd_rn(acc, st.dot(wv[gs]));
-#endif
                     } else {
                         st.update(hj, he, wv[gs]);
                     }
@@ -1485,23 +1353,13 @@ __device__ __forceinline__ void fused_pass(uint32_t cols, uint32_t lim, uint32_t
             }
             __syncwarp();
             if (lane == 0) mbar_arrive(empty + stage);
-#if FUSED_STAGE_CTR
-            if (++rs == S) {
-                rs = 0;
-                rph ^= 1;
-            }
-#else
             ++it;
-#endif
         }
         if constexpr (kDot) {
-            acc = warp_sum(__dadd_rn(__dadd_rn(acc, acc2), __dadd_rn(acc3, acc4)));
+            acc = warp_sum(__dadd_rn(acc, acc2));
             if (lane == 0) red[warp * cols + j] = acc;
         }
     }
-#if FUSED_STAGE_CTR
-    it = it0 + cols * min(nch, static_cast<uint32_t>(kChunks));
-#endif
     if constexpr (!kDot) {
         // the update also touched the rows past the CTA's range: w = 0 there
 #pragma unroll
@@ -1511,17 +1369,13 @@ __device__ __forceinline__ void fused_pass(uint32_t cols, uint32_t lim, uint32_t
     }
 }
 
-// Every CTA but the last few holds kFusedMaxSteps steps: a specialisation
-// without the per-step bounds checks (FUSED_FULL_SPEC).
 template <int F, bool kDot>
 __device__ __forceinline__ void fused_pass_any(uint32_t cols, uint32_t lim, uint32_t steps, uint32_t nch,
                                                unsigned char* stages, uint64_t* full, uint64_t* empty, uint32_t& it,
                                                double wv[][4], double* red, const double* hsm) {
-#if FUSED_FULL_SPEC
     if (steps == static_cast<uint32_t>(kFusedMaxSteps))
         fused_pass<F, kDot, true>(cols, lim, steps, nch, stages, full, empty, it, wv, red, hsm);
     else
-#endif
         fused_pass<F, kDot, false>(cols, lim, steps, nch, stages, full, empty, it, wv, red, hsm);
 }
 
@@ -1546,7 +1400,7 @@ __device__ __forceinline__ void dot_partials_out(const double* red, uint32_t col
 // the gate turns out closed its coefficients are simply not used. With the
 // previous gate closed the dot2 pass waits for the gate (R1 = [hn1] only,
 // then R2'[u] in region 2).
-template <int F, bool kFold>
+template <int F>
 __global__ void __launch_bounds__(kFThreads, kFCtasPerSM) arnoldi_fused_kernel(FusedArgs a) {
     constexpr int S = FGeo<F>::stages;
     constexpr uint32_t PAY = FBytes<F>::pay, UPAY = FBytes<F>::upay, UEX = FBytes<F>::uex, SB = fstage_bytes<F>();
@@ -1590,45 +1444,6 @@ __global__ void __launch_bounds__(kFThreads, kFCtasPerSM) arnoldi_fused_kernel(F
         // ---------------- producer: [SpMV tiles], dot1 (rev), update1, [dot2 (rev), update2]
         const uint64_t policy = policy_evict_normal();
         uint32_t it = 0;
-        if constexpr (kFold) {
-            // CSR tiles of this CTA's rows; the entry ranges of 32 tiles are
-            // fetched by the whole warp at once, lane 0 issues the copies
-            const uint64_t n = a.B.n;
-            const uint32_t ntile = (lim + kFoldRows - 1) / kFoldRows;
-            const uint64_t pol_stream = policy_evict_first();
-            for (uint32_t tb = 0; tb < ntile; tb += 32) {
-                const uint32_t tj = tb + lane;
-                uint64_t mk0 = 0, mk1 = 0;
-                if (tj < ntile) {
-                    const uint64_t ra = min(n, r0 + static_cast<uint64_t>(tj) * kFoldRows);
-                    const uint64_t rb = min(n, min(r1, ra + kFoldRows));
-                    mk0 = static_cast<uint64_t>(__ldg(a.rp + ra));
-                    mk1 = static_cast<uint64_t>(__ldg(a.rp + rb));
-                }
-                for (uint32_t j = 0; j < 32 && tb + j < ntile; ++j, ++it) {
-                    const uint64_t k0 = __shfl_sync(0xFFFFFFFFu, mk0, j), k1 = __shfl_sync(0xFFFFFFFFu, mk1, j);
-                    if (lane == 0) {
-                        const uint64_t ra = min(n, r0 + static_cast<uint64_t>(tb + j) * kFoldRows);
-                        const uint64_t rb = min(n, min(r1, ra + kFoldRows));
-                        const int stage = it % S;
-                        mbar_wait(empty + stage, ((it / S) & 1) ^ 1);
-                        unsigned char* dst = stages + stage * SB;
-                        const uint64_t av = k0 / 2 * 2, ac = k0 / 4 * 4, ar = ra / 4 * 4;
-                        const uint64_t av1 = min((k1 + 1) / 2 * 2, a.nnz / 2 * 2);
-                        const uint64_t ac1 = min((k1 + 3) / 4 * 4, a.nnz / 4 * 4);
-                        const uint64_t ar1 = min((rb + 1 + 3) / 4 * 4, (n + 1) / 4 * 4);
-                        const uint32_t bv = av1 > av ? static_cast<uint32_t>((av1 - av) * 8) : 0u;
-                        const uint32_t bc = ac1 > ac ? static_cast<uint32_t>((ac1 - ac) * 4) : 0u;
-                        const uint32_t br = ar1 > ar ? static_cast<uint32_t>((ar1 - ar) * 4) : 0u;
-                        mbar_arrive_expect_tx(full + stage, bv + bc + br);
-                        if (bv) bulk_g2s(dst, a.va + av, bv, full + stage, pol_stream);
-                        if (bc) bulk_g2s(dst + kFoldValBytes, a.ci + ac, bc, full + stage, pol_stream);
-                        if (br) bulk_g2s(dst + kFoldValBytes + kFoldColBytes, a.rp + ar, br, full + stage, pol_stream);
-                    }
-                    __syncwarp();
-                }
-            }
-        }
         if (lane != 0) return;
         const uint64_t u0 = r0 / kUnitRows;
         for (int pass = 0; pass < 4; ++pass) {
@@ -1661,75 +1476,14 @@ __global__ void __launch_bounds__(kFThreads, kFCtasPerSM) arnoldi_fused_kernel(F
 
     // ---------------- consumers
     FTRACE(0);
-    if (a.trace && threadIdx.x == 0) a.trace[32 + 2048 + blockIdx.x] = global_ns();
     uint32_t it = 0;
-    double om_part = 0.0;  // this CTA's <w, w> (folded SpMV)
-    if constexpr (kFold) {
-        // w = A x for this CTA's rows (sparse.cpp:43-56 order: each row from
-        // +0.0, mul then add, entries in row order -- bit-identical), one
-        // 256-row CSR tile per ring stage, one row per thread; the rows go
-        // to w_scratch and come back to their owners below (CTA-local).
-        const uint64_t n = a.B.n;
-        const uint32_t ntile = (lim + kFoldRows - 1) / kFoldRows;
-        static_assert(kFConsumers == 2 * kFoldRows, "two consumer halves, one row per thread");
-        const uint32_t half = threadIdx.x / kFoldRows, t = threadIdx.x % kFoldRows;
-        for (uint32_t tj = 0; tj < ntile; ++tj, ++it) {
-            const int stage = it % S;
-            mbar_wait(full + stage, (it / S) & 1);
-            const uint64_t ra = min(n, r0 + static_cast<uint64_t>(tj) * kFoldRows);
-            const uint64_t rb = min(n, min(r1, ra + kFoldRows));
-            // the halves take alternate tiles (both arrive on every stage)
-            if ((tj & 1u) == half && t < rb - ra) {
-                const unsigned char* st = stages + stage * SB;
-                const double* sv = reinterpret_cast<const double*>(st);
-                const int32_t* sc = reinterpret_cast<const int32_t*>(st + kFoldValBytes);
-                const int32_t* sr = reinterpret_cast<const int32_t*>(st + kFoldValBytes + kFoldColBytes);
-                const uint64_t r = ra + t;
-                const bool rtail = rb + 1 > (n + 1) / 4 * 4;  // row offsets past the copied window
-                const uint64_t k0 = rtail ? static_cast<uint64_t>(__ldg(a.rp + ra)) : static_cast<uint64_t>(sr[0]);
-                const uint64_t ka = rtail ? static_cast<uint64_t>(__ldg(a.rp + r)) : static_cast<uint64_t>(sr[t]);
-                const uint64_t ke = rtail ? static_cast<uint64_t>(__ldg(a.rp + r + 1)) : static_cast<uint64_t>(sr[t + 1]);
-                const uint64_t av = k0 / 2 * 2, ac = k0 / 4 * 4;
-                const uint64_t av1 = a.nnz / 2 * 2, ac1 = a.nnz / 4 * 4;
-                double acc = 0.0;
-                for (uint64_t k = ka; k < ke; k += 8) {
-                    int32_t c[8];
-                    double v[8], xv[8];
-#pragma unroll
-                    for (int u = 0; u < 8; ++u) {
-                        const uint64_t kk = k + u;
-                        const bool in = kk < ke;
-                        c[u] = in ? (kk < ac1 ? sc[kk - ac] : __ldg(a.ci + kk)) : 0;
-                        v[u] = in ? (kk < av1 ? sv[kk - av] : __ldg(a.va + kk)) : 0.0;
-                    }
-#pragma unroll
-                    for (int u = 0; u < 8; ++u) xv[u] = k + u < ke ? __ldg(a.x + c[u]) : 0.0;
-#pragma unroll
-                    for (int u = 0; u < 8; ++u)
-                        if (k + u < ke) acc = __dadd_rn(acc, __dmul_rn(v[u], xv[u]));
-                }
-                a.w_scratch[r] = acc;
-                om_part = __dadd_rn(om_part, __dmul_rn(acc, acc));
-            }
-            __syncwarp();
-            if (lane == 0) mbar_arrive(empty + stage);
-        }
-        consumer_sync();  // w_scratch rows of this CTA are written
-        FTRACE(20);
-    }
     double wv[kFusedMaxSteps][4];
     const uint64_t wend = min(r1, a.B.n);
-    const double* wsrc = kFold ? a.w_scratch : a.w;
 #pragma unroll
     for (int s = 0; s < kFusedMaxSteps; ++s) {
         const uint64_t r = r0 + s * kFStepRows + 4u * threadIdx.x;
         if (s < static_cast<int>(steps)) {
-            if constexpr (kFold) {  // written in this launch: L2 loads, not the read-only path
-#pragma unroll
-                for (int k = 0; k < 4; ++k) wv[s][k] = r + k < wend ? __ldcg(wsrc + r + k) : 0.0;
-            } else {
-                load_w(wsrc, wend, r, wv[s]);
-            }
+            load_w(a.w, wend, r, wv[s]);
         } else {
             wv[s][0] = wv[s][1] = wv[s][2] = wv[s][3] = 0.0;
         }
@@ -1744,26 +1498,21 @@ __global__ void __launch_bounds__(kFThreads, kFCtasPerSM) arnoldi_fused_kernel(F
     // dot1 -> h
     fused_pass_any<F, true>(cols, lim, steps, nch, stages, full, empty, it, wv, red, hsm);
     FTRACE(2);
-    if (a.trace && threadIdx.x == 0) a.trace[32 + blockIdx.x] = global_ns();
     dot_partials_out(red, cols, P, gs);
-    if constexpr (kFold) {
-        // <w, w> of the folded SpMV rides along with h
-        const double om_cta = cta_wnorm_sum(om_part, nred);
-        if (threadIdx.x == 0) P[static_cast<uint64_t>(cols) * gs + blockIdx.x] = om_cta;
-    }
-    grid_allreduce(a.bar, seq++, P, gs, cols + (kFold ? 1u : 0u), hsm, a.trace);
-    const double omega2 = kFold ? hsm[cols] : a.slot[2];
+    grid_allreduce(a.bar, seq++, P, gs, cols, hsm, a.trace);
+    // omega^2 (from the SpMV epilogue) kept in shared memory until the gate
+    // (a register would be spilled and a global reload costs an L2 round
+    // trip on the critical path)
+    if (threadIdx.x == 0) scal[1] = a.slot[2];
     if (cta0)
         for (uint32_t j = threadIdx.x; j < cols; j += kFConsumers) {
             a.slot[3 + j] = hsm[j];
             if (a.host_slot) a.host_slot[3 + j] = hsm[j];
         }
-    if (kFold && cta0 && threadIdx.x == 0) a.slot[2] = omega2;
     FTRACE(3);
     // update1
     fused_pass_any<F, false>(cols, lim, steps, nch, stages, full, empty, it, wv, red, hsm);
     FTRACE(4);
-    if (a.trace && threadIdx.x == 0) a.trace[32 + 1024 + blockIdx.x] = global_ns();
     const double hn1_part = cta_wnorm2(wv, nred);
     double* const P1 = P + region;
     if (spec) {
@@ -1777,6 +1526,7 @@ __global__ void __launch_bounds__(kFThreads, kFCtasPerSM) arnoldi_fused_kernel(F
     else grid_allreduce(a.bar, seq++, P1 + static_cast<uint64_t>(cols) * gs, gs, 1, hsm + cols);
     FTRACE(6);
     const double hn1 = hsm[cols];
+    const double omega2 = scal[1];  // written before R1's barriers
     // gmres.cpp:51 on the device (same IEEE ops as the host)
     const bool gate = sqrt(hn1) < a.eta * sqrt(omega2);
     if (threadIdx.x == 0) {
@@ -1807,11 +1557,30 @@ __global__ void __launch_bounds__(kFThreads, kFCtasPerSM) arnoldi_fused_kernel(F
         // update2 (u in hsm)
         fused_pass_any<F, false>(cols, lim, steps, nch, stages, full, empty, it, wv, red, hsm);
         FTRACE(8);
-        const double p = cta_wnorm2(wv, nred);
-        double* const P3 = P + 3 * region;
-        if (threadIdx.x == 0) P3[blockIdx.x] = p;
-        grid_allreduce(a.bar, seq++, P3, gs, 1, scal, a.trace);
-        hn2 = scal[0];
+        // h_next^2 of the second pass (gmres.cpp:66): ||w1 - V u||^2 =
+        // hn1 - 2 u.(V^T w1) + u^T (V^T V) u = hn1 - |u|^2 + u^T E u with
+        // u = V^T w1 and V^T V = I + E, |E| <~ 2^-p for a basis stored with
+        // p significant bits (kOrthBits). When |u|^2 <= 2^(p-52) hn1 the
+        // Pythagorean value hn1 - |u|^2 is within 2^-52 hn1 of the explicit
+        // norm -- rounding level, below the tree sum's reduction-order noise
+        // -- and the grid all-reduce of ||w2||^2 is skipped. That is the
+        // usual case for FRSZ2-32/f32/f64 (u is the rounding residue of the
+        // first pass); otherwise (and mostly for FRSZ2-16/21, f16) the
+        // explicit norm is reduced. Every CTA holds the same u, so |u|^2
+        // (xor butterfly: identical in every lane) and the branch are uniform.
+        double uu = 0.0;
+        for (uint32_t j = lane; j < cols; j += 32) uu = __dadd_rn(uu, __dmul_rn(hsm[j], hsm[j]));
+        uu = warp_sum(uu);
+        constexpr double kPyth = pow2(kOrthBits<F> - 52);
+        if (uu <= kPyth * hn1) {
+            hn2 = __dsub_rn(hn1, uu);
+        } else {
+            const double p = cta_wnorm2(wv, nred);
+            double* const P3 = P + 3 * region;
+            if (threadIdx.x == 0) P3[blockIdx.x] = p;
+            grid_allreduce(a.bar, seq++, P3, gs, 1, scal, a.trace);
+            hn2 = scal[0];
+        }
         if (cta0 && threadIdx.x == 0) {
             a.slot[1] = hn2;
             if (a.host_slot) a.host_slot[1] = hn2;
@@ -1840,8 +1609,8 @@ unsigned long long* fused_trace_buffer() {
     }();
     if (!on) return nullptr;
     if (!g_trace) {
-        CBGX_CUDA(cudaMalloc(&g_trace, (32 + 3 * 1024) * sizeof(unsigned long long)));
-        CBGX_CUDA(cudaMemset(g_trace, 0, (32 + 3 * 1024) * sizeof(unsigned long long)));
+        CBGX_CUDA(cudaMalloc(&g_trace, (kTraceBase + kTracePhases * 1024) * sizeof(unsigned long long)));
+        CBGX_CUDA(cudaMemset(g_trace, 0, (kTraceBase + kTracePhases * 1024) * sizeof(unsigned long long)));
     }
     return g_trace;
 }
@@ -1870,15 +1639,9 @@ int fused_grid(uint64_t n, uint32_t max_cols) {
             per_sm = it->second;
         } else {
             // the attribute is per kernel, not per size: set the maximum once
-            // the attribute is per kernel: both variants
-            CBGX_CUDA(cudaFuncSetAttribute(arnoldi_fused_kernel<F, false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+            CBGX_CUDA(cudaFuncSetAttribute(arnoldi_fused_kernel<F>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                            227 * 1024));
-            CBGX_CUDA(cudaFuncSetAttribute(arnoldi_fused_kernel<F, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                           227 * 1024));
-            int p2 = 0;
-            CBGX_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, arnoldi_fused_kernel<F, false>, kFThreads, smem));
-            CBGX_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&p2, arnoldi_fused_kernel<F, true>, kFThreads, smem));
-            per_sm = std::min(per_sm, p2);
+            CBGX_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, arnoldi_fused_kernel<F>, kFThreads, smem));
             int coop = 0;
             CBGX_CUDA(cudaDeviceGetAttribute(&coop, cudaDevAttrCooperativeLaunch, current_device()));
             if (!coop) per_sm = 0;
@@ -1901,7 +1664,7 @@ int fused_grid(uint64_t n, uint32_t max_cols) {
 template <int F> struct FusedLaunch {
     static void run(const cbgx_basis& V, uint32_t cols, const double* w, double* v_out, double* slot,
                     uint32_t u_off, double eta, uint32_t max_cols, double* host_slot, bool pdl,
-                    const FoldArg& fold, Workspace* ws, cudaStream_t st, bool* done) {
+                    Workspace* ws, cudaStream_t st, bool* done) {
         // geometry fixed by the solver's capacity so it never changes mid-solve
         const int grid = fused_grid<F>(V.n, max_cols);
         *done = false;
@@ -1931,13 +1694,6 @@ template <int F> struct FusedLaunch {
         a.trace = fused_trace_buffer();
         a.host_slot = host_slot;
         a.rot = g_fused_rot;
-        a.fold = fold.A != nullptr;
-        a.rp = fold.A ? static_cast<const int32_t*>(fold.A->d_row_ptr) : nullptr;
-        a.ci = fold.A ? fold.A->d_col_idx : nullptr;
-        a.va = fold.A ? fold.A->d_values : nullptr;
-        a.nnz = fold.A ? fold.A->nnz : 0;
-        a.x = fold.x;
-        a.w_scratch = fold.w;
         cudaLaunchConfig_t lc = {};
         lc.gridDim = dim3(grid);
         lc.blockDim = dim3(kFThreads);
@@ -1951,8 +1707,7 @@ template <int F> struct FusedLaunch {
         lc.attrs = at;
         lc.numAttrs = pdl ? 2 : 1;
         note_launch();
-        if (a.fold) CBGX_CUDA(cudaLaunchKernelEx(&lc, arnoldi_fused_kernel<F, true>, a));
-        else CBGX_CUDA(cudaLaunchKernelEx(&lc, arnoldi_fused_kernel<F, false>, a));
+        CBGX_CUDA(cudaLaunchKernelEx(&lc, arnoldi_fused_kernel<F>, a));
         ws->fused_launches = seq + 1;
         *done = true;
     }
@@ -2004,13 +1759,11 @@ bool fused_eligible(const cbgx_basis& V, uint64_t max_cols) {
 
 bool launch_arnoldi_fused(const cbgx_basis& V, uint32_t cols, const double* w, double* v_out, double* slot,
                           uint32_t u_off, double eta, uint32_t max_cols, double* host_slot, bool pdl,
-                          const FoldArg& fold, Workspace* ws, cudaStream_t st) {
+                          Workspace* ws, cudaStream_t st) {
     if (cols + 1 > V.capacity) throw Error(CBGX_ERANGE, "basis: cannot write column");
-    if (fold.A && (fold.A->row_ptr_bits != 32 || fold.A->n_rows != V.n))
-        throw Error(CBGX_EINVAL, "fused: folded SpMV needs int32 row offsets and n rows");
     bool done = false;
-    dispatch_fmt<FusedLaunch>(fmt_of(V), V, cols, w, v_out, slot, u_off, eta, max_cols, host_slot, pdl, fold, ws,
-                              st, &done);
+    dispatch_fmt<FusedLaunch>(fmt_of(V), V, cols, w, v_out, slot, u_off, eta, max_cols, host_slot, pdl, ws, st,
+                              &done);
     CBGX_CUDA(cudaGetLastError());
     return done;
 }
@@ -2118,8 +1871,7 @@ int cbgx_arnoldi_fused_step(const cbgx_basis* V, uint32_t cols, uint32_t max_col
         const unsigned hist = speculate ? 0u : 1u;
         CBGX_CUDA(cudaMemcpyAsync(c + Workspace::kFusedGate, &hist, sizeof(unsigned), cudaMemcpyHostToDevice, st));
         const uint32_t u_off = 3 + max_cols + 1;
-        if (!launch_arnoldi_fused(*V, cols, d_w, d_v_out, d_slot, u_off, eta, max_cols, nullptr, false, FoldArg{}, w,
-                                  st))
+        if (!launch_arnoldi_fused(*V, cols, d_w, d_v_out, d_slot, u_off, eta, max_cols, nullptr, false, w, st))
             throw Error(CBGX_EINVAL, "fused: not eligible for this basis (n, capacity, format or device)");
         CBGX_CUDA(cudaStreamSynchronize(st));  // `hist` is a host stack value
     });
@@ -2132,7 +1884,7 @@ int cbgx_debug_fused_rotation(uint32_t rot) {
 int cbgx_debug_fused_trace(uint64_t* out, int count) {
     return guard([&] {
         if (!g_trace) throw Error(CBGX_EINVAL, "trace: set CBGX_TRACE_FUSED=1 before the first fused launch");
-        CBGX_CUDA(cudaMemcpy(out, g_trace, std::min(count, 32 + 3 * 1024) * sizeof(uint64_t), cudaMemcpyDeviceToHost));
+        CBGX_CUDA(cudaMemcpy(out, g_trace, std::min(count, kTraceBase + kTracePhases * 1024) * sizeof(uint64_t), cudaMemcpyDeviceToHost));
     });
 }
 

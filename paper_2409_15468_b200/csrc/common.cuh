@@ -165,15 +165,8 @@ __device__ __forceinline__ void store4(double* p, const double v[4], bool stream
 // instruction (I2F.F64.U32) issues on the XU pipe, 16 lanes/clk/SM, which
 // the FRSZ2 decode saturated (ncu: XU pipe 74% in the fused CGS kernel);
 // DADD runs at the FP64 rate.
-#ifndef FRSZ_CONV_I2F
-#define FRSZ_CONV_I2F 0
-#endif
 __device__ __forceinline__ double u32_to_f64(uint32_t m) {
-#if FRSZ_CONV_I2F
-    return __uint2double_rn(m);  // XU pipe (A/B builds)
-#else
     return __dsub_rn(__hiloint2double(0x43300000, static_cast<int>(m)), 0x1p52);
-#endif
 }
 
 // Per-block decode context for the fixed-rate formats (L <= 32).
@@ -245,19 +238,6 @@ struct ScaleArg {
 __device__ __forceinline__ double warp_sum(double v) {
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1) v = __dadd_rn(v, __shfl_xor_sync(0xFFFFFFFFu, v, o));
-    return v;
-}
-
-// Two warp sums in one butterfly: the first level exchanges a for b between
-// the half-warps, then each half reduces one of them. Returns a's sum in lane
-// 0 and b's in lane 16 -- bit-identical to warp_sum (a butterfly's additions
-// are the same pairs, and x + y == y + x).
-__device__ __forceinline__ double warp_sum2(double a, double b) {
-    const bool hi = (threadIdx.x & 16) != 0;
-    double v = hi ? b : a;
-    v = __dadd_rn(v, __shfl_xor_sync(0xFFFFFFFFu, hi ? a : b, 16));
-#pragma unroll
-    for (int o = 8; o > 0; o >>= 1) v = __dadd_rn(v, __shfl_xor_sync(0xFFFFFFFFu, v, o));
     return v;
 }
 

@@ -136,18 +136,9 @@ void launch_cgs_update(const cbgx_basis& V, uint64_t first, uint32_t cols, const
 bool fused_eligible(const cbgx_basis& V, uint64_t max_cols);
 // host_slot: mapped pinned copy of the step slot written by the kernel (no
 // D2H copy in the stream); pdl: programmatic dependent launch.
-// fold.A != nullptr: the kernel computes w = A x itself (SpMV folded into the
-// step, 256-row CSR tiles through the same ring; int32 row offsets, every
-// 256-row tile within kFoldEntries entries) and ignores `w`; omega^2 is
-// then produced by the kernel (slot[2]).
-struct FoldArg {
-    const cbgx_csr* A = nullptr;
-    const double* x = nullptr;  // SpMV input (n rows)
-    double* w = nullptr;        // n-row scratch
-};
 bool launch_arnoldi_fused(const cbgx_basis& V, uint32_t cols, const double* w, double* v_out, double* slot,
                           uint32_t u_off, double eta, uint32_t max_cols, double* host_slot, bool pdl,
-                          const FoldArg& fold, Workspace* ws, cudaStream_t st);
+                          Workspace* ws, cudaStream_t st);
 void launch_basis_write(const cbgx_basis& V, uint64_t j, const double* x, const ScaleArg& scale,
                         double* v_out, uint64_t* bad, cudaStream_t st);
 void launch_basis_read(const cbgx_basis& V, uint64_t j, uint64_t first, uint64_t count, double* out,

@@ -314,14 +314,6 @@ void Solver::solve(const double* d_b, const double* d_x0, double* d_x, cbgx_hist
             fused_state_ = (!multi && !halo_ && red == CBGX_REDUCE_TREE && fused_eligible(V_, m)) ? 1 : 2;
         }
         const bool use_fused = fused_state_ == 1 && !(cfg_.flags & CBGX_SOLVER_NO_FUSION);
-        // Optional: SpMV folded into the fused step (CSR tiles through the
-        // same ring, w never leaves the CTA) when its tiles fit a ring stage
-        // and row offsets are int32. Measured on B200 (128^3): 8.48 ms vs
-        // 7.95 ms for the separate staged SpMV + programmatic dependent
-        // launch -- the standalone kernel keeps more rows in flight -- so it
-        // is opt-in (CBGX_SOLVER_FOLD). 256-row tiles within 2048 entries
-        // imply the kernel's 192-row ones.
-        const bool fold = use_fused && tile_rows_ == 256 && A_.row_ptr_bits == 32 && (cfg_.flags & CBGX_SOLVER_FOLD);
         // One Arnoldi step on the device (gmres.cpp:210-234 minus the host
         // Givens): spmv, CGS pass, gated second pass, scaled write of the
         // next column, and one D2H of the step's slot. `used` columns are in
@@ -343,29 +335,19 @@ void Solver::solve(const double* d_b, const double* d_x0, double* d_x, cbgx_hist
             // programmatic dependent launches (each starts while the previous
             // kernel drains) unless phase timing puts events between them.
             const bool pdl = use_fused && !timer.on;
-            if (!fold) {
-                timer.begin(CBGX_PHASE_SPMV);
-                spmv(d_v_, nullptr, d_w_, sl + kOmega, st, pdl);  // w = A v, omega^2
-                timer.end();
-                count(CBGX_PHASE_SPMV, spmv_bytes);
-            }
+            timer.begin(CBGX_PHASE_SPMV);
+            spmv(d_v_, nullptr, d_w_, sl + kOmega, st, pdl);  // w = A v, omega^2
+            timer.end();
+            count(CBGX_PHASE_SPMV, spmv_bytes);
             if (use_fused) {
                 // one cooperative launch: dot, update, gated second pass and
                 // the scaled write of column used+1, w register-resident
                 timer.begin(CBGX_PHASE_ORTHO);
-                FoldArg fa;
-                if (fold) {
-                    fa.A = &A_;
-                    fa.x = d_v_;
-                    fa.w = d_w_;
-                }
                 const bool ok = launch_arnoldi_fused(V_, cols, d_w_, d_v_, sl, static_cast<uint32_t>(kU(m)), cfg_.eta,
-                                                     static_cast<uint32_t>(m), d_hpinned_ + p * slot, pdl, fa, &ws_,
-                                                     st);
+                                                     static_cast<uint32_t>(m), d_hpinned_ + p * slot, pdl, &ws_, st);
                 timer.end();
                 if (!ok) throw Error(CBGX_EINTERNAL, "fused orthogonalisation became ineligible");
                 count(CBGX_PHASE_ORTHO, 2.0 * cols * bpv * n + 8.0 * n + 8.0 * n + bpv * n);
-                if (fold) count(CBGX_PHASE_SPMV, spmv_bytes, 0);  // folded into the same launch
             } else {
                 timer.begin(CBGX_PHASE_DOT);
                 launch_cgs_dot(V_, 0, cols, d_w_, 0, red, sl + kH, &ws_, st, GateArg{}, !multi);  // h = V^T w

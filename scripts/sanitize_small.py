@@ -1,6 +1,6 @@
 """Small end-to-end exercise of every kernel family for compute-sanitizer:
 codec (3 fast formats + generic), basis write/read, split CGS, fused
-orthogonalisation (+ folded SpMV variant), staged / plain / SELL /
+orthogonalisation, staged / plain / SELL /
 dictionary SpMV (ELL4 and ragged SELL layouts, build + apply), read sweep,
 host drop-in solve."""
 import sys
@@ -39,11 +39,11 @@ for kind, nx in ((0, 20), (2, 14), (1, 18)):
     D.spmv(x, b=x)
     b = cbg.spmv(A, torch.from_numpy(cbg.sin_problem_host(n)).cuda())
     for fmt in ("frsz2-32", "f64"):
-        for fold, dic in ((False, True), (False, False), (True, False)):
-            S = cbg.Solver(A, cbg.GmresConfig(restart=20, storage_format=cbg.StorageFormat.parse(fmt), fold=fold,
+        for dic in (True, False):
+            S = cbg.Solver(A, cbg.GmresConfig(restart=20, storage_format=cbg.StorageFormat.parse(fmt), 
                                               dict_spmv=dic, max_total_iterations=60))
             r = S.solve(b)
-            print(kind, fmt, fold, r.total_iterations, r.final_rrn, flush=True)
+            print(kind, fmt, dic, r.total_iterations, r.final_rrn, flush=True)
     rp = A.row_ptr.cpu().numpy().astype(np.uint64)
     ci = A.col_idx.cpu().numpy().astype(np.uint64)
     va = A.values.cpu().numpy()

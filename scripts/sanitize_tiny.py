@@ -14,9 +14,8 @@ A = cbg.stencil(0, 12)
 n = 12 ** 3
 b = cbg.spmv(A, torch.from_numpy(cbg.sin_problem_host(n)).cuda())
 cbg.spmv_staged(A, b, cbg.spmv_plan(A), want_norm=True)
-for fold in (False, True):
-    S = cbg.Solver(A, cbg.GmresConfig(restart=8, storage_format=cbg.StorageFormat.parse(sys.argv[1] if len(sys.argv) > 1 else "frsz2-21"), fold=fold,
-                                      max_total_iterations=10))
-    print(fold, S.solve(b).total_iterations, flush=True)
+S = cbg.Solver(A, cbg.GmresConfig(restart=8, storage_format=cbg.StorageFormat.parse(sys.argv[1] if len(sys.argv) > 1 else "frsz2-21"),
+                                  max_total_iterations=10))
+print(S.solve(b).total_iterations, flush=True)
 torch.cuda.synchronize()
 print("tiny done")
