@@ -438,12 +438,19 @@ void Solver::solve(const double* d_b, const double* d_x0, double* d_x, cbgx_hist
             bool cycle_done = false;
             // Steps that can run in this cycle (restart and iteration cap).
             const uint64_t max_steps = std::min<uint64_t>(m, cfg_.max_total_iterations - iter);
-            enqueue_step(0, 0);
-            uint64_t enqueued = 1;
+            uint64_t enqueued = 0;
+            double rrn_prev = 0.0, rrn_last = 0.0;  // implicit RRN after steps used-2, used-1
             while (!cycle_done) {
                 // Look one step ahead: the device works on step used+1 while
-                // the host runs Givens on step `used`.
-                if (enqueued < max_steps) {
+                // the host runs Givens on step `used` -- unless step `used`
+                // is predicted to end the cycle by convergence (the last
+                // residual ratio carried one step: rrn_last^2 / rrn_prev <=
+                // 4 target), where the lookahead step would be wasted work
+                // (the cycle's largest Arnoldi step). A wrong prediction only
+                // exposes the host's Givens latency for that step.
+                const bool near = used >= 2 && rrn_last * (rrn_last / rrn_prev) <= 4.0 * cfg_.target_rrn;
+                const uint64_t want = used + (near ? 1 : 2);
+                while (enqueued < max_steps && enqueued < want) {
                     enqueue_step(enqueued, static_cast<int>(enqueued & 1));
                     ++enqueued;
                 }
@@ -482,6 +489,8 @@ void Solver::solve(const double* d_b, const double* d_x0, double* d_x, cbgx_hist
                 lsq.add_column(hcol.data(), used + 2, &estimate);
                 ++used;
                 const double implicit_rrn = estimate / norm_b;
+                rrn_prev = rrn_last;
+                rrn_last = implicit_rrn;
                 cycle_done = breakdown || implicit_rrn <= cfg_.target_rrn || used == m ||
                              iter >= cfg_.max_total_iterations;
                 if (!cycle_done) push(iter, implicit_rrn, false);
