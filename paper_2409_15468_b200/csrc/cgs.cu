@@ -494,6 +494,19 @@ __device__ __forceinline__ unsigned ld_acquire_u32(const unsigned* p) {
     asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
     return v;
 }
+// Poll with relaxed loads and acquire once the target is seen: an acquire
+// load at gpu scope invalidates the SM's L1 (CCTL.IVALL) on every spin,
+// under the co-resident CTA's feet.
+__device__ __forceinline__ unsigned ld_relaxed_u32(const unsigned* p) {
+    unsigned v;
+    asm volatile("ld.relaxed.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+    return v;
+}
+__device__ __forceinline__ void wait_count(const unsigned* p, unsigned target) {
+    while (ld_relaxed_u32(p) < target) {
+    }
+    (void)ld_acquire_u32(p);
+}
 
 __device__ __forceinline__ void split_consumer_sync() {
     asm volatile("bar.sync 1, %0;" ::"n"(kConsumers) : "memory");
@@ -759,8 +772,7 @@ cgs_dot_dyn_kernel(BasisView B, uint64_t first, uint32_t cols, const double* __r
     if (threadIdx.x == 0) {
         __threadfence();
         atomicAdd(arrive, 1u);
-        while (ld_acquire_u32(arrive) < gridDim.x) {
-        }
+        wait_count(arrive, gridDim.x);
     }
     __syncthreads();
     // columns k = blockIdx.x, blockIdx.x + gridDim.x, ...: every thread sums
@@ -1108,7 +1120,16 @@ __device__ __forceinline__ unsigned long long global_ns() {
 }
 // phase timestamps of every CTA: trace[kTraceBase + phase * 1024 + cta]
 constexpr int kTraceBase = 32, kTracePhases = 24;
+// Compiled in only for diagnostic builds (CBGX_NVFLAGS_EXTRA=-DCBGX_FUSED_TRACE=1,
+// scripts/fused_phases.py): the timer reads are not free.
+#ifndef CBGX_FUSED_TRACE
+#define CBGX_FUSED_TRACE 0
+#endif
+#if CBGX_FUSED_TRACE
 #define FTRACE(i) do { if (a.trace && threadIdx.x == 0) a.trace[kTraceBase + (i) * 1024 + blockIdx.x] = global_ns(); } while (0)
+#else
+#define FTRACE(i) do { } while (0)
+#endif
 
 __device__ __forceinline__ void consumer_sync() {
     asm volatile("bar.sync 1, %0;" ::"n"(kFConsumers) : "memory");
@@ -1118,11 +1139,6 @@ __device__ __forceinline__ void red_release_add(unsigned* p, unsigned v) {
     asm volatile("red.release.gpu.global.add.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
 }
 
-__device__ __forceinline__ unsigned ld_acquire(const unsigned* p) {
-    unsigned v;
-    asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
-    return v;
-}
 
 // Row shares of the fused grid: equal shares of 128-row units. (Weighted
 // shares -- fewer rows for the second CTA of an SM, which streams ~10%
@@ -1158,12 +1174,10 @@ __device__ __forceinline__ void grid_allreduce(unsigned* bar, unsigned seq, cons
                                                unsigned long long* trace = nullptr) {
     consumer_sync();
     if (threadIdx.x == 0) {
-        if (trace && blockIdx.x == 0) trace[11 + 2 * seq] = global_ns();
+        if (CBGX_FUSED_TRACE && trace && blockIdx.x == 0) trace[11 + 2 * seq] = global_ns();
         red_release_add(bar, 1u);
-        const unsigned target = (seq + 1) * gridDim.x;
-        while (ld_acquire(bar) < target) {
-        }
-        if (trace && blockIdx.x == 0) trace[12 + 2 * seq] = global_ns();
+        wait_count(bar, (seq + 1) * gridDim.x);
+        if (CBGX_FUSED_TRACE && trace && blockIdx.x == 0) trace[12 + 2 * seq] = global_ns();
     }
     consumer_sync();
     uint32_t R = 32;
@@ -1607,7 +1621,7 @@ unsigned long long* fused_trace_buffer() {
         const char* e = getenv("CBGX_TRACE_FUSED");
         return e && e[0] == '1';
     }();
-    if (!on) return nullptr;
+    if (!on || !CBGX_FUSED_TRACE) return nullptr;
     if (!g_trace) {
         CBGX_CUDA(cudaMalloc(&g_trace, (kTraceBase + kTracePhases * 1024) * sizeof(unsigned long long)));
         CBGX_CUDA(cudaMemset(g_trace, 0, (kTraceBase + kTracePhases * 1024) * sizeof(unsigned long long)));
@@ -1883,7 +1897,7 @@ int cbgx_debug_fused_rotation(uint32_t rot) {
 
 int cbgx_debug_fused_trace(uint64_t* out, int count) {
     return guard([&] {
-        if (!g_trace) throw Error(CBGX_EINVAL, "trace: set CBGX_TRACE_FUSED=1 before the first fused launch");
+        if (!g_trace) throw Error(CBGX_EINVAL, "trace: build with CBGX_NVFLAGS_EXTRA=-DCBGX_FUSED_TRACE=1 and set CBGX_TRACE_FUSED=1 before the first fused launch");
         CBGX_CUDA(cudaMemcpy(out, g_trace, std::min(count, kTraceBase + kTracePhases * 1024) * sizeof(uint64_t), cudaMemcpyDeviceToHost));
     });
 }

@@ -2,7 +2,9 @@
 every CTA): where the launch time goes -- column passes vs waiting at the
 grid all-reduces -- and how the pass times spread over the CTAs.
 
+    CBGX_NVFLAGS_EXTRA=-DCBGX_FUSED_TRACE=1 python -c "from paper_2409_15468_b200 import build as b; b.build(force=True)"
     python scripts/fused_phases.py [edge] [fmt] [its,...]
+(the trace points are compiled out of production builds)
 """
 import os
 import sys
