@@ -119,6 +119,48 @@ class ClockSampler:
                 "sm_max_mhz": self.max_mhz, "reasons": sorted(self.reasons), "samples": len(self.samples)}
 
 
+def cpu_model():
+    try:
+        with open("/proc/cpuinfo") as f:
+            for line in f:
+                if line.startswith("model name"):
+                    return line.split(":", 1)[1].strip()
+    except OSError:
+        pass
+    return "unknown"
+
+
+def read_peak_gbs(torch):
+    """Measured read-only streaming bandwidth (torch sum over 4 GiB of fp64,
+    best of 5, CUDA events): the second roofline denominator BASELINE.md asks
+    for beside the copy-based MEASURED_PEAKS.json figure."""
+    x = torch.ones(1 << 29, dtype=torch.float64, device="cuda")
+    best = None
+    for _ in range(6):
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record()
+        x.sum()
+        e1.record()
+        torch.cuda.synchronize()
+        t = e0.elapsed_time(e1)
+        best = t if best is None else min(best, t)
+    del x
+    torch.cuda.empty_cache()
+    return round((8 << 29) / best / 1e6, 1)
+
+
+def shared_config(workload, fmt, n, nnz, ours, world=1, l2="", spmv=""):
+    """The config dict both arms print (same keys; values describe each arm)."""
+    return {
+        "workload": f"CB-GMRES(100) {fmt} basis, {workload}: n={n}, nnz={nnz}",
+        "format": fmt, "restart": 100, "target_rrn": 1e-10, "eta": 0.70710678118654752, "x0": "zeros",
+        "reduction": "tree (deterministic, fixed shape)" if ours else "sequential (the reference's order)",
+        "l2": l2, "spmv": spmv,
+        "parallelism": (f"row-partition x{world}" if world > 1 else "single GPU") if ours
+        else "single host thread (the reference has no threading)",
+    }
+
+
 def dist_env():
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
@@ -257,6 +299,19 @@ def run_ours(args):
         del s64
         torch.cuda.empty_cache()
 
+    # ---- the same solve with the general CSR SpMV path (no dictionary copy):
+    # what a matrix outside the dictionary pattern (> 255 distinct values or
+    # column offsets, e.g. SuiteSparse systems) gets
+    csr_path = None
+    if world == 1 and not args.no_fp64:
+        sc = cbg.Solver(A, cbg.GmresConfig(storage_format=cbg.StorageFormat.parse(fmt), dict_spmv=False))
+        ms_csr, r_csr, _, _ = timed_solves(sc, max(1, args.steps // 2), 1)
+        csr_path = {"ms_per_solve": round(ms_csr, 4), "iterations": r_csr[-1].total_iterations,
+                    "final_rrn": r_csr[-1].final_rrn,
+                    "spmv": "staged (bulk-copy) CSR kernel, 12 B per entry"}
+        del sc
+        torch.cuda.empty_cache()
+
     # ---- end to end through the public API with host buffers
     e2e = None
     if not args.no_e2e:
@@ -322,6 +377,7 @@ def run_ours(args):
         cpu = cpu_baseline(kind, nx, pe, fmt)
 
     clocks = sampler.summary()
+    read_peak = read_peak_gbs(torch) if rank == 0 else None
     if rank == 0:
         bpv = FMT_BYTES[fmt]
         line = {
@@ -337,25 +393,22 @@ def run_ours(args):
             "vs_baseline": None,
             "dtype": "f64",
             "data": "synthetic: device-generated 3-D stencil, generate_problem sin RHS (glibc sin, sequential norm)",
-            "config": {
-                "workload": f"CB-GMRES(100) {fmt} basis, {args.workload}: n={n}, nnz={nnz if world == 1 else 'partitioned'}",
-                "format": fmt, "restart": 100, "target_rrn": 1e-10, "eta": 0.70710678118654752,
-                "x0": "zeros", "reduction": "tree (deterministic, fixed shape)",
-                "l2": "inputs larger than L2: per solve the basis grows to %.0f MB (up to %.0f MB at m=100) "
-                      "plus the matrix (%s) vs 126 MB L2; no explicit flush"
-                      % (last.total_iterations * bpv * rows / 1e6, 101 * bpv * rows / 1e6,
-                         "2-byte dictionary codes, ~%.0f MB" % (2 * 4 * -(-nnz // (4 * rows)) * rows / 1e6) if world == 1
-                         else "CSR %.0f MB" % ((nnz * 12 + 4 * (rows + 1)) / 1e6)),
-                "spmv": ("dictionary-coded ELL4 copy of the CSR (<=255 distinct values and column offsets; "
-                         "bit-identical to the CSR SpMV), built at setup" if world == 1
-                         else "CSR with halo exchange (row partition)"),
-                "parallelism": f"row-partition x{world}" if world > 1 else "single GPU",
-            },
+            "config": shared_config(
+                args.workload, fmt, n, nnz if world == 1 else "partitioned", True, world,
+                l2="inputs larger than L2: per solve the basis grows to %.0f MB (up to %.0f MB at m=100) "
+                   "plus the matrix (%s) vs 126 MB L2; no explicit flush"
+                   % (last.total_iterations * bpv * rows / 1e6, 101 * bpv * rows / 1e6,
+                      "2-byte dictionary codes, ~%.0f MB" % (2 * 4 * -(-nnz // (4 * rows)) * rows / 1e6) if world == 1
+                      else "CSR %.0f MB" % ((nnz * 12 + 4 * (rows + 1)) / 1e6)),
+                spmv=("dictionary-coded ELL4 copy of the CSR (<=255 distinct values and column offsets; "
+                      "bit-identical to the CSR SpMV), built at setup" if world == 1
+                      else "CSR with halo exchange (row partition)")),
             "iterations": last.total_iterations,
             "restarts": last.restarts,
             "final_rrn": last.final_rrn,
             "converged": last.converged,
             "fp64_basis": ref64,
+            "csr_spmv_path": csr_path,
             "phase_ms_per_solve": {p: round(v, 4) for p, v in ph_ms.items() if v},
             "ms_per_solve_phase_timed": round(ms_phased, 4),
             "phase_gbs": {p: round(ph_bytes[p] / (ph_ms[p] * 1e-3) / 1e9, 1) for p in ph_ms if ph_ms[p] > 0},
@@ -367,6 +420,9 @@ def run_ours(args):
                 "peak_source": peak_kind,
                 "unit": "GB/s",
                 "frac": round(achieved / peak, 4) if achieved else None,
+                "frac_datasheet_8000": round(achieved / 8000.0, 4) if achieved else None,
+                "read_peak_gbs": read_peak,
+                "frac_read_peak": round(achieved / read_peak, 4) if achieved and read_peak else None,
                 "traffic": traffic_for(kernel_name)[0],
                 "traffic_source": "ncu dram__bytes_read.sum + dram__bytes_write.sum per launch, averaged over one "
                                   "solve's launches of this kernel (%s); compare with algorithmic_bytes_per_launch"
@@ -470,10 +526,31 @@ def cpu_baseline(kind, nx, pe, fmt, budget_s=60.0):
         if time.perf_counter() - t0 > budget_s / 2 or solves >= 1:
             break
     dt = (time.perf_counter() - t0) / solves
-    return {"value": round(dt * 1e3, 1), "unit": "ms", "cores": 1, "kind": kindname,
-            "sample": f"{solves} full gmres_solve(s) of the same workload ({its} iterations), "
-                      f"single thread (the reference has no threading), {os.cpu_count()} host cores present",
-            "iterations": its}
+    out = {"value": round(dt * 1e3, 1), "unit": "ms", "cores": 1, "kind": kindname,
+           "sample": f"{solves} full gmres_solve(s) of the same workload ({its} iterations), "
+                     f"single thread (the reference has no threading), 1 thread of {os.cpu_count()} cores, "
+                     f"{cpu_model()}; AVX2 kernel table (CBG_KERNELS unset)",
+           "cpu_model": cpu_model(), "host_cores": os.cpu_count(), "iterations": its}
+    if kindname == "reference":
+        out["scalar_kernels_ms"] = reference_scalar_ms(kind, nx, pe, fmt)
+    return out
+
+
+def reference_scalar_ms(kind, nx, pe, fmt):
+    """The same reference solve once with CBG_KERNELS=scalar (kernels.cpp:22-36
+    selects the table once per process, so it runs in a child process)."""
+    import subprocess
+    code = ("import sys,time,numpy as np; sys.path.insert(0, %r); from oracle import pyoracle as po; "
+            "P=po.Port(); R=po.Ref(); rp,ci,va=P.stencil(%d,%d,pe=%r); n=rp.size-1; b=np.zeros(n); xs=np.zeros(n); "
+            "R.lib.ref_generate_problem(n,rp,ci,va,b,xs); t=time.perf_counter(); "
+            "R.gmres(rp,ci,va,b,fmt=%r,restart=100,target=1e-10); print((time.perf_counter()-t)*1e3)"
+            % (ROOT, kind, nx, pe, fmt))
+    try:
+        r = subprocess.run([sys.executable, "-c", code], env=dict(os.environ, CBG_KERNELS="scalar"),
+                           capture_output=True, text=True, timeout=300)
+        return round(float(r.stdout.strip().splitlines()[-1]), 1)
+    except Exception:  # noqa: BLE001
+        return None
 
 
 # ---------------------------------------------------------- reference arm
@@ -516,17 +593,20 @@ def run_reference(args):
     ms = statistics.mean(times) * 1e3
     sample = (f"{len(times)} of {args.steps} requested full solves (+{warm} warm-up) of CB-GMRES(100) "
               f"{args.format} on {args.workload} (n={n}), {its} iterations, final RRN {fr:.6e}; bounded to "
-              f"~{budget:.0f}s; single thread (the reference has no threading; {os.cpu_count()} cores present)")
+              f"~{budget:.0f}s; single thread (the reference has no threading): 1 thread of {os.cpu_count()} cores, "
+              f"{cpu_model()}")
     print(json.dumps({
         "impl": "reference",
         "metric": f"cbgmres_{args.format.replace('-', '_')}_time_to_solution",
         "value": round(ms, 2), "unit": "ms", "n_gpus": world, "steps": len(times), "warmup": warm,
         "ms_per_step": round(ms, 2), "higher_is_better": False, "scaling": "strong",
         "vs_baseline": None, "dtype": "f64", "data": "synthetic (same stencil + sin RHS)",
-        "config": {"workload": f"CB-GMRES(100) {args.format} basis, {args.workload}: n={n}, nnz={int(rp[-1])}",
-                   "format": args.format, "restart": 100, "target_rrn": 1e-10},
+        "config": shared_config(args.workload, args.format, n, int(rp[-1]), False,
+                                l2="host memory (CPU reference)",
+                                spmv="CSR sparse.cpp:43-56 (size_t indices), host"),
         "iterations": its, "final_rrn": fr,
-        "cpu_baseline": {"value": round(ms, 2), "unit": "ms", "cores": 1, "kind": kindname, "sample": sample},
+        "cpu_baseline": {"value": round(ms, 2), "unit": "ms", "cores": 1, "kind": kindname, "sample": sample,
+                         "cpu_model": cpu_model(), "host_cores": os.cpu_count()},
         "e2e": {"value": round(ms, 2), "unit": "ms", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }), flush=True)
 
