@@ -195,13 +195,33 @@ __device__ __forceinline__ double frsz_dot(const Codes4& c, uint32_t e, const do
     return s;
 }
 
+// The 4 decoded values, fast path only (caller checked e > L - 2).
+template <int L>
+__device__ __forceinline__ void frsz_decode_fast(const Codes4& c, uint32_t e, double v[4]) {
+    const double sc = __hiloint2double(static_cast<int>((e - (L - 2)) << 20), 0);
+#pragma unroll
+    for (int k = 0; k < 4; ++k) v[k] = __dmul_rn(signed_i2f(c.mag[k], c.sgn[k]), sc);
+}
+
+// v[k] * mul in one rounding: +-mag * RN(scale * mul), exact-equivalent to
+// RN(decode(v) * mul) whenever scale * mul is itself exact (normal; the
+// caller checks the block exponent range): decode(v) = +-mag * scale is
+// exact and so is the scaling.
+template <int L>
+__device__ __forceinline__ double frsz_smul(uint32_t e, double mul) {
+    return __dmul_rn(__hiloint2double(static_cast<int>((e - (L - 2)) << 20), 0), mul);
+}
+template <int L>
+__device__ __forceinline__ void frsz_decode_mul(const Codes4& c, double smul, double v[4]) {
+#pragma unroll
+    for (int k = 0; k < 4; ++k) v[k] = __dmul_rn(signed_i2f(c.mag[k], c.sgn[k]), smul);
+}
+
 // The 4 decoded values (warp-uniform fast/exact split like frsz_dot).
 template <int L>
 __device__ __forceinline__ void frsz_decode(const Codes4& c, uint32_t e, double v[4]) {
     if (__builtin_expect(__all_sync(0xFFFFFFFFu, e > L - 2), 1)) {
-        const double sc = __hiloint2double(static_cast<int>((e - (L - 2)) << 20), 0);
-#pragma unroll
-        for (int k = 0; k < 4; ++k) v[k] = __dmul_rn(signed_i2f(c.mag[k], c.sgn[k]), sc);
+        frsz_decode_fast<L>(c, e, v);
         return;
     }
     slow_decode<L>(c, e, v);
@@ -271,6 +291,9 @@ template <> struct Step<kZ32> {
     __device__ __forceinline__ double dot_fast(const double w[4]) const { return fast_dot<32>(codes(), e, w); }
     __device__ __forceinline__ bool upd_ok(double h, int he) const { return frsz_upd_ok<32>(e, h, he); }
     __device__ __forceinline__ void update_fast(double h, int, double w[4]) const { frsz_update_fast<32>(codes(), e, h, w); }
+    __device__ __forceinline__ void decode_fast(double v[4]) const { frsz_decode_fast<32>(codes(), e, v); }
+    __device__ __forceinline__ double smul(double mul) const { return frsz_smul<32>(e, mul); }
+    __device__ __forceinline__ void decode_mul(double sm, double v[4]) const { frsz_decode_mul<32>(codes(), sm, v); }
 };
 
 template <> struct Step<kZ16> {
@@ -296,6 +319,9 @@ template <> struct Step<kZ16> {
     __device__ __forceinline__ double dot_fast(const double w[4]) const { return fast_dot<16>(codes(), e, w); }
     __device__ __forceinline__ bool upd_ok(double h, int he) const { return frsz_upd_ok<16>(e, h, he); }
     __device__ __forceinline__ void update_fast(double h, int, double w[4]) const { frsz_update_fast<16>(codes(), e, h, w); }
+    __device__ __forceinline__ void decode_fast(double v[4]) const { frsz_decode_fast<16>(codes(), e, v); }
+    __device__ __forceinline__ double smul(double mul) const { return frsz_smul<16>(e, mul); }
+    __device__ __forceinline__ void decode_mul(double sm, double v[4]) const { frsz_decode_mul<16>(codes(), sm, v); }
 };
 
 template <> struct Step<kZ21> {
@@ -333,6 +359,9 @@ template <> struct Step<kZ21> {
     __device__ __forceinline__ double dot_fast(const double w[4]) const { return fast_dot<21>(codes(), e, w); }
     __device__ __forceinline__ bool upd_ok(double h, int he) const { return frsz_upd_ok<21>(e, h, he); }
     __device__ __forceinline__ void update_fast(double h, int, double w[4]) const { frsz_update_fast<21>(codes(), e, h, w); }
+    __device__ __forceinline__ void decode_fast(double v[4]) const { frsz_decode_fast<21>(codes(), e, v); }
+    __device__ __forceinline__ double smul(double mul) const { return frsz_smul<21>(e, mul); }
+    __device__ __forceinline__ void decode_mul(double sm, double v[4]) const { frsz_decode_mul<21>(codes(), sm, v); }
 };
 
 template <> struct Step<kF64> {

@@ -78,16 +78,20 @@ __host__ __device__ constexpr uint32_t stage_bytes() {
 }
 
 // Split [s0, s1) into ceil(len/sub) sub-tiles of near-equal size (so no CTA
-// ends with a 1-step remainder that costs a full ring round per column).
+// ends with a 1-step remainder that costs a full ring round per column):
+// the first `rem` tiles hold base + 1 steps, the others base. One division
+// per launch; the per-tile bounds are multiply-adds (the per-stage 64-bit
+// divisions of len * i / count showed up in the consumer loops).
 struct SubTiles {
-    uint64_t s0, len, count;
-    __device__ __forceinline__ uint64_t begin(uint64_t i) const { return s0 + len * i / count; }
-    __device__ __forceinline__ uint64_t end(uint64_t i) const { return s0 + len * (i + 1) / count; }
+    uint64_t s0, count, base, rem;
+    __device__ __forceinline__ uint64_t begin(uint64_t i) const { return s0 + i * base + min(i, rem); }
+    __device__ __forceinline__ uint64_t end(uint64_t i) const { return begin(i + 1); }
 };
 template <int F>
 __device__ __forceinline__ SubTiles sub_tiles(uint64_t s0, uint64_t s1) {
     const uint64_t len = s1 - s0;
-    return SubTiles{s0, len, (len + Geo<F>::sub - 1) / Geo<F>::sub};
+    const uint64_t count = (len + Geo<F>::sub - 1) / Geo<F>::sub;
+    return SubTiles{s0, count, count ? len / count : 0, count ? len % count : 0};
 }
 
 // ---- shared-memory step loaders (r = local row of the thread's 4 rows) ----
@@ -932,6 +936,150 @@ void allow_smem(K kernel) {
     done.insert(key);
 }
 
+// ------------------------------------------------------------ read sweep
+// The device analogue of the reference's read benchmark (bench.cpp:55-96,
+// the paper's Fig. 3) on the CGS decode path: a producer lane bulk-copies
+// the column's sub-tiles (Geo<F>::sub steps of 1024 rows, payload +
+// exponents) into the split kernels' ring; the consumer warps read a
+// stage's exponents first, take ONE warp vote for the fast decode, decode 4
+// values per thread per step from shared memory, apply `intensity`
+// multiply-adds (buf = buf * mul + add, two roundings as the reference's
+// -ffp-contract=off build) and fold them into a per-thread sum. Static,
+// balanced step ranges per CTA, so the checksum's tree (CTA partials in CTA
+// order) depends only on the grid -- deterministic.
+template <int F, bool kFull>
+__device__ __forceinline__ double stage_sweep(const unsigned char* pay, const uint32_t* ex, const StageOff<F>& o,
+                                              uint32_t steps, uint64_t row0, uint64_t n, int intensity, double mul,
+                                              double add, bool fold_ok, uint32_t e_lo, uint32_t e_span) {
+    constexpr int SUB = Geo<F>::sub;
+    Step<F> st[SUB];
+    bool fast = true;
+    if constexpr (FmtInfo<F>::frsz) {
+#pragma unroll
+        for (int s = 0; s < SUB; ++s)
+            if (kFull || s < static_cast<int>(steps)) {
+                st[s].e = ex[32 * s];
+                fast &= st[s].fast();
+            }
+        fast = __all_sync(0xFFFFFFFFu, fast);
+    }
+    // decode the whole stage, then ONE multiply-add loop over its 4 * SUB
+    // values (the loop control amortised over the stage). FRSZ2 fast path:
+    // the first multiply is folded into the decode (+-mag * RN(scale * mul),
+    // bit-identical to RN(decode * mul) when scale * mul is exact -- voted
+    // with the decode path), saving one FP64 multiply per value.
+    double v[SUB][4];
+    bool folded = false;
+    if constexpr (FmtInfo<F>::frsz) {
+        // scale * mul is exact iff it stays normal: a range of block
+        // exponents fixed by mul's exponent (integer check on e, no FP test)
+        bool ok = fast && fold_ok;
+        if (ok) {
+#pragma unroll
+            for (int s = 0; s < SUB; ++s)
+                if (kFull || s < static_cast<int>(steps)) ok &= st[s].e - e_lo <= e_span;
+        }
+        folded = __all_sync(0xFFFFFFFFu, ok);
+        if (__builtin_expect(folded, 1)) {
+#pragma unroll
+            for (int s = 0; s < SUB; ++s) {
+                if (!kFull && s >= static_cast<int>(steps)) {
+                    v[s][0] = v[s][1] = v[s][2] = v[s][3] = 0.0;
+                    continue;
+                }
+                step_lds_at<F>(st[s], pay, ex, o, s, false);
+                st[s].decode_mul(st[s].smul(mul), v[s]);
+#pragma unroll
+                for (int k = 0; k < 4; ++k) v[s][k] = __dadd_rn(v[s][k], add);
+            }
+        }
+    }
+    if (!folded) {
+#pragma unroll
+        for (int s = 0; s < SUB; ++s) {
+            if (!kFull && s >= static_cast<int>(steps)) {
+                v[s][0] = v[s][1] = v[s][2] = v[s][3] = 0.0;
+                continue;
+            }
+            if constexpr (FmtInfo<F>::frsz) {
+                step_lds_at<F>(st[s], pay, ex, o, s, false);
+                if (__builtin_expect(fast, 1)) st[s].decode_fast(v[s]);
+                else st[s].decode(v[s]);
+            } else {
+                step_lds_at<F>(st[s], pay, ex, o, s);
+                st[s].decode(v[s]);
+            }
+        }
+    }
+#pragma unroll 1
+    for (int t = folded ? 1 : 0; t < intensity; ++t)
+#pragma unroll
+        for (int s = 0; s < SUB; ++s)
+#pragma unroll
+            for (int k = 0; k < 4; ++k) v[s][k] = __dadd_rn(__dmul_rn(v[s][k], mul), add);
+    // n % 32 == 0: a thread's 4 rows are all inside or all past n
+    double acc = 0.0;
+    const bool all_in = kFull && row0 + (SUB - 1) * static_cast<uint64_t>(kStepRows) < n;
+#pragma unroll
+    for (int s = 0; s < SUB; ++s)
+        if (all_in || ((kFull || s < static_cast<int>(steps)) && row0 + static_cast<uint64_t>(s) * kStepRows < n))
+            acc = __dadd_rn(acc, __dadd_rn(__dadd_rn(v[s][0], v[s][1]), __dadd_rn(v[s][2], v[s][3])));
+    return acc;
+}
+
+template <int F>
+__global__ void __launch_bounds__(kThreads, split_min_blocks<F>())
+read_sweep_kernel(BasisView B, uint64_t col, uint64_t n, int intensity, double mul, double add,
+                  double* __restrict__ partials, unsigned* __restrict__ ticket, double* __restrict__ out) {
+    constexpr int S = Geo<F>::stages;
+    constexpr uint32_t PAY = Geo<F>::pay;
+    extern __shared__ __align__(128) unsigned char smem[];
+    __shared__ double red[kWarps + 1];
+    const Ring R = ring_setup<F>(smem);
+    __syncthreads();
+    uint64_t s0, s1;
+    cta_steps(n, s0, s1);
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    double acc = 0.0;
+    if (warp == kConsumerWarps) {
+        if (lane == 0) produce<F>(R, B, col, 1, s0, s1, false);
+    } else {
+        const StageOff<F> off;
+        const SubTiles T = sub_tiles<F>(s0, s1);
+        // Block exponents e for which scale(e) * mul is exact (normal):
+        // scale = 2^(e - 1023 - (L - 2)), mul = m 2^(E - 1023) with m in
+        // [1, 2) -> biased exponent of the product E + e - 1023 - (L - 2)
+        // must lie in [1, 2046]. Only for a normal, nonzero mul.
+        constexpr int L = FmtInfo<F>::L;
+        const int E = static_cast<int>((__double_as_longlong(mul) >> 52) & 0x7FF);
+        const int lo = max(1 - E + 1023 + (L - 2), L - 1);  // also the fast decode's e > L - 2
+        const int hi = min(2046 - E + 1023 + (L - 2), 2046);
+        const bool fold_ok = FmtInfo<F>::frsz && E >= 1 && E <= 2046 && hi >= lo;
+        const uint32_t e_lo = static_cast<uint32_t>(lo);
+        const uint32_t e_span = hi >= lo ? static_cast<uint32_t>(hi - lo) : 0u;
+        for (uint64_t t = 0; t < T.count; ++t) {
+            const int stage = static_cast<int>(t % S);
+            mbar_wait(R.full + stage, static_cast<uint32_t>((t / S) & 1));
+            const uint64_t sb = T.begin(t);
+            const uint32_t steps = static_cast<uint32_t>(T.end(t) - sb);
+            const unsigned char* pay = R.stages + stage * stage_bytes<F>();
+            const uint32_t* ex = reinterpret_cast<const uint32_t*>(pay + Geo<F>::sub * PAY);
+            const uint64_t row0 = sb * kStepRows + 4u * threadIdx.x;
+            acc = __dadd_rn(acc, steps == static_cast<uint32_t>(Geo<F>::sub)
+                                     ? stage_sweep<F, true>(pay + off.pay, ex + off.ex, off, steps, row0, n, intensity,
+                                                            mul, add, fold_ok, e_lo, e_span)
+                                     : stage_sweep<F, false>(pay + off.pay, ex + off.ex, off, steps, row0, n,
+                                                             intensity, mul, add, fold_ok, e_lo, e_span));
+            __syncwarp();
+            if (lane == 0) mbar_arrive(R.empty + stage);
+        }
+    }
+    acc = warp_sum(acc);
+    if (lane == 0) red[warp] = acc;  // the producer warp contributes +0.0
+    __syncthreads();
+    block_finalize(red, kWarps + 1, 1, partials, ticket, out);
+}
+
 // Dynamic tile scheduling for the split CGS kernels (measured on B200:
 // update at n = 2^26, k = 100 0.85 -> 1.03 of the HBM peak).
 template <int F> struct DotLaunch {
@@ -1014,6 +1162,16 @@ template <int F> struct WriteLaunch {
     }
 };
 
+template <int F> struct SweepLaunch {
+    static void run(const BasisView& B, uint64_t col, uint64_t n, int intensity, double mul, double add,
+                    double* out, Workspace* ws, cudaStream_t st) {
+        const size_t smem = ring_smem<F>(0) + 64;
+        allow_smem(read_sweep_kernel<F>);
+        const int grid = ring_grid(read_sweep_kernel<F>, n, smem);
+        CBGX_K(read_sweep_kernel<F><<<grid, kThreads, smem, st>>>(B, col, n, intensity, mul, add,
+                                                                 ws->get_partials(grid), ws->get_counter(), out));
+    }
+};
 template <int F> struct ReadLaunch {
     static void run(const BasisView& B, uint64_t j, uint64_t first, uint64_t count, double* out,
                     cudaStream_t st) {
@@ -1780,6 +1938,12 @@ bool launch_arnoldi_fused(const cbgx_basis& V, uint32_t cols, const double* w, d
                               &done);
     CBGX_CUDA(cudaGetLastError());
     return done;
+}
+
+void launch_read_sweep(const cbgx_basis& V, uint64_t col, uint64_t n, int intensity, double mul, double add,
+                       double* out, Workspace* ws, cudaStream_t st) {
+    dispatch_fmt<SweepLaunch>(fmt_of(V), view_of(V), col, n, intensity, mul, add, out, ws, st);
+    CBGX_CUDA(cudaGetLastError());
 }
 
 void launch_basis_read(const cbgx_basis& V, uint64_t j, uint64_t first, uint64_t count, double* out,

@@ -141,6 +141,9 @@ bool launch_arnoldi_fused(const cbgx_basis& V, uint32_t cols, const double* w, d
                           Workspace* ws, cudaStream_t st);
 void launch_basis_write(const cbgx_basis& V, uint64_t j, const double* x, const ScaleArg& scale,
                         double* v_out, uint64_t* bad, cudaStream_t st);
+// Read benchmark sweep of one basis column (readbench.cu's C-ABI).
+void launch_read_sweep(const cbgx_basis& V, uint64_t col, uint64_t n, int intensity, double mul, double add,
+                       double* out, Workspace* ws, cudaStream_t st);
 void launch_basis_read(const cbgx_basis& V, uint64_t j, uint64_t first, uint64_t count, double* out,
                        cudaStream_t st);
 
