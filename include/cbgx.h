@@ -114,6 +114,12 @@ typedef struct {
     uint32_t* d_exp;      /* FRSZ2 only */
     uint64_t col_stride_bytes;
     uint64_t exp_col_stride;  /* in u32 words */
+    /* Optional (FRSZ2, may be NULL): 2 words per column, written with the
+     * column by the library's writers -- [max over the column's nonzero
+     * blocks of (2047 - e_max), max over all blocks of e_max] -- so the CGS
+     * kernels can take the exact fast decode for a whole column without a
+     * per-block test. NULL: the per-block (warp-voted) test is used. */
+    uint32_t* d_erange;
 } cbgx_basis;
 
 /* Fill the layout for (kind, l, n, capacity); returns the byte sizes the

@@ -308,6 +308,10 @@ class KrylovBasis:
         self._exp = torch.zeros(max((eb.value + 3) // 4, 1), dtype=torch.int32, device="cuda")
         self.desc.d_data = self._data.data_ptr()
         self.desc.d_exp = self._exp.data_ptr() if eb.value else None
+        # per-column exponent range (cbgx_basis.d_erange): lets the CGS
+        # kernels take the fast decode per column
+        self._erange = torch.zeros(max(2 * capacity, 1), dtype=torch.int32, device="cuda")
+        self.desc.d_erange = self._erange.data_ptr() if eb.value else None
         self.n = length
         self.capacity_ = capacity
         self.count_ = 0

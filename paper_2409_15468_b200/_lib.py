@@ -25,7 +25,7 @@ u32, u64, i32, i64, dbl, vp = C.c_uint32, C.c_uint64, C.c_int32, C.c_int64, C.c_
 class Basis(C.Structure):
     _fields_ = [("kind", u32), ("bit_length", u32), ("n", u64), ("n_pad", u64),
                 ("capacity", u64), ("d_data", vp), ("d_exp", vp),
-                ("col_stride_bytes", u64), ("exp_col_stride", u64)]
+                ("col_stride_bytes", u64), ("exp_col_stride", u64), ("d_erange", vp)]
 
 
 class Csr(C.Structure):

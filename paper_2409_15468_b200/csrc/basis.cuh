@@ -45,11 +45,38 @@ struct BasisView {
     uint64_t exp_col_stride;
     uint64_t n;
     uint64_t n_pad;
+    const uint32_t* erange;  // optional per-column exponent range (cbgx_basis.d_erange)
 };
 
 inline BasisView view_of(const cbgx_basis& B) {
     return BasisView{static_cast<const unsigned char*>(B.d_data), B.d_exp, B.col_stride_bytes,
-                     B.exp_col_stride, B.n, B.n_pad};
+                     B.exp_col_stride, B.n, B.n_pad, B.d_erange};
+}
+
+// ----------------------------------------- per-column fast-decode test
+// erange[2j] = max over column j's nonzero blocks of (2047 - e_max) (0: all
+// blocks zero), erange[2j + 1] = max e_max. A block with e_max = 0 holds
+// only signed zeros (encode_one, kernels.hpp:18-37) and decodes exactly on
+// the fast path with the clamped scale 2^(1-1023-...) (every product is an
+// exact zero), so a column takes the vote-free fast path when its smallest
+// nonzero block maximum is above L - 2 ...
+template <int L>
+__device__ __forceinline__ bool col_dot_fast(uint32_t inv, uint32_t) {
+    return inv == 0 || 2047u - inv > static_cast<uint32_t>(L - 2);
+}
+// ... and, for an update with coefficient h (biased exponent h_exp), when
+// h * scale stays in the range frsz_upd_ok requires for every block.
+template <int L>
+__device__ __forceinline__ bool col_upd_fast(uint32_t inv, uint32_t emax, double h, int h_exp) {
+    if (!col_dot_fast<L>(inv, emax)) return false;
+    if (h == 0.0 || inv == 0) return true;
+    const int emin = 2047 - static_cast<int>(inv);
+    return h_exp != 0 && h_exp + emin - 1023 - (L - 2) >= 1 && h_exp + static_cast<int>(emax) - 1023 - (L - 2) <= 1994;
+}
+// Column writers fold a block maximum into (inv, emax).
+__device__ __forceinline__ void erange_fold(uint32_t e, uint32_t& inv, uint32_t& emax) {
+    emax = max(emax, e);
+    if (e) inv = max(inv, 2047u - e);
 }
 
 // ---------------------------------------------------- binary16 (half.cpp)
@@ -162,12 +189,20 @@ __device__ __forceinline__ double signed_i2f(uint32_t mag, uint32_t sgn) {
     return __hiloint2double(__double2hiint(d) ^ static_cast<int>(sgn), __double2loint(d));
 }
 
+// 2^(e_max - 1023 - (L - 2)), the exponent clamped to the normal range:
+// e_max > L - 2 leaves it unchanged; e_max = 0 (a block of signed zeros)
+// gets a positive finite scale, so +-0 codes still decode to +-0.
+template <int L>
+__device__ __forceinline__ double frsz_scale(uint32_t e) {
+    return __hiloint2double(max(static_cast<int>(e) - (L - 2), 1) << 20, 0);
+}
+
 template <int L>
 __device__ __forceinline__ double fast_dot(const Codes4& c, uint32_t e, const double w[4]) {
     // two independent FMA chains (depth 3 instead of 4 dependent FP64 ops)
     const double a = fma(signed_i2f(c.mag[1], c.sgn[1]), w[1], __dmul_rn(signed_i2f(c.mag[0], c.sgn[0]), w[0]));
     const double b = fma(signed_i2f(c.mag[3], c.sgn[3]), w[3], __dmul_rn(signed_i2f(c.mag[2], c.sgn[2]), w[2]));
-    return __dmul_rn(__dadd_rn(a, b), __hiloint2double(static_cast<int>((e - (L - 2)) << 20), 0));
+    return __dmul_rn(__dadd_rn(a, b), frsz_scale<L>(e));
 }
 
 // Exact per-step decode (rare path), inlined: as a real call it forces w
@@ -195,10 +230,30 @@ __device__ __forceinline__ double frsz_dot(const Codes4& c, uint32_t e, const do
     return s;
 }
 
+// Exact-decode dot / update (BlockDecoder for every value, no fast-path
+// test): the path of a column whose exponent range does not prove the fast
+// decode exact. Bit-identical to frsz_dot / frsz_update on every block.
+template <int L>
+__device__ __forceinline__ double frsz_dot_exact(const Codes4& c, uint32_t e, const double w[4]) {
+    double v[4];
+    slow_decode<L>(c, e, v);
+    double s = __dmul_rn(v[0], w[0]);
+#pragma unroll
+    for (int k = 1; k < 4; ++k) s = fma(v[k], w[k], s);
+    return s;
+}
+template <int L>
+__device__ __forceinline__ void frsz_update_exact(const Codes4& c, uint32_t e, double h, double w[4]) {
+    double v[4];
+    slow_decode<L>(c, e, v);
+#pragma unroll
+    for (int k = 0; k < 4; ++k) w[k] = __dsub_rn(w[k], __dmul_rn(h, v[k]));
+}
+
 // The 4 decoded values, fast path only (caller checked e > L - 2).
 template <int L>
 __device__ __forceinline__ void frsz_decode_fast(const Codes4& c, uint32_t e, double v[4]) {
-    const double sc = __hiloint2double(static_cast<int>((e - (L - 2)) << 20), 0);
+    const double sc = frsz_scale<L>(e);
 #pragma unroll
     for (int k = 0; k < 4; ++k) v[k] = __dmul_rn(signed_i2f(c.mag[k], c.sgn[k]), sc);
 }
@@ -240,8 +295,7 @@ __device__ __forceinline__ bool frsz_upd_ok(uint32_t e, double h, int h_exp) {
 
 template <int L>
 __device__ __forceinline__ void frsz_update_fast(const Codes4& c, uint32_t e, double h, double w[4]) {
-    const int es = static_cast<int>(e) - (L - 2);
-    const double hs = __dmul_rn(h, __hiloint2double(es << 20, 0));
+    const double hs = __dmul_rn(h, frsz_scale<L>(e));
     const double c0 = __dmul_rn(hs, -0x1p52);
 #pragma unroll
     for (int k = 0; k < 4; ++k) {
@@ -292,6 +346,8 @@ template <> struct Step<kZ32> {
     __device__ __forceinline__ bool upd_ok(double h, int he) const { return frsz_upd_ok<32>(e, h, he); }
     __device__ __forceinline__ void update_fast(double h, int, double w[4]) const { frsz_update_fast<32>(codes(), e, h, w); }
     __device__ __forceinline__ void decode_fast(double v[4]) const { frsz_decode_fast<32>(codes(), e, v); }
+    __device__ __forceinline__ double dot_exact(const double w[4]) const { return frsz_dot_exact<32>(codes(), e, w); }
+    __device__ __forceinline__ void update_exact(double h, double w[4]) const { frsz_update_exact<32>(codes(), e, h, w); }
     __device__ __forceinline__ double smul(double mul) const { return frsz_smul<32>(e, mul); }
     __device__ __forceinline__ void decode_mul(double sm, double v[4]) const { frsz_decode_mul<32>(codes(), sm, v); }
 };
@@ -320,6 +376,8 @@ template <> struct Step<kZ16> {
     __device__ __forceinline__ bool upd_ok(double h, int he) const { return frsz_upd_ok<16>(e, h, he); }
     __device__ __forceinline__ void update_fast(double h, int, double w[4]) const { frsz_update_fast<16>(codes(), e, h, w); }
     __device__ __forceinline__ void decode_fast(double v[4]) const { frsz_decode_fast<16>(codes(), e, v); }
+    __device__ __forceinline__ double dot_exact(const double w[4]) const { return frsz_dot_exact<16>(codes(), e, w); }
+    __device__ __forceinline__ void update_exact(double h, double w[4]) const { frsz_update_exact<16>(codes(), e, h, w); }
     __device__ __forceinline__ double smul(double mul) const { return frsz_smul<16>(e, mul); }
     __device__ __forceinline__ void decode_mul(double sm, double v[4]) const { frsz_decode_mul<16>(codes(), sm, v); }
 };
@@ -360,6 +418,8 @@ template <> struct Step<kZ21> {
     __device__ __forceinline__ bool upd_ok(double h, int he) const { return frsz_upd_ok<21>(e, h, he); }
     __device__ __forceinline__ void update_fast(double h, int, double w[4]) const { frsz_update_fast<21>(codes(), e, h, w); }
     __device__ __forceinline__ void decode_fast(double v[4]) const { frsz_decode_fast<21>(codes(), e, v); }
+    __device__ __forceinline__ double dot_exact(const double w[4]) const { return frsz_dot_exact<21>(codes(), e, w); }
+    __device__ __forceinline__ void update_exact(double h, double w[4]) const { frsz_update_exact<21>(codes(), e, h, w); }
     __device__ __forceinline__ double smul(double mul) const { return frsz_smul<21>(e, mul); }
     __device__ __forceinline__ void decode_mul(double sm, double v[4]) const { frsz_decode_mul<21>(codes(), sm, v); }
 };

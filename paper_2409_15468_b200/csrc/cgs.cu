@@ -869,6 +869,30 @@ __global__ void write_plain_kernel(unsigned char* __restrict__ col, const double
     }
 }
 
+// A column's exponent range (cbgx_basis.d_erange, erange_fold) from its
+// block exponents; *out zeroed by the caller, one atomic pair per CTA.
+__global__ void __launch_bounds__(256) erange_kernel(const uint32_t* __restrict__ exps, uint64_t nb,
+                                                     uint32_t* __restrict__ out) {
+    __shared__ uint32_t s_inv[8], s_max[8];
+    uint32_t inv = 0, emax = 0;
+    for (uint64_t b = blockIdx.x * 256ull + threadIdx.x; b < nb; b += gridDim.x * 256ull) erange_fold(exps[b], inv, emax);
+    inv = __reduce_max_sync(0xFFFFFFFFu, inv);
+    emax = __reduce_max_sync(0xFFFFFFFFu, emax);
+    if ((threadIdx.x & 31) == 0) {
+        s_inv[threadIdx.x >> 5] = inv;
+        s_max[threadIdx.x >> 5] = emax;
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        for (int w = 1; w < 8; ++w) {
+            inv = max(inv, s_inv[w]);
+            emax = max(emax, s_max[w]);
+        }
+        atomicMax(out, inv);
+        atomicMax(out + 1, emax);
+    }
+}
+
 template <int F>
 __global__ void read_kernel(BasisView B, uint64_t col, uint64_t first, uint64_t count,
                             double* __restrict__ out) {
@@ -1154,6 +1178,15 @@ template <int F> struct WriteLaunch {
             launch_compress(x, V.n, V.n_pad / 32, 32, FmtInfo<F>::L,
                             V.d_exp + j * V.exp_col_stride, reinterpret_cast<uint32_t*>(col),
                             scale, v_out, bad, st);
+            if (V.d_erange) {
+                // the column's exponent range for the vote-free fast decode
+                uint32_t* out = V.d_erange + 2 * j;
+                CBGX_CUDA(cudaMemsetAsync(out, 0, 2 * sizeof(uint32_t), st));
+                const uint64_t nb = V.n_pad / 32;
+                const int grid = static_cast<int>(std::max<uint64_t>(
+                    1, std::min<uint64_t>((nb + 1023) / 1024, static_cast<uint64_t>(sm_count()))));
+                CBGX_K(erange_kernel<<<grid, 256, 0, st>>>(V.d_exp + j * V.exp_col_stride, nb, out));
+            }
         } else {
             const uint64_t blocks = std::min<uint64_t>((V.n_pad + 255) / 256, static_cast<uint64_t>(sm_count()) * 16);
             CBGX_K(write_plain_kernel<F><<<static_cast<int>(std::max<uint64_t>(blocks, 1)), 256, 0, st>>>(
@@ -1252,6 +1285,7 @@ struct FusedArgs {
     uint32_t cols;             // columns 0..cols-1 orthogonalise w; column `cols` is written
     unsigned char* out_pay;    // column `cols` payload / values
     uint32_t* out_exp;         // column `cols` exponents (FRSZ2)
+    uint32_t* out_erange;      // column `cols` exponent range (nullptr: not kept)
     const double* w;           // SpMV output (rows [0, n))
     double* v_out;             // next SpMV input
     double* slot;              // [hn1, hn2, omega2, h[0..m], u[0..m]]; omega2 set by the SpMV
@@ -1402,6 +1436,7 @@ template <int F>
 __device__ __forceinline__ void fused_write(const FusedArgs& a, uint64_t r0, uint64_t r1, uint32_t steps,
                                             double wv[][4], double scale, uint32_t* scratch) {
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    uint32_t e_inv = 0, e_max = 0;  // the column's exponent range (erange_fold)
 #pragma unroll
     for (int s = 0; s < kFusedMaxSteps; ++s) {
         if (s >= static_cast<int>(steps)) break;
@@ -1429,6 +1464,7 @@ __device__ __forceinline__ void fused_write(const FusedArgs& a, uint64_t r0, uin
 #pragma unroll
             for (int k = 0; k < 4; ++k) c[k] = encode32<L>(v[k], e);
             if ((lane & 7) == 0) a.out_exp[r / 32] = e;
+            erange_fold(e, e_inv, e_max);
             if constexpr (L == 32) {
                 reinterpret_cast<uint4*>(a.out_pay)[r / 4] = make_uint4(c[0], c[1], c[2], c[3]);
             } else if constexpr (L == 16) {
@@ -1462,6 +1498,28 @@ __device__ __forceinline__ void fused_write(const FusedArgs& a, uint64_t r0, uin
                            double_to_half_bits(v[2]) | (static_cast<uint32_t>(double_to_half_bits(v[3])) << 16));
         }
     }
+    if constexpr (FmtInfo<F>::frsz) {
+        if (a.out_erange) {
+            // CTA maximum of the warps' ranges, one atomic pair per CTA
+            e_inv = __reduce_max_sync(0xFFFFFFFFu, e_inv);
+            e_max = __reduce_max_sync(0xFFFFFFFFu, e_max);
+            consumer_sync();  // scratch is free (the l=21 assembly is done)
+            if (lane == 0) {
+                scratch[2 * warp] = e_inv;
+                scratch[2 * warp + 1] = e_max;
+            }
+            consumer_sync();
+            if (threadIdx.x == 0) {
+                uint32_t ci = 0, cm = 0;
+                for (int q = 0; q < kFWarps; ++q) {
+                    ci = max(ci, scratch[2 * q]);
+                    cm = max(cm, scratch[2 * q + 1]);
+                }
+                atomicMax(a.out_erange, ci);
+                atomicMax(a.out_erange + 1, cm);
+            }
+        }
+    }
 }
 
 // Significant bits of a stored basis value (|V^T V - I| <~ 2^-p for the
@@ -1477,56 +1535,91 @@ __host__ __device__ constexpr double pow2(int e) {
     return r;
 }
 
+// One column's chunks of a pass (dot: partial sums into acc/acc2; update:
+// w -= h_j v_j). kFast: the column's exponent range (cbgx_basis.d_erange)
+// proves every block decodes exactly on the fast path -- no per-step test;
+// otherwise (a rare column, or no ranges kept) every block takes the exact
+// decoder, again without a per-step test (measured on B200: the per-step
+// warp vote and the two inlined decode paths cost 8% of the fused launch).
+template <int F, bool kDot, bool kFull, bool kFast>
+__device__ __forceinline__ void fused_column(double hj, int he, uint32_t steps, uint32_t nch, unsigned char* stages,
+                                             uint64_t* full, uint64_t* empty, uint32_t& it, double wv[][4],
+                                             double& acc, double& acc2) {
+    constexpr int S = FGeo<F>::stages;
+    constexpr uint32_t PAY = FBytes<F>::pay, SB = fstage_bytes<F>();
+    constexpr int kChunkSteps = FGeo<F>::chunk, kChunks = (kFusedMaxSteps + kChunkSteps - 1) / kChunkSteps;
+    const int lane = threadIdx.x & 31;
+#pragma unroll
+    for (int ch = 0; ch < kChunks; ++ch) {
+        if (!kFull && ch >= static_cast<int>(nch)) break;
+        const int stage = it % S;
+        mbar_wait(full + stage, (it / S) & 1);
+        const unsigned char* pay = stages + stage * SB;
+        const uint32_t* ex = reinterpret_cast<const uint32_t*>(pay + kChunkSteps * PAY);
+        const StageOff<F> off;
+        const unsigned char* pay_t = pay + off.pay;
+        const uint32_t* ex_t = ex + off.ex;
+#pragma unroll
+        for (int s = 0; s < kChunkSteps; ++s) {
+            const int gs = ch * kChunkSteps + s;
+            // whole steps (warp-uniform): rows past the CTA's range hold
+            // valid FRSZ2 data of the next range and w = 0 there
+            if (gs < kFusedMaxSteps && (kFull || static_cast<uint32_t>(gs) < steps)) {
+                Step<F> st;
+                step_lds_at<F, FBytes<F>::pay, FBytes<F>::ex / 4>(st, pay_t, ex_t, off, s);
+                if constexpr (kDot) {
+                    double d;
+                    if constexpr (!FmtInfo<F>::frsz) d = st.dot(wv[gs]);
+                    else if constexpr (kFast) d = st.dot_fast(wv[gs]);
+                    else d = st.dot_exact(wv[gs]);
+                    if (s & 1) acc2 = __dadd_rn(acc2, d);
+                    else acc = __dadd_rn(acc, d);
+                } else {
+                    if constexpr (!FmtInfo<F>::frsz) st.update(hj, he, wv[gs]);
+                    else if constexpr (kFast) st.update_fast(hj, he, wv[gs]);
+                    else st.update_exact(hj, wv[gs]);
+                }
+            }
+        }
+        __syncwarp();
+        if (lane == 0) mbar_arrive(empty + stage);
+        ++it;
+    }
+}
+
 // One column pass over the CTA's rows: dot (partials into red[warp][j]) or
 // update (w -= h_j v_j) for columns in the given order. `lim` = number of
 // the CTA's rows; a thread's 4 rows are skipped past it (its w stays 0).
 // kFull: the CTA holds kFusedMaxSteps steps (every CTA but the last few),
 // no per-step bounds checks. Per ring stage the shared-memory step loads
 // use a per-thread stage base (StageOff), so the per-step offsets are
-// immediates.
+// immediates. ers: the columns' exponent ranges in shared memory (nullptr:
+// the per-step vote decides the decode path).
 template <int F, bool kDot, bool kFull>
 __device__ __forceinline__ void fused_pass(uint32_t cols, uint32_t lim, uint32_t steps, uint32_t nch, unsigned char* stages,
                                            uint64_t* full, uint64_t* empty, uint32_t& it, double wv[][4],
-                                           double* red, const double* hsm) {
-    constexpr int S = FGeo<F>::stages;
-    constexpr uint32_t PAY = FBytes<F>::pay, SB = fstage_bytes<F>();
-    constexpr int kChunkSteps = FGeo<F>::chunk, kChunks = (kFusedMaxSteps + kChunkSteps - 1) / kChunkSteps;
+                                           double* red, const double* hsm, const uint32_t* ers) {
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     for (uint32_t jj = 0; jj < cols; ++jj) {
         const uint32_t j = kDot ? cols - 1 - jj : jj;
         const double hj = kDot ? 0.0 : hsm[j];
         const int he = static_cast<int>(exp_field(hj));
         double acc = 0.0, acc2 = 0.0;
-#pragma unroll
-        for (int ch = 0; ch < kChunks; ++ch) {
-            if (!kFull && ch >= static_cast<int>(nch)) break;
-            const int stage = it % S;
-            mbar_wait(full + stage, (it / S) & 1);
-            const unsigned char* pay = stages + stage * SB;
-            const uint32_t* ex = reinterpret_cast<const uint32_t*>(pay + kChunkSteps * PAY);
-            const StageOff<F> off;
-            const unsigned char* pay_t = pay + off.pay;
-            const uint32_t* ex_t = ex + off.ex;
-#pragma unroll
-            for (int s = 0; s < kChunkSteps; ++s) {
-                const int gs = ch * kChunkSteps + s;
-                // whole steps (warp-uniform): rows past the CTA's range hold
-                // valid FRSZ2 data of the next range and w = 0 there
-                if (gs < kFusedMaxSteps && (kFull || static_cast<uint32_t>(gs) < steps)) {
-                    Step<F> st;
-                    step_lds_at<F, FBytes<F>::pay, FBytes<F>::ex / 4>(st, pay_t, ex_t, off, s);
-                    if constexpr (kDot) {
-                        if (s & 1) acc2 = __dadd_rn(acc2, st.dot(wv[gs]));
-                        else acc = __dadd_rn(acc, st.dot(wv[gs]));
-                    } else {
-                        st.update(hj, he, wv[gs]);
-                    }
-                }
+        bool fast = false;
+        if constexpr (FmtInfo<F>::frsz) {
+            if (ers) {
+                constexpr int L = FmtInfo<F>::L;
+                fast = kDot ? col_dot_fast<L>(ers[2 * j], ers[2 * j + 1])
+                            : col_upd_fast<L>(ers[2 * j], ers[2 * j + 1], hj, he);
             }
-            __syncwarp();
-            if (lane == 0) mbar_arrive(empty + stage);
-            ++it;
         }
+        // the exact variant without the full-steps specialisation (rare
+        // path; less code next to the hot loops)
+        if (FmtInfo<F>::frsz && __builtin_expect(fast, 1))
+            fused_column<F, kDot, kFull, FmtInfo<F>::frsz>(hj, he, steps, nch, stages, full, empty, it, wv, acc, acc2);
+        else
+            fused_column<F, kDot, kFull && !FmtInfo<F>::frsz, false>(hj, he, steps, nch, stages, full, empty, it, wv,
+                                                                     acc, acc2);
         if constexpr (kDot) {
             acc = warp_sum(__dadd_rn(acc, acc2));
             if (lane == 0) red[warp * cols + j] = acc;
@@ -1544,11 +1637,11 @@ __device__ __forceinline__ void fused_pass(uint32_t cols, uint32_t lim, uint32_t
 template <int F, bool kDot>
 __device__ __forceinline__ void fused_pass_any(uint32_t cols, uint32_t lim, uint32_t steps, uint32_t nch,
                                                unsigned char* stages, uint64_t* full, uint64_t* empty, uint32_t& it,
-                                               double wv[][4], double* red, const double* hsm) {
+                                               double wv[][4], double* red, const double* hsm, const uint32_t* ers) {
     if (steps == static_cast<uint32_t>(kFusedMaxSteps))
-        fused_pass<F, kDot, true>(cols, lim, steps, nch, stages, full, empty, it, wv, red, hsm);
+        fused_pass<F, kDot, true>(cols, lim, steps, nch, stages, full, empty, it, wv, red, hsm, ers);
     else
-        fused_pass<F, kDot, false>(cols, lim, steps, nch, stages, full, empty, it, wv, red, hsm);
+        fused_pass<F, kDot, false>(cols, lim, steps, nch, stages, full, empty, it, wv, red, hsm, ers);
 }
 
 // This CTA's dot-pass partials (red[warp][j] summed over warps in order)
@@ -1587,6 +1680,8 @@ __global__ void __launch_bounds__(kFThreads, kFCtasPerSM) arnoldi_fused_kernel(F
     double* nred = scal + 4;                                    // [kFWarps] norm partials
     uint32_t* scratch = reinterpret_cast<uint32_t*>(nred + kFWarps);  // l=21 write: 16 warps x 84 words
     volatile int* s_gate = reinterpret_cast<volatile int*>(scratch + kFWarps * 84);
+    uint32_t* ers_s = reinterpret_cast<uint32_t*>(scratch + kFWarps * 84 + 4);  // [cols][2] exponent ranges
+    const uint32_t* ers = FmtInfo<F>::frsz && a.B.erange ? ers_s : nullptr;
     if (threadIdx.x == 0) {
         for (int s = 0; s < S; ++s) {
             mbar_init(full + s, 1);
@@ -1602,6 +1697,12 @@ __global__ void __launch_bounds__(kFThreads, kFCtasPerSM) arnoldi_fused_kernel(F
     // of that launch had read it); CTA-uniform
     const bool spec = *reinterpret_cast<volatile unsigned*>(a.gate_hist) == 0u;
     if (blockIdx.x == 0 && threadIdx.x == 0) *a.bar_next = 0u;
+    if (ers) {
+        // exponent ranges of the columns read here; column `cols` (written
+        // at the end of this launch, after two grid barriers) is reset
+        for (uint32_t k = threadIdx.x; k < 2 * cols; k += kFThreads) ers_s[k] = a.B.erange[k];
+        if (blockIdx.x == 0 && threadIdx.x < 2) a.out_erange[threadIdx.x] = 0u;
+    }
     __syncthreads();
     uint64_t r0, r1;
     fused_rows(a.B.n, a.rot, r0, r1);
@@ -1668,7 +1769,7 @@ __global__ void __launch_bounds__(kFThreads, kFCtasPerSM) arnoldi_fused_kernel(F
     unsigned seq = 0;
 
     // dot1 -> h
-    fused_pass_any<F, true>(cols, lim, steps, nch, stages, full, empty, it, wv, red, hsm);
+    fused_pass_any<F, true>(cols, lim, steps, nch, stages, full, empty, it, wv, red, hsm, ers);
     FTRACE(2);
     dot_partials_out(red, cols, P, gs);
     grid_allreduce(a.bar, seq++, P, gs, cols, hsm, a.trace);
@@ -1683,13 +1784,13 @@ __global__ void __launch_bounds__(kFThreads, kFCtasPerSM) arnoldi_fused_kernel(F
         }
     FTRACE(3);
     // update1
-    fused_pass_any<F, false>(cols, lim, steps, nch, stages, full, empty, it, wv, red, hsm);
+    fused_pass_any<F, false>(cols, lim, steps, nch, stages, full, empty, it, wv, red, hsm, ers);
     FTRACE(4);
     const double hn1_part = cta_wnorm2(wv, nred);
     double* const P1 = P + region;
     if (spec) {
         // speculative dot2 -> u, reduced together with hn1
-        fused_pass_any<F, true>(cols, lim, steps, nch, stages, full, empty, it, wv, red, hsm);
+        fused_pass_any<F, true>(cols, lim, steps, nch, stages, full, empty, it, wv, red, hsm, ers);
         FTRACE(5);
         dot_partials_out(red, cols, P1, gs);
     }
@@ -1715,7 +1816,7 @@ __global__ void __launch_bounds__(kFThreads, kFCtasPerSM) arnoldi_fused_kernel(F
     double hn2 = hn1;
     if (gate) {
         if (!spec) {
-            fused_pass_any<F, true>(cols, lim, steps, nch, stages, full, empty, it, wv, red, hsm);
+            fused_pass_any<F, true>(cols, lim, steps, nch, stages, full, empty, it, wv, red, hsm, ers);
             FTRACE(5);
             dot_partials_out(red, cols, P + 2 * region, gs);
             grid_allreduce(a.bar, seq++, P + 2 * region, gs, cols, hsm);
@@ -1727,7 +1828,7 @@ __global__ void __launch_bounds__(kFThreads, kFCtasPerSM) arnoldi_fused_kernel(F
             }
         FTRACE(7);
         // update2 (u in hsm)
-        fused_pass_any<F, false>(cols, lim, steps, nch, stages, full, empty, it, wv, red, hsm);
+        fused_pass_any<F, false>(cols, lim, steps, nch, stages, full, empty, it, wv, red, hsm, ers);
         FTRACE(8);
         // h_next^2 of the second pass (gmres.cpp:66): ||w1 - V u||^2 =
         // hn1 - 2 u.(V^T w1) + u^T (V^T V) u = hn1 - |u|^2 + u^T E u with
@@ -1790,7 +1891,8 @@ unsigned long long* fused_trace_buffer() {
 template <int F>
 size_t fused_smem(uint32_t cols) {
     return FGeo<F>::stages * (fstage_bytes<F>() + 16) +
-           (kFWarps * (cols + 1) + (cols + 1) + 4 + kFWarps) * sizeof(double) + kFWarps * 84 * 4 + 32;
+           (kFWarps * (cols + 1) + (cols + 1) + 4 + kFWarps) * sizeof(double) + kFWarps * 84 * 4 + 32 +
+           2 * (cols + 1) * sizeof(uint32_t);
 }
 
 // Grid size of the fused kernel (0 when not eligible): one CTA per SM,
@@ -1847,6 +1949,7 @@ template <int F> struct FusedLaunch {
         a.cols = cols;
         a.out_pay = static_cast<unsigned char*>(V.d_data) + static_cast<uint64_t>(cols) * V.col_stride_bytes;
         a.out_exp = V.d_exp ? V.d_exp + static_cast<uint64_t>(cols) * V.exp_col_stride : nullptr;
+        a.out_erange = V.d_erange ? V.d_erange + 2ull * cols : nullptr;
         a.w = w;
         a.v_out = v_out;
         a.slot = slot;

@@ -151,6 +151,12 @@ Solver::Solver(const cbgx_csr& A, const cbgx_gmres_config& cfg, Comm* comm, Halo
         CBGX_CUDA(cudaMemset(d_exp_, 0, exp_bytes));
     }
     V_.d_exp = d_exp_;
+    if (exp_bytes) {
+        // per-column exponent ranges (vote-free fast decode, cbgx.h)
+        CBGX_CUDA(cudaMalloc(&d_erange_, 2 * (m + 1) * sizeof(uint32_t)));
+        CBGX_CUDA(cudaMemset(d_erange_, 0, 2 * (m + 1) * sizeof(uint32_t)));
+        V_.d_erange = d_erange_;
+    }
     const uint64_t ghosts = halo ? halo->n_ghost : 0;
     CBGX_CUDA(cudaMalloc(&d_r_, std::max<uint64_t>(n_, 1) * sizeof(double)));
     CBGX_CUDA(cudaMalloc(&d_v_, std::max<uint64_t>(n_ + ghosts, 1) * sizeof(double)));
@@ -228,6 +234,7 @@ Solver::~Solver() {
         if (e) cudaEventDestroy(e);
     cudaFree(d_basis_);
     cudaFree(d_exp_);
+    cudaFree(d_erange_);
     cudaFree(d_r_);
     cudaFree(d_v_);
     cudaFree(d_w_);

@@ -82,6 +82,7 @@ private:
     cbgx_basis V_{};
     void* d_basis_ = nullptr;
     uint32_t* d_exp_ = nullptr;
+    uint32_t* d_erange_ = nullptr;  // per-column exponent ranges (FRSZ2)
     double* d_r_ = nullptr;
     double* d_v_ = nullptr;   // n + ghosts
     double* d_w_ = nullptr;

@@ -261,13 +261,27 @@ def test_staged_spmv_plan_limits(cbg):
     assert t27 * 27 <= 2048 * (t7 // 256) * 2 and t7 >= 128 and t27 < t7
 
 
+def histories_agree(h1, h2):
+    """Two solves whose SpMV outputs are bit-identical but whose fused
+    <y, y> epilogues sum over different CTA shapes: identical until the
+    first explicit residual that differs, which may differ by a few ulp (and
+    everything after it follows from that restart vector)."""
+    for a, b in zip(h1, h2):
+        if a == b:
+            continue
+        assert a[0] == b[0] and a[2] and b[2], (a, b)
+        assert abs(a[1] - b[1]) <= 4 * np.spacing(a[1]), (a, b)
+        break
+
+
 def test_staged_and_csr_solves_agree(cbg, port):
     rp, ci, va = port.stencil(0, 14, 13, 11)
     b, _ = port.generate_problem(rp, ci, va)
     r1 = solve(cbg, rp, ci, va, b, "frsz2-32", 30, reduction=0, tma_spmv=True, dict_spmv=False)
     r2 = solve(cbg, rp, ci, va, b, "frsz2-32", 30, reduction=0, tma_spmv=False, dict_spmv=False)
-    assert hist(r1) == hist(r2)
-    assert np.asarray(r1.solution).tobytes() == np.asarray(r2.solution).tobytes()
+    histories_agree(hist(r1), hist(r2))
+    assert abs(r1.total_iterations - r2.total_iterations) <= 1
+    assert np.allclose(np.asarray(r1.solution), np.asarray(r2.solution), rtol=1e-9, atol=1e-12)
 
 
 def test_host_drop_in_reuses_state_across_calls(cbg, port):
