@@ -241,10 +241,22 @@ __device__ __forceinline__ double stage_dot(const unsigned char* pay, const uint
 
 template <int F, bool kFull>
 __device__ __forceinline__ void stage_update(const unsigned char* pay, const uint32_t* ex, const StageOff<F>& o,
-                                             uint32_t steps, double hj, int he, double (&wv)[Geo<F>::sub][4]) {
+                                             uint32_t steps, double hj, int he, double (&wv)[Geo<F>::sub][4],
+                                             bool colfast) {
     constexpr int SUB = Geo<F>::sub;
     Step<F> st[SUB];
     if constexpr (FmtInfo<F>::frsz) {
+        if (colfast) {
+            // the column's exponent range proves the fast update exact for
+            // every block (col_upd_fast): no stage vote
+#pragma unroll
+            for (int s = 0; s < SUB; ++s)
+                if (kFull || s < steps) {
+                    step_lds_at<F>(st[s], pay, ex, o, s);
+                    st[s].update_fast(hj, he, wv[s]);
+                }
+            return;
+        }
         bool ok = true;
 #pragma unroll
         for (int s = 0; s < SUB; ++s)
@@ -269,6 +281,23 @@ __device__ __forceinline__ void stage_update(const unsigned char* pay, const uin
             st[s].update(hj, he, wv[s]);
         }
 }
+
+// Per-column fast-update flags of a split update launch (shared memory,
+// one byte per column; nullptr: no exponent ranges kept): col_upd_fast of
+// the column's range and its coefficient (hs = the signed coefficients).
+template <int F>
+__device__ __forceinline__ void set_colfast(const BasisView& B, uint64_t first, uint32_t cols, const double* hs,
+                                            uint8_t* cfl) {
+    if constexpr (FmtInfo<F>::frsz) {
+        if (!B.erange) return;
+        for (uint32_t k = threadIdx.x; k < cols; k += blockDim.x) {
+            const double hk = hs[k];
+            cfl[k] = col_upd_fast<FmtInfo<F>::L>(B.erange[2 * (first + k)], B.erange[2 * (first + k) + 1], hk,
+                                                 static_cast<int>(exp_field(hk)));
+        }
+    }
+}
+__device__ __forceinline__ bool colfast(const uint8_t* cfl, uint32_t j) { return cfl && cfl[j]; }
 
 __device__ __forceinline__ void load_w(const double* __restrict__ w, uint64_t n, uint64_t r, double out[4]) {
     if (r + 3 < n) {
@@ -423,7 +452,9 @@ cgs_update_kernel(BasisView B, uint64_t first, uint32_t cols, const double* __re
     const Ring R = ring_setup<F>(smem);
     double* hs = reinterpret_cast<double*>(R.empty + S);  // [cols]
     double* red = hs + cols;                               // [kWarps]
+    uint8_t* cfl = B.erange ? reinterpret_cast<uint8_t*>(red + kWarps) : nullptr;  // [cols]
     for (uint32_t k = threadIdx.x; k < cols; k += kThreads) hs[k] = h_sign * h[k];
+    set_colfast<F>(B, first, cols, hs, cfl);
     if (threadIdx.x < kWarps) red[threadIdx.x] = 0.0;
     __syncthreads();
     uint64_t s0, s1;
@@ -452,8 +483,9 @@ cgs_update_kernel(BasisView B, uint64_t first, uint32_t cols, const double* __re
                 const uint32_t* ex = reinterpret_cast<const uint32_t*>(pay + Geo<F>::sub * PAY);
                 const double hj = hs[j];
                 const int he = static_cast<int>(exp_field(hj));
-                if (steps == Geo<F>::sub) stage_update<F, true>(pay + off.pay, ex + off.ex, off, steps, hj, he, wv);
-                else stage_update<F, false>(pay + off.pay, ex + off.ex, off, steps, hj, he, wv);
+                const bool cf = colfast(cfl, j);
+                if (steps == Geo<F>::sub) stage_update<F, true>(pay + off.pay, ex + off.ex, off, steps, hj, he, wv, cf);
+                else stage_update<F, false>(pay + off.pay, ex + off.ex, off, steps, hj, he, wv, cf);
                 __syncwarp();
                 if (lane == 0) mbar_arrive(R.empty + stage);
             }
@@ -516,6 +548,8 @@ __device__ __forceinline__ void split_consumer_sync() {
     asm volatile("bar.sync 1, %0;" ::"n"(kConsumers) : "memory");
 }
 
+
+
 template <int F>
 __global__ void __launch_bounds__(kThreads, split_min_blocks<F>())
 cgs_update_dyn_kernel(BasisView B, uint64_t first, uint32_t cols, const double* __restrict__ h,
@@ -530,8 +564,10 @@ cgs_update_dyn_kernel(BasisView B, uint64_t first, uint32_t cols, const double* 
     double* hs = reinterpret_cast<double*>(R.empty + S);  // [cols]
     double* red = hs + cols;                               // [kWarps]
     uint32_t* tid_ring = reinterpret_cast<uint32_t*>(red + kWarps);  // [S]
+    uint8_t* cfl = B.erange ? reinterpret_cast<uint8_t*>(tid_ring + S) : nullptr;  // [cols]
     __shared__ bool s_last;
     for (uint32_t k = threadIdx.x; k < cols; k += kThreads) hs[k] = h_sign * h[k];
+    set_colfast<F>(B, first, cols, hs, cfl);
     __syncthreads();
     const uint64_t nsteps = (B.n + kStepRows - 1) / kStepRows;
     const uint32_t ntiles = static_cast<uint32_t>((nsteps + Geo<F>::sub - 1) / Geo<F>::sub);
@@ -590,8 +626,9 @@ cgs_update_dyn_kernel(BasisView B, uint64_t first, uint32_t cols, const double* 
                 const uint32_t* ex = reinterpret_cast<const uint32_t*>(pay + Geo<F>::sub * PAY);
                 const double hj = hs[j];
                 const int he = static_cast<int>(exp_field(hj));
-                if (steps == Geo<F>::sub) stage_update<F, true>(pay + off.pay, ex + off.ex, off, steps, hj, he, wv);
-                else stage_update<F, false>(pay + off.pay, ex + off.ex, off, steps, hj, he, wv);
+                const bool cf = colfast(cfl, j);
+                if (steps == Geo<F>::sub) stage_update<F, true>(pay + off.pay, ex + off.ex, off, steps, hj, he, wv, cf);
+                else stage_update<F, false>(pay + off.pay, ex + off.ex, off, steps, hj, he, wv, cf);
                 __syncwarp();
                 if (lane == 0) mbar_arrive(R.empty + stage);
             }
@@ -1148,7 +1185,7 @@ template <int F> struct UpdateLaunch {
                     const GateArg& gate) {
         const bool fused_norm = norm && reduction == CBGX_REDUCE_TREE;
         if (cols > 0 || fused_norm) {
-            const size_t smem = ring_smem<F>(cols + kWarps) + 64;
+            const size_t smem = ring_smem<F>(cols + kWarps) + 64 + cols;
             allow_smem(cgs_update_dyn_kernel<F>);
             const int grid = ring_grid(cgs_update_dyn_kernel<F>, B.n, smem);
             const uint64_t nsteps = (B.n + kStepRows - 1) / kStepRows;
@@ -1159,7 +1196,7 @@ template <int F> struct UpdateLaunch {
             return;
         }
         if (cols > 0 || fused_norm) {
-            const size_t smem = ring_smem<F>(cols + kWarps);
+            const size_t smem = ring_smem<F>(cols + kWarps) + cols;
             allow_smem(cgs_update_kernel<F>);
             const int grid = ring_grid(cgs_update_kernel<F>, B.n, smem);
             double* partials = fused_norm ? ws->get_partials(grid) : nullptr;
