@@ -382,10 +382,169 @@ dsell_spmv_kernel(uint64_t n_rows, const uint64_t* __restrict__ soff, uint32_t e
     block_finalize(red, kSW, 1, partials, ticket, norm_out);
 }
 
+// ---------------------------------------------------- pair-coded ELL8
+// Structured-grid matrices hold few distinct (value, column offset) PAIRS
+// (a constant-coefficient stencil: one per offset). When there are at most
+// 255, each entry becomes ONE byte indexing a pair table {value, offset} in
+// shared memory: half the code bytes of the 2-byte (value, offset) codes,
+// and per entry one 16-byte shared load instead of two lookups plus field
+// extraction (the SpMV is instruction-bound: ~190 instructions per 32-row
+// slice with 2-byte codes on B200). Rows are padded to a multiple of 8
+// entries (one 8-byte code load per 8 entries); 0xFF = padding = (+0.0,
+// offset 0), unpredicated as in dsell_spmv_kernel.
+
+// Which 2-byte codes occur: a per-CTA shared bitmap, merged with atomicOr.
+__global__ void __launch_bounds__(256) pair_mark_kernel(const uint16_t* __restrict__ codes, uint64_t count,
+                                                        unsigned* __restrict__ bitmap) {
+    __shared__ unsigned sb[2048];
+    for (uint32_t i = threadIdx.x; i < 2048; i += 256) sb[i] = 0u;
+    __syncthreads();
+    const uint4* c8 = reinterpret_cast<const uint4*>(codes);
+    for (uint64_t i = blockIdx.x * 256ull + threadIdx.x; i < count / 8; i += gridDim.x * 256ull) {
+        const uint4 q = __ldcs(c8 + i);
+        const uint32_t w[4] = {q.x, q.y, q.z, q.w};
+#pragma unroll
+        for (int k = 0; k < 8; ++k) {
+            const uint32_t c = (w[k / 2] >> (16 * (k & 1))) & 0xFFFFu;
+            if (c != kPad) {
+                const unsigned bit = 1u << (c & 31);
+                if (!(sb[c >> 5] & bit)) atomicOr(sb + (c >> 5), bit);
+            }
+        }
+    }
+    __syncthreads();
+    for (uint32_t i = threadIdx.x; i < 2048; i += 256)
+        if (sb[i]) atomicOr(bitmap + i, sb[i]);
+}
+
+// ELL4 2-byte codes -> ELL8 pair bytes (entry k of row 32s+lane at byte
+// ((s * g8 + k / 8) * 32 + lane) * 8 + k % 8).
+__global__ void __launch_bounds__(256) pair_convert_kernel(const uint16_t* __restrict__ codes, uint64_t nslices,
+                                                           uint32_t g4, uint32_t g8, const uint8_t* __restrict__ map8,
+                                                           uint8_t* __restrict__ out) {
+    const uint64_t total = nslices * 32 * g8;  // 8-byte output groups
+    for (uint64_t i = blockIdx.x * 256ull + threadIdx.x; i < total; i += gridDim.x * 256ull) {
+        const uint64_t lane = i % 32, sg = i / 32, sl = sg / g8, g = sg % g8;
+        uint32_t lo = 0, hi = 0;
+#pragma unroll
+        for (int k = 0; k < 8; ++k) {
+            const uint32_t e = static_cast<uint32_t>(g) * 8 + k;  // entry index in the row
+            uint32_t b = 0xFFu;
+            if (e < 4 * g4) {
+                const uint16_t c = codes[((sl * g4 + e / 4) * 32 + lane) * 4 + (e & 3)];
+                if (c != kPad) b = map8[c];
+            }
+            if (k < 4) lo |= b << (8 * k);
+            else hi |= b << (8 * (k - 4));
+        }
+        reinterpret_cast<uint2*>(out)[i] = make_uint2(lo, hi);
+    }
+}
+
+// 5 CTAs/SM (48 registers): 22.5 us at 7-pt 128^3 in the solve (ncu), vs
+// 24.0 at 6 CTAs (40 registers: rematerialised loop constants); two slices
+// per warp iteration (both slices' gathers in flight): 24.6 us.
+#ifndef PELL_MIN_BLOCKS
+#define PELL_MIN_BLOCKS 5
+#endif
+// Row r's result: a NaN sum (a non-finite x[rc] under a padding entry) is
+// recomputed over the real entries only; then y[r] (or b[r] - ...) and the
+// norm partial.
+template <int MODE>
+__device__ __forceinline__ void pell_finish(double s, int32_t r, uint64_t n_rows, uint32_t g8, const uint2* cp,
+                                            const double2* tab, const double* __restrict__ x,
+                                            const double* __restrict__ b, double* __restrict__ y, int with_norm,
+                                            double& acc) {
+    if (static_cast<uint64_t>(r) >= n_rows) return;
+    if (isnan(s)) {
+        s = 0.0;
+        for (uint32_t g = 0; g < g8; ++g) {
+            const uint2 q = __ldcs(cp + 32 * g);
+            for (int k = 0; k < 8; ++k) {
+                const uint32_t idx = ((k < 4 ? q.x : q.y) >> (8 * (k & 3))) & 0xFFu;
+                if (idx != 0xFFu)
+                    s = __dadd_rn(s, __dmul_rn(tab[idx].x, __ldg(x + r + __double2loint(tab[idx].y) / 8)));
+            }
+        }
+    }
+    if (MODE == 1) s = __dsub_rn(__ldg(b + r), s);
+    y[r] = s;
+    if (with_norm) acc = __dadd_rn(acc, __dmul_rn(s, s));
+}
+// MODE 0: y = A x.  MODE 1: y = b - A x. One warp per 32-row slice, lane =
+// row; products and sums in row order from +0.0 (sparse.cpp:50-52), padding
+// entries add +-0 (see dsell_spmv_kernel) and a NaN sum is recomputed
+// exactly; bit-identical to spmv().
+template <int MODE>
+__global__ void __launch_bounds__(256, PELL_MIN_BLOCKS)
+pell_spmv_kernel(uint64_t n_rows, uint32_t g8, const uint8_t* __restrict__ codes, const int32_t* __restrict__ p_off,
+                 const double* __restrict__ p_val, const double* __restrict__ x, const double* __restrict__ b,
+                 double* __restrict__ y, int with_norm, double* __restrict__ partials, unsigned* __restrict__ ticket,
+                 double* __restrict__ norm_out) {
+    // pair table: .x = value, .y = the column offset in BYTES (off * 8) in
+    // the low word -- one 16-byte shared load per entry, and the gather
+    // address is the slice's row pointer plus a sign-extended 32-bit offset
+    __shared__ double2 tab[256];
+    __shared__ double red[8];
+    for (uint32_t i = threadIdx.x; i < 256; i += 256)
+        tab[i] = make_double2(i == 255 ? 0.0 : p_val[i], __hiloint2double(0, i == 255 ? 0 : 8 * p_off[i]));
+    __syncthreads();
+    pdl_trigger();
+    const int lane = threadIdx.x & 31;
+    const uint64_t nsl = (n_rows + 31) / 32;
+    const uint64_t nw = static_cast<uint64_t>(gridDim.x) * 8;
+    uint64_t sl = (blockIdx.x * 256ull + threadIdx.x) / 32;
+    // running pointers: the warp's slice advances by nw slices per iteration
+    const uint64_t cstep = nw * g8 * 32;  // in 8-byte groups
+    const uint2* cp = reinterpret_cast<const uint2*>(codes) + sl * g8 * 32 + lane;
+    int32_t r = static_cast<int32_t>(sl * 32 + lane);
+    const int32_t rstep = static_cast<int32_t>(nw * 32);
+    const int32_t rlast = static_cast<int32_t>(n_rows - 1);
+    double acc = 0.0;
+    uint2 nxt = make_uint2(0xFFFFFFFFu, 0xFFFFFFFFu);
+    if (sl < nsl) nxt = __ldcs(cp);  // codes do not depend on the predecessor
+    pdl_wait();
+    for (; sl < nsl; sl += nw, cp += cstep, r += rstep) {
+        const int32_t rc = min(r, rlast);
+        const char* xr = reinterpret_cast<const char*>(x + rc);
+        uint2 cur = nxt;
+        if (sl + nw < nsl) nxt = __ldcs(cp + cstep);
+        double s = 0.0;
+        for (uint32_t g = 0; g < g8; ++g) {
+            if (g) cur = __ldcs(cp + 32 * g);
+            double v[8], xv[8];
+#pragma unroll
+            for (int k = 0; k < 8; ++k) {
+                const uint32_t idx = ((k < 4 ? cur.x : cur.y) >> (8 * (k & 3))) & 0xFFu;
+                const double2 t = tab[idx];
+                v[k] = t.x;
+                xv[k] = __ldg(reinterpret_cast<const double*>(xr + __double2loint(t.y)));
+            }
+#pragma unroll
+            for (int k = 0; k < 8; ++k) s = __dadd_rn(s, __dmul_rn(v[k], xv[k]));
+        }
+        pell_finish<MODE>(s, r, n_rows, g8, cp, tab, x, b, y, with_norm, acc);
+    }
+    if (!with_norm) return;
+    acc = warp_sum(acc);
+    if (lane == 0) red[threadIdx.x >> 5] = acc;
+    __syncthreads();
+    block_finalize(red, 8, 1, partials, ticket, norm_out);
+}
+
 int dict_grid(uint64_t rows) {
     const uint64_t want = (rows + kDThreads - 1) / kDThreads;
     const uint64_t cap = static_cast<uint64_t>(sm_count()) * 8;
     return static_cast<int>(std::max<uint64_t>(1, std::min(want, cap)));
+}
+
+// Pair-coded ELL8 SpMV switch (A/B: CBGX_PELL=0 keeps the 2-byte codes).
+bool pell_enabled() {
+    static const bool v = [] {
+        const char* e = getenv("CBGX_PELL");
+        return !e || atoi(e) != 0;
+    }();
+    return v;
 }
 
 template <typename T>
@@ -395,6 +554,64 @@ void ensure(T*& p, uint64_t& cap, uint64_t need) {
     p = nullptr;
     CBGX_CUDA(cudaMalloc(reinterpret_cast<void**>(&p), std::max<uint64_t>(need, 1) * sizeof(T)));
     cap = need;
+}
+
+// The pair-coded ELL8 copy from the ELL4 2-byte codes (see pell_spmv_kernel):
+// one pass marks the 2-byte codes present, the host numbers them (one round
+// trip of 8 KB), one pass rewrites the codes as bytes. D.ell8_w stays 0 (the
+// 2-byte kernel is used) for SELL layouts or more than 255 pairs.
+void build_pairs(DictSell& D, const std::vector<int32_t>& d_off, const std::vector<double>& d_val, cudaStream_t st) {
+    D.ell8_w = 0;
+    if (!D.ell_w || !pell_enabled()) return;
+    uint64_t cap = 0;
+    if (!D.bitmap) {
+        ensure(D.bitmap, cap, 2048);
+        ensure(D.map8, cap, 65536);
+        ensure(D.pair_val, cap, 256);
+        ensure(D.pair_off, cap, 256);
+    }
+    CBGX_CUDA(cudaMemsetAsync(D.bitmap, 0, 2048 * sizeof(unsigned), st));
+    const int grid = static_cast<int>(std::max<uint64_t>(1, std::min<uint64_t>((D.entries / 8 + 255) / 256, sm_count() * 4ull)));
+    CBGX_K(pair_mark_kernel<<<grid, 256, 0, st>>>(D.codes, D.entries, D.bitmap));
+    CBGX_CUDA(cudaGetLastError());
+    std::vector<unsigned> bm(2048);
+    CBGX_CUDA(cudaMemcpyAsync(bm.data(), D.bitmap, 2048 * sizeof(unsigned), cudaMemcpyDeviceToHost, st));
+    CBGX_CUDA(cudaStreamSynchronize(st));
+    std::vector<uint8_t> map(65536, 0xFF);
+    std::vector<double> pv(256, 0.0);
+    std::vector<int32_t> po(256, 0);
+    uint32_t np = 0;
+    for (uint32_t c = 0; c < 65536; ++c) {
+        if (!(bm[c >> 5] >> (c & 31) & 1u)) continue;
+        if (np == 255) return;  // more than 255 pairs: keep the 2-byte codes
+        map[c] = static_cast<uint8_t>(np);
+        pv[np] = d_val[c >> 8];
+        po[np] = d_off[c & 0xFF];
+        ++np;
+    }
+    const uint32_t g4 = D.ell_w / 4, g8 = (D.ell_w + 7) / 8;
+    const uint64_t bytes = D.nslices * 32 * 8ull * g8;
+    if (bytes > D.codes8_cap) {
+        if (D.codes8) CBGX_CUDA(cudaFree(D.codes8));
+        D.codes8 = nullptr;
+        D.codes8_cap = 0;
+        size_t free_b = 0, total_b = 0;
+        CBGX_CUDA(cudaMemGetInfo(&free_b, &total_b));
+        if (static_cast<double>(bytes) > 0.5 * static_cast<double>(free_b)) return;
+        ensure(D.codes8, D.codes8_cap, bytes);
+    }
+    CBGX_CUDA(cudaMemcpyAsync(D.map8, map.data(), 65536, cudaMemcpyHostToDevice, st));
+    CBGX_CUDA(cudaMemcpyAsync(D.pair_val, pv.data(), 256 * sizeof(double), cudaMemcpyHostToDevice, st));
+    CBGX_CUDA(cudaMemcpyAsync(D.pair_off, po.data(), 256 * sizeof(int32_t), cudaMemcpyHostToDevice, st));
+    const uint64_t groups = D.nslices * 32 * g8;
+    const int g2 = static_cast<int>(std::max<uint64_t>(1, std::min<uint64_t>((groups + 255) / 256, sm_count() * 8ull)));
+    CBGX_K(pair_convert_kernel<<<g2, 256, 0, st>>>(D.codes, D.nslices, g4, g8, D.map8, D.codes8));
+    CBGX_CUDA(cudaGetLastError());
+    // the host vectors above are read by the async copies: finish them here
+    CBGX_CUDA(cudaStreamSynchronize(st));
+    D.entries8 = bytes;
+    D.ell8_w = 8 * g8;
+    D.n_pair = np;
 }
 
 // Builds (or rebuilds, reusing D's buffers) the dictionary copy of A. One
@@ -502,6 +719,7 @@ bool dict_build(const cbgx_csr& A, double reserve_bytes, cudaStream_t st, DictSe
         CBGX_CUDA(cudaStreamSynchronize(st));
         if (long_rows) return false;
     }
+    build_pairs(D, d_off, d_val, st);
     D.ready = true;
     return true;
 }
@@ -510,7 +728,9 @@ bool dict_build(const cbgx_csr& A, double reserve_bytes, cudaStream_t st, DictSe
 
 DictSell::~DictSell() {
     for (void* p : {static_cast<void*>(codes), static_cast<void*>(soff), static_cast<void*>(off), static_cast<void*>(val),
-                    static_cast<void*>(tabs), static_cast<void*>(flags), static_cast<void*>(idx)})
+                    static_cast<void*>(tabs), static_cast<void*>(flags), static_cast<void*>(idx),
+                    static_cast<void*>(codes8), static_cast<void*>(pair_val), static_cast<void*>(pair_off),
+                    static_cast<void*>(map8), static_cast<void*>(bitmap)})
         if (p) cudaFree(p);
 }
 
@@ -550,10 +770,40 @@ static void dict_launch(const cbgx_csr& A, const DictSell& D, const double* x, c
                                  static_cast<const double*>(D.val), x, b, y, fused, partials, ticket, norm));
 }
 
+template <int MODE>
+static void pell_launch(const cbgx_csr& A, const DictSell& D, const double* x, const double* b, double* y, int fused,
+                        double* norm, Workspace* ws, cudaStream_t st, bool pdl) {
+    static int per_sm = -1;
+    if (per_sm < 0) {
+        CBGX_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, pell_spmv_kernel<MODE>, 256, 0));
+        per_sm = std::max(per_sm, 1);
+    }
+    const uint64_t want = (D.nslices + 7) / 8;
+    const int grid = static_cast<int>(std::max<uint64_t>(1, std::min<uint64_t>(want, static_cast<uint64_t>(sm_count()) * per_sm)));
+    double* partials = fused ? ws->get_partials(grid) : nullptr;
+    unsigned* ticket = fused ? ws->get_counter() : nullptr;
+    cudaLaunchConfig_t lc = {};
+    lc.gridDim = dim3(grid);
+    lc.blockDim = dim3(256);
+    lc.stream = st;
+    cudaLaunchAttribute at[1];
+    at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    at[0].val.programmaticStreamSerializationAllowed = 1;
+    lc.attrs = at;
+    lc.numAttrs = pdl ? 1 : 0;
+    note_launch();
+    CBGX_CUDA(cudaLaunchKernelEx(&lc, pell_spmv_kernel<MODE>, A.n_rows, D.ell8_w / 8,
+                                 static_cast<const uint8_t*>(D.codes8), static_cast<const int32_t*>(D.pair_off),
+                                 static_cast<const double*>(D.pair_val), x, b, y, fused, partials, ticket, norm));
+}
+
 void launch_spmv_dict(const cbgx_csr& A, const DictSell& D, const double* x, const double* b, double* y, double* norm,
                       int reduction, Workspace* ws, cudaStream_t st, bool pdl) {
     const int fused = norm && reduction == CBGX_REDUCE_TREE;
-    if (D.ell_w) {
+    if (D.ell8_w) {
+        if (b) pell_launch<1>(A, D, x, b, y, fused, norm, ws, st, pdl);
+        else pell_launch<0>(A, D, x, b, y, fused, norm, ws, st, pdl);
+    } else if (D.ell_w) {
         if (b) dict_launch<1, true>(A, D, x, b, y, fused, norm, ws, st, pdl);
         else dict_launch<0, true>(A, D, x, b, y, fused, norm, ws, st, pdl);
     } else {

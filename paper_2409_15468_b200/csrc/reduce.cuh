@@ -90,6 +90,19 @@ struct DictSell {
     uint32_t n_off = 0, n_val = 0;
     uint32_t ell_w = 0;  // > 0: ELL4 layout, every row padded to this width
     bool ready = false;
+    // Pair-coded ELL8 copy (when the matrix holds <= 255 distinct (value,
+    // column offset) pairs): 1-byte codes into one pair table, rows padded
+    // to a multiple of 8 entries (0xFF = padding). Used by the SpMV when set.
+    uint8_t* codes8 = nullptr;
+    uint64_t entries8 = 0, codes8_cap = 0;
+    uint32_t ell8_w = 0;   // > 0: the pair-coded copy is valid
+    uint32_t n_pair = 0;
+    double* pair_val = nullptr;   // [256]
+    int32_t* pair_off = nullptr;  // [256]
+    uint8_t* map8 = nullptr;      // [65536] 2-byte code -> pair index
+    unsigned* bitmap = nullptr;   // [2048] codes present
+    // matrix bytes one SpMV streams (the codes actually read)
+    double code_bytes() const { return ell8_w ? static_cast<double>(entries8) : 2.0 * static_cast<double>(entries); }
     // build scratch and capacities (kept across rebuilds)
     unsigned long long* tabs = nullptr;
     unsigned* flags = nullptr;

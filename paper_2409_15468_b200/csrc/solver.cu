@@ -273,7 +273,7 @@ void Solver::solve(const double* d_b, const double* d_x0, double* d_x, cbgx_hist
     const int fmt = fmt_from_cfg(cfg_);
     const double bpv = stored_bytes_per_value(fmt);
     const double rp_bytes = A_.row_ptr_bits / 8.0;
-    const double spmv_bytes = dict_ && dict_->ready ? dict_->entries * 2.0 + (dict_->nslices + 1) * 8.0 + 16.0 * n
+    const double spmv_bytes = dict_ && dict_->ready ? dict_->code_bytes() + (dict_->ell_w ? 0.0 : (dict_->nslices + 1) * 8.0) + 16.0 * n
                                     : A_.nnz * 12.0 + (n + 1) * rp_bytes + 16.0 * n;
     const bool multi = comm_ && comm_->size() > 1;
     uint64_t hist_len = 0;
