@@ -388,7 +388,8 @@ int cbgx_halo_destroy(cbgx_halo* h);
  * (ghosts owned by each rank). */
 int cbgx_halo_plan(int nranks, int rank, const uint64_t* row_ranges, uint64_t n_global,
                    const int64_t* gcols, uint64_t nnz, int32_t* local_cols_out,
-                   int64_t* ghosts_out, uint64_t* n_ghosts, uint64_t* need_per_rank);
+                   int64_t* ghosts_out, uint64_t* n_ghosts, uint64_t* need_per_rank,
+                   uint64_t* own_offset);
 /* Owner side: global rows requested by a peer -> local row indices to pack. */
 int cbgx_halo_send_index(uint64_t row_begin, uint64_t row_end, const int64_t* requested,
                          uint64_t count, int32_t* send_idx_out);
@@ -396,6 +397,13 @@ int cbgx_halo_send_index(uint64_t row_begin, uint64_t row_end, const int64_t* re
  * all-gather: out[k] = sum_r gathered[r*count + k], r = 0..nranks-1 in order. */
 int cbgx_sum_ranks_host(int nranks, uint64_t count, const double* gathered, double* out);
 uint64_t cbgx_halo_ghosts(const cbgx_halo* h);
+/* Where the own rows start in a local vector: 0 for the compact layout
+ * [own rows | ghosts]; the number of ghost rows below the own rows for the
+ * window layout [lower ghosts | own rows | upper ghosts], which the plan
+ * picks when the ghosts are the contiguous rows next to the own block (a
+ * slab partition of a banded matrix) -- column offsets col - row then
+ * survive the remap and the dictionary SpMV applies to the local matrix. */
+uint64_t cbgx_halo_own_offset(const cbgx_halo* h);
 /* fill d_vec[n_local .. n_local+ghosts) from the owners' rows (collective) */
 int cbgx_halo_exchange(cbgx_halo* h, double* d_vec, void* stream);
 

@@ -118,7 +118,8 @@ def lib():
             "cbgx_halo_create": ([vp, u64, u64, u64, vp, u64, vp, P(vp)], C.c_int),
             "cbgx_halo_destroy": ([vp], C.c_int),
             "cbgx_halo_ghosts": ([vp], u64),
-            "cbgx_halo_plan": ([C.c_int, C.c_int, vp, u64, vp, u64, vp, vp, P(u64), vp], C.c_int),
+            "cbgx_halo_own_offset": ([vp], u64),
+            "cbgx_halo_plan": ([C.c_int, C.c_int, vp, u64, vp, u64, vp, vp, P(u64), vp, P(u64)], C.c_int),
             "cbgx_halo_send_index": ([u64, u64, vp, u64, vp], C.c_int),
             "cbgx_sum_ranks_host": ([C.c_int, u64, vp, vp], C.c_int),
             "cbgx_malloc": ([P(vp), u64], C.c_int),

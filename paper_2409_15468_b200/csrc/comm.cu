@@ -39,6 +39,18 @@ __global__ void sum_ranks_kernel(const double* __restrict__ g, int P, uint64_t c
     }
 }
 
+// sum_ranks_kernel for a packed vector, element 0 and the rest to two places
+__global__ void sum_ranks_split_kernel(const double* __restrict__ g, int P, uint64_t count, double* __restrict__ first,
+                                       double* __restrict__ rest) {
+    for (uint64_t k = blockIdx.x * static_cast<uint64_t>(blockDim.x) + threadIdx.x; k < count;
+         k += static_cast<uint64_t>(gridDim.x) * blockDim.x) {
+        double s = g[k];
+        for (int r = 1; r < P; ++r) s = __dadd_rn(s, g[static_cast<uint64_t>(r) * count + k]);
+        if (k == 0) *first = s;
+        else rest[k - 1] = s;
+    }
+}
+
 __global__ void gather_rows_kernel(const double* __restrict__ v, const int32_t* __restrict__ idx,
                                    uint64_t count, double* __restrict__ out) {
     for (uint64_t k = blockIdx.x * static_cast<uint64_t>(blockDim.x) + threadIdx.x; k < count;
@@ -112,6 +124,11 @@ void sum_gathered(const double* g, int P, size_t count, double* out, cudaStream_
     CBGX_CUDA(cudaGetLastError());
 }
 
+void sum_gathered_split(const double* g, int P, size_t count, double* first, double* rest, cudaStream_t st) {
+    CBGX_K(sum_ranks_split_kernel<<<1, 128, 0, st>>>(g, P, count, first, rest));
+    CBGX_CUDA(cudaGetLastError());
+}
+
 class NcclComm final : public Comm {
 public:
     NcclComm(const ncclUniqueId& id, int nranks, int rank) : rank_(rank), size_(nranks) {
@@ -126,6 +143,12 @@ public:
         double* g = static_cast<double*>(gather_.get(count * size_ * sizeof(double)));
         check_nccl(nccl().AllGather(d_vals, g, count * sizeof(double), ncclChar, comm_, st), "ncclAllGather");
         sum_gathered(g, size_, count, d_vals, st);
+    }
+    void sum_partials_split(const double* d_src, size_t count, double* d_first, double* d_rest,
+                            cudaStream_t st) override {
+        double* g = static_cast<double*>(gather_.get(count * size_ * sizeof(double)));
+        check_nccl(nccl().AllGather(d_src, g, count * sizeof(double), ncclChar, comm_, st), "ncclAllGather");
+        sum_gathered_split(g, size_, count, d_first, d_rest, st);
     }
     void allgather(const void* d_send, void* d_recv, size_t bytes, cudaStream_t st) override {
         check_nccl(nccl().AllGather(d_send, d_recv, bytes, ncclChar, comm_, st), "ncclAllGather");
@@ -168,6 +191,13 @@ public:
         double* g = static_cast<double*>(gather_.get(count * sh_->size * sizeof(double)));
         allgather(d_vals, g, count * sizeof(double), st);
         sum_gathered(g, sh_->size, count, d_vals, st);
+        CBGX_CUDA(cudaStreamSynchronize(st));
+    }
+    void sum_partials_split(const double* d_src, size_t count, double* d_first, double* d_rest,
+                            cudaStream_t st) override {
+        double* g = static_cast<double*>(gather_.get(count * sh_->size * sizeof(double)));
+        allgather(d_src, g, count * sizeof(double), st);
+        sum_gathered_split(g, sh_->size, count, d_first, d_rest, st);
         CBGX_CUDA(cudaStreamSynchronize(st));
     }
     void allgather(const void* d_send, void* d_recv, size_t bytes, cudaStream_t st) override {
@@ -215,16 +245,19 @@ void Halo::exchange(double* d_vec, cudaStream_t st) const {
     const uint64_t total = send_offsets.empty() ? 0 : send_offsets.back();
     if (total) {
         CBGX_K(gather_rows_kernel<<<static_cast<int>(std::min<uint64_t>((total + 255) / 256, 1024)), 256, 0, st>>>(
-            d_vec, d_send_idx, total, d_send_buf));
+            d_vec + own_offset(), d_send_idx, total, d_send_buf));
         CBGX_CUDA(cudaGetLastError());
     }
     std::vector<Comm::Msg> sends, recvs;
     for (size_t i = 0; i < send_peers.size(); ++i)
         sends.push_back({send_peers[i], d_send_buf + send_offsets[i],
                          (send_offsets[i + 1] - send_offsets[i]) * sizeof(double)});
-    for (size_t i = 0; i < recv_peers.size(); ++i)
-        recvs.push_back({recv_peers[i], d_vec + n_local + recv_offsets[i],
-                         (recv_offsets[i + 1] - recv_offsets[i]) * sizeof(double)});
+    for (size_t i = 0; i < recv_peers.size(); ++i) {
+        // a peer's ghosts are contiguous and on one side of the own rows
+        const uint64_t p = recv_offsets[i];
+        const uint64_t at = window ? (p < win_lo ? p : p + n_local) : n_local + p;
+        recvs.push_back({recv_peers[i], d_vec + at, (recv_offsets[i + 1] - recv_offsets[i]) * sizeof(double)});
+    }
     comm->exchange(sends, recvs, st);
 }
 
@@ -235,6 +268,8 @@ struct HaloPlan {
     std::vector<int64_t> ghosts;     // sorted global indices not owned here
     std::vector<uint64_t> need;      // need[o]: ghosts owned by rank o
     std::vector<int32_t> local_cols; // remapped columns
+    bool window = false;             // ghosts laid out around the own rows (see below)
+    uint64_t win_lo = 0;             // window: ghosts below the own rows (= own rows' offset)
 };
 
 HaloPlan plan_halo(int P, int me, const uint64_t* ranges, uint64_t n_global, const int64_t* cols, uint64_t nnz) {
@@ -262,18 +297,36 @@ HaloPlan plan_halo(int P, int me, const uint64_t* ranges, uint64_t n_global, con
     H.ghosts.erase(std::unique(H.ghosts.begin(), H.ghosts.end()), H.ghosts.end());
     H.need.assign(P, 0);
     for (int64_t g : H.ghosts) ++H.need[owner(g)];
-    // own -> c - rb; ghost -> n_local + position (ghosts sorted by global
-    // index == grouped by owner rank); each row keeps its nonzero order, so
-    // the local SpMV accumulates in the reference's order.
-    H.local_cols.resize(nnz);
     const uint64_t n_local = re - rb;
+    // Window layout when the ghosts below the own rows are exactly the rows
+    // [rb - n_lo, rb) and those above exactly [re, re + n_hi) (a banded
+    // matrix on a slab partition: the neighbouring planes): the local vector
+    // is [lower ghosts | own rows | upper ghosts] = the global rows
+    // [rb - n_lo, re + n_hi), so every column offset (col - row) of the
+    // global matrix survives the remap (shifted by n_lo) and the dictionary
+    // SpMV applies. Otherwise the compact layout [own rows | ghosts].
+    const uint64_t n_lo = static_cast<uint64_t>(std::lower_bound(H.ghosts.begin(), H.ghosts.end(),
+                                                                 static_cast<int64_t>(rb)) - H.ghosts.begin());
+    const uint64_t n_hi = H.ghosts.size() - n_lo;
+    H.window = (n_lo == 0 || (H.ghosts[0] == static_cast<int64_t>(rb - n_lo) &&
+                              H.ghosts[n_lo - 1] == static_cast<int64_t>(rb) - 1)) &&
+               (n_hi == 0 || (H.ghosts[n_lo] == static_cast<int64_t>(re) &&
+                              H.ghosts.back() == static_cast<int64_t>(re + n_hi) - 1));
+    H.win_lo = H.window ? n_lo : 0;
+    // own -> own offset + c - rb; ghost at sorted position p -> p (below) or
+    // p + n_local (above) in the window layout, n_local + p in the compact
+    // one (ghosts sorted by global index == grouped by owner rank); each row
+    // keeps its nonzero order, so the local SpMV accumulates in the
+    // reference's order.
+    H.local_cols.resize(nnz);
     for (uint64_t k = 0; k < nnz; ++k) {
         const int64_t c = cols[k];
         if (static_cast<uint64_t>(c) >= rb && static_cast<uint64_t>(c) < re) {
-            H.local_cols[k] = static_cast<int32_t>(c - static_cast<int64_t>(rb));
+            H.local_cols[k] = static_cast<int32_t>(H.win_lo + (c - static_cast<int64_t>(rb)));
         } else {
-            const auto it = std::lower_bound(H.ghosts.begin(), H.ghosts.end(), c);
-            H.local_cols[k] = static_cast<int32_t>(n_local + static_cast<uint64_t>(it - H.ghosts.begin()));
+            const uint64_t p = static_cast<uint64_t>(std::lower_bound(H.ghosts.begin(), H.ghosts.end(), c) -
+                                                     H.ghosts.begin());
+            H.local_cols[k] = static_cast<int32_t>(H.window ? (p < n_lo ? p : p + n_local) : n_local + p);
         }
     }
     return H;
@@ -312,6 +365,8 @@ std::unique_ptr<Halo> make_halo(Comm* comm, uint64_t rb, uint64_t re, uint64_t n
     }
     HaloPlan plan = plan_halo(P, me, ranges.data(), n_global, cols.data(), nnz);
     H->n_ghost = plan.ghosts.size();
+    H->window = plan.window;
+    H->win_lo = plan.win_lo;
     std::vector<uint64_t> counts(static_cast<size_t>(P) * P);
     {
         Scratch s;
@@ -420,7 +475,7 @@ int cbgx_halo_create(cbgx_comm* c, uint64_t row_begin, uint64_t row_end, uint64_
 
 int cbgx_halo_plan(int nranks, int rank, const uint64_t* row_ranges, uint64_t n_global, const int64_t* gcols,
                    uint64_t nnz, int32_t* local_cols_out, int64_t* ghosts_out, uint64_t* n_ghosts,
-                   uint64_t* need_per_rank) {
+                   uint64_t* need_per_rank, uint64_t* own_offset) {
     return guard([&] {
         if (nranks < 1 || rank < 0 || rank >= nranks) throw Error(CBGX_EINVAL, "halo: bad rank");
         const HaloPlan p = plan_halo(nranks, rank, row_ranges, n_global, gcols, nnz);
@@ -428,8 +483,11 @@ int cbgx_halo_plan(int nranks, int rank, const uint64_t* row_ranges, uint64_t n_
         if (ghosts_out) std::copy(p.ghosts.begin(), p.ghosts.end(), ghosts_out);
         if (n_ghosts) *n_ghosts = p.ghosts.size();
         if (need_per_rank) std::copy(p.need.begin(), p.need.end(), need_per_rank);
+        if (own_offset) *own_offset = p.win_lo;
     });
 }
+
+uint64_t cbgx_halo_own_offset(const cbgx_halo* h) { return h ? h->impl->own_offset() : 0; }
 
 int cbgx_halo_send_index(uint64_t row_begin, uint64_t row_end, const int64_t* requested, uint64_t count,
                          int32_t* send_idx_out) {

@@ -480,7 +480,7 @@ __global__ void __launch_bounds__(256, PELL_MIN_BLOCKS)
 pell_spmv_kernel(uint64_t n_rows, uint32_t g8, const uint8_t* __restrict__ codes, const int32_t* __restrict__ p_off,
                  const double* __restrict__ p_val, const double* __restrict__ x, const double* __restrict__ b,
                  double* __restrict__ y, int with_norm, double* __restrict__ partials, unsigned* __restrict__ ticket,
-                 double* __restrict__ norm_out) {
+                 double* __restrict__ norm_out, uint64_t s_begin, uint64_t s_end, int accumulate) {
     // pair table: .x = value, .y = the column offset in BYTES (off * 8) in
     // the low word -- one 16-byte shared load per entry, and the gather
     // address is the slice's row pointer plus a sign-extended 32-bit offset
@@ -491,9 +491,9 @@ pell_spmv_kernel(uint64_t n_rows, uint32_t g8, const uint8_t* __restrict__ codes
     __syncthreads();
     pdl_trigger();
     const int lane = threadIdx.x & 31;
-    const uint64_t nsl = (n_rows + 31) / 32;
+    const uint64_t nsl = s_end;  // slices [s_begin, s_end)
     const uint64_t nw = static_cast<uint64_t>(gridDim.x) * 8;
-    uint64_t sl = (blockIdx.x * 256ull + threadIdx.x) / 32;
+    uint64_t sl = s_begin + (blockIdx.x * 256ull + threadIdx.x) / 32;
     // running pointers: the warp's slice advances by nw slices per iteration
     const uint64_t cstep = nw * g8 * 32;  // in 8-byte groups
     const uint2* cp = reinterpret_cast<const uint2*>(codes) + sl * g8 * 32 + lane;
@@ -529,7 +529,7 @@ pell_spmv_kernel(uint64_t n_rows, uint32_t g8, const uint8_t* __restrict__ codes
     acc = warp_sum(acc);
     if (lane == 0) red[threadIdx.x >> 5] = acc;
     __syncthreads();
-    block_finalize(red, 8, 1, partials, ticket, norm_out);
+    block_finalize(red, 8, 1, partials, ticket, norm_out, accumulate != 0);
 }
 
 int dict_grid(uint64_t rows) {
@@ -772,13 +772,16 @@ static void dict_launch(const cbgx_csr& A, const DictSell& D, const double* x, c
 
 template <int MODE>
 static void pell_launch(const cbgx_csr& A, const DictSell& D, const double* x, const double* b, double* y, int fused,
-                        double* norm, Workspace* ws, cudaStream_t st, bool pdl) {
+                        double* norm, Workspace* ws, cudaStream_t st, bool pdl, uint64_t s_begin = 0,
+                        uint64_t s_end = ~0ull, bool accumulate = false) {
     static int per_sm = -1;
     if (per_sm < 0) {
         CBGX_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, pell_spmv_kernel<MODE>, 256, 0));
         per_sm = std::max(per_sm, 1);
     }
-    const uint64_t want = (D.nslices + 7) / 8;
+    s_end = std::min<uint64_t>(s_end, D.nslices);
+    if (s_begin >= s_end) return;
+    const uint64_t want = (s_end - s_begin + 7) / 8;
     const int grid = static_cast<int>(std::max<uint64_t>(1, std::min<uint64_t>(want, static_cast<uint64_t>(sm_count()) * per_sm)));
     double* partials = fused ? ws->get_partials(grid) : nullptr;
     unsigned* ticket = fused ? ws->get_counter() : nullptr;
@@ -794,7 +797,51 @@ static void pell_launch(const cbgx_csr& A, const DictSell& D, const double* x, c
     note_launch();
     CBGX_CUDA(cudaLaunchKernelEx(&lc, pell_spmv_kernel<MODE>, A.n_rows, D.ell8_w / 8,
                                  static_cast<const uint8_t*>(D.codes8), static_cast<const int32_t*>(D.pair_off),
-                                 static_cast<const double*>(D.pair_val), x, b, y, fused, partials, ticket, norm));
+                                 static_cast<const double*>(D.pair_val), x, b, y, fused, partials, ticket, norm,
+                                 s_begin, s_end, static_cast<int>(accumulate)));
+}
+
+void launch_spmv_pell_range(const cbgx_csr& A, const DictSell& D, const double* x, double* y, double* norm,
+                            uint64_t s_begin, uint64_t s_end, bool accumulate, Workspace* ws, cudaStream_t st) {
+    if (!D.ell8_w) throw Error(CBGX_EINTERNAL, "spmv: pair-coded copy missing");
+    pell_launch<0>(A, D, x, nullptr, y, norm ? 1 : 0, norm, ws, st, false, s_begin, s_end, accumulate);
+}
+
+namespace {
+template <typename RP>
+__global__ void ghost_rows_kernel(const RP* __restrict__ rp, const int32_t* __restrict__ ci, uint64_t n, int64_t lo,
+                                  unsigned long long* __restrict__ out) {
+    for (uint64_t r = blockIdx.x * 256ull + threadIdx.x; r < n; r += gridDim.x * 256ull) {
+        bool below = false, above = false;
+        for (uint64_t k = static_cast<uint64_t>(rp[r]); k < static_cast<uint64_t>(rp[r + 1]); ++k) {
+            const int64_t c = ci[k];
+            below |= c < lo;
+            above |= c >= lo + static_cast<int64_t>(n);
+        }
+        if (below) atomicMax(out, static_cast<unsigned long long>(r + 1));
+        if (above) atomicMin(out + 1, static_cast<unsigned long long>(r));
+    }
+}
+}  // namespace
+
+void ghost_row_bounds(const cbgx_csr& A, uint64_t lo, uint64_t out[2], cudaStream_t st) {
+    unsigned long long* d = nullptr;
+    CBGX_CUDA(cudaMalloc(reinterpret_cast<void**>(&d), 2 * sizeof(unsigned long long)));
+    const unsigned long long init[2] = {0ull, static_cast<unsigned long long>(A.n_rows)};
+    CBGX_CUDA(cudaMemcpyAsync(d, init, sizeof(init), cudaMemcpyHostToDevice, st));
+    const int grid = static_cast<int>(std::max<uint64_t>(1, std::min<uint64_t>((A.n_rows + 255) / 256, sm_count() * 8ull)));
+    if (A.row_ptr_bits == 32)
+        CBGX_K(ghost_rows_kernel<int32_t><<<grid, 256, 0, st>>>(static_cast<const int32_t*>(A.d_row_ptr), A.d_col_idx,
+                                                                  A.n_rows, static_cast<int64_t>(lo), d));
+    else
+        CBGX_K(ghost_rows_kernel<int64_t><<<grid, 256, 0, st>>>(static_cast<const int64_t*>(A.d_row_ptr), A.d_col_idx,
+                                                                  A.n_rows, static_cast<int64_t>(lo), d));
+    unsigned long long h[2];
+    CBGX_CUDA(cudaMemcpyAsync(h, d, sizeof(h), cudaMemcpyDeviceToHost, st));
+    CBGX_CUDA(cudaStreamSynchronize(st));
+    CBGX_CUDA(cudaFree(d));
+    out[0] = h[0];
+    out[1] = h[1];
 }
 
 void launch_spmv_dict(const cbgx_csr& A, const DictSell& D, const double* x, const double* b, double* y, double* norm,

@@ -41,7 +41,7 @@ __device__ __forceinline__ double lane_sum_rows(const double* __restrict__ parti
 __device__ __forceinline__ void block_finalize(const double* red, int nwarps, uint32_t ncol,
                                                double* __restrict__ partials,
                                                unsigned* __restrict__ ticket,
-                                               double* __restrict__ out) {
+                                               double* __restrict__ out, bool accumulate = false) {
     __shared__ bool s_last;
     for (uint32_t k = threadIdx.x; k < ncol; k += blockDim.x) {
         double s = red[k];
@@ -59,7 +59,8 @@ __device__ __forceinline__ void block_finalize(const double* red, int nwarps, ui
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, nw = blockDim.x >> 5;
     for (uint32_t k = warp; k < ncol; k += nw) {
         const double s = warp_sum(lane_sum_rows(partials, ncol, k, gridDim.x, lane));
-        if (lane == 0) out[k] = s;
+        // accumulate: add to the value an earlier launch left (a split SpMV)
+        if (lane == 0) out[k] = accumulate ? __dadd_rn(out[k], s) : s;
     }
     if (threadIdx.x == 0) *ticket = 0u;
 }
@@ -117,6 +118,14 @@ struct DictSell {
 bool build_dict_sell(const cbgx_csr& A, double reserve_bytes, cudaStream_t st, DictSell& D);
 void launch_spmv_dict(const cbgx_csr& A, const DictSell& D, const double* x, const double* b, double* y, double* norm,
                       int reduction, Workspace* ws, cudaStream_t st, bool pdl = false);
+// Pair-coded SpMV of the 32-row slices [s_begin, s_end) (D.ell8_w != 0); the
+// norm (tree order) is written, or added to *norm when `accumulate`.
+void launch_spmv_pell_range(const cbgx_csr& A, const DictSell& D, const double* x, double* y, double* norm,
+                            uint64_t s_begin, uint64_t s_end, bool accumulate, Workspace* ws, cudaStream_t st);
+// Rows touching the halo of a local matrix whose own columns are
+// [lo, lo + n_rows): out[0] = 1 + last row with a column below lo (0: none),
+// out[1] = first row with a column >= lo + n_rows (n_rows: none). Synchronous.
+void ghost_row_bounds(const cbgx_csr& A, uint64_t lo, uint64_t out[2], cudaStream_t st);
 
 // Staged (TMA) CSR SpMV: plan_spmv_tiles returns the tile height (32..256
 // rows, 0 when some tile would exceed the stage capacity).

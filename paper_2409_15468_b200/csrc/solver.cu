@@ -163,6 +163,7 @@ Solver::Solver(const cbgx_csr& A, const cbgx_gmres_config& cfg, Comm* comm, Halo
     CBGX_CUDA(cudaMalloc(&d_w_, std::max<uint64_t>(n_, 1) * sizeof(double)));
     const size_t scal = 2 * kSlot(m) + 2 * m + 16;
     CBGX_CUDA(cudaMalloc(&d_scal_, scal * sizeof(double)));
+    if (comm_ && comm_->size() > 1) CBGX_CUDA(cudaMalloc(&d_pack_, 2 * (m + 2) * sizeof(double)));
     CBGX_CUDA(cudaMemset(d_scal_, 0, scal * sizeof(double)));
     // mapped: the fused orthogonalisation writes the step slot straight into
     // it (no device-to-host copy between the step's kernels)
@@ -187,9 +188,9 @@ void Solver::setup_matrix(bool before_basis, cudaStream_t st, const unsigned lon
     if (stats) A_.max_row_nnz = static_cast<uint32_t>(stats[0]);
     if (A_.max_row_nnz == 0) A_.max_row_nnz = csr_max_row_nnz(A_, st);
     // Dictionary-coded SELL-32 (dsell.cu) when the matrix has <= 255 distinct
-    // values and column offsets: 2 B per entry instead of 12 (single rank:
-    // halo-remapped columns are not offset-structured).
-    if (!halo_ && !(cfg_.flags & CBGX_SOLVER_NO_DICT_SPMV) && A_.max_row_nnz <= 64) {
+    // values and column offsets: 2 B per entry instead of 12 (single rank,
+    // or a halo in the window layout, which keeps the column offsets).
+    if ((!halo_ || halo_->window) && !(cfg_.flags & CBGX_SOLVER_NO_DICT_SPMV) && A_.max_row_nnz <= 64) {
         uint64_t db = 0, eb = 0;
         if (before_basis) {
             cbgx_basis tmp{};
@@ -197,7 +198,18 @@ void Solver::setup_matrix(bool before_basis, cudaStream_t st, const unsigned lon
         }
         if (!dict_) dict_ = std::make_unique<DictSell>();
         // reserve: the basis (when not allocated yet) + the solver vectors
-        if (build_dict_sell(A_, static_cast<double>(db + eb) + 8.0 * n_ * 8, st, *dict_)) return;
+        if (build_dict_sell(A_, static_cast<double>(db + eb) + 8.0 * n_ * 8, st, *dict_)) {
+            int_s0_ = int_s1_ = 0;
+            if (halo_ && comm_ && comm_->size() > 1 && dict_->ell8_w) {
+                // interior slices: every row of them has only own columns
+                uint64_t gb[2];
+                ghost_row_bounds(A_, halo_->own_offset(), gb, st);
+                int_s0_ = (gb[0] + 31) / 32;
+                int_s1_ = gb[1] / 32;
+                if (int_s0_ >= int_s1_) int_s0_ = int_s1_ = 0;
+            }
+            return;
+        }
     }
     uint32_t plan = 0;
     if (!(cfg_.flags & CBGX_SOLVER_NO_TMA_SPMV)) plan = stats ? plan_from_stats(stats) : plan_spmv_tiles(A_, st);
@@ -239,7 +251,11 @@ Solver::~Solver() {
     cudaFree(d_v_);
     cudaFree(d_w_);
     cudaFree(d_scal_);
+    cudaFree(d_pack_);
     cudaFreeHost(h_pinned_);
+    if (side_) cudaStreamDestroy(side_);
+    if (ev_v_) cudaEventDestroy(ev_v_);
+    if (ev_h_) cudaEventDestroy(ev_h_);
 }
 
 void Solver::spmv(const double* x, const double* b, double* y, double* norm, cudaStream_t st, bool pdl) {
@@ -247,6 +263,30 @@ void Solver::spmv(const double* x, const double* b, double* y, double* norm, cud
     else if (tile_rows_) launch_spmv_tma(A_, tile_rows_, x, b, y, norm, static_cast<int>(cfg_.reduction), &ws_, st, pdl);
     else if (sell_) launch_spmv_sell(A_, *sell_, x, b, y, norm, static_cast<int>(cfg_.reduction), &ws_, st);
     else launch_spmv(A_, x, b, y, norm, static_cast<int>(cfg_.reduction), &ws_, st);
+}
+
+void Solver::halo_spmv(double* v, double* y, double* norm, cudaStream_t st) {
+    if (int_s1_ > int_s0_ && dict_ && dict_->ready && dict_->ell8_w) {
+        if (!side_) {
+            CBGX_CUDA(cudaStreamCreateWithFlags(&side_, cudaStreamNonBlocking));
+            CBGX_CUDA(cudaEventCreateWithFlags(&ev_v_, cudaEventDisableTiming));
+            CBGX_CUDA(cudaEventCreateWithFlags(&ev_h_, cudaEventDisableTiming));
+        }
+        // exchange on the side stream once v is written; the interior rows
+        // meanwhile; then the boundary rows (norm partials added in a fixed
+        // order: interior, lower boundary, upper boundary)
+        CBGX_CUDA(cudaEventRecord(ev_v_, st));
+        CBGX_CUDA(cudaStreamWaitEvent(side_, ev_v_, 0));
+        halo_->exchange(v, side_);
+        CBGX_CUDA(cudaEventRecord(ev_h_, side_));
+        launch_spmv_pell_range(A_, *dict_, v, y, norm, int_s0_, int_s1_, false, &ws_, st);
+        CBGX_CUDA(cudaStreamWaitEvent(st, ev_h_, 0));
+        launch_spmv_pell_range(A_, *dict_, v, y, norm, 0, int_s0_, true, &ws_, st);
+        launch_spmv_pell_range(A_, *dict_, v, y, norm, int_s1_, dict_->nslices, true, &ws_, st);
+        return;
+    }
+    halo_->exchange(v, st);
+    spmv(v, nullptr, y, norm, st);
 }
 
 void Solver::reduce(double* d_vals, size_t count, cudaStream_t st) {
@@ -276,6 +316,9 @@ void Solver::solve(const double* d_b, const double* d_x0, double* d_x, cbgx_hist
     const double spmv_bytes = dict_ && dict_->ready ? dict_->code_bytes() + (dict_->ell_w ? 0.0 : (dict_->nslices + 1) * 8.0) + 16.0 * n
                                     : A_.nnz * 12.0 + (n + 1) * rp_bytes + 16.0 * n;
     const bool multi = comm_ && comm_->size() > 1;
+    // own rows of the SpMV input vector (after the lower ghosts in the
+    // halo's window layout)
+    const uint64_t vo = halo_ ? halo_->own_offset() : 0;
     uint64_t hist_len = 0;
     auto push = [&](uint64_t it, double rrn, bool ex) {
         if (hist && hist_len < hist->capacity) {
@@ -333,24 +376,20 @@ void Solver::solve(const double* d_b, const double* d_x0, double* d_x, cbgx_hist
             gate.hn1 = sl + kHn1;
             gate.omega2 = sl + kOmega;
             gate.eta = cfg_.eta;
-            if (halo_) {
-                timer.begin(CBGX_PHASE_COMM);
-                halo_->exchange(d_v_, st);
-                timer.end();
-            }
             // In the fused path the SpMV and the orthogonalisation are
             // programmatic dependent launches (each starts while the previous
             // kernel drains) unless phase timing puts events between them.
             const bool pdl = use_fused && !timer.on;
             timer.begin(CBGX_PHASE_SPMV);
-            spmv(d_v_, nullptr, d_w_, sl + kOmega, st, pdl);  // w = A v, omega^2
+            if (halo_) halo_spmv(d_v_, d_w_, sl + kOmega, st);  // halo exchange + w = A v, omega^2
+            else spmv(d_v_, nullptr, d_w_, sl + kOmega, st, pdl);  // w = A v, omega^2
             timer.end();
             count(CBGX_PHASE_SPMV, spmv_bytes);
             if (use_fused) {
                 // one cooperative launch: dot, update, gated second pass and
                 // the scaled write of column used+1, w register-resident
                 timer.begin(CBGX_PHASE_ORTHO);
-                const bool ok = launch_arnoldi_fused(V_, cols, d_w_, d_v_, sl, static_cast<uint32_t>(kU(m)), cfg_.eta,
+                const bool ok = launch_arnoldi_fused(V_, cols, d_w_, d_v_ + vo, sl, static_cast<uint32_t>(kU(m)), cfg_.eta,
                                                      static_cast<uint32_t>(m), d_hpinned_ + p * slot, pdl, &ws_, st);
                 timer.end();
                 if (!ok) throw Error(CBGX_EINTERNAL, "fused orthogonalisation became ineligible");
@@ -366,20 +405,30 @@ void Solver::solve(const double* d_b, const double* d_x0, double* d_x, cbgx_hist
                     timer.end();
                 }
                 timer.begin(CBGX_PHASE_UPDATE);
-                launch_cgs_update(V_, 0, cols, sl + kH, 1.0, d_w_, sl + kHn1, red, &ws_, st);  // w -= V h
+                // w -= V h; ||w||^2 (multi-rank: into the packed slot the
+                // second pass's partials follow)
+                double* pk = multi ? d_pack_ + p * (m + 2) : nullptr;
+                launch_cgs_update(V_, 0, cols, sl + kH, 1.0, d_w_, multi ? pk : sl + kHn1, red, &ws_, st);
                 timer.end();
                 count(CBGX_PHASE_UPDATE, cols * bpv * n + 16.0 * n);
                 if (multi) {
+                    // Second CGS pass run speculatively (re-orthogonalisation is
+                    // the rule on these problems), so hn1 and u cross the ranks
+                    // in ONE collective; the gate then decides on the device
+                    // whether update2 runs and the host whether u is used.
+                    timer.begin(CBGX_PHASE_DOT);
+                    launch_cgs_dot(V_, 0, cols, d_w_, 0, red, pk + 1, &ws_, st, GateArg{}, false);
+                    timer.end();
                     timer.begin(CBGX_PHASE_COMM);
-                    reduce(sl + kHn1, 1, st);
+                    comm_->sum_partials_split(pk, cols + 1, sl + kHn1, sl + kU(m), st);
+                    timer.end();
+                } else {
+                    // Second CGS pass, gated on the device by the reference's test
+                    // h_next < eta * omega (gmres.cpp:51-68); empty launches otherwise.
+                    timer.begin(CBGX_PHASE_DOT);
+                    launch_cgs_dot(V_, 0, cols, d_w_, 0, red, sl + kU(m), &ws_, st, gate, true);
                     timer.end();
                 }
-                // Second CGS pass, gated on the device by the reference's test
-                // h_next < eta * omega (gmres.cpp:51-68); empty launches otherwise.
-                timer.begin(CBGX_PHASE_DOT);
-                launch_cgs_dot(V_, 0, cols, d_w_, 0, red, sl + kU(m), &ws_, st, gate, !multi);
-                timer.end();
-                if (multi) reduce(sl + kU(m), cols, st);
                 timer.begin(CBGX_PHASE_UPDATE);
                 launch_cgs_update(V_, 0, cols, sl + kU(m), 1.0, d_w_, sl + kHn2, red, &ws_, st, gate);
                 timer.end();
@@ -393,7 +442,7 @@ void Solver::solve(const double* d_b, const double* d_x0, double* d_x, cbgx_hist
                 sc.mode = 2;
                 sc.gate = gate;
                 timer.begin(CBGX_PHASE_WRITE);
-                launch_basis_write(V_, used + 1, d_w_, sc, d_v_, nullptr, st);
+                launch_basis_write(V_, used + 1, d_w_, sc, d_v_ + vo, nullptr, st);
                 timer.end();
                 count(CBGX_PHASE_WRITE, 16.0 * n + bpv * n);
             }
@@ -409,7 +458,7 @@ void Solver::solve(const double* d_b, const double* d_x0, double* d_x, cbgx_hist
             timer.begin(CBGX_PHASE_RESIDUAL);
             const double* xin = d_x;
             if (halo_) {
-                CBGX_CUDA(cudaMemcpyAsync(d_v_, d_x, n * sizeof(double), cudaMemcpyDeviceToDevice, st));
+                CBGX_CUDA(cudaMemcpyAsync(d_v_ + vo, d_x, n * sizeof(double), cudaMemcpyDeviceToDevice, st));
                 halo_->exchange(d_v_, st);
                 xin = d_v_;
             }
@@ -437,7 +486,7 @@ void Solver::solve(const double* d_b, const double* d_x0, double* d_x, cbgx_hist
             ScaleArg sc0;
             sc0.src = rn;
             sc0.mode = 1;
-            launch_basis_write(V_, 0, d_r_, sc0, d_v_, nullptr, st);
+            launch_basis_write(V_, 0, d_r_, sc0, d_v_ + vo, nullptr, st);
             timer.end();
             count(CBGX_PHASE_WRITE, 16.0 * n + bpv * n);
 

@@ -23,6 +23,11 @@ struct Comm {
     // sum over ranks taken in rank order 0..P-1 (identical on every rank,
     // independent of the collective's algorithm).
     virtual void sum_partials(double* d_vals, size_t count, cudaStream_t st) = 0;
+    // The same combine for a packed vector d_src[0..count): the sum of
+    // element 0 goes to *d_first, of elements 1.. to d_rest[0..count-1)
+    // (two slots of the step that are not adjacent -- one collective).
+    virtual void sum_partials_split(const double* d_src, size_t count, double* d_first, double* d_rest,
+                                    cudaStream_t st) = 0;
     // Gather `bytes` from every rank into d_recv[rank * bytes].
     virtual void allgather(const void* d_send, void* d_recv, size_t bytes, cudaStream_t st) = 0;
     struct Msg {
@@ -47,8 +52,13 @@ struct Halo {
     std::vector<uint64_t> recv_offsets;   // into ghost region (size peers+1)
     int32_t* d_send_idx = nullptr;        // local row indices to pack
     double* d_send_buf = nullptr;
+    // window layout: the local vector is [win_lo ghosts | own rows | ghosts]
+    // (global rows [rb - win_lo, re + ...)); compact: [own rows | ghosts]
+    bool window = false;
+    uint64_t win_lo = 0;
+    uint64_t own_offset() const { return window ? win_lo : 0; }
     ~Halo();
-    void exchange(double* d_vec, cudaStream_t st) const;  // fills d_vec[n_local..)
+    void exchange(double* d_vec, cudaStream_t st) const;  // fills the ghost slots of d_vec
 };
 
 class Solver {
@@ -71,6 +81,10 @@ private:
     PhaseTimer* timer_ = nullptr;
     void reduce(double* d_vals, size_t count, cudaStream_t st);
     void spmv(const double* x, const double* b, double* y, double* norm, cudaStream_t st, bool pdl = false);
+    // Halo exchange of v + w = A v (+ ||w||^2): with a pair-coded window-
+    // layout matrix, the interior rows (no ghost columns) overlap the
+    // exchange, which runs on a side stream; otherwise exchange, then SpMV.
+    void halo_spmv(double* v, double* y, double* norm, cudaStream_t st);
     double fetch_scalar(const double* d, cudaStream_t st);
     void setup_matrix(bool before_basis, cudaStream_t st, const unsigned long long* stats = nullptr);
 
@@ -86,10 +100,16 @@ private:
     double* d_r_ = nullptr;
     double* d_v_ = nullptr;   // n + ghosts
     double* d_w_ = nullptr;
-    double* d_scal_ = nullptr;   // [0] omega^2 [1] hn^2 [2] ||b||^2 [3] ||r||^2 [4..] h / u / y
+    double* d_scal_ = nullptr;
+    double* d_pack_ = nullptr;   // multi-rank: per slot parity [hn1, u[0..m]] partials (one collective)   // [0] omega^2 [1] hn^2 [2] ||b||^2 [3] ||r||^2 [4..] h / u / y
     double* h_pinned_ = nullptr;
     double* d_hpinned_ = nullptr;  // device alias of the mapped h_pinned_
     cudaEvent_t step_ev_[2] = {nullptr, nullptr};
+    // interior slices [int_s0_, int_s1_) of the local matrix (no ghost
+    // columns) for the overlapped halo SpMV; side stream and its events
+    uint64_t int_s0_ = 0, int_s1_ = 0;
+    cudaStream_t side_ = nullptr;
+    cudaEvent_t ev_v_ = nullptr, ev_h_ = nullptr;
     int fused_state_ = 0;
     std::unique_ptr<Sell> sell_;
     std::unique_ptr<DictSell> dict_;  // dictionary-coded SELL-32 (preferred when it applies)

@@ -56,7 +56,9 @@ class NcclComm:
 
 class DistStencil:
     """This rank's rows of a 3-D stencil (generated on the device), columns
-    remapped to [own rows | ghosts] by a collective halo plan."""
+    remapped by a collective halo plan to the window layout [lower ghost
+    planes | own rows | upper ghost planes] (column offsets preserved, so the
+    dictionary SpMV applies) or, for other partitions, [own rows | ghosts]."""
 
     def __init__(self, comm: NcclComm, kind: int, nx: int, ny: int, nz: int, pe: float = 0.0):
         torch = _torch()
@@ -80,6 +82,9 @@ class DistStencil:
         del g64
         self.halo = h
         self.ghosts = L.cbgx_halo_ghosts(h)
+        # own rows' position in a local vector (window layout: after the
+        # lower ghost rows, cbgx_halo_own_offset)
+        self.own_off = L.cbgx_halo_own_offset(h)
         self.A = DeviceCsr(rows, rows + self.ghosts, rp, lci, va)
         self.comm = comm
 
@@ -93,11 +98,12 @@ class DistStencil:
         xs = np.empty(rows, np.float64)
         check(lib().cbgx_sin_solution(self.n, self.rb, rows, xs.ctypes.data, 0))
         xe = torch.zeros(rows + self.ghosts, dtype=torch.float64, device="cuda")
-        xe[:rows] = torch.from_numpy(xs).cuda()
+        o = self.own_off
+        xe[o:o + rows] = torch.from_numpy(xs).cuda()
         self.halo_exchange(xe)
         b = torch.empty(max(rows, 1), dtype=torch.float64, device="cuda")
         check(lib().cbgx_csr_spmv(ctypes.byref(self.A.desc), _ptr(xe), _ptr(b), None, 0, None, _stream()))
-        return b[:rows], xe[:rows]
+        return b[:rows], xe[o:o + rows]
 
     def __del__(self):
         try:

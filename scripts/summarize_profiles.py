@@ -51,7 +51,7 @@ for f in sorted(os.listdir(run)):
     elif f.endswith(".csv") and "launch" in f:
         shutil.copy(p, os.path.join(out, f))
         s = subprocess.run([sys.executable, "scripts/launch_stats.py", p], capture_output=True, text=True).stdout
-        md += ["## launch list (one timed solve + setup; cold-cache, serialised)", "", "```", s.strip(), "```", ""]
+        md += ["## launch list (TWO solves -- scripts/one_solve.py runs one warm-up and one timed solve -- plus setup; cold-cache, serialised: divide the counts by 2 per solve)", "", "```", s.strip(), "```", ""]
     elif f.endswith(".json") or f.endswith(".txt"):
         shutil.copy(p, os.path.join(out, f))
 with open(os.path.join(out, "SUMMARY.md"), "w") as fh:

@@ -56,8 +56,10 @@ def _worker(rank, world, port, kind, dims, out_q):
         ghosts = np.zeros(max(nnz, 1), np.int64)
         ng = ctypes.c_uint64()
         need = np.zeros(world, np.uint64)
+        own = ctypes.c_uint64()
         _lib.check(L.cbgx_halo_plan(world, rank, ranges.ctypes.data, n, gcols.ctypes.data, nnz,
-                                    lcols.ctypes.data, ghosts.ctypes.data, ctypes.byref(ng), need.ctypes.data))
+                                    lcols.ctypes.data, ghosts.ctypes.data, ctypes.byref(ng), need.ctypes.data,
+                                    ctypes.byref(own)))
         ghosts = ghosts[:ng.value]
         # requests grouped by owner (ghosts are sorted by global index)
         owner = np.searchsorted(ranges[0::2].astype(np.int64), ghosts, side="right") - 1
@@ -82,7 +84,16 @@ def _worker(rank, world, port, kind, dims, out_q):
         ghost_vals = np.concatenate([all_sends[o][rank] for o in range(world) if o != rank and o in reqs
                                      and len(reqs[o])] or [np.zeros(0)])
         assert np.array_equal(ghost_vals, x[ghosts])
-        x_ext = np.concatenate([x_local, ghost_vals])
+        o = own.value
+        if o:
+            # window layout: the local vector is the global rows [rb - o, re + ...),
+            # so every column offset survives the remap (shifted by o)
+            x_ext = np.concatenate([ghost_vals[:o], x_local, ghost_vals[o:]])
+            assert np.array_equal(x_ext, x[rb - o:rb - o + x_ext.size])
+            lr = np.repeat(np.arange(re_ - rb), np.diff(rp[rb:re_ + 1]).astype(np.int64))
+            assert np.array_equal(lcols[:nnz].astype(np.int64) - lr - o, gcols - (lr + rb))
+        else:
+            x_ext = np.concatenate([x_local, ghost_vals])
         # local SpMV with the oracle's row-sequential kernel on remapped columns
         lrp = (rp[rb:re_ + 1] - rp[rb]).astype(np.uint64)
         y_local = P.spmv(lrp, lcols[:nnz].astype(np.uint64), np.ascontiguousarray(va[k0:k1]), x_ext)
@@ -100,9 +111,9 @@ def _worker(rank, world, port, kind, dims, out_q):
         assert len(set(combined)) == 1
         ref = P.dot(y_global, y_global)
         assert abs(out[0] - ref) <= 1e-12 * abs(ref)
-        out_q.put((rank, "ok", int(ng.value)))
+        out_q.put((rank, "ok", int(ng.value), int(o)))
     except Exception as e:  # noqa: BLE001
-        out_q.put((rank, repr(e), 0))
+        out_q.put((rank, repr(e), 0, 0))
         raise
     finally:
         dist.destroy_process_group()
@@ -122,6 +133,9 @@ def test_partitioned_halo_and_reduction(kind, dims, world):
     assert all(r[1] == "ok" for r in res), res
     assert all(p.exitcode == 0 for p in procs)
     assert sum(r[2] for r in res) > 0   # some ghosts actually crossed ranks
+    # z-slab partitions of 3-D stencils take the window layout on every rank
+    # that has a lower neighbour
+    assert all(r[3] > 0 for r in res if r[0] > 0), res
 
 
 def test_row_blocks():

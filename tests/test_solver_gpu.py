@@ -189,12 +189,16 @@ def test_device_solver_determinism(cbg, port):
     assert r1.solution.cpu().numpy().tobytes() == r2.solution.cpu().numpy().tobytes()
 
 
-@pytest.mark.parametrize("parts", [2, 3, 4])
-def test_partitioned_local_matches_single(cbg, port, parts):
-    """P row blocks as P threads on one GPU (in-process communicator)."""
+@pytest.mark.parametrize("parts,edge", [(2, 16), (3, 16), (4, 16), (8, 16), (8, 128)])
+def test_partitioned_local_matches_single(cbg, port, parts, edge):
+    """P row blocks as P threads on one GPU (in-process communicator). The
+    row blocks of a 3-D stencil take the window halo layout (cbgx.h
+    cbgx_halo_own_offset), so every rank runs the pair-coded dictionary
+    SpMV with the interior rows split from the boundary ones -- the same
+    code path as P GPUs over NCCL; the config-2 size at P = 8 included."""
     import ctypes
     from paper_2409_15468_b200 import _lib
-    rp, ci, va = port.stencil(0, 16, 16, 16)
+    rp, ci, va = port.stencil(0, edge, edge, edge)
     b, _ = port.generate_problem(rp, ci, va)
     n = rp.size - 1
     cfg = cbg.GmresConfig(restart=30, storage_format=cbg.StorageFormat.frsz2_format(32))
