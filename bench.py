@@ -398,11 +398,13 @@ def run_ours(args):
                 l2="inputs larger than L2: per solve the basis grows to %.0f MB (up to %.0f MB at m=100) "
                    "plus the matrix (%s) vs 126 MB L2; no explicit flush"
                    % (last.total_iterations * bpv * rows / 1e6, 101 * bpv * rows / 1e6,
-                      "2-byte dictionary codes, ~%.0f MB" % (2 * 4 * -(-nnz // (4 * rows)) * rows / 1e6) if world == 1
-                      else "CSR %.0f MB" % ((nnz * 12 + 4 * (rows + 1)) / 1e6)),
-                spmv=("dictionary-coded ELL4 copy of the CSR (<=255 distinct values and column offsets; "
-                      "bit-identical to the CSR SpMV), built at setup" if world == 1
-                      else "CSR with halo exchange (row partition)")),
+                      "1-byte dictionary codes, ~%.0f MB" % (8 * -(-nnz // (8 * rows)) * rows / 1e6) if world == 1
+                      else "1-byte dictionary codes per rank"),
+                spmv=("pair-coded dictionary ELL8 copy of the CSR (1-byte codes into <=255 distinct (value, "
+                      "column offset) pairs; bit-identical to the CSR SpMV), built at setup" if world == 1
+                      else "pair-coded dictionary copy of each rank's rows in the window halo layout "
+                           "[lower ghost planes | own rows | upper ghost planes]; interior rows overlap the "
+                           "NCCL halo exchange")),
             "iterations": last.total_iterations,
             "restarts": last.restarts,
             "final_rrn": last.final_rrn,

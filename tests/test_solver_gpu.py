@@ -214,6 +214,10 @@ def test_partitioned_local_matches_single(cbg, port, parts, edge):
     assert r.converged
     assert abs(r.total_iterations - single.total_iterations) <= 2
     assert np.allclose(r.solution, single.solution, rtol=1e-7, atol=1e-12)
+    # rank 0 streamed dictionary codes, not CSR (12 B per entry): the window
+    # halo layout kept the column offsets
+    nnz0 = int(rp[-1]) / parts
+    assert st.phase_bytes[0] / max(st.phase_launches[0], 1) < 6.0 * nnz0
 
 
 def _ragged_csr(rng, n, max_len, empty_frac=0.1, long_rows=()):
