@@ -366,6 +366,10 @@ int cbgx_debug_fused_rotation(uint32_t rot);
  * partial vector is all-gathered and summed in rank order (deterministic,
  * identical on all ranks); SpMV ghosts move by a halo exchange. */
 int cbgx_nccl_unique_id(uint8_t out[128]);
+/* P communicators of one process, rank r driven by its own host thread (an
+ * in-process stand-in for P GPUs: copies instead of NCCL, the same halo,
+ * overlap and collective code paths) -- out[0..nranks). For tests. */
+int cbgx_comm_create_local_group(int nranks, cbgx_comm** out);
 int cbgx_comm_create_nccl(const uint8_t unique_id[128], int nranks, int rank,
                           cbgx_comm** out);
 int cbgx_comm_destroy(cbgx_comm* c);

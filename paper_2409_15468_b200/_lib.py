@@ -113,6 +113,7 @@ def lib():
             "cbgx_gmres_solve_host": ([u64, vp, vp, vp, vp, vp, P(GmresConfig), vp, P(History), P(SolveStats)], C.c_int),
             "cbgx_nccl_unique_id": ([vp], C.c_int),
             "cbgx_comm_create_nccl": ([vp, C.c_int, C.c_int, P(vp)], C.c_int),
+            "cbgx_comm_create_local_group": ([C.c_int, vp], C.c_int),
             "cbgx_comm_destroy": ([vp], C.c_int),
             "cbgx_comm_rank": ([vp, P(C.c_int), P(C.c_int)], C.c_int),
             "cbgx_halo_create": ([vp, u64, u64, u64, vp, u64, vp, P(vp)], C.c_int),

@@ -451,6 +451,14 @@ int cbgx_comm_create_nccl(const uint8_t uid[128], int nranks, int rank, cbgx_com
     });
 }
 
+int cbgx_comm_create_local_group(int nranks, cbgx_comm** out) {
+    return guard([&] {
+        if (!out || nranks < 1) throw Error(CBGX_EINVAL, "comm: bad arguments");
+        auto shared = std::make_shared<LocalShared>(nranks);
+        for (int r = 0; r < nranks; ++r) out[r] = new cbgx_comm{std::make_unique<LocalComm>(shared, r)};
+    });
+}
+
 int cbgx_comm_destroy(cbgx_comm* c) {
     return guard([&] { delete c; });
 }

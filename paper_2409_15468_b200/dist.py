@@ -54,6 +54,27 @@ class NcclComm:
             pass
 
 
+class LocalComms:
+    """P in-process communicators (cbgx_comm_create_local_group): rank r is
+    driven by its own host thread on the current device -- exercises the
+    NCCL path's halo / overlap / collective code on one GPU."""
+
+    class _One:
+        def __init__(self, h, rank, world):
+            self.h, self.rank, self.world = h, rank, world
+
+        def __del__(self):
+            try:
+                lib().cbgx_comm_destroy(self.h)
+            except Exception:
+                pass
+
+    def __init__(self, world: int):
+        arr = (ctypes.c_void_p * world)()
+        check(lib().cbgx_comm_create_local_group(world, arr))
+        self.comms = [LocalComms._One(ctypes.c_void_p(arr[r]), r, world) for r in range(world)]
+
+
 class DistStencil:
     """This rank's rows of a 3-D stencil (generated on the device), columns
     remapped by a collective halo plan to the window layout [lower ghost
