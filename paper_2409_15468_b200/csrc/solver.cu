@@ -597,7 +597,7 @@ cbgx_gmres_config checked(const cbgx_gmres_config* cfg) {
 struct HostSolveCache {
     std::mutex mu;
     cudaStream_t st = nullptr, st2 = nullptr;
-    cudaEvent_t ev_idx = nullptr, ev_narrow = nullptr;
+    cudaEvent_t ev_idx = nullptr, ev_narrow = nullptr, ev_va = nullptr, ev_setup = nullptr;
     uint64_t cap_n = 0, cap_nnz = 0;
     uint64_t* d_rp64 = nullptr;
     uint64_t* d_ci64 = nullptr;
@@ -629,8 +629,10 @@ struct HostSolveCache {
         if (st2) cudaStreamDestroy(st2);
         if (ev_idx) cudaEventDestroy(ev_idx);
         if (ev_narrow) cudaEventDestroy(ev_narrow);
+        if (ev_va) cudaEventDestroy(ev_va);
+        if (ev_setup) cudaEventDestroy(ev_setup);
         st = st2 = nullptr;
-        ev_idx = ev_narrow = nullptr;
+        ev_idx = ev_narrow = ev_va = ev_setup = nullptr;
     }
     void ensure(uint64_t n, uint64_t nnz, bool wide) {
         (void)wide;
@@ -638,6 +640,8 @@ struct HostSolveCache {
         if (!st2) CBGX_CUDA(cudaStreamCreateWithFlags(&st2, cudaStreamNonBlocking));
         if (!ev_idx) CBGX_CUDA(cudaEventCreateWithFlags(&ev_idx, cudaEventDisableTiming));
         if (!ev_narrow) CBGX_CUDA(cudaEventCreateWithFlags(&ev_narrow, cudaEventDisableTiming));
+        if (!ev_va) CBGX_CUDA(cudaEventCreateWithFlags(&ev_va, cudaEventDisableTiming));
+        if (!ev_setup) CBGX_CUDA(cudaEventCreateWithFlags(&ev_setup, cudaEventDisableTiming));
         if (!h_bad) CBGX_CUDA(cudaMallocHost(&h_bad, 6 * sizeof(uint64_t)));
         if (n <= cap_n && nnz <= cap_nnz && d_bad) return;
         solver.reset();  // it points into the buffers
@@ -744,24 +748,31 @@ int cbgx_gmres_solve_host(uint64_t n, const uint64_t* row_ptrs, const uint64_t* 
         cbgx_csr A{n, n, nnz, d_rp, wide ? 64u : 32u, H.d_ci, H.d_va};
         // the SpMV set-up statistics ride along with the range check: one sync
         launch_csr_stats(A, reinterpret_cast<unsigned long long*>(H.d_bad + 1), H.st2);
-        CBGX_CUDA(cudaEventRecord(H.ev_narrow, H.st2));
         CBGX_CUDA(cudaMemcpyAsync(H.d_va, values, nnz * 8, cudaMemcpyHostToDevice, st));
+        CBGX_CUDA(cudaEventRecord(H.ev_va, st));
         CBGX_CUDA(cudaMemcpyAsync(H.d_b, b, n * 8, cudaMemcpyHostToDevice, st));
         CBGX_CUDA(cudaMemcpyAsync(H.d_x0, x0, n * 8, cudaMemcpyHostToDevice, st));
         if (prof) CBGX_CUDA(cudaStreamSynchronize(st));
         const auto t1 = tnow();
-        CBGX_CUDA(cudaStreamWaitEvent(st, H.ev_narrow, 0));
-        CBGX_CUDA(cudaMemcpyAsync(H.h_bad, H.d_bad, 6 * 8, cudaMemcpyDeviceToHost, st));
-        CBGX_CUDA(cudaStreamSynchronize(st));
+        // the range check and statistics (second stream) while b and x0 still
+        // upload on the first
+        CBGX_CUDA(cudaMemcpyAsync(H.h_bad, H.d_bad, 6 * 8, cudaMemcpyDeviceToHost, H.st2));
+        CBGX_CUDA(cudaStreamSynchronize(H.st2));
         if (*H.h_bad) throw Error(CBGX_EINVAL, "csr: column index out of range");
         const unsigned long long* csr_stats = reinterpret_cast<const unsigned long long*>(H.h_bad + 1);
         const auto t2 = tnow();
         // One solver per configuration and shape, kept between calls (its
         // basis, vectors and workspaces); only the matrix-dependent SpMV
-        // state is recomputed for the new contents.
+        // state is recomputed for the new contents -- on the second stream,
+        // once the values are in, overlapped with the b / x0 upload.
         if (H.solver && H.solver->rows() == n && same_config(H.solver->config(), c)) {
-            H.solver->rebind(A, st, csr_stats);
+            CBGX_CUDA(cudaStreamWaitEvent(H.st2, H.ev_va, 0));
+            H.solver->rebind(A, H.st2, csr_stats);
+            CBGX_CUDA(cudaEventRecord(H.ev_setup, H.st2));
+            CBGX_CUDA(cudaStreamWaitEvent(st, H.ev_setup, 0));
         } else {
+            // a new solver sets itself up on the legacy stream: everything first
+            CBGX_CUDA(cudaStreamSynchronize(st));
             H.solver.reset();
             H.solver = std::make_unique<Solver>(A, c, nullptr, nullptr);
         }
