@@ -1,8 +1,10 @@
 """Small end-to-end exercise of every kernel family for compute-sanitizer:
-codec (3 fast formats + generic), basis write/read, split CGS, fused
-orthogonalisation, staged / plain / SELL /
-dictionary SpMV (ELL4 and ragged SELL layouts, build + apply), read sweep,
-host drop-in solve."""
+codec (3 fast formats + generic), basis write/read (+ exponent ranges),
+split CGS, fused orthogonalisation (fast and exact columns, one fused step
+through the C-ABI), staged / plain / SELL / dictionary SpMV (2-byte ELL4,
+ragged SELL, 1-byte pair codes, slice ranges), read sweep, host drop-in
+solve, partitioned solve on in-process ranks (window halo, overlapped
+interior SpMV, merged collectives)."""
 import sys
 
 import numpy as np
@@ -68,5 +70,33 @@ try:
     Dr.spmv(torch.from_numpy(rng.standard_normal(nr)).cuda(), want_norm=True)
 except Exception as e:  # many distinct offsets: refused (still exercises the scan kernel)
     print("dict refused:", e)
+# one fused Arnoldi step with a tiny-block column (exact decoder) and an
+# all-zero block (clamped fast scale)
+n5 = 40000
+B5 = cbg.KrylovBasis(n5, 8, cbg.StorageFormat.parse("frsz2-32"))
+cols = rng.standard_normal((4, n5))
+cols[1, 32:64] *= 1e-300
+cols[2, 64:96] = 0.0
+for j in range(4):
+    B5.write_vector(j, cols[j])
+w5 = torch.from_numpy(rng.standard_normal(n5)).cuda()
+B5.arnoldi_fused_step(4, w5, float((w5 * w5).sum()), 7)
+# partitioned solve: P ranks as threads (halo, pell slice ranges, merged collectives)
+import ctypes  # noqa: E402
+from paper_2409_15468_b200 import _lib  # noqa: E402
+from oracle import pyoracle as po  # noqa: E402
+P = po.Port()
+rp, ci, va = P.stencil(0, 16, 16, 16)
+bb, _ = P.generate_problem(rp, ci, va)
+nn = rp.size - 1
+cfg = cbg.GmresConfig(restart=20, storage_format=cbg.StorageFormat.parse("frsz2-32"), max_total_iterations=40)
+xx = np.zeros(nn)
+h, bufs = cbg._history_buffers(2 * cfg.max_total_iterations + 4)
+st = _lib.SolveStats()
+c = cfg.c()
+_lib.check(_lib.lib().cbgx_gmres_solve_partitioned_local(nn, rp.ctypes.data, ci.ctypes.data, va.ctypes.data,
+                                                         bb.ctypes.data, np.zeros(nn).ctypes.data, ctypes.byref(c),
+                                                         3, xx.ctypes.data, ctypes.byref(h), ctypes.byref(st)))
+print("partitioned", st.total_iterations, flush=True)
 torch.cuda.synchronize()
 print("sanitize_small done")
