@@ -229,20 +229,11 @@ __device__ __forceinline__ void unpack8(uint2 a, uint2 b, uint16_t (&c)[8]) {
 // MODE 0: y = A x.  MODE 1: y = b - A x. Persistent grid (one wave), one
 // warp per 32-row slice. kEll: ELL4 layout (uniform width, 8-byte groups of
 // 4 codes, no offset table).
-#ifndef DSELL_PADFREE
-#define DSELL_PADFREE 1
-#endif
 #ifndef DSELL_SPMV_THREADS
 #define DSELL_SPMV_THREADS 256
 #endif
-#ifndef DSELL_CODES_LDG
-#define DSELL_CODES_LDG 0  // 0: streaming (evict-first) code loads
-#endif
-#if DSELL_CODES_LDG
-#define CLD(p) __ldg(p)
-#else
+// the codes stream once per SpMV: evict-first loads (L1-cached __ldg measured neutral)
 #define CLD(p) __ldcs(p)
-#endif
 constexpr int kST = DSELL_SPMV_THREADS;
 constexpr int kSW = kST / 32;
 #ifndef DSELL_MIN_BLOCKS
@@ -294,7 +285,6 @@ dsell_spmv_kernel(uint64_t n_rows, const uint64_t* __restrict__ soff, uint32_t e
                 if (g4 > 1) n1 = CLD(c4 + (nx * g4 + 1) * 32 + lane);
             }
             double s = 0.0;
-#if DSELL_PADFREE
             // Padding codes decode to (offset 0, value +0.0): the gather reads
             // x[r] (clamped into range for the rows past n) and adds 0 * x[r]
             // = +-0, which leaves s unchanged (s starts at +0.0 and is never
@@ -302,7 +292,6 @@ dsell_spmv_kernel(uint64_t n_rows, const uint64_t* __restrict__ soff, uint32_t e
             // (which a non-finite x[r] under a padding code could cause) is
             // recomputed exactly below.
             const int32_t rc = static_cast<uint64_t>(r) < n_rows ? r : static_cast<int32_t>(n_rows - 1);
-#endif
             for (uint32_t g = 0; g < g4; g += 2) {
                 if (g) {
                     a0 = CLD(c4 + (sl * g4 + g) * 32 + lane);
@@ -312,17 +301,12 @@ dsell_spmv_kernel(uint64_t n_rows, const uint64_t* __restrict__ soff, uint32_t e
                 }
                 uint16_t c[8];
                 unpack8(a0, a1, c);
-#if DSELL_PADFREE
                 double xv[8];
 #pragma unroll
                 for (int i = 0; i < 8; ++i) xv[i] = __ldg(x + (rc + s_o[c[i] & 0xFF]));
 #pragma unroll
                 for (int i = 0; i < 8; ++i) s = __dadd_rn(s, __dmul_rn(s_v[c[i] >> 8], xv[i]));
-#else
-                s = batch8(c, r, s_o, s_v, x, s);
-#endif
             }
-#if DSELL_PADFREE
             if (isnan(s) && static_cast<uint64_t>(r) < n_rows) {
                 s = 0.0;
                 for (uint32_t g = 0; g < g4; g += 2) {
@@ -334,7 +318,6 @@ dsell_spmv_kernel(uint64_t n_rows, const uint64_t* __restrict__ soff, uint32_t e
                     s = batch8(c, r, s_o, s_v, x, s);
                 }
             }
-#endif
             if (static_cast<uint64_t>(r) < n_rows) {
                 if (MODE == 1) s = __dsub_rn(__ldg(b + r), s);
                 y[r] = s;
