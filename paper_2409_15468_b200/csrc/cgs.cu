@@ -1323,6 +1323,9 @@ struct FusedArgs {
     unsigned char* out_pay;    // column `cols` payload / values
     uint32_t* out_exp;         // column `cols` exponents (FRSZ2)
     uint32_t* out_erange;      // column `cols` exponent range (nullptr: not kept)
+    unsigned long long* fx;      // this launch's fixed-point accumulators: 2 regions + flag
+    unsigned long long* fx_next; // the next launch's set: zeroed here (CTA 0)
+    uint32_t fx_region;          // words per region (3 x (max_cols + 2))
     const double* w;           // SpMV output (rows [0, n))
     double* v_out;             // next SpMV input
     double* slot;              // [hn1, hn2, omega2, h[0..m], u[0..m]]; omega2 set by the SpMV
@@ -1389,6 +1392,86 @@ __device__ __forceinline__ void fused_rows(uint64_t n, uint32_t rot, uint64_t& r
     r1 = u1 * kUnitRows;
 }
 
+// ------------------------------------------- fixed-point grid reductions
+// The fused kernel's two grid reductions (h; u and hn1) are also accumulated
+// as exact fixed-point sums: a CTA partial p becomes the integer
+// X = p * 2^(kFxF - e) (truncated below the resolution 2^(e - kFxF), e a
+// per-value scale exponent fixed before the launch from omega), split into
+// three signed 42-bit chunks, each added with one red.global.add.u64 into its
+// own 64-bit word (296 chunks < 2^51: no word overflows). Integer addition is
+// associative, so the sums are exact, deterministic and independent of the
+// arrival order; after the barrier every CTA reads 3 words per value (ONE
+// load batch instead of the value-major table's 2-19, by k) and rounds the
+// 126-bit integer to double once. A partial >= 2^(e+6), a non-finite
+// partial, a non-positive or non-finite omega^2, or an hn1 too small for 50
+// significant bits sends every CTA (uniformly: the same flag and sums) to
+// the value-major table path, which is always written too.
+constexpr int kFxF = 110;
+constexpr unsigned long long kFxM = (1ull << 42) - 1;
+
+__device__ __forceinline__ bool fx_split(double p, int e, long long c[3]) {
+    const unsigned long long bits = static_cast<unsigned long long>(__double_as_longlong(p));
+    c[0] = c[1] = c[2] = 0;
+    if (p == 0.0) return true;
+    int ex = static_cast<int>((bits >> 52) & 0x7FF);
+    if (ex == 0x7FF) return false;
+    unsigned long long m = bits & ((1ull << 52) - 1);
+    if (ex) m |= 1ull << 52;
+    else ex = 1;
+    const int sh = ex - 1075 + kFxF - e;  // X = m * 2^sh, X < 2^116 for sh <= 63
+    if (sh > 63) return false;
+    unsigned long long lo = 0, hi = 0;
+    if (sh >= 0) {
+        lo = m << sh;
+        hi = sh ? m >> (64 - sh) : 0ull;
+    } else if (sh > -64) {
+        lo = m >> (-sh);
+    }
+    const long long q0 = static_cast<long long>(lo & kFxM), q1 = static_cast<long long>(((lo >> 42) | (hi << 22)) & kFxM),
+                    q2 = static_cast<long long>(hi >> 20);
+    const bool neg = bits >> 63;
+    c[0] = neg ? -q0 : q0;
+    c[1] = neg ? -q1 : q1;
+    c[2] = neg ? -q2 : q2;
+    return true;
+}
+
+// w0 + w1 2^42 + w2 2^84, rounded to nearest-even, times 2^(e - kFxF).
+// Sets *small when |X| < 2^60 (fewer than 50 significant bits above the
+// truncation noise of 296 partials).
+__device__ __forceinline__ double fx_join(long long w0, long long w1, long long w2, int e, bool* small) {
+    const __int128 X = static_cast<__int128>(w0) + (static_cast<__int128>(w1) << 42) + (static_cast<__int128>(w2) << 84);
+    if (X == 0) {
+        *small = true;
+        return 0.0;
+    }
+    const bool neg = X < 0;
+    const unsigned __int128 M = neg ? -static_cast<unsigned __int128>(X) : static_cast<unsigned __int128>(X);
+    const unsigned long long hi = static_cast<unsigned long long>(M >> 64), lo = static_cast<unsigned long long>(M);
+    const int top = hi ? 127 - __clzll(static_cast<long long>(hi)) : 63 - __clzll(static_cast<long long>(lo));
+    *small = top < 60;
+    double v;
+    if (top <= 52) {
+        v = static_cast<double>(lo);  // exact
+        v = ldexp(v, e - kFxF);
+    } else {
+        const int shift = top - 52;
+        unsigned long long mant = static_cast<unsigned long long>(M >> shift);
+        const unsigned __int128 rem = M & ((static_cast<unsigned __int128>(1) << shift) - 1);
+        const unsigned __int128 half = static_cast<unsigned __int128>(1) << (shift - 1);
+        if (rem > half || (rem == half && (mant & 1ull))) ++mant;  // 2^53 stays exact
+        v = ldexp(static_cast<double>(mant), shift + e - kFxF);
+    }
+    return neg ? -v : v;
+}
+
+__device__ __forceinline__ void fx_red(unsigned long long* w, const long long c[3]) {
+#pragma unroll
+    for (int i = 0; i < 3; ++i)
+        asm volatile("red.relaxed.gpu.global.add.u64 [%0], %1;" ::"l"(w + i), "l"(static_cast<unsigned long long>(c[i]))
+                     : "memory");
+}
+
 // Grid all-reduce among the consumer warps of all (co-resident) CTAs, one
 // barrier hop. Partials are value-major: value k of CTA c at
 // region[k * gs + c]. Thread 0 arrives with a release add on the launch's
@@ -1398,9 +1481,7 @@ __device__ __forceinline__ void fused_rows(uint64_t n, uint32_t rot, uint64_t& r
 // 16-B pairs g, g+R, ... (loads batched so they are all in flight), then a
 // butterfly over the R lanes -- so all CTAs hold bit-identical results and
 // nobody waits for another CTA to publish them. count <= kFConsumers.
-__device__ __forceinline__ void grid_allreduce(unsigned* bar, unsigned seq, const double* region, uint32_t gs,
-                                               uint32_t count, double* out_smem,
-                                               unsigned long long* trace = nullptr) {
+__device__ __forceinline__ void grid_barrier(unsigned* bar, unsigned seq, unsigned long long* trace) {
     consumer_sync();
     if (threadIdx.x == 0) {
         if (CBGX_FUSED_TRACE && trace && blockIdx.x == 0) trace[11 + 2 * seq] = global_ns();
@@ -1409,6 +1490,10 @@ __device__ __forceinline__ void grid_allreduce(unsigned* bar, unsigned seq, cons
         if (CBGX_FUSED_TRACE && trace && blockIdx.x == 0) trace[12 + 2 * seq] = global_ns();
     }
     consumer_sync();
+}
+
+// The value-major table reduction (after the barrier).
+__device__ __forceinline__ void table_reduce(const double* region, uint32_t gs, uint32_t count, double* out_smem) {
     uint32_t R = 32;
     while (R > 1 && R * count > static_cast<uint32_t>(kFConsumers)) R >>= 1;
     const uint32_t t = threadIdx.x, k = t / R, g = t % R;
@@ -1437,6 +1522,49 @@ __device__ __forceinline__ void grid_allreduce(unsigned* bar, unsigned seq, cons
     for (uint32_t off = R >> 1; off >= 1; off >>= 1) v = __dadd_rn(v, __shfl_xor_sync(0xFFFFFFFFu, v, off));
     if (g == 0 && k < count) out_smem[k] = v;
     consumer_sync();
+}
+
+__device__ __forceinline__ void grid_allreduce(unsigned* bar, unsigned seq, const double* region, uint32_t gs,
+                                               uint32_t count, double* out_smem,
+                                               unsigned long long* trace = nullptr) {
+    grid_barrier(bar, seq, trace);
+    table_reduce(region, gs, count, out_smem);
+}
+
+// Fixed-point variant: `acc` holds the count x 3 accumulator words, `flag`
+// the overflow word (bit `fbit`), values k < count use scale exponent e,
+// value `nlast` (if < count) e_last and must keep 50 significant bits.
+// fx_ok == false (scales unusable this launch): table path.
+__device__ __forceinline__ void grid_allreduce_fx(unsigned* bar, unsigned seq, const double* region, uint32_t gs,
+                                                  uint32_t count, double* out_smem, const unsigned long long* acc,
+                                                  const unsigned long long* flag, unsigned fbit, bool fx_ok, int e,
+                                                  uint32_t nlast, int e_last, volatile int* s_flag,
+                                                  unsigned long long* trace = nullptr) {
+    grid_barrier(bar, seq, trace);
+    if (fx_ok) {
+        const uint32_t t = threadIdx.x;
+        long long w0 = 0, w1 = 0, w2 = 0;
+        unsigned long long f = 0;
+        if (t < count) {
+            w0 = static_cast<long long>(__ldcg(acc + 3 * t));
+            w1 = static_cast<long long>(__ldcg(acc + 3 * t + 1));
+            w2 = static_cast<long long>(__ldcg(acc + 3 * t + 2));
+        }
+        if (t == count) f = __ldcg(flag);
+        bool small = false;
+        double v = 0.0;
+        if (t < count) v = fx_join(w0, w1, w2, t == nlast ? e_last : e, &small);
+        if (t == count) *s_flag = (f >> fbit) & 1ull ? 1 : 0;
+        consumer_sync();
+        if (t == nlast && small) *s_flag = 1;
+        consumer_sync();
+        if (*s_flag == 0) {
+            if (t < count) out_smem[t] = v;
+            consumer_sync();
+            return;
+        }
+    }
+    table_reduce(region, gs, count, out_smem);
 }
 
 // CTA sum of one value per consumer thread (warp butterflies, then the warp
@@ -1683,12 +1811,19 @@ __device__ __forceinline__ void fused_pass_any(uint32_t cols, uint32_t lim, uint
 
 // This CTA's dot-pass partials (red[warp][j] summed over warps in order)
 // into the value-major region: region[j * gs + cta].
-__device__ __forceinline__ void dot_partials_out(const double* red, uint32_t cols, double* region, uint32_t gs) {
+__device__ __forceinline__ void dot_partials_out(const double* red, uint32_t cols, double* region, uint32_t gs,
+                                                 unsigned long long* acc = nullptr, unsigned long long* flag = nullptr,
+                                                 unsigned fbit = 0, int e = 0) {
     consumer_sync();
     for (uint32_t j = threadIdx.x; j < cols; j += kFConsumers) {
         double s = red[j];
         for (int w = 1; w < kFWarps; ++w) s = __dadd_rn(s, red[w * cols + j]);
         region[static_cast<uint64_t>(j) * gs + blockIdx.x] = s;
+        if (acc) {
+            long long c[3];
+            if (fx_split(s, e, c)) fx_red(acc + 3 * j, c);
+            else atomicOr(flag, 1ull << fbit);
+        }
     }
 }
 
@@ -1740,6 +1875,13 @@ __global__ void __launch_bounds__(kFThreads, kFCtasPerSM) arnoldi_fused_kernel(F
         for (uint32_t k = threadIdx.x; k < 2 * cols; k += kFThreads) ers_s[k] = a.B.erange[k];
         if (blockIdx.x == 0 && threadIdx.x < 2) a.out_erange[threadIdx.x] = 0u;
     }
+    // the next launch's fixed-point accumulators (it starts after this grid)
+    if (blockIdx.x == 0)
+        for (uint32_t k = threadIdx.x; k < 2 * a.fx_region + 1; k += kFThreads) a.fx_next[k] = 0ull;
+    // omega^2 (from the SpMV epilogue) kept in shared memory: the gate and
+    // the fixed-point scales need it (a register would be spilled and a
+    // global reload costs an L2 round trip on the critical path)
+    if (threadIdx.x == 0) scal[1] = a.slot[2];
     __syncthreads();
     uint64_t r0, r1;
     fused_rows(a.B.n, a.rot, r0, r1);
@@ -1799,6 +1941,16 @@ __global__ void __launch_bounds__(kFThreads, kFCtasPerSM) arnoldi_fused_kernel(F
         }
     }
     FTRACE(1);
+    // fixed-point scales from omega (see fx_split): h and u partials at
+    // e_h (|p| < 2^(e_h + 6) fits), hn1 partials at e_n
+    const double om2 = scal[1];
+    const int E2 = static_cast<int>((static_cast<unsigned long long>(__double_as_longlong(om2)) >> 52) & 0x7FF) - 1023;
+    const bool fx_ok = om2 > 0.0 && E2 > -1023 && E2 < 1024 && E2 < 700 && E2 > -700;
+    const int e_h = ((E2 + 2) >> 1) + 8, e_n = E2 + 1 + 8;
+    unsigned long long* const fx0 = fx_ok ? a.fx : nullptr;
+    unsigned long long* const fx1 = fx_ok ? a.fx + a.fx_region : nullptr;
+    unsigned long long* const fxflag = a.fx + 2 * a.fx_region;
+    volatile int* const s_fx = s_gate + 1;
     const uint32_t gs = a.gs;
     const uint64_t region = static_cast<uint64_t>(cols + 1) * gs;
     double* const P = a.partials;
@@ -1808,12 +1960,8 @@ __global__ void __launch_bounds__(kFThreads, kFCtasPerSM) arnoldi_fused_kernel(F
     // dot1 -> h
     fused_pass_any<F, true>(cols, lim, steps, nch, stages, full, empty, it, wv, red, hsm, ers);
     FTRACE(2);
-    dot_partials_out(red, cols, P, gs);
-    grid_allreduce(a.bar, seq++, P, gs, cols, hsm, a.trace);
-    // omega^2 (from the SpMV epilogue) kept in shared memory until the gate
-    // (a register would be spilled and a global reload costs an L2 round
-    // trip on the critical path)
-    if (threadIdx.x == 0) scal[1] = a.slot[2];
+    dot_partials_out(red, cols, P, gs, fx0, fxflag, 0, e_h);
+    grid_allreduce_fx(a.bar, seq++, P, gs, cols, hsm, a.fx, fxflag, 0, fx_ok, e_h, ~0u, 0, s_fx, a.trace);
     if (cta0)
         for (uint32_t j = threadIdx.x; j < cols; j += kFConsumers) {
             a.slot[3 + j] = hsm[j];
@@ -1829,14 +1977,22 @@ __global__ void __launch_bounds__(kFThreads, kFCtasPerSM) arnoldi_fused_kernel(F
         // speculative dot2 -> u, reduced together with hn1
         fused_pass_any<F, true>(cols, lim, steps, nch, stages, full, empty, it, wv, red, hsm, ers);
         FTRACE(5);
-        dot_partials_out(red, cols, P1, gs);
+        dot_partials_out(red, cols, P1, gs, fx1, fxflag, 1, e_h);
     }
-    if (threadIdx.x == 0) P1[static_cast<uint64_t>(cols) * gs + blockIdx.x] = hn1_part;
-    if (spec) grid_allreduce(a.bar, seq++, P1, gs, cols + 1, hsm, a.trace);
+    if (threadIdx.x == 0) {
+        P1[static_cast<uint64_t>(cols) * gs + blockIdx.x] = hn1_part;
+        if (spec && fx1) {
+            long long c[3];
+            if (fx_split(hn1_part, e_n, c)) fx_red(fx1 + 3 * cols, c);
+            else atomicOr(fxflag, 2ull);
+        }
+    }
+    if (spec) grid_allreduce_fx(a.bar, seq++, P1, gs, cols + 1, hsm, a.fx + a.fx_region, fxflag, 1, fx_ok, e_h, cols, e_n,
+                                s_fx, a.trace);
     else grid_allreduce(a.bar, seq++, P1 + static_cast<uint64_t>(cols) * gs, gs, 1, hsm + cols);
     FTRACE(6);
     const double hn1 = hsm[cols];
-    const double omega2 = scal[1];  // written before R1's barriers
+    const double omega2 = om2;
     // gmres.cpp:51 on the device (same IEEE ops as the host)
     const bool gate = sqrt(hn1) < a.eta * sqrt(omega2);
     if (threadIdx.x == 0) {
@@ -1987,6 +2143,7 @@ template <int F> struct FusedLaunch {
         a.out_pay = static_cast<unsigned char*>(V.d_data) + static_cast<uint64_t>(cols) * V.col_stride_bytes;
         a.out_exp = V.d_exp ? V.d_exp + static_cast<uint64_t>(cols) * V.exp_col_stride : nullptr;
         a.out_erange = V.d_erange ? V.d_erange + 2ull * cols : nullptr;
+        a.fx_region = 3 * (max_cols + 2);
         a.w = w;
         a.v_out = v_out;
         a.slot = slot;
@@ -2003,6 +2160,12 @@ template <int F> struct FusedLaunch {
         a.bar = c + Workspace::kFusedBar + (seq & 1) * 32;
         a.bar_next = c + Workspace::kFusedBar + ((seq + 1) & 1) * 32;
         a.gate_hist = c + Workspace::kFusedGate;
+        {
+            const size_t per_set = 2 * static_cast<size_t>(a.fx_region) + 1;
+            unsigned long long* fx = ws->get_fx(per_set);
+            a.fx = fx + (seq & 1) * ws->fx_words;
+            a.fx_next = fx + ((seq + 1) & 1) * ws->fx_words;
+        }
         a.trace = fused_trace_buffer();
         a.host_slot = host_slot;
         a.rot = g_fused_rot;

@@ -50,6 +50,21 @@ int sm_count() {
 Workspace::~Workspace() {
     if (partials) cudaFree(partials);
     if (counters) cudaFree(counters);
+    if (fx) cudaFree(fx);
+}
+
+unsigned long long* Workspace::get_fx(size_t words_per_set) {
+    if (words_per_set > fx_words) {
+        // a grown buffer starts zeroed (both sets): the launch sequence's
+        // invariant (the set a launch uses is zero) holds from here on
+        if (fx) CBGX_CUDA(cudaFree(fx));
+        fx = nullptr;
+        CBGX_CUDA(cudaMalloc(&fx, 2 * words_per_set * sizeof(unsigned long long)));
+        CBGX_CUDA(cudaMemset(fx, 0, 2 * words_per_set * sizeof(unsigned long long)));
+        CBGX_CUDA(cudaStreamSynchronize(nullptr));
+        fx_words = words_per_set;
+    }
+    return fx;
 }
 
 double* Workspace::get_partials(size_t doubles) {

@@ -22,8 +22,13 @@ struct Workspace {
     double* partials = nullptr;
     size_t partial_cap = 0;
     unsigned* counters = nullptr;
+    // fused kernel: two alternating sets of fixed-point grid accumulators
+    // (zero-initialised; each launch zeroes the set the next one uses)
+    unsigned long long* fx = nullptr;
+    size_t fx_words = 0;  // per set
     double* get_partials(size_t doubles);
     unsigned* get_counter();
+    unsigned long long* get_fx(size_t words_per_set);
     ~Workspace();
 };
 
