@@ -1329,6 +1329,8 @@ struct FusedArgs {
     const double* w;           // SpMV output (rows [0, n))
     double* v_out;             // next SpMV input
     double* slot;              // [hn1, hn2, omega2, h[0..m], u[0..m]]; omega2 set by the SpMV
+    const double* om_parts;    // the SpMV's per-CTA omega^2 partials (nullptr: omega2 from slot[2])
+    uint32_t om_count;
     uint32_t u_off;            // index of u in slot
     double eta;
     double* partials;          // kRegions regions of (cols + 1) x gs doubles (value-major)
@@ -1881,7 +1883,7 @@ __global__ void __launch_bounds__(kFThreads, kFCtasPerSM) arnoldi_fused_kernel(F
     // omega^2 (from the SpMV epilogue) kept in shared memory: the gate and
     // the fixed-point scales need it (a register would be spilled and a
     // global reload costs an L2 round trip on the critical path)
-    if (threadIdx.x == 0) scal[1] = a.slot[2];
+    if (threadIdx.x == 0 && !a.om_parts) scal[1] = a.slot[2];
     __syncthreads();
     uint64_t r0, r1;
     fused_rows(a.B.n, a.rot, r0, r1);
@@ -1928,6 +1930,10 @@ __global__ void __launch_bounds__(kFThreads, kFCtasPerSM) arnoldi_fused_kernel(F
 
     // ---------------- consumers
     FTRACE(0);
+    // the SpMV's omega^2 partials: loads issued before w's, summed after
+    double omp = 0.0;
+    if (a.om_parts)
+        for (uint32_t k = threadIdx.x; k < a.om_count; k += kFConsumers) omp = __dadd_rn(omp, __ldcg(a.om_parts + k));
     uint32_t it = 0;
     double wv[kFusedMaxSteps][4];
     const uint64_t wend = min(r1, a.B.n);
@@ -1941,6 +1947,15 @@ __global__ void __launch_bounds__(kFThreads, kFCtasPerSM) arnoldi_fused_kernel(F
         }
     }
     FTRACE(1);
+    if (a.om_parts) {
+        // the same fixed order in every CTA: bit-identical omega^2 grid-wide
+        const double om = cta_wnorm_sum(omp, nred);
+        if (threadIdx.x == 0) {
+            scal[1] = om;
+            if (blockIdx.x == 0) a.slot[2] = om;
+        }
+        consumer_sync();
+    }
     // fixed-point scales from omega (see fx_split): h and u partials at
     // e_h (|p| < 2^(e_h + 6) fits), hn1 partials at e_n
     const double om2 = scal[1];
@@ -2131,7 +2146,7 @@ int fused_grid(uint64_t n, uint32_t max_cols) {
 template <int F> struct FusedLaunch {
     static void run(const cbgx_basis& V, uint32_t cols, const double* w, double* v_out, double* slot,
                     uint32_t u_off, double eta, uint32_t max_cols, double* host_slot, bool pdl,
-                    Workspace* ws, cudaStream_t st, bool* done) {
+                    Workspace* ws, cudaStream_t st, uint32_t om_count, bool* done) {
         // geometry fixed by the solver's capacity so it never changes mid-solve
         const int grid = fused_grid<F>(V.n, max_cols);
         *done = false;
@@ -2147,6 +2162,8 @@ template <int F> struct FusedLaunch {
         a.w = w;
         a.v_out = v_out;
         a.slot = slot;
+        a.om_parts = om_count ? ws->omega_parts : nullptr;
+        a.om_count = om_count;
         a.u_off = u_off;
         a.eta = eta;
         a.gs = static_cast<uint32_t>((grid + 1) / 2 * 2);
@@ -2234,11 +2251,13 @@ bool fused_eligible(const cbgx_basis& V, uint64_t max_cols) {
 
 bool launch_arnoldi_fused(const cbgx_basis& V, uint32_t cols, const double* w, double* v_out, double* slot,
                           uint32_t u_off, double eta, uint32_t max_cols, double* host_slot, bool pdl,
-                          Workspace* ws, cudaStream_t st) {
+                          Workspace* ws, cudaStream_t st, uint32_t om_count) {
     if (cols + 1 > V.capacity) throw Error(CBGX_ERANGE, "basis: cannot write column");
+    if (om_count && (!ws->omega_parts || om_count > ws->omega_cap))
+        throw Error(CBGX_EINTERNAL, "fused: omega partials missing");
     bool done = false;
     dispatch_fmt<FusedLaunch>(fmt_of(V), V, cols, w, v_out, slot, u_off, eta, max_cols, host_slot, pdl, ws, st,
-                              &done);
+                              om_count, &done);
     CBGX_CUDA(cudaGetLastError());
     return done;
 }

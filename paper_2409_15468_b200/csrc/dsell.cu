@@ -458,20 +458,33 @@ __device__ __forceinline__ void pell_finish(double s, int32_t r, uint64_t n_rows
 // row; products and sums in row order from +0.0 (sparse.cpp:50-52), padding
 // entries add +-0 (see dsell_spmv_kernel) and a NaN sum is recomputed
 // exactly; bit-identical to spmv().
-template <int MODE>
+// G1: every row fits one 8-byte code word (g8 == 1, <= 8 entries per row:
+// 7-point stencils): the row's 8 table offsets are read first, all 8
+// gathers issued back to back (32-bit byte offsets from x), then the values
+// and the row-order sum -- fewer live registers than holding 8 (value,
+// offset) pairs across the gathers, so the loads are not serialised.
+#ifndef PELL_G1
+#define PELL_G1 1
+#endif
+#ifndef PELL_GRID_MULT
+#define PELL_GRID_MULT 1
+#endif
+template <int MODE, int G1>
 __global__ void __launch_bounds__(256, PELL_MIN_BLOCKS)
 pell_spmv_kernel(uint64_t n_rows, uint32_t g8, const uint8_t* __restrict__ codes, const int32_t* __restrict__ p_off,
                  const double* __restrict__ p_val, const double* __restrict__ x, const double* __restrict__ b,
                  double* __restrict__ y, int with_norm, double* __restrict__ partials, unsigned* __restrict__ ticket,
-                 double* __restrict__ norm_out, uint64_t s_begin, uint64_t s_end, int accumulate) {
+                 double* __restrict__ norm_out, uint64_t s_begin, uint64_t s_end, int accumulate, uint32_t n_pair) {
     // pair table: .x = value, .y = the column offset in BYTES (off * 8) in
     // the low word -- one 16-byte shared load per entry, and the gather
     // address is the slice's row pointer plus a sign-extended 32-bit offset
     __shared__ double2 tab[256];
     __shared__ double red[8];
-    for (uint32_t i = threadIdx.x; i < 256; i += 256)
-        tab[i] = make_double2(i == 255 ? 0.0 : p_val[i], __hiloint2double(0, i == 255 ? 0 : 8 * p_off[i]));
-    __syncthreads();
+    // only the n_pair used entries and the padding entry 255 are read
+    if (threadIdx.x < n_pair)
+        tab[threadIdx.x] = make_double2(p_val[threadIdx.x], __hiloint2double(0, 8 * p_off[threadIdx.x]));
+    else if (threadIdx.x == 255)
+        tab[255] = make_double2(0.0, __hiloint2double(0, 0));
     pdl_trigger();
     const int lane = threadIdx.x & 31;
     const uint64_t nsl = s_end;  // slices [s_begin, s_end)
@@ -486,6 +499,7 @@ pell_spmv_kernel(uint64_t n_rows, uint32_t g8, const uint8_t* __restrict__ codes
     double acc = 0.0;
     uint2 nxt = make_uint2(0xFFFFFFFFu, 0xFFFFFFFFu);
     if (sl < nsl) nxt = __ldcs(cp);  // codes do not depend on the predecessor
+    __syncthreads();
     pdl_wait();
     for (; sl < nsl; sl += nw, cp += cstep, r += rstep) {
         const int32_t rc = min(r, rlast);
@@ -493,6 +507,22 @@ pell_spmv_kernel(uint64_t n_rows, uint32_t g8, const uint8_t* __restrict__ codes
         uint2 cur = nxt;
         if (sl + nw < nsl) nxt = __ldcs(cp + cstep);
         double s = 0.0;
+        if constexpr (G1) {
+            const uint32_t* tw = reinterpret_cast<const uint32_t*>(tab);
+            const uint32_t rb = static_cast<uint32_t>(rc) * 8u;
+            uint32_t idx[8];
+            double xv[8];
+#pragma unroll
+            for (int k = 0; k < 8; ++k) idx[k] = ((k < 4 ? cur.x : cur.y) >> (8 * (k & 3))) & 0xFFu;
+#pragma unroll
+            for (int k = 0; k < 8; ++k)
+                xv[k] = __ldg(reinterpret_cast<const double*>(reinterpret_cast<const char*>(x) +
+                                                              static_cast<uint64_t>(rb + tw[4 * idx[k] + 2])));
+#pragma unroll
+            for (int k = 0; k < 8; ++k) s = __dadd_rn(s, __dmul_rn(tab[idx[k]].x, xv[k]));
+            pell_finish<MODE>(s, r, n_rows, g8, cp, tab, x, b, y, with_norm, acc);
+            continue;
+        }
         for (uint32_t g = 0; g < g8; ++g) {
             if (g) cur = __ldcs(cp + 32 * g);
             double v[8], xv[8];
@@ -512,6 +542,16 @@ pell_spmv_kernel(uint64_t n_rows, uint32_t g8, const uint8_t* __restrict__ codes
     acc = warp_sum(acc);
     if (lane == 0) red[threadIdx.x >> 5] = acc;
     __syncthreads();
+    if (with_norm == 2) {
+        // per-CTA partials only (warps in order): the consumer sums them
+        // after the kernel boundary -- no fence, ticket or last-block tail
+        if (threadIdx.x == 0) {
+            double t = red[0];
+            for (int w = 1; w < 8; ++w) t = __dadd_rn(t, red[w]);
+            partials[blockIdx.x] = t;
+        }
+        return;
+    }
     block_finalize(red, 8, 1, partials, ticket, norm_out, accumulate != 0);
 }
 
@@ -735,9 +775,10 @@ static void dict_launch(const cbgx_csr& A, const DictSell& D, const double* x, c
         per_sm = std::max(per_sm, 1);
     }
     const uint64_t want = (D.nslices + kSW - 1) / kSW;
-    const int grid = static_cast<int>(std::max<uint64_t>(1, std::min<uint64_t>(want, static_cast<uint64_t>(sm_count()) * per_sm)));
-    double* partials = fused ? ws->get_partials(grid) : nullptr;
-    unsigned* ticket = fused ? ws->get_counter() : nullptr;
+    const int grid = static_cast<int>(std::max<uint64_t>(1, std::min<uint64_t>(want, static_cast<uint64_t>(sm_count()) * per_sm * PELL_GRID_MULT)));
+    // fused == 2: per-CTA omega^2 partials into ws->omega_parts (no ticket)
+    double* partials = fused == 2 ? ws->get_omega_parts(grid) : fused ? ws->get_partials(grid) : nullptr;
+    unsigned* ticket = fused == 1 ? ws->get_counter() : nullptr;
     cudaLaunchConfig_t lc = {};
     lc.gridDim = dim3(grid);
     lc.blockDim = dim3(kST);
@@ -754,20 +795,21 @@ static void dict_launch(const cbgx_csr& A, const DictSell& D, const double* x, c
 }
 
 template <int MODE>
-static void pell_launch(const cbgx_csr& A, const DictSell& D, const double* x, const double* b, double* y, int fused,
+static uint32_t pell_launch(const cbgx_csr& A, const DictSell& D, const double* x, const double* b, double* y, int fused,
                         double* norm, Workspace* ws, cudaStream_t st, bool pdl, uint64_t s_begin = 0,
                         uint64_t s_end = ~0ull, bool accumulate = false) {
     static int per_sm = -1;
     if (per_sm < 0) {
-        CBGX_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, pell_spmv_kernel<MODE>, 256, 0));
+        CBGX_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, pell_spmv_kernel<MODE, 0>, 256, 0));
         per_sm = std::max(per_sm, 1);
     }
     s_end = std::min<uint64_t>(s_end, D.nslices);
-    if (s_begin >= s_end) return;
+    if (s_begin >= s_end) return 0;
     const uint64_t want = (s_end - s_begin + 7) / 8;
-    const int grid = static_cast<int>(std::max<uint64_t>(1, std::min<uint64_t>(want, static_cast<uint64_t>(sm_count()) * per_sm)));
-    double* partials = fused ? ws->get_partials(grid) : nullptr;
-    unsigned* ticket = fused ? ws->get_counter() : nullptr;
+    const int grid = static_cast<int>(std::max<uint64_t>(1, std::min<uint64_t>(want, static_cast<uint64_t>(sm_count()) * per_sm * PELL_GRID_MULT)));
+    // fused == 2: per-CTA omega^2 partials into ws->omega_parts (no ticket)
+    double* partials = fused == 2 ? ws->get_omega_parts(grid) : fused ? ws->get_partials(grid) : nullptr;
+    unsigned* ticket = fused == 1 ? ws->get_counter() : nullptr;
     cudaLaunchConfig_t lc = {};
     lc.gridDim = dim3(grid);
     lc.blockDim = dim3(256);
@@ -778,10 +820,19 @@ static void pell_launch(const cbgx_csr& A, const DictSell& D, const double* x, c
     lc.attrs = at;
     lc.numAttrs = pdl ? 1 : 0;
     note_launch();
-    CBGX_CUDA(cudaLaunchKernelEx(&lc, pell_spmv_kernel<MODE>, A.n_rows, D.ell8_w / 8,
+    // G1's gather offsets are 32-bit byte offsets into x
+    const bool g1 = PELL_G1 && D.ell8_w == 8 && std::max(A.n_rows, A.n_cols) * 8 < (1ull << 32);
+    CBGX_CUDA(cudaLaunchKernelEx(&lc, g1 ? pell_spmv_kernel<MODE, 1> : pell_spmv_kernel<MODE, 0>, A.n_rows, D.ell8_w / 8,
                                  static_cast<const uint8_t*>(D.codes8), static_cast<const int32_t*>(D.pair_off),
                                  static_cast<const double*>(D.pair_val), x, b, y, fused, partials, ticket, norm,
-                                 s_begin, s_end, static_cast<int>(accumulate)));
+                                 s_begin, s_end, static_cast<int>(accumulate), D.n_pair));
+    return static_cast<uint32_t>(grid);
+}
+
+uint32_t launch_spmv_pell_parts(const cbgx_csr& A, const DictSell& D, const double* x, double* y, Workspace* ws,
+                                cudaStream_t st, bool pdl) {
+    if (!D.ell8_w) return 0;
+    return pell_launch<0>(A, D, x, nullptr, y, 2, nullptr, ws, st, pdl);
 }
 
 void launch_spmv_pell_range(const cbgx_csr& A, const DictSell& D, const double* x, double* y, double* norm,

@@ -120,6 +120,11 @@ void launch_spmv_dict(const cbgx_csr& A, const DictSell& D, const double* x, con
                       int reduction, Workspace* ws, cudaStream_t st, bool pdl = false);
 // Pair-coded SpMV of the 32-row slices [s_begin, s_end) (D.ell8_w != 0); the
 // norm (tree order) is written, or added to *norm when `accumulate`.
+// Pair-coded SpMV y = A x whose CTAs leave their omega^2 = ||y||^2 partials
+// in ws->omega_parts (the fused orthogonalisation sums them); returns the
+// partial count, 0 when D has no pair-coded copy (nothing launched).
+uint32_t launch_spmv_pell_parts(const cbgx_csr& A, const DictSell& D, const double* x, double* y, Workspace* ws,
+                                cudaStream_t st, bool pdl);
 void launch_spmv_pell_range(const cbgx_csr& A, const DictSell& D, const double* x, double* y, double* norm,
                             uint64_t s_begin, uint64_t s_end, bool accumulate, Workspace* ws, cudaStream_t st);
 // Rows touching the halo of a local matrix whose own columns are
@@ -158,9 +163,12 @@ void launch_cgs_update(const cbgx_basis& V, uint64_t first, uint32_t cols, const
 bool fused_eligible(const cbgx_basis& V, uint64_t max_cols);
 // host_slot: mapped pinned copy of the step slot written by the kernel (no
 // D2H copy in the stream); pdl: programmatic dependent launch.
+// om_count > 0: omega^2 is the fixed-order sum of the SpMV's om_count CTA
+// partials in ws->omega_parts (launch_spmv_pell_parts), computed by every
+// CTA; otherwise it is read from slot[2].
 bool launch_arnoldi_fused(const cbgx_basis& V, uint32_t cols, const double* w, double* v_out, double* slot,
                           uint32_t u_off, double eta, uint32_t max_cols, double* host_slot, bool pdl,
-                          Workspace* ws, cudaStream_t st);
+                          Workspace* ws, cudaStream_t st, uint32_t om_count = 0);
 void launch_basis_write(const cbgx_basis& V, uint64_t j, const double* x, const ScaleArg& scale,
                         double* v_out, uint64_t* bad, cudaStream_t st);
 // Read benchmark sweep of one basis column (readbench.cu's C-ABI).

@@ -51,6 +51,7 @@ Workspace::~Workspace() {
     if (partials) cudaFree(partials);
     if (counters) cudaFree(counters);
     if (fx) cudaFree(fx);
+    if (omega_parts) cudaFree(omega_parts);
 }
 
 unsigned long long* Workspace::get_fx(size_t words_per_set) {
@@ -77,6 +78,16 @@ double* Workspace::get_partials(size_t doubles) {
         partial_cap = cap;
     }
     return partials;
+}
+
+double* Workspace::get_omega_parts(size_t doubles) {
+    if (doubles > omega_cap) {
+        if (omega_parts) CBGX_CUDA(cudaFree(omega_parts));
+        omega_parts = nullptr;
+        CBGX_CUDA(cudaMalloc(&omega_parts, doubles * sizeof(double)));
+        omega_cap = doubles;
+    }
+    return omega_parts;
 }
 
 unsigned* Workspace::get_counter() {

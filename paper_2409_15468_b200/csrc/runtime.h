@@ -26,7 +26,13 @@ struct Workspace {
     // (zero-initialised; each launch zeroes the set the next one uses)
     unsigned long long* fx = nullptr;
     size_t fx_words = 0;  // per set
+    // per-CTA omega^2 partials of the SpMV that feeds the fused kernel
+    // (summed by every fused CTA; separate from `partials`, which the fused
+    // kernel's grid reductions use)
+    double* omega_parts = nullptr;
+    size_t omega_cap = 0;
     double* get_partials(size_t doubles);
+    double* get_omega_parts(size_t doubles);
     unsigned* get_counter();
     unsigned long long* get_fx(size_t words_per_set);
     ~Workspace();

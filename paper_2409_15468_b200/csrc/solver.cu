@@ -46,6 +46,16 @@ constexpr size_t kH = 3;
 inline size_t kU(uint64_t m) { return kH + m + 1; }
 inline size_t kSlot(uint64_t m) { return (kU(m) + m + 1 + 3) / 4 * 4; }
 
+// A/B switch: CBGX_OMEGA_PARTS=0 keeps the SpMV's own last-block omega^2
+// reduction in the fused path.
+bool omega_parts_enabled() {
+    static const bool v = [] {
+        const char* e = getenv("CBGX_OMEGA_PARTS");
+        return !e || atoi(e) != 0;
+    }();
+    return v;
+}
+
 struct BreakdownError : Error {
     BreakdownError(const std::string& m, uint64_t it) : Error(CBGX_EBREAKDOWN, m, it) {}
 };
@@ -381,8 +391,17 @@ void Solver::solve(const double* d_b, const double* d_x0, double* d_x, cbgx_hist
             // kernel drains) unless phase timing puts events between them.
             const bool pdl = use_fused && !timer.on;
             timer.begin(CBGX_PHASE_SPMV);
-            if (halo_) halo_spmv(d_v_, d_w_, sl + kOmega, st);  // halo exchange + w = A v, omega^2
-            else spmv(d_v_, nullptr, d_w_, sl + kOmega, st, pdl);  // w = A v, omega^2
+            // fused path over the pair-coded SpMV: omega^2 stays as per-CTA
+            // partials that every fused CTA sums (no last-block tail here)
+            uint32_t om_count = 0;
+            if (use_fused && !halo_ && dict_ && dict_->ready && dict_->ell8_w && omega_parts_enabled())
+                om_count = launch_spmv_pell_parts(A_, *dict_, d_v_, d_w_, &ws_, st, pdl);
+            if (om_count) {
+            } else if (halo_) {
+                halo_spmv(d_v_, d_w_, sl + kOmega, st);  // halo exchange + w = A v, omega^2
+            } else {
+                spmv(d_v_, nullptr, d_w_, sl + kOmega, st, pdl);  // w = A v, omega^2
+            }
             timer.end();
             count(CBGX_PHASE_SPMV, spmv_bytes);
             if (use_fused) {
@@ -390,7 +409,8 @@ void Solver::solve(const double* d_b, const double* d_x0, double* d_x, cbgx_hist
                 // the scaled write of column used+1, w register-resident
                 timer.begin(CBGX_PHASE_ORTHO);
                 const bool ok = launch_arnoldi_fused(V_, cols, d_w_, d_v_ + vo, sl, static_cast<uint32_t>(kU(m)), cfg_.eta,
-                                                     static_cast<uint32_t>(m), d_hpinned_ + p * slot, pdl, &ws_, st);
+                                                     static_cast<uint32_t>(m), d_hpinned_ + p * slot, pdl, &ws_, st,
+                                                     om_count);
                 timer.end();
                 if (!ok) throw Error(CBGX_EINTERNAL, "fused orthogonalisation became ineligible");
                 count(CBGX_PHASE_ORTHO, 2.0 * cols * bpv * n + 8.0 * n + 8.0 * n + bpv * n);

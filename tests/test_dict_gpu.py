@@ -137,7 +137,9 @@ def test_solves_through_dictionary_match_csr(cbg, port, fmt):
     t1, t0 = run(0, True), run(0, False)
     assert abs(t1.total_iterations - t0.total_iterations) <= 2
     assert t1.converged and t1.final_rrn <= 1e-10
-    assert np.allclose(np.asarray(t1.solution), np.asarray(t0.solution), rtol=1e-7, atol=1e-12)
+    # both solves stop at RRN <= 1e-10: near-zero components may differ at that level
+    x1, x0 = np.asarray(t1.solution), np.asarray(t0.solution)
+    assert np.allclose(x1, x0, rtol=1e-7, atol=1e-9 * np.abs(x0).max())
 
 
 @pytest.mark.parametrize("special", [np.inf, -np.inf, np.nan])

@@ -66,4 +66,5 @@ def test_dist_stencil_solver_on_local_ranks(cbg, kind, edge, parts, fmt):
     its = {o[3] for o in out}
     assert len(its) == 1 and all(o[4] for o in out)   # ranks agree (replicated Givens)
     assert abs(its.pop() - r1.total_iterations) <= max(2, 0.02 * r1.total_iterations)
-    assert np.allclose(x, r1.solution.cpu().numpy(), rtol=1e-7, atol=1e-11)
+    x1 = r1.solution.cpu().numpy()
+    assert np.allclose(x, x1, rtol=1e-7, atol=1e-9 * np.abs(x1).max())

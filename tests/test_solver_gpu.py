@@ -213,7 +213,7 @@ def test_partitioned_local_matches_single(cbg, port, parts, edge):
     r = cbg._result(st, h, bufs, x)
     assert r.converged
     assert abs(r.total_iterations - single.total_iterations) <= 2
-    assert np.allclose(r.solution, single.solution, rtol=1e-7, atol=1e-12)
+    assert np.allclose(r.solution, single.solution, rtol=1e-7, atol=1e-9 * np.abs(single.solution).max())
     # rank 0 streamed dictionary codes, not CSR (12 B per entry): the window
     # halo layout kept the column offsets
     nnz0 = int(rp[-1]) / parts
@@ -289,7 +289,8 @@ def test_staged_and_csr_solves_agree(cbg, port):
     r2 = solve(cbg, rp, ci, va, b, "frsz2-32", 30, reduction=0, tma_spmv=False, dict_spmv=False)
     histories_agree(hist(r1), hist(r2))
     assert abs(r1.total_iterations - r2.total_iterations) <= 1
-    assert np.allclose(np.asarray(r1.solution), np.asarray(r2.solution), rtol=1e-9, atol=1e-12)
+    assert np.allclose(np.asarray(r1.solution), np.asarray(r2.solution), rtol=1e-9,
+                       atol=1e-9 * np.abs(np.asarray(r2.solution)).max())
 
 
 def test_host_drop_in_reuses_state_across_calls(cbg, port):
