@@ -424,11 +424,11 @@ __global__ void __launch_bounds__(256) pair_convert_kernel(const uint16_t* __res
     }
 }
 
-// 5 CTAs/SM (48 registers): 22.5 us at 7-pt 128^3 in the solve (ncu), vs
-// 24.0 at 6 CTAs (40 registers: rematerialised loop constants); two slices
-// per warp iteration (both slices' gathers in flight): 24.6 us.
+// 4 CTAs/SM: 7-pt 128^3 SpMV phase 0.975 vs 0.993 ms per solve at 5 (48
+// registers), 1.007 at 6, 1.072 at 8; two slices per warp iteration (both
+// slices' gathers in flight) was slower (24.6 vs 22.5 us).
 #ifndef PELL_MIN_BLOCKS
-#define PELL_MIN_BLOCKS 5
+#define PELL_MIN_BLOCKS 4
 #endif
 // Row r's result: a NaN sum (a non-finite x[rc] under a padding entry) is
 // recomputed over the real entries only; then y[r] (or b[r] - ...) and the
