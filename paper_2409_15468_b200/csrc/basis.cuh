@@ -394,13 +394,17 @@ template <> struct Step<kZ21> {
         e = __ldg(B.exp + col * B.exp_col_stride + r / 32);
     }
     __device__ __forceinline__ Codes4 codes() const {
-        // code k sits at bit sh + 21k of the 128-bit little-endian window w0..w3
-        const uint32_t o1 = sh + 21, o2 = sh + 42, o3 = sh + 63;
+        // code k sits at bit sh + 21k of the 128-bit little-endian window
+        // w0..w3 (sh + 84 <= 112): shift the window right by the thread's sh
+        // once (three funnel shifts), then the codes are at the fixed bits
+        // 0, 21, 42, 63 -- constant shifts, no per-code selects
         uint32_t c[4];
-        c[0] = __funnelshift_r(w0, w1, sh);
-        c[1] = o1 < 32 ? __funnelshift_r(w0, w1, o1) : __funnelshift_r(w1, w2, o1 - 32);
-        c[2] = o2 < 64 ? __funnelshift_r(w1, w2, o2 - 32) : __funnelshift_r(w2, w3, o2 - 64);
-        c[3] = o3 < 64 ? __funnelshift_r(w1, w2, o3 - 32) : __funnelshift_r(w2, w3, o3 - 64);
+        const uint32_t x0 = __funnelshift_r(w0, w1, sh), x1 = __funnelshift_r(w1, w2, sh),
+                       x2 = __funnelshift_r(w2, w3, sh);
+        c[0] = x0;
+        c[1] = __funnelshift_r(x0, x1, 21);
+        c[2] = x1 >> 10;
+        c[3] = __funnelshift_r(x1, x2, 31);
         Codes4 k;
 #pragma unroll
         for (int i = 0; i < 4; ++i) {
