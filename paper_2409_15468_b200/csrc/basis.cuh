@@ -266,6 +266,17 @@ template <int L>
 __device__ __forceinline__ double frsz_smul(uint32_t e, double mul) {
     return __dmul_rn(__hiloint2double(static_cast<int>((e - (L - 2)) << 20), 0), mul);
 }
+// The same products with one FP64 instruction per value: (2^52 + mag) *
+// smul - 2^52 * smul is exactly mag * smul before the FMA's single rounding
+// (c0 = -2^52 * smul, exact while smul <= 2^971: the caller's exponent
+// range), then the sign -- RN is symmetric.
+__device__ __forceinline__ void frsz_decode_mul_fma(const Codes4& c, double smul, double c0, double v[4]) {
+#pragma unroll
+    for (int k = 0; k < 4; ++k) {
+        const double p = fma(__hiloint2double(0x43300000, static_cast<int>(c.mag[k])), smul, c0);
+        v[k] = __hiloint2double(__double2hiint(p) ^ static_cast<int>(c.sgn[k]), __double2loint(p));
+    }
+}
 template <int L>
 __device__ __forceinline__ void frsz_decode_mul(const Codes4& c, double smul, double v[4]) {
 #pragma unroll
@@ -350,6 +361,7 @@ template <> struct Step<kZ32> {
     __device__ __forceinline__ void update_exact(double h, double w[4]) const { frsz_update_exact<32>(codes(), e, h, w); }
     __device__ __forceinline__ double smul(double mul) const { return frsz_smul<32>(e, mul); }
     __device__ __forceinline__ void decode_mul(double sm, double v[4]) const { frsz_decode_mul<32>(codes(), sm, v); }
+    __device__ __forceinline__ void decode_mul_fma(double sm, double c0, double v[4]) const { frsz_decode_mul_fma(codes(), sm, c0, v); }
 };
 
 template <> struct Step<kZ16> {
@@ -380,6 +392,7 @@ template <> struct Step<kZ16> {
     __device__ __forceinline__ void update_exact(double h, double w[4]) const { frsz_update_exact<16>(codes(), e, h, w); }
     __device__ __forceinline__ double smul(double mul) const { return frsz_smul<16>(e, mul); }
     __device__ __forceinline__ void decode_mul(double sm, double v[4]) const { frsz_decode_mul<16>(codes(), sm, v); }
+    __device__ __forceinline__ void decode_mul_fma(double sm, double c0, double v[4]) const { frsz_decode_mul_fma(codes(), sm, c0, v); }
 };
 
 template <> struct Step<kZ21> {
@@ -426,6 +439,7 @@ template <> struct Step<kZ21> {
     __device__ __forceinline__ void update_exact(double h, double w[4]) const { frsz_update_exact<21>(codes(), e, h, w); }
     __device__ __forceinline__ double smul(double mul) const { return frsz_smul<21>(e, mul); }
     __device__ __forceinline__ void decode_mul(double sm, double v[4]) const { frsz_decode_mul<21>(codes(), sm, v); }
+    __device__ __forceinline__ void decode_mul_fma(double sm, double c0, double v[4]) const { frsz_decode_mul_fma(codes(), sm, c0, v); }
 };
 
 template <> struct Step<kF64> {

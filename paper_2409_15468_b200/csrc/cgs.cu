@@ -1088,6 +1088,40 @@ __device__ __forceinline__ double stage_sweep(const unsigned char* pay, const ui
     return acc;
 }
 
+// The read sweep's common case, streamed step by step: an FRSZ2 stage whose
+// rows are all below n, intensity 1, and every block exponent inside the
+// folded-multiply range (one vote). No decoded-stage array and no per-step
+// bounds: ~8 instructions per value instead of ~13. Otherwise the general
+// stage_sweep.
+template <int F>
+__device__ __forceinline__ double stage_sweep1(const unsigned char* pay, const uint32_t* ex, const StageOff<F>& o,
+                                               uint64_t row0, uint64_t n, double mul, double add, bool fold_ok,
+                                               uint32_t e_lo, uint32_t e_span, uint32_t e_span1) {
+    constexpr int SUB = Geo<F>::sub;
+    Step<F> st[SUB];
+    bool ok = fold_ok;
+#pragma unroll
+    for (int s = 0; s < SUB; ++s) {
+        st[s].e = ex[32 * s];
+        // implies the fast decode (e_lo > L - 2) and 2^52 * scale * mul finite
+        ok &= st[s].e - e_lo <= e_span1;
+    }
+    if (__builtin_expect(!__all_sync(0xFFFFFFFFu, ok), 0))
+        return stage_sweep<F, true>(pay, ex, o, SUB, row0, n, 1, mul, add, fold_ok, e_lo, e_span);
+    double acc = 0.0;
+#pragma unroll
+    for (int s = 0; s < SUB; ++s) {
+        step_lds_at<F>(st[s], pay, ex, o, s, false);
+        double v[4];
+        const double sm = st[s].smul(mul);
+        st[s].decode_mul_fma(sm, __dmul_rn(sm, -0x1p52), v);
+#pragma unroll
+        for (int k = 0; k < 4; ++k) v[k] = __dadd_rn(v[k], add);
+        acc = __dadd_rn(acc, __dadd_rn(__dadd_rn(v[0], v[1]), __dadd_rn(v[2], v[3])));
+    }
+    return acc;
+}
+
 template <int F>
 __global__ void __launch_bounds__(kThreads, split_min_blocks<F>())
 read_sweep_kernel(BasisView B, uint64_t col, uint64_t n, int intensity, double mul, double add,
@@ -1118,21 +1152,43 @@ read_sweep_kernel(BasisView B, uint64_t col, uint64_t n, int intensity, double m
         const bool fold_ok = FmtInfo<F>::frsz && E >= 1 && E <= 2046 && hi >= lo;
         const uint32_t e_lo = static_cast<uint32_t>(lo);
         const uint32_t e_span = hi >= lo ? static_cast<uint32_t>(hi - lo) : 0u;
+        // the streamed path's FMA decode also needs 2^52 * scale * mul finite
+        const bool fold1 = fold_ok && hi - 52 >= lo;
+        const uint32_t e_span1 = fold1 ? static_cast<uint32_t>(hi - 52 - lo) : 0u;
+        // ring position as 32-bit counters (a 64-bit t % S costs ~20
+        // instructions per stage)
+        uint32_t stage = 0, phase = 0;
         for (uint64_t t = 0; t < T.count; ++t) {
-            const int stage = static_cast<int>(t % S);
-            mbar_wait(R.full + stage, static_cast<uint32_t>((t / S) & 1));
+            mbar_wait(R.full + stage, phase);
             const uint64_t sb = T.begin(t);
             const uint32_t steps = static_cast<uint32_t>(T.end(t) - sb);
             const unsigned char* pay = R.stages + stage * stage_bytes<F>();
             const uint32_t* ex = reinterpret_cast<const uint32_t*>(pay + Geo<F>::sub * PAY);
             const uint64_t row0 = sb * kStepRows + 4u * threadIdx.x;
-            acc = __dadd_rn(acc, steps == static_cast<uint32_t>(Geo<F>::sub)
-                                     ? stage_sweep<F, true>(pay + off.pay, ex + off.ex, off, steps, row0, n, intensity,
-                                                            mul, add, fold_ok, e_lo, e_span)
-                                     : stage_sweep<F, false>(pay + off.pay, ex + off.ex, off, steps, row0, n,
-                                                             intensity, mul, add, fold_ok, e_lo, e_span));
+            const bool full = steps == static_cast<uint32_t>(Geo<F>::sub);
+            double a;
+            bool streamed = false;
+            if constexpr (FmtInfo<F>::frsz) {
+                if (full && intensity == 1 && fold1 && (sb + Geo<F>::sub) * kStepRows <= n) {
+                    a = stage_sweep1<F>(pay + off.pay, ex + off.ex, off, row0, n, mul, add, fold_ok, e_lo, e_span,
+                                        e_span1);
+                    streamed = true;
+                }
+            }
+            if (streamed) {
+            } else if (full)
+                a = stage_sweep<F, true>(pay + off.pay, ex + off.ex, off, steps, row0, n, intensity, mul, add, fold_ok,
+                                         e_lo, e_span);
+            else
+                a = stage_sweep<F, false>(pay + off.pay, ex + off.ex, off, steps, row0, n, intensity, mul, add,
+                                          fold_ok, e_lo, e_span);
+            acc = __dadd_rn(acc, a);
             __syncwarp();
             if (lane == 0) mbar_arrive(R.empty + stage);
+            if (++stage == S) {
+                stage = 0;
+                phase ^= 1u;
+            }
         }
     }
     acc = warp_sum(acc);

@@ -174,6 +174,18 @@ def test_read_sweep_checksum(cbg, port, fmt):
         want = float(np.sum(buf, dtype=np.float64))
         got = cbg.read_sweep(B, 1, n, inten, mul, add)
         assert abs(got - want) <= 1e-12 * np.sum(np.abs(buf)), (fmt, inten, got, want)
+    # block exponents near the top of the folded-multiply range (2^52 * scale
+    # * mul would overflow): the streamed FMA decode hands those stages to
+    # the general path
+    if fmt.startswith("frsz2"):
+        vb = v * 2.0 ** 500
+        Bb = cbg.KrylovBasis(n, 1, cbg.StorageFormat.parse(fmt))
+        Bb.write_vector(0, vb)
+        decb = port.basis_roundtrip(fmt, vb)
+        mulb = 2.0 ** 505
+        want = float(np.sum(decb * mulb + add, dtype=np.float64))
+        got = cbg.read_sweep(Bb, 0, n, 1, mulb, add)
+        assert abs(got - want) <= 1e-12 * np.sum(np.abs(decb * mulb)), (fmt, got, want)
     # partial length (multiple of 32) and argument checks
     got = cbg.read_sweep(B, 1, 64, 1, 1.0, 0.0)
     assert abs(got - float(np.sum(dec[:64]))) <= 1e-14
