@@ -89,16 +89,19 @@ class ClockSampler:
             self.nv = None
             self.err = str(e)
 
+    def _sample(self):
+        try:
+            self.samples.append(self.nv.nvmlDeviceGetClockInfo(self.h, self.nv.NVML_CLOCK_SM))
+            r = self.nv.nvmlDeviceGetCurrentClocksEventReasons(self.h)
+            for name, bit in self.REASONS.items():
+                if r & bit and name != "gpu_idle":
+                    self.reasons.add(name)
+        except Exception:  # noqa: BLE001
+            pass
+
     def _run(self):
         while not self._stop.is_set():
-            try:
-                self.samples.append(self.nv.nvmlDeviceGetClockInfo(self.h, self.nv.NVML_CLOCK_SM))
-                r = self.nv.nvmlDeviceGetCurrentClocksEventReasons(self.h)
-                for name, bit in self.REASONS.items():
-                    if r & bit and name != "gpu_idle":
-                        self.reasons.add(name)
-            except Exception:  # noqa: BLE001
-                pass
+            self._sample()
             time.sleep(self.period)
 
     def __enter__(self):
@@ -111,6 +114,10 @@ class ClockSampler:
         self._stop.set()
         if self.nv:
             self.t.join()
+            # one more reading at the end of the timed region (the work is
+            # still queued/finishing): at least two samples per region even
+            # when the host thread starves the sampler
+            self._sample()
 
     def summary(self):
         if not self.nv:
