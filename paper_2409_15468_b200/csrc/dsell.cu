@@ -466,9 +466,6 @@ __device__ __forceinline__ void pell_finish(double s, int32_t r, uint64_t n_rows
 #ifndef PELL_G1
 #define PELL_G1 1
 #endif
-#ifndef PELL_GRID_MULT
-#define PELL_GRID_MULT 1
-#endif
 template <int MODE, int G1>
 __global__ void __launch_bounds__(256, PELL_MIN_BLOCKS)
 pell_spmv_kernel(uint64_t n_rows, uint32_t g8, const uint8_t* __restrict__ codes, const int32_t* __restrict__ p_off,
@@ -775,7 +772,7 @@ static void dict_launch(const cbgx_csr& A, const DictSell& D, const double* x, c
         per_sm = std::max(per_sm, 1);
     }
     const uint64_t want = (D.nslices + kSW - 1) / kSW;
-    const int grid = static_cast<int>(std::max<uint64_t>(1, std::min<uint64_t>(want, static_cast<uint64_t>(sm_count()) * per_sm * PELL_GRID_MULT)));
+    const int grid = static_cast<int>(std::max<uint64_t>(1, std::min<uint64_t>(want, static_cast<uint64_t>(sm_count()) * per_sm)));
     // fused == 2: per-CTA omega^2 partials into ws->omega_parts (no ticket)
     double* partials = fused == 2 ? ws->get_omega_parts(grid) : fused ? ws->get_partials(grid) : nullptr;
     unsigned* ticket = fused == 1 ? ws->get_counter() : nullptr;
@@ -806,7 +803,7 @@ static uint32_t pell_launch(const cbgx_csr& A, const DictSell& D, const double* 
     s_end = std::min<uint64_t>(s_end, D.nslices);
     if (s_begin >= s_end) return 0;
     const uint64_t want = (s_end - s_begin + 7) / 8;
-    const int grid = static_cast<int>(std::max<uint64_t>(1, std::min<uint64_t>(want, static_cast<uint64_t>(sm_count()) * per_sm * PELL_GRID_MULT)));
+    const int grid = static_cast<int>(std::max<uint64_t>(1, std::min<uint64_t>(want, static_cast<uint64_t>(sm_count()) * per_sm)));
     // fused == 2: per-CTA omega^2 partials into ws->omega_parts (no ticket)
     double* partials = fused == 2 ? ws->get_omega_parts(grid) : fused ? ws->get_partials(grid) : nullptr;
     unsigned* ticket = fused == 1 ? ws->get_counter() : nullptr;
