@@ -405,10 +405,11 @@ def run_ours(args):
                 l2="inputs larger than L2: per solve the basis grows to %.0f MB (up to %.0f MB at m=100) "
                    "plus the matrix (%s) vs 126 MB L2; no explicit flush"
                    % (last.total_iterations * bpv * rows / 1e6, 101 * bpv * rows / 1e6,
-                      "1-byte dictionary codes, ~%.0f MB" % (8 * -(-nnz // (8 * rows)) * rows / 1e6) if world == 1
+                      "1-byte row-pattern ids, ~%.0f MB" % (rows / 1e6) if world == 1
                       else "1-byte dictionary codes per rank"),
-                spmv=("pair-coded dictionary ELL8 copy of the CSR (1-byte codes into <=255 distinct (value, "
-                      "column offset) pairs; bit-identical to the CSR SpMV), built at setup" if world == 1
+                spmv=("row-pattern coded dictionary copy of the CSR (one byte per row into <=255 distinct rows "
+                      "of (value, column offset) pairs -- 27 for a 7-point box stencil; bit-identical to the CSR "
+                      "SpMV), built at setup" if world == 1
                       else "pair-coded dictionary copy of each rank's rows in the window halo layout "
                            "[lower ghost planes | own rows | upper ghost planes]; interior rows overlap the "
                            "NCCL halo exchange")),

@@ -224,6 +224,14 @@ int cbgx_csr_spmv_staged(const cbgx_csr* A, uint32_t tile_rows, const double* d_
 typedef struct cbgx_dict_csr cbgx_dict_csr;
 int cbgx_csr_dict_create(const cbgx_csr* A, cbgx_dict_csr** out, void* stream);
 int cbgx_csr_dict_info(const cbgx_dict_csr* D, uint32_t* n_offsets, uint32_t* n_values, uint64_t* entries);
+/* create with a ceiling on the coding level: 0 = 2-byte codes (value index,
+ * offset index), 1 = 1-byte pair codes when <= 255 distinct (value, offset)
+ * pairs, 2 = one byte per ROW when the pair-coded rows take <= 255 distinct
+ * patterns (constant-coefficient stencils; default of cbgx_csr_dict_create).
+ * layout: level in use (0 SELL / 1 ELL4 2-byte / 2 pair-coded ELL8 / 3 row
+ * patterns), the pair and pattern counts. */
+int cbgx_csr_dict_create2(const cbgx_csr* A, uint32_t max_level, cbgx_dict_csr** out, void* stream);
+int cbgx_csr_dict_layout(const cbgx_dict_csr* D, uint32_t* level, uint32_t* n_pairs, uint32_t* n_patterns);
 int cbgx_csr_dict_spmv(const cbgx_csr* A, const cbgx_dict_csr* D, const double* d_x, const double* d_b, double* d_y,
                        double* d_ynorm2, int reduction, cbgx_workspace* ws, void* stream);
 void cbgx_csr_dict_destroy(cbgx_dict_csr* D);

@@ -602,11 +602,21 @@ class DictCsr:
     2-byte codes into <= 255 distinct values and column offsets. Raises
     CbgxError for matrices outside that pattern."""
 
-    def __init__(self, a: DeviceCsr):
+    def __init__(self, a: DeviceCsr, max_level: int = 2):
+        """max_level: 0 = 2-byte codes, 1 = up to 1-byte pair codes,
+        2 = up to one pattern byte per row (cbgx_csr_dict_create2)."""
         import ctypes
         self.a = a
         self.h = ctypes.c_void_p()
-        check(lib().cbgx_csr_dict_create(ctypes.byref(a.desc), ctypes.byref(self.h), _stream()))
+        check(lib().cbgx_csr_dict_create2(ctypes.byref(a.desc), max_level, ctypes.byref(self.h), _stream()))
+
+    def layout(self):
+        """(level, pairs, patterns): level 0 SELL / 1 ELL4 2-byte codes /
+        2 pair-coded ELL8 / 3 row patterns."""
+        import ctypes
+        lv, npr, npt = ctypes.c_uint32(), ctypes.c_uint32(), ctypes.c_uint32()
+        check(lib().cbgx_csr_dict_layout(self.h, ctypes.byref(lv), ctypes.byref(npr), ctypes.byref(npt)))
+        return lv.value, npr.value, npt.value
 
     def info(self):
         import ctypes

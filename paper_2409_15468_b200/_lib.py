@@ -95,6 +95,8 @@ def lib():
             "cbgx_csr_spmv_staged": ([P(Csr), C.c_uint32, vp, vp, vp, vp, C.c_int, vp, vp], C.c_int),
             "cbgx_csr_dict_create": ([P(Csr), P(vp), vp], C.c_int),
             "cbgx_csr_dict_info": ([vp, P(C.c_uint32), P(C.c_uint32), P(C.c_uint64)], C.c_int),
+            "cbgx_csr_dict_create2": ([P(Csr), C.c_uint32, P(vp), vp], C.c_int),
+            "cbgx_csr_dict_layout": ([vp, P(C.c_uint32), P(C.c_uint32), P(C.c_uint32)], C.c_int),
             "cbgx_csr_dict_spmv": ([P(Csr), vp, vp, vp, vp, vp, C.c_int, vp, vp], C.c_int),
             "cbgx_csr_dict_destroy": ([vp], None),
             "cbgx_dot": ([vp, vp, u64, C.c_int, vp, vp, vp], C.c_int),

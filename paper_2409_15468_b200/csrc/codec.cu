@@ -26,10 +26,10 @@ constexpr int kWarps = kThreads / 32;
 // A warp step covers 128 rows = 4 blocks; lane l owns rows 4l..4l+3 (all in
 // block l/8), so every lane moves 16-32 B per global access: 2x16 B of fp64
 // and 16 B (l=32) / 8 B (l=16) of codes, the block exponent reduced over 8
-// lanes with 3 shuffles. l=21 codes are assembled (compress) or unpacked
-// (decompress) through an 84-word per-warp shared-memory window so the
-// global side stays coalesced. kSteps warp steps are in flight per
-// iteration to keep enough bytes outstanding per SM.
+// lanes with 3 shuffles. l=21 codes are assembled with funnel shifts and one
+// shuffle (compress) or unpacked through an 84-word per-warp shared-memory
+// window (decompress) so the global side stays coalesced. kSteps warp steps
+// are in flight per iteration to keep enough bytes outstanding per SM.
 constexpr int kSteps = 4;
 
 template <int L, bool kScale>
@@ -38,9 +38,7 @@ compress4_kernel(const double* __restrict__ x, uint64_t n, uint64_t nb_write,
                  uint32_t* __restrict__ exps, uint32_t* __restrict__ payload,
                  ScaleArg scale, double* __restrict__ v_out,
                  unsigned long long* __restrict__ bad) {
-    __shared__ uint32_t wbuf_all[kWarps][84];
     const int lane = threadIdx.x & 31;
-    uint32_t* wbuf = wbuf_all[threadIdx.x >> 5];
     const double s = kScale ? scale.value() : 1.0;
     const uint64_t nsteps = (nb_write + 3) / 4;
     const uint64_t warp = (static_cast<uint64_t>(blockIdx.x) * kWarps) + (threadIdx.x >> 5);
@@ -92,22 +90,25 @@ compress4_kernel(const double* __restrict__ x, uint64_t n, uint64_t nb_write,
             } else if constexpr (L == 16) {
                 if (live) reinterpret_cast<uint2*>(payload)[r / 4] = make_uint2(c[0] | (c[1] << 16), c[2] | (c[3] << 16));
             } else {
-                for (int i = lane; i < 84; i += 32) wbuf[i] = 0u;
-                __syncwarp();
-                const uint32_t bit0 = (lane >> 3) * 672u + (lane & 7) * 84u;
-#pragma unroll
-                for (int k = 0; k < 4; ++k) {
-                    const uint32_t b = bit0 + 21u * k, q = b >> 5, sh = b & 31u;
-                    atomicOr(wbuf + q, c[k] << sh);
-                    if (sh > 11) atomicOr(wbuf + q + 1, c[k] >> (32 - sh));
-                }
-                __syncwarp();
+                // Lane L's four codes are bits [84 L, 84 L + 84) of the step's
+                // 84-word stream (block L/8 starts at 672 (L/8), value 4 (L%8)
+                // + k at 21 k). The lane writes the words that START in its
+                // range: at bit offsets o, o + 32 (and o + 64 when o < 20),
+                // o = -84 L mod 32; a word reaching past the range takes the
+                // next lane's first bits (one shuffle) -- funnel shifts of the
+                // lane's 84-bit string, no shared memory.
+                const uint32_t w0 = c[0] | (c[1] << 21);
+                const uint32_t w1 = (c[1] >> 11) | (c[2] << 10) | (c[3] << 31);
+                const uint32_t nb0 = __shfl_down_sync(0xFFFFFFFFu, w0, 1);
+                const uint32_t w2 = (c[3] >> 1) | (nb0 << 20), w3 = nb0 >> 12;
+                const uint32_t o = (32u - ((20u * lane) & 31u)) & 31u;
+                const uint32_t i0 = (84u * lane + o) >> 5;
                 const uint64_t b0 = (s0 + u) * 4;  // first block of the step
-                uint32_t* dst = payload + b0 * 21;
+                uint32_t* dst = payload + b0 * 21 + i0;
                 const uint64_t words = (min(nb_write, b0 + 4) - b0) * 21;
-                for (int i = lane; i < 84; i += 32)
-                    if (static_cast<uint64_t>(i) < words) dst[i] = wbuf[i];
-                __syncwarp();
+                if (i0 < words) dst[0] = __funnelshift_r(w0, w1, o);
+                if (i0 + 1 < words) dst[1] = __funnelshift_r(w1, w2, o);
+                if (o < 20u && i0 + 2 < words) dst[2] = __funnelshift_r(w2, w3, o);
             }
         }
     }

@@ -552,6 +552,205 @@ pell_spmv_kernel(uint64_t n_rows, uint32_t g8, const uint8_t* __restrict__ codes
     block_finalize(red, 8, 1, partials, ticket, norm_out, accumulate != 0);
 }
 
+// ---------------------------------------------------------------------------
+// Row-pattern coded SpMV. A constant-coefficient stencil has very few distinct
+// ROWS of pair codes (7-point on a box: 27 -- interior, faces, edges,
+// corners). When the matrix holds <= 255 distinct rows of the pair-coded
+// copy, every row becomes ONE byte (its pattern id) and the table
+// {8G element offsets (int32), 8G values (fp64)} of each pattern sits in
+// shared memory: per row 2G + 4G 16-byte shared loads instead of one shared
+// load and a byte extraction per entry, and per entry one 32-bit add plus one
+// IMAD.WIDE for the gather address. Padding entries are (offset 0, +0.0):
+// same bit-identity argument as the pair-coded kernel, a NaN sum recomputed
+// over the pattern's real entries. Products and sums in row order:
+// bit-identical to spmv() (sparse.cpp:50-52).
+// ---------------------------------------------------------------------------
+__device__ __forceinline__ unsigned long long mix64(unsigned long long z) {
+    z = (z ^ (z >> 30)) * 0xBF58476D1CE4E5B9ull;
+    z = (z ^ (z >> 27)) * 0x94D049BB133111EBull;
+    return z ^ (z >> 31);
+}
+// hash of one row's G code words (never 0: 0 marks an empty slot)
+__device__ __forceinline__ unsigned long long row_key(const uint2* __restrict__ cp, uint32_t g8) {
+    unsigned long long h = 0x632BE59BD9B4E019ull;
+    for (uint32_t g = 0; g < g8; ++g) {
+        const uint2 q = cp[32 * g];
+        h = mix64(h ^ (static_cast<unsigned long long>(q.y) << 32 | q.x));
+    }
+    return h ? h : 1ull;
+}
+constexpr uint32_t kPatSlots = 1024;  // global table; per-CTA table below
+constexpr uint32_t kPatLocal = 512;
+constexpr uint32_t kPatTabMax = 40u * 1024u;  // dynamic shared memory of the pattern tables
+// offset of a padding entry: a gather of x[r] times +0.0 (a NaN sum is
+// recomputed over the pattern's leading real entries). Predicating padding
+// entries off instead measured no faster (L1 requests saved, issue lost).
+constexpr int32_t kPatPad = 0;
+
+// Pass 1: the distinct row patterns, deduplicated per CTA in shared memory,
+// then merged into the global table; the CTA that claims a global slot writes
+// the row's code words next to it. *bad: a table overflowed.
+__global__ void __launch_bounds__(256) pat_scan_kernel(const uint2* __restrict__ codes8, uint64_t rows, uint32_t g8,
+                                                       unsigned long long* __restrict__ gkeys,
+                                                       uint2* __restrict__ gwords, unsigned* __restrict__ bad) {
+    __shared__ unsigned long long sk[kPatLocal];
+    __shared__ uint32_t srow[kPatLocal];
+    for (uint32_t i = threadIdx.x; i < kPatLocal; i += 256) sk[i] = 0ull;
+    __syncthreads();
+    bool over = false;
+    for (uint64_t r = blockIdx.x * 256ull + threadIdx.x; r < rows; r += gridDim.x * 256ull) {
+        const uint2* cp = codes8 + (r / 32) * g8 * 32 + (r % 32);
+        const unsigned long long h = row_key(cp, g8);
+        uint32_t s = static_cast<uint32_t>(h) & (kPatLocal - 1), p = 0;
+        for (; p < kPatLocal; ++p, s = (s + 1) & (kPatLocal - 1)) {
+            unsigned long long k = *reinterpret_cast<volatile unsigned long long*>(sk + s);
+            if (k == h) break;
+            if (k == 0ull) {
+                k = atomicCAS(sk + s, 0ull, h);
+                if (k == 0ull) { srow[s] = static_cast<uint32_t>(r); break; }
+                if (k == h) break;
+            }
+        }
+        over |= p == kPatLocal;
+    }
+    __syncthreads();
+    for (uint32_t i = threadIdx.x; i < kPatLocal; i += 256) {
+        const unsigned long long h = sk[i];
+        if (!h) continue;
+        uint32_t s = static_cast<uint32_t>(h >> 32) & (kPatSlots - 1), p = 0;
+        for (; p < kPatSlots; ++p, s = (s + 1) & (kPatSlots - 1)) {
+            unsigned long long k = *reinterpret_cast<volatile unsigned long long*>(gkeys + s);
+            if (k == h) break;
+            if (k == 0ull) {
+                k = atomicCAS(gkeys + s, 0ull, h);
+                if (k == 0ull) {
+                    const uint64_t r = srow[i];
+                    const uint2* cp = codes8 + (r / 32) * g8 * 32 + (r % 32);
+                    for (uint32_t g = 0; g < g8; ++g) gwords[s * 4 + g] = cp[32 * g];
+                    break;
+                }
+                if (k == h) break;
+            }
+        }
+        over |= p == kPatSlots;
+    }
+    if (over) atomicOr(bad, 1u);
+}
+
+// Pass 2: every row's pattern id, verified word by word against the pattern
+// (a hash collision sets *bad and the matrix keeps the pair-coded kernel).
+__global__ void __launch_bounds__(256) pat_map_kernel(const uint2* __restrict__ codes8, uint64_t rows, uint32_t g8,
+                                                      const unsigned long long* __restrict__ gkeys,
+                                                      const uint8_t* __restrict__ slot_id,
+                                                      const uint2* __restrict__ pwords, uint8_t* __restrict__ pid,
+                                                      unsigned* __restrict__ bad) {
+    __shared__ unsigned long long sk[kPatSlots];
+    __shared__ uint8_t sid[kPatSlots];
+    for (uint32_t i = threadIdx.x; i < kPatSlots; i += 256) {
+        sk[i] = gkeys[i];
+        sid[i] = slot_id[i];
+    }
+    __syncthreads();
+    bool wrong = false;
+    for (uint64_t r = blockIdx.x * 256ull + threadIdx.x; r < rows; r += gridDim.x * 256ull) {
+        const uint2* cp = codes8 + (r / 32) * g8 * 32 + (r % 32);
+        const unsigned long long h = row_key(cp, g8);
+        uint32_t s = static_cast<uint32_t>(h >> 32) & (kPatSlots - 1), p = 0;
+        while (p < kPatSlots && sk[s] != h && sk[s] != 0ull) { s = (s + 1) & (kPatSlots - 1); ++p; }
+        if (p == kPatSlots || sk[s] != h) { wrong = true; continue; }
+        const uint32_t id = sid[s];
+        for (uint32_t g = 0; g < g8; ++g) {
+            const uint2 a = cp[32 * g], b = pwords[id * g8 + g];
+            wrong |= a.x != b.x || a.y != b.y;
+        }
+        pid[r] = static_cast<uint8_t>(id);
+    }
+    if (wrong) atomicOr(bad, 1u);
+}
+
+template <int MODE, int G>
+__global__ void __launch_bounds__(256, PELL_MIN_BLOCKS)
+ppat_spmv_kernel(uint64_t n_rows, const uint8_t* __restrict__ pid, const uint4* __restrict__ ptab, uint32_t ptab_u4,
+                 const uint8_t* __restrict__ pcnt, const double* __restrict__ x, const double* __restrict__ b, double* __restrict__ y, int with_norm,
+                 double* __restrict__ partials, unsigned* __restrict__ ticket, double* __restrict__ norm_out,
+                 uint64_t s_begin, uint64_t s_end, int accumulate) {
+    // pattern p: int32 off[8G] at p * 96G (kPatPad = padding), then fp64 val[8G]
+    extern __shared__ uint4 stab[];
+    __shared__ double red[8];
+    for (uint32_t i = threadIdx.x; i < ptab_u4; i += 256) stab[i] = ptab[i];
+    pdl_trigger();
+    const int lane = threadIdx.x & 31;
+    const uint64_t nw = static_cast<uint64_t>(gridDim.x) * 8;
+    const uint64_t sl = s_begin + (blockIdx.x * 256ull + threadIdx.x) / 32;
+    const uint32_t iters = sl < s_end ? static_cast<uint32_t>((s_end - sl + nw - 1) / nw) : 0u;
+    int32_t r = static_cast<int32_t>(sl * 32 + lane);
+    const int32_t rstep = static_cast<int32_t>(nw * 32);
+    const int32_t nr = static_cast<int32_t>(n_rows);
+    double acc = 0.0;
+    uint32_t nxt = 0;
+    if (iters) nxt = __ldcs(pid + r);  // ids do not depend on the predecessor
+    __syncthreads();
+    pdl_wait();
+    const char* tb = reinterpret_cast<const char*>(stab);
+    for (uint32_t it = 0; it < iters; ++it, r += rstep) {
+        const uint32_t p = nxt;
+        if (it + 1 < iters) nxt = __ldcs(pid + r + rstep);
+        const char* pb = tb + p * (96u * G);
+        // rows past n_rows (the last slice's fill) are all padding: they
+        // gather x[n_rows - 1]
+        const double* xb = x + min(r, nr - 1);
+        // opaque row pointer: each gather address is then ONE IMAD.WIDE of
+        // the entry's offset (ptxas would otherwise re-associate r + off in
+        // 64 bits: four instructions per gather)
+        asm("" : "+l"(xb));
+        double s = 0.0;
+#pragma unroll
+        for (int g = 0; g < G; ++g) {
+            const int4 o0 = *reinterpret_cast<const int4*>(pb + 32 * g);
+            const int4 o1 = *reinterpret_cast<const int4*>(pb + 32 * g + 16);
+            const int32_t o[8] = {o0.x, o0.y, o0.z, o0.w, o1.x, o1.y, o1.z, o1.w};
+            double xv[8];
+#pragma unroll
+            for (int k = 0; k < 8; ++k) xv[k] = __ldg(xb + o[k]);
+#pragma unroll
+            for (int k = 0; k < 8; k += 2) {
+                const double2 v = *reinterpret_cast<const double2*>(pb + 32 * G + 64 * g + 8 * k);
+                s = __dadd_rn(s, __dmul_rn(v.x, xv[k]));
+                s = __dadd_rn(s, __dmul_rn(v.y, xv[k + 1]));
+            }
+        }
+        if (isnan(s) && r < nr) {
+            // a padding entry (offset 0, +0.0; real entries come first)
+            // multiplied a non-finite x[r]: recompute over the real entries
+            const uint32_t cnt = __ldg(pcnt + p);
+            s = 0.0;
+#pragma unroll 1
+            for (uint32_t e = 0; e < cnt; ++e) {
+                const int32_t oe = reinterpret_cast<const int32_t*>(pb + 32 * (e / 8))[e % 8];
+                const double ve = reinterpret_cast<const double*>(pb + 32 * G + 64 * (e / 8))[e % 8];
+                s = __dadd_rn(s, __dmul_rn(ve, __ldg(xb + oe)));
+            }
+        }
+        if (r >= nr) continue;
+        if (MODE == 1) s = __dsub_rn(__ldg(b + r), s);
+        y[r] = s;
+        if (with_norm) acc = __dadd_rn(acc, __dmul_rn(s, s));
+    }
+    if (!with_norm) return;
+    acc = warp_sum(acc);
+    if (lane == 0) red[threadIdx.x >> 5] = acc;
+    __syncthreads();
+    if (with_norm == 2) {
+        if (threadIdx.x == 0) {
+            double t = red[0];
+            for (int w = 1; w < 8; ++w) t = __dadd_rn(t, red[w]);
+            partials[blockIdx.x] = t;
+        }
+        return;
+    }
+    block_finalize(red, 8, 1, partials, ticket, norm_out, accumulate != 0);
+}
+
 int dict_grid(uint64_t rows) {
     const uint64_t want = (rows + kDThreads - 1) / kDThreads;
     const uint64_t cap = static_cast<uint64_t>(sm_count()) * 8;
@@ -576,13 +775,97 @@ void ensure(T*& p, uint64_t& cap, uint64_t need) {
     cap = need;
 }
 
+// Row-pattern switch (A/B: CBGX_PPAT=0 keeps the pair-coded kernel).
+bool ppat_enabled() {
+    static const bool v = [] {
+        const char* e = getenv("CBGX_PPAT");
+        return !e || atoi(e) != 0;
+    }();
+    return v;
+}
+
+// The row-pattern copy from the pair codes (see ppat_spmv_kernel): a scan
+// collects the distinct rows (one 40 KB host round trip), the host builds the
+// pattern tables, a map pass writes one id byte per row and verifies it (one
+// more 4-byte round trip). D.n_pat stays 0 on more than 255 patterns.
+void build_patterns(DictSell& D, const std::vector<int32_t>& po, const std::vector<double>& pv, cudaStream_t st) {
+    D.n_pat = 0;
+    const uint32_t g8 = D.ell8_w / 8;
+    if (!ppat_enabled() || D.max_level < 2 || g8 < 1 || g8 > 4) return;
+    uint64_t cap = 0;
+    if (!D.pkeys) {
+        ensure(D.pkeys, cap, kPatSlots);
+        ensure(D.pwords, cap, kPatSlots * 4);
+        ensure(D.pslot, cap, kPatSlots);
+    }
+    const uint64_t rows = D.nslices * 32;
+    CBGX_CUDA(cudaMemsetAsync(D.pkeys, 0, kPatSlots * sizeof(unsigned long long), st));
+    CBGX_CUDA(cudaMemsetAsync(D.flags, 0, sizeof(unsigned), st));
+    const int grid = static_cast<int>(std::max<uint64_t>(1, std::min<uint64_t>((rows + 255) / 256, sm_count() * 2ull)));
+    const uint2* c8 = reinterpret_cast<const uint2*>(D.codes8);
+    CBGX_K(pat_scan_kernel<<<grid, 256, 0, st>>>(c8, rows, g8, D.pkeys, D.pwords, D.flags));
+    CBGX_CUDA(cudaGetLastError());
+    std::vector<unsigned long long> keys(kPatSlots);
+    std::vector<uint2> words(kPatSlots * 4);
+    unsigned bad = 0;
+    CBGX_CUDA(cudaMemcpyAsync(keys.data(), D.pkeys, kPatSlots * sizeof(unsigned long long), cudaMemcpyDeviceToHost, st));
+    CBGX_CUDA(cudaMemcpyAsync(words.data(), D.pwords, kPatSlots * 4 * sizeof(uint2), cudaMemcpyDeviceToHost, st));
+    CBGX_CUDA(cudaMemcpyAsync(&bad, D.flags, sizeof(unsigned), cudaMemcpyDeviceToHost, st));
+    CBGX_CUDA(cudaStreamSynchronize(st));
+    if (bad) return;
+    std::vector<uint8_t> slot(kPatSlots, 0);
+    std::vector<uint2> pw;
+    uint32_t np = 0;
+    for (uint32_t i = 0; i < kPatSlots; ++i) {
+        if (!keys[i]) continue;
+        if (np == 255) return;
+        slot[i] = static_cast<uint8_t>(np++);
+        for (uint32_t g = 0; g < g8; ++g) pw.push_back(words[i * 4 + g]);
+    }
+    const uint32_t stride = 96 * g8;  // bytes per pattern
+    if (np * stride > kPatTabMax) return;
+    if (np == 0) return;
+    std::vector<uint8_t> tab(static_cast<size_t>(np) * stride, 0);
+    std::vector<uint8_t> cnt(np, 0);
+    for (uint32_t p = 0; p < np; ++p) {
+        int32_t* off = reinterpret_cast<int32_t*>(tab.data() + p * stride);
+        double* val = reinterpret_cast<double*>(tab.data() + p * stride + 32 * g8);
+        for (uint32_t e = 0; e < 8 * g8; ++e) {
+            const uint2 w = pw[p * g8 + e / 8];
+            const uint32_t k = e % 8;
+            const uint32_t c = ((k < 4 ? w.x : w.y) >> (8 * (k & 3))) & 0xFFu;
+            off[e] = c == 0xFFu ? kPatPad : po[c];
+            val[e] = c == 0xFFu ? 0.0 : pv[c];
+            // real entries first, then padding (dict_fill_kernel, pair_convert_kernel)
+            if (c != 0xFFu) cnt[p] = static_cast<uint8_t>(e + 1);
+        }
+    }
+    if (!D.ptab) CBGX_CUDA(cudaMalloc(reinterpret_cast<void**>(&D.ptab), kPatTabMax));
+    if (!D.pcnt) CBGX_CUDA(cudaMalloc(reinterpret_cast<void**>(&D.pcnt), 256));
+    CBGX_CUDA(cudaMemcpyAsync(D.pcnt, cnt.data(), np, cudaMemcpyHostToDevice, st));
+    ensure(D.pid, D.pid_cap, rows);
+    uint2* d_pw = D.pwords;  // dense pattern words reuse the scratch (after the copy back)
+    CBGX_CUDA(cudaMemcpyAsync(D.ptab, tab.data(), tab.size(), cudaMemcpyHostToDevice, st));
+    CBGX_CUDA(cudaMemcpyAsync(D.pslot, slot.data(), kPatSlots, cudaMemcpyHostToDevice, st));
+    CBGX_CUDA(cudaMemcpyAsync(d_pw, pw.data(), pw.size() * sizeof(uint2), cudaMemcpyHostToDevice, st));
+    CBGX_K(pat_map_kernel<<<grid, 256, 0, st>>>(c8, rows, g8, D.pkeys, D.pslot, d_pw, D.pid, D.flags));
+    CBGX_CUDA(cudaGetLastError());
+    CBGX_CUDA(cudaMemcpyAsync(&bad, D.flags, sizeof(unsigned), cudaMemcpyDeviceToHost, st));
+    // the host vectors above are read by the async copies: finish them here
+    CBGX_CUDA(cudaStreamSynchronize(st));
+    if (bad) return;
+    D.ptab_u4 = static_cast<uint32_t>(tab.size() / 16);
+    D.n_pat = np;
+}
+
 // The pair-coded ELL8 copy from the ELL4 2-byte codes (see pell_spmv_kernel):
 // one pass marks the 2-byte codes present, the host numbers them (one round
 // trip of 8 KB), one pass rewrites the codes as bytes. D.ell8_w stays 0 (the
 // 2-byte kernel is used) for SELL layouts or more than 255 pairs.
 void build_pairs(DictSell& D, const std::vector<int32_t>& d_off, const std::vector<double>& d_val, cudaStream_t st) {
     D.ell8_w = 0;
-    if (!D.ell_w || !pell_enabled()) return;
+    D.n_pat = 0;
+    if (!D.ell_w || !pell_enabled() || D.max_level < 1) return;
     uint64_t cap = 0;
     if (!D.bitmap) {
         ensure(D.bitmap, cap, 2048);
@@ -632,6 +915,7 @@ void build_pairs(DictSell& D, const std::vector<int32_t>& d_off, const std::vect
     D.entries8 = bytes;
     D.ell8_w = 8 * g8;
     D.n_pair = np;
+    build_patterns(D, po, pv, st);
 }
 
 // Builds (or rebuilds, reusing D's buffers) the dictionary copy of A. One
@@ -750,7 +1034,9 @@ DictSell::~DictSell() {
     for (void* p : {static_cast<void*>(codes), static_cast<void*>(soff), static_cast<void*>(off), static_cast<void*>(val),
                     static_cast<void*>(tabs), static_cast<void*>(flags), static_cast<void*>(idx),
                     static_cast<void*>(codes8), static_cast<void*>(pair_val), static_cast<void*>(pair_off),
-                    static_cast<void*>(map8), static_cast<void*>(bitmap)})
+                    static_cast<void*>(map8), static_cast<void*>(bitmap), static_cast<void*>(pid),
+                    static_cast<void*>(ptab), static_cast<void*>(pkeys), static_cast<void*>(pwords),
+                    static_cast<void*>(pslot), static_cast<void*>(pcnt)})
         if (p) cudaFree(p);
 }
 
@@ -817,6 +1103,17 @@ static uint32_t pell_launch(const cbgx_csr& A, const DictSell& D, const double* 
     lc.attrs = at;
     lc.numAttrs = pdl ? 1 : 0;
     note_launch();
+    if (D.n_pat && std::max(A.n_rows, A.n_cols) < (1ull << 31)) {
+        const uint32_t G = D.ell8_w / 8;
+        auto k = G == 1 ? ppat_spmv_kernel<MODE, 1> : G == 2 ? ppat_spmv_kernel<MODE, 2>
+               : G == 3 ? ppat_spmv_kernel<MODE, 3> : ppat_spmv_kernel<MODE, 4>;
+        lc.dynamicSmemBytes = static_cast<size_t>(D.ptab_u4) * 16;
+        CBGX_CUDA(cudaLaunchKernelEx(&lc, k, A.n_rows, static_cast<const uint8_t*>(D.pid),
+                                     static_cast<const uint4*>(D.ptab), D.ptab_u4,
+                                     static_cast<const uint8_t*>(D.pcnt), x, b, y, fused, partials, ticket,
+                                     norm, s_begin, s_end, static_cast<int>(accumulate)));
+        return static_cast<uint32_t>(grid);
+    }
     // G1's gather offsets are 32-bit byte offsets into x
     const bool g1 = PELL_G1 && D.ell8_w == 8 && std::max(A.n_rows, A.n_cols) * 8 < (1ull << 32);
     CBGX_CUDA(cudaLaunchKernelEx(&lc, g1 ? pell_spmv_kernel<MODE, 1> : pell_spmv_kernel<MODE, 0>, A.n_rows, D.ell8_w / 8,
@@ -902,12 +1199,18 @@ struct cbgx_dict_csr {
 extern "C" {
 
 int cbgx_csr_dict_create(const cbgx_csr* A, cbgx_dict_csr** out, void* stream) {
+    return cbgx_csr_dict_create2(A, 2, out, stream);
+}
+
+int cbgx_csr_dict_create2(const cbgx_csr* A, uint32_t max_level, cbgx_dict_csr** out, void* stream) {
     return guard([&] {
         if (!A || !out) throw Error(CBGX_EINVAL, "dict: null argument");
         if (A->row_ptr_bits != 32 && A->row_ptr_bits != 64) throw Error(CBGX_EINVAL, "csr: row_ptr_bits must be 32 or 64");
         *out = nullptr;
         if (A->n_cols < A->n_rows) throw Error(CBGX_EINVAL, "dict: needs n_cols >= n_rows");
+        if (max_level > 2) throw Error(CBGX_EINVAL, "dict: max_level must be 0, 1 or 2");
         auto D = std::make_unique<DictSell>();
+        D->max_level = max_level;
         if (!build_dict_sell(*A, 0.0, as_stream(stream), *D))
             throw Error(CBGX_EINVAL, "dict: matrix does not fit the dictionary format (more than 255 distinct values or column offsets, or a row longer than max_row_nnz)");
         CBGX_CUDA(cudaStreamSynchronize(as_stream(stream)));
@@ -921,6 +1224,16 @@ int cbgx_csr_dict_info(const cbgx_dict_csr* D, uint32_t* n_offsets, uint32_t* n_
         if (n_offsets) *n_offsets = D->d->n_off;
         if (n_values) *n_values = D->d->n_val;
         if (entries) *entries = D->d->entries;
+    });
+}
+
+int cbgx_csr_dict_layout(const cbgx_dict_csr* D, uint32_t* level, uint32_t* n_pairs, uint32_t* n_patterns) {
+    return guard([&] {
+        if (!D) throw Error(CBGX_EINVAL, "dict: null handle");
+        const DictSell& d = *D->d;
+        if (level) *level = d.n_pat ? 3u : d.ell8_w ? 2u : d.ell_w ? 1u : 0u;
+        if (n_pairs) *n_pairs = d.ell8_w ? d.n_pair : 0u;
+        if (n_patterns) *n_patterns = d.n_pat;
     });
 }
 

@@ -89,6 +89,9 @@ struct DictSell {
     uint64_t nslices = 0;
     uint64_t entries = 0;
     uint32_t n_off = 0, n_val = 0;
+    // build options (cbgx_csr_dict_create2): 0 = 2-byte codes only,
+    // 1 = up to pair codes, 2 = up to row patterns (default)
+    uint32_t max_level = 2;
     uint32_t ell_w = 0;  // > 0: ELL4 layout, every row padded to this width
     bool ready = false;
     // Pair-coded ELL8 copy (when the matrix holds <= 255 distinct (value,
@@ -102,8 +105,22 @@ struct DictSell {
     int32_t* pair_off = nullptr;  // [256]
     uint8_t* map8 = nullptr;      // [65536] 2-byte code -> pair index
     unsigned* bitmap = nullptr;   // [2048] codes present
+    // Row-pattern copy (when the pair-coded rows take <= 255 distinct
+    // patterns): one byte per row into a table of {offsets, values} per
+    // pattern. Used by the SpMV when n_pat > 0.
+    uint8_t* pid = nullptr;
+    uint64_t pid_cap = 0;
+    uint4* ptab = nullptr;        // n_pat * 96 * G bytes
+    uint8_t* pcnt = nullptr;      // [256] leading real entries per pattern
+    uint32_t n_pat = 0, ptab_u4 = 0;
+    unsigned long long* pkeys = nullptr;  // build scratch [1024]
+    uint2* pwords = nullptr;              // build scratch [1024 * 4]
+    uint8_t* pslot = nullptr;             // build scratch [1024]
     // matrix bytes one SpMV streams (the codes actually read)
-    double code_bytes() const { return ell8_w ? static_cast<double>(entries8) : 2.0 * static_cast<double>(entries); }
+    double code_bytes() const {
+        return n_pat ? static_cast<double>(nslices) * 32.0
+                     : ell8_w ? static_cast<double>(entries8) : 2.0 * static_cast<double>(entries);
+    }
     // build scratch and capacities (kept across rebuilds)
     unsigned long long* tabs = nullptr;
     unsigned* flags = nullptr;

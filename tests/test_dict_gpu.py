@@ -35,20 +35,28 @@ def few_valued(rng, n, max_len, offsets, values, empty_frac=0.1):
 
 
 def check_paths(cbg, port, rp, ci, va, seed):
+    """Every coding level the matrix admits (2-byte codes, pair codes, row
+    patterns -- cbgx_csr_dict_create2) gives the reference's y, b - A x and
+    norms bit for bit. Returns the default (highest-level) copy."""
     n = rp.size - 1
     A = cbg.DeviceCsr.from_host(cbg.CsrMatrix(n, n, rp, ci, va))
-    D = cbg.DictCsr(A)
     rng = np.random.default_rng(seed)
     x = rng.standard_normal(n)
-    ref = port.spmv(rp, ci, va, x)
-    y, nrm = D.spmv(x, want_norm=True)
-    assert y.cpu().numpy().tobytes() == ref.tobytes()
-    assert abs(nrm.item() - float(ref @ ref)) <= 1e-12 * max(1.0, float(ref @ ref))
-    _, nrm_ref = D.spmv(x, want_norm=True, reduction=1)
-    assert nrm_ref.item() == port.dot(ref, ref)
     b = rng.standard_normal(n)
-    r = D.spmv(x, b=b)
-    assert r.cpu().numpy().tobytes() == (b - ref).tobytes()
+    ref = port.spmv(rp, ci, va, x)
+    levels = set()
+    for max_level in (0, 1, 2):
+        D = cbg.DictCsr(A, max_level=max_level)
+        level = D.layout()[0]
+        assert level <= max_level + 1
+        levels.add(level)
+        y, nrm = D.spmv(x, want_norm=True)
+        assert y.cpu().numpy().tobytes() == ref.tobytes(), level
+        assert abs(nrm.item() - float(ref @ ref)) <= 1e-12 * max(1.0, float(ref @ ref))
+        _, nrm_ref = D.spmv(x, want_norm=True, reduction=1)
+        assert nrm_ref.item() == port.dot(ref, ref)
+        r = D.spmv(x, b=b)
+        assert r.cpu().numpy().tobytes() == (b - ref).tobytes(), level
     return D
 
 
@@ -60,6 +68,23 @@ def test_stencils_bit_exact(cbg, port, kind, dims, pe):
     no, nv, ne = D.info()
     assert no == {0: 7, 1: 7, 2: 27}[kind] and nv <= 7
     assert ne >= ci.size and ne % 32 == 0
+    # constant-coefficient stencils on a box: one pattern per (x, y, z)
+    # boundary class, 3^3 = 27 row patterns (+1: the all-padding rows that
+    # fill the last 32-row slice) -> the row-pattern kernel
+    if kind != 1:
+        n = rp.size - 1
+        assert D.layout() == (3, no, 27 + (n % 32 != 0))
+
+
+def test_row_patterns_beyond_255_fall_back_to_pairs(cbg, port):
+    """<= 255 pairs but more than 255 distinct rows: the pair-coded kernel."""
+    rng = np.random.default_rng(11)
+    n = 6000
+    offsets = np.array([-40, -7, -3, -1, 0, 1, 2, 5, 9, 33])
+    rp, ci, va = few_valued(rng, n, 8, offsets, np.array([1.5]), empty_frac=0.02)
+    D = check_paths(cbg, port, rp, ci, va, 3)
+    level, npairs, npat = D.layout()
+    assert level == 2 and npairs == 10 and npat == 0
 
 
 @pytest.mark.parametrize("nx,ny,pe,dec", [(10, 10, 1.0, 0.0), (37, 29, 3.0, 0.0), (8, 8, 1.0, 12.0)])
