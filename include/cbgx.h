@@ -227,9 +227,11 @@ int cbgx_csr_dict_info(const cbgx_dict_csr* D, uint32_t* n_offsets, uint32_t* n_
 /* create with a ceiling on the coding level: 0 = 2-byte codes (value index,
  * offset index), 1 = 1-byte pair codes when <= 255 distinct (value, offset)
  * pairs, 2 = one byte per ROW when the pair-coded rows take <= 255 distinct
- * patterns (constant-coefficient stencils; default of cbgx_csr_dict_create).
+ * patterns, 3 = uniform slots when those patterns' offsets embed into one
+ * sorted list of <= 32 offsets with one value each (constant-coefficient
+ * stencils; the default of cbgx_csr_dict_create).
  * layout: level in use (0 SELL / 1 ELL4 2-byte / 2 pair-coded ELL8 / 3 row
- * patterns), the pair and pattern counts. */
+ * patterns / 4 uniform slots), the pair and pattern counts. */
 int cbgx_csr_dict_create2(const cbgx_csr* A, uint32_t max_level, cbgx_dict_csr** out, void* stream);
 int cbgx_csr_dict_layout(const cbgx_dict_csr* D, uint32_t* level, uint32_t* n_pairs, uint32_t* n_patterns);
 int cbgx_csr_dict_spmv(const cbgx_csr* A, const cbgx_dict_csr* D, const double* d_x, const double* d_b, double* d_y,

@@ -602,9 +602,10 @@ class DictCsr:
     2-byte codes into <= 255 distinct values and column offsets. Raises
     CbgxError for matrices outside that pattern."""
 
-    def __init__(self, a: DeviceCsr, max_level: int = 2):
+    def __init__(self, a: DeviceCsr, max_level: int = 3):
         """max_level: 0 = 2-byte codes, 1 = up to 1-byte pair codes,
-        2 = up to one pattern byte per row (cbgx_csr_dict_create2)."""
+        2 = up to one pattern byte per row, 3 = up to uniform slots
+        (cbgx_csr_dict_create2)."""
         import ctypes
         self.a = a
         self.h = ctypes.c_void_p()
@@ -612,7 +613,7 @@ class DictCsr:
 
     def layout(self):
         """(level, pairs, patterns): level 0 SELL / 1 ELL4 2-byte codes /
-        2 pair-coded ELL8 / 3 row patterns."""
+        2 pair-coded ELL8 / 3 row patterns / 4 uniform slots."""
         import ctypes
         lv, npr, npt = ctypes.c_uint32(), ctypes.c_uint32(), ctypes.c_uint32()
         check(lib().cbgx_csr_dict_layout(self.h, ctypes.byref(lv), ctypes.byref(npr), ctypes.byref(npt)))

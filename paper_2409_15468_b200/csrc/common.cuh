@@ -60,15 +60,19 @@ __device__ __forceinline__ uint32_t exp_field(double x) {
 }
 
 // kernels.hpp:18-37 for 2 <= L <= 32, given the block's e_max.
+// The magnitude sig >> sh (sig = the 53-bit significand, sh = 54 - L +
+// e_max - e >= 22) never uses sig's low 21 bits: it is t >> (sh - 21) with
+// t = sig >> 21 (one funnel shift; the exponent and sign bits of the high
+// word shift out) and a clamped shift (0 once sh - 21 >= 32) -- no 64-bit
+// shift.
 template <int L>
 __device__ __forceinline__ uint32_t encode32(double x, uint32_t e_max) {
     const uint32_t hi = static_cast<uint32_t>(__double2hiint(x));
     const uint32_t lo = static_cast<uint32_t>(__double2loint(x));
     const uint32_t sgn = (hi >> 31) << (L - 1);
     const uint32_t e = (hi >> 20) & 0x7FFu;
-    const uint64_t sig = (static_cast<uint64_t>((hi & 0xFFFFFu) | 0x100000u) << 32) | lo;
-    const int sh = 54 - L + static_cast<int>(e_max) - static_cast<int>(e);  // >= 22 for L<=32
-    const uint32_t mag = sh >= 64 ? 0u : static_cast<uint32_t>(sig >> sh);
+    const uint32_t t = __funnelshift_l(lo, hi | 0x100000u, 11);
+    const uint32_t mag = __funnelshift_rc(t, 0u, 33u - L + e_max - e);  // e <= e_max: shift >= 1
     return e == 0 ? sgn : (sgn | mag);
 }
 

@@ -18,6 +18,7 @@
 #include <cub/device/device_scan.cuh>
 
 #include <algorithm>
+#include <cmath>
 #include <cstdlib>
 #include <cstring>
 #include <vector>
@@ -751,6 +752,85 @@ ppat_spmv_kernel(uint64_t n_rows, const uint8_t* __restrict__ pid, const uint4* 
     block_finalize(red, 8, 1, partials, ticket, norm_out, accumulate != 0);
 }
 
+// Uniform-slot patterns (a constant-coefficient stencil): the real column
+// offsets of every row pattern, in row order, embed into ONE sorted list of
+// S <= 32 slots, and every slot carries one value whatever the pattern. A
+// row is then its pattern's slot mask: per slot present, one gather of
+// x[r + off[u]] and one multiply-add by val[u] -- offsets and values are
+// kernel parameters (constant bank operands, no shared-memory table loads).
+// An absent slot gathers nothing and multiplies +0.0: with every slot value
+// finite (checked at build) that adds +-0, which leaves the row sum unchanged
+// (it starts at +0.0 and is never -0.0), so the row sums its real entries in
+// row order: bit-identical to spmv() (sparse.cpp:50-52) for any x.
+struct USlots {
+    int32_t off[32];
+    double val[32];
+};
+
+template <int MODE, int S>
+__global__ void __launch_bounds__(256, PELL_MIN_BLOCKS)
+uslot_spmv_kernel(uint64_t n_rows, const uint8_t* __restrict__ pid, const uint32_t* __restrict__ pmask,
+                  uint32_t n_pat, const __grid_constant__ USlots us, const double* __restrict__ x,
+                  const double* __restrict__ b, double* __restrict__ y, int with_norm,
+                  double* __restrict__ partials, unsigned* __restrict__ ticket, double* __restrict__ norm_out,
+                  uint64_t s_begin, uint64_t s_end, int accumulate) {
+    __shared__ uint32_t smask[256];
+    __shared__ double red[8];
+    if (threadIdx.x < n_pat) smask[threadIdx.x] = pmask[threadIdx.x];
+    pdl_trigger();
+    const int lane = threadIdx.x & 31;
+    const uint64_t nw = static_cast<uint64_t>(gridDim.x) * 8;
+    const uint64_t sl = s_begin + (blockIdx.x * 256ull + threadIdx.x) / 32;
+    const uint32_t iters = sl < s_end ? static_cast<uint32_t>((s_end - sl + nw - 1) / nw) : 0u;
+    int32_t r = static_cast<int32_t>(sl * 32 + lane);
+    const int32_t rstep = static_cast<int32_t>(nw * 32);
+    const int32_t nr = static_cast<int32_t>(n_rows);
+    double acc = 0.0;
+    uint32_t nxt = 0;
+    const uint8_t* pp = pid + r;  // running pointer to the next slice's ids
+    if (iters) nxt = __ldcs(pp);  // ids do not depend on the predecessor
+    __syncthreads();
+    pdl_wait();
+    for (uint32_t it = 0; it < iters; ++it, r += rstep) {
+        const uint32_t m = smask[nxt];
+        pp += rstep;
+        if (it + 1 < iters) nxt = __ldcs(pp);
+        const double* xb = x + min(r, nr - 1);
+        asm("" : "+l"(xb));  // one IMAD.WIDE per gather (see ppat_spmv_kernel)
+        double s = 0.0;
+#pragma unroll
+        for (int g = 0; g < S; g += 8) {
+            constexpr int kMax = 8;
+            double xv[kMax];
+#pragma unroll
+            for (int k = 0; k < kMax; ++k) {
+                xv[k] = 0.0;
+                if (g + k < S && (m >> (g + k) & 1u)) xv[k] = __ldg(xb + us.off[g + k]);
+            }
+#pragma unroll
+            for (int k = 0; k < kMax; ++k)
+                if (g + k < S) s = __dadd_rn(s, __dmul_rn(us.val[g + k], xv[k]));
+        }
+        if (r >= nr) continue;
+        if (MODE == 1) s = __dsub_rn(__ldg(b + r), s);
+        y[r] = s;
+        if (with_norm) acc = __dadd_rn(acc, __dmul_rn(s, s));
+    }
+    if (!with_norm) return;
+    acc = warp_sum(acc);
+    if (lane == 0) red[threadIdx.x >> 5] = acc;
+    __syncthreads();
+    if (with_norm == 2) {
+        if (threadIdx.x == 0) {
+            double t = red[0];
+            for (int w = 1; w < 8; ++w) t = __dadd_rn(t, red[w]);
+            partials[blockIdx.x] = t;
+        }
+        return;
+    }
+    block_finalize(red, 8, 1, partials, ticket, norm_out, accumulate != 0);
+}
+
 int dict_grid(uint64_t rows) {
     const uint64_t want = (rows + kDThreads - 1) / kDThreads;
     const uint64_t cap = static_cast<uint64_t>(sm_count()) * 8;
@@ -790,6 +870,7 @@ bool ppat_enabled() {
 // more 4-byte round trip). D.n_pat stays 0 on more than 255 patterns.
 void build_patterns(DictSell& D, const std::vector<int32_t>& po, const std::vector<double>& pv, cudaStream_t st) {
     D.n_pat = 0;
+    D.n_slots = 0;
     const uint32_t g8 = D.ell8_w / 8;
     if (!ppat_enabled() || D.max_level < 2 || g8 < 1 || g8 > 4) return;
     uint64_t cap = 0;
@@ -856,6 +937,43 @@ void build_patterns(DictSell& D, const std::vector<int32_t>& po, const std::vect
     if (bad) return;
     D.ptab_u4 = static_cast<uint32_t>(tab.size() / 16);
     D.n_pat = np;
+    // uniform slots: every pattern's real offsets increasing, their union
+    // <= 32 slots, one value per slot
+    D.n_slots = 0;
+    if (D.max_level < 3) return;
+    std::vector<int32_t> u;
+    for (uint32_t p = 0; p < np; ++p) {
+        const int32_t* off = reinterpret_cast<const int32_t*>(tab.data() + p * stride);
+        for (uint32_t e = 0; e < cnt[p]; ++e) {
+            if (e && off[e] <= off[e - 1]) return;
+            u.push_back(off[e]);
+        }
+    }
+    std::sort(u.begin(), u.end());
+    u.erase(std::unique(u.begin(), u.end()), u.end());
+    if (u.empty() || u.size() > 32) return;
+    USlots us{};
+    std::vector<bool> seen(u.size(), false);
+    std::vector<uint32_t> mask(np, 0u);
+    for (uint32_t p = 0; p < np; ++p) {
+        const int32_t* off = reinterpret_cast<const int32_t*>(tab.data() + p * stride);
+        const double* val = reinterpret_cast<const double*>(tab.data() + p * stride + 32 * g8);
+        for (uint32_t e = 0; e < cnt[p]; ++e) {
+            const uint32_t k = static_cast<uint32_t>(std::lower_bound(u.begin(), u.end(), off[e]) - u.begin());
+            if (seen[k] && std::memcmp(&us.val[k], &val[e], 8) != 0) return;
+            if (!std::isfinite(val[e])) return;  // absent slots multiply +0.0
+            us.val[k] = val[e];
+            seen[k] = true;
+            mask[p] |= 1u << k;
+        }
+    }
+    for (size_t k = 0; k < u.size(); ++k) us.off[k] = u[k];
+    if (!D.pmask) CBGX_CUDA(cudaMalloc(reinterpret_cast<void**>(&D.pmask), 256 * sizeof(uint32_t)));
+    CBGX_CUDA(cudaMemcpyAsync(D.pmask, mask.data(), np * sizeof(uint32_t), cudaMemcpyHostToDevice, st));
+    CBGX_CUDA(cudaStreamSynchronize(st));
+    static_assert(sizeof(USlots) <= sizeof(D.uslots), "USlots storage");
+    std::memcpy(D.uslots, &us, sizeof(USlots));
+    D.n_slots = static_cast<uint32_t>(u.size());
 }
 
 // The pair-coded ELL8 copy from the ELL4 2-byte codes (see pell_spmv_kernel):
@@ -865,6 +983,7 @@ void build_patterns(DictSell& D, const std::vector<int32_t>& po, const std::vect
 void build_pairs(DictSell& D, const std::vector<int32_t>& d_off, const std::vector<double>& d_val, cudaStream_t st) {
     D.ell8_w = 0;
     D.n_pat = 0;
+    D.n_slots = 0;
     if (!D.ell_w || !pell_enabled() || D.max_level < 1) return;
     uint64_t cap = 0;
     if (!D.bitmap) {
@@ -1036,7 +1155,7 @@ DictSell::~DictSell() {
                     static_cast<void*>(codes8), static_cast<void*>(pair_val), static_cast<void*>(pair_off),
                     static_cast<void*>(map8), static_cast<void*>(bitmap), static_cast<void*>(pid),
                     static_cast<void*>(ptab), static_cast<void*>(pkeys), static_cast<void*>(pwords),
-                    static_cast<void*>(pslot), static_cast<void*>(pcnt)})
+                    static_cast<void*>(pslot), static_cast<void*>(pcnt), static_cast<void*>(pmask)})
         if (p) cudaFree(p);
 }
 
@@ -1103,6 +1222,18 @@ static uint32_t pell_launch(const cbgx_csr& A, const DictSell& D, const double* 
     lc.attrs = at;
     lc.numAttrs = pdl ? 1 : 0;
     note_launch();
+    if (D.n_slots && std::max(A.n_rows, A.n_cols) < (1ull << 31)) {
+        const uint32_t S = D.n_slots;
+        auto k = S == 7 ? uslot_spmv_kernel<MODE, 7> : S == 27 ? uslot_spmv_kernel<MODE, 27>
+               : S <= 8 ? uslot_spmv_kernel<MODE, 8> : S <= 16 ? uslot_spmv_kernel<MODE, 16>
+               : S <= 24 ? uslot_spmv_kernel<MODE, 24> : uslot_spmv_kernel<MODE, 32>;
+        USlots us;
+        std::memcpy(&us, D.uslots, sizeof(USlots));
+        CBGX_CUDA(cudaLaunchKernelEx(&lc, k, A.n_rows, static_cast<const uint8_t*>(D.pid),
+                                     static_cast<const uint32_t*>(D.pmask), D.n_pat, us, x, b, y, fused, partials,
+                                     ticket, norm, s_begin, s_end, static_cast<int>(accumulate)));
+        return static_cast<uint32_t>(grid);
+    }
     if (D.n_pat && std::max(A.n_rows, A.n_cols) < (1ull << 31)) {
         const uint32_t G = D.ell8_w / 8;
         auto k = G == 1 ? ppat_spmv_kernel<MODE, 1> : G == 2 ? ppat_spmv_kernel<MODE, 2>
@@ -1199,7 +1330,7 @@ struct cbgx_dict_csr {
 extern "C" {
 
 int cbgx_csr_dict_create(const cbgx_csr* A, cbgx_dict_csr** out, void* stream) {
-    return cbgx_csr_dict_create2(A, 2, out, stream);
+    return cbgx_csr_dict_create2(A, 3, out, stream);
 }
 
 int cbgx_csr_dict_create2(const cbgx_csr* A, uint32_t max_level, cbgx_dict_csr** out, void* stream) {
@@ -1208,7 +1339,7 @@ int cbgx_csr_dict_create2(const cbgx_csr* A, uint32_t max_level, cbgx_dict_csr**
         if (A->row_ptr_bits != 32 && A->row_ptr_bits != 64) throw Error(CBGX_EINVAL, "csr: row_ptr_bits must be 32 or 64");
         *out = nullptr;
         if (A->n_cols < A->n_rows) throw Error(CBGX_EINVAL, "dict: needs n_cols >= n_rows");
-        if (max_level > 2) throw Error(CBGX_EINVAL, "dict: max_level must be 0, 1 or 2");
+        if (max_level > 3) throw Error(CBGX_EINVAL, "dict: max_level must be 0, 1, 2 or 3");
         auto D = std::make_unique<DictSell>();
         D->max_level = max_level;
         if (!build_dict_sell(*A, 0.0, as_stream(stream), *D))
@@ -1231,7 +1362,7 @@ int cbgx_csr_dict_layout(const cbgx_dict_csr* D, uint32_t* level, uint32_t* n_pa
     return guard([&] {
         if (!D) throw Error(CBGX_EINVAL, "dict: null handle");
         const DictSell& d = *D->d;
-        if (level) *level = d.n_pat ? 3u : d.ell8_w ? 2u : d.ell_w ? 1u : 0u;
+        if (level) *level = d.n_slots ? 4u : d.n_pat ? 3u : d.ell8_w ? 2u : d.ell_w ? 1u : 0u;
         if (n_pairs) *n_pairs = d.ell8_w ? d.n_pair : 0u;
         if (n_patterns) *n_patterns = d.n_pat;
     });

@@ -90,8 +90,9 @@ struct DictSell {
     uint64_t entries = 0;
     uint32_t n_off = 0, n_val = 0;
     // build options (cbgx_csr_dict_create2): 0 = 2-byte codes only,
-    // 1 = up to pair codes, 2 = up to row patterns (default)
-    uint32_t max_level = 2;
+    // 1 = up to pair codes, 2 = up to row patterns, 3 = up to uniform slots
+    // (default)
+    uint32_t max_level = 3;
     uint32_t ell_w = 0;  // > 0: ELL4 layout, every row padded to this width
     bool ready = false;
     // Pair-coded ELL8 copy (when the matrix holds <= 255 distinct (value,
@@ -112,6 +113,11 @@ struct DictSell {
     uint64_t pid_cap = 0;
     uint4* ptab = nullptr;        // n_pat * 96 * G bytes
     uint8_t* pcnt = nullptr;      // [256] leading real entries per pattern
+    // Uniform-slot copy (n_slots > 0): the patterns' offsets embed into one
+    // list of <= 32 slots with one value each; pmask[p] = the slots of p
+    uint32_t n_slots = 0;
+    uint32_t* pmask = nullptr;    // [256]
+    alignas(8) unsigned char uslots[384];  // USlots (dsell.cu): int32 off[32], fp64 val[32]
     uint32_t n_pat = 0, ptab_u4 = 0;
     unsigned long long* pkeys = nullptr;  // build scratch [1024]
     uint2* pwords = nullptr;              // build scratch [1024 * 4]

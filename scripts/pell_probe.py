@@ -38,7 +38,7 @@ def call(norm):
 
 
 ref = cbg.spmv(A, x)
-for level in (0, 1, 2):
+for level in (0, 1, 2, 3):
   D = cbg.DictCsr(A, max_level=level)
   lay = D.layout()
   call(False)

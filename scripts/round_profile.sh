@@ -21,12 +21,14 @@ python scripts/traffic_from_launches.py "$OUT/ncu_launches.csv" "$OUT/traffic.js
 # full captures: fused orthogonalisation (mid-cycle launch), dictionary SpMV, codec, CGS micro at n = 2^26
 timeout 600 ncu --set full --clock-control none --import-source on -k regex:arnoldi_fused -s 63 -c 1 -o "$OUT/ncu_fused" \
     python scripts/one_solve.py poisson128 frsz2-32 > /dev/null 2>&1
-timeout 600 ncu --set full --clock-control none --import-source on -k regex:pell_spmv -s 30 -c 1 -o "$OUT/ncu_spmv" \
+timeout 600 ncu --set full --clock-control none --import-source on -k regex:uslot_spmv -s 30 -c 1 -o "$OUT/ncu_spmv" \
     python scripts/one_solve.py poisson128 frsz2-32 > /dev/null 2>&1
 timeout 600 ncu --set full --clock-control none --import-source on -k regex:decompress4 -s 3 -c 1 -o "$OUT/ncu_decompress" \
     python scripts/quick_perf.py > /dev/null 2>&1
 timeout 600 ncu --set full --clock-control none --import-source on -k regex:compress4 -s 3 -c 1 -o "$OUT/ncu_compress" \
     python scripts/quick_perf.py > /dev/null 2>&1
+timeout 600 ncu --set full --clock-control none --import-source on -k regex:compress4 -s 2 -c 1 -o "$OUT/ncu_compress21" \
+    python scripts/codec_one.py 21 > /dev/null 2>&1
 # split CGS kernels (dynamic tiles) at n = 2^26, k = 100, per FRSZ2 format: the
 # reports stay on the box (size), their raw metric pages come back as CSV
 for f in frsz2-32 frsz2-21 frsz2-16; do

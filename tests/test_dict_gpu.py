@@ -36,8 +36,9 @@ def few_valued(rng, n, max_len, offsets, values, empty_frac=0.1):
 
 def check_paths(cbg, port, rp, ci, va, seed):
     """Every coding level the matrix admits (2-byte codes, pair codes, row
-    patterns -- cbgx_csr_dict_create2) gives the reference's y, b - A x and
-    norms bit for bit. Returns the default (highest-level) copy."""
+    patterns, uniform slots -- cbgx_csr_dict_create2) gives the reference's
+    y, b - A x and norms bit for bit. Returns the default (highest-level)
+    copy."""
     n = rp.size - 1
     A = cbg.DeviceCsr.from_host(cbg.CsrMatrix(n, n, rp, ci, va))
     rng = np.random.default_rng(seed)
@@ -45,7 +46,7 @@ def check_paths(cbg, port, rp, ci, va, seed):
     b = rng.standard_normal(n)
     ref = port.spmv(rp, ci, va, x)
     levels = set()
-    for max_level in (0, 1, 2):
+    for max_level in (0, 1, 2, 3):
         D = cbg.DictCsr(A, max_level=max_level)
         level = D.layout()[0]
         assert level <= max_level + 1
@@ -70,10 +71,11 @@ def test_stencils_bit_exact(cbg, port, kind, dims, pe):
     assert ne >= ci.size and ne % 32 == 0
     # constant-coefficient stencils on a box: one pattern per (x, y, z)
     # boundary class, 3^3 = 27 row patterns (+1: the all-padding rows that
-    # fill the last 32-row slice) -> the row-pattern kernel
+    # fill the last 32-row slice), every offset with one value -> the
+    # uniform-slot kernel (level 4) over the patterns
     if kind != 1:
         n = rp.size - 1
-        assert D.layout() == (3, no, 27 + (n % 32 != 0))
+        assert D.layout() == (4, no, 27 + (n % 32 != 0))
 
 
 def test_row_patterns_beyond_255_fall_back_to_pairs(cbg, port):
@@ -85,6 +87,23 @@ def test_row_patterns_beyond_255_fall_back_to_pairs(cbg, port):
     D = check_paths(cbg, port, rp, ci, va, 3)
     level, npairs, npat = D.layout()
     assert level == 2 and npairs == 10 and npat == 0
+
+
+def test_row_patterns_without_uniform_slots(cbg, port):
+    """Few row patterns whose offsets carry different values per pattern:
+    the row-pattern kernel (level 3), not the uniform-slot one."""
+    n = 4096
+    rows = []
+    for r in range(n):
+        k = r % 3  # three row kinds: (-2, -1, 0, +1) with a per-kind value set
+        vals = [(0.5, -1.0, 4.0, -1.0), (0.25, -2.0, 5.0, -0.5), (0.5, -1.0, 6.0, -1.0)][k]
+        rows.append([(c, v) for c, v in zip((r - 2, r - 1, r, r + 1), vals) if 0 <= c < n])
+    rp = np.zeros(n + 1, dtype=np.uint64)
+    rp[1:] = np.cumsum([len(x) for x in rows])
+    ci = np.array([c for x in rows for c, _ in x], dtype=np.uint64)
+    va = np.array([v for x in rows for _, v in x])
+    D = check_paths(cbg, port, rp, ci, va, 5)
+    assert D.layout()[0] == 3
 
 
 @pytest.mark.parametrize("nx,ny,pe,dec", [(10, 10, 1.0, 0.0), (37, 29, 3.0, 0.0), (8, 8, 1.0, 12.0)])
