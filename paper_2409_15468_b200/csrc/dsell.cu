@@ -766,9 +766,15 @@ struct USlots {
     int32_t off[32];
     double val[32];
 };
+#ifndef USLOT_U
+#define USLOT_U 1
+#endif
+#ifndef USLOT_MIN_BLOCKS
+#define USLOT_MIN_BLOCKS PELL_MIN_BLOCKS
+#endif
 
 template <int MODE, int S>
-__global__ void __launch_bounds__(256, PELL_MIN_BLOCKS)
+__global__ void __launch_bounds__(256, USLOT_MIN_BLOCKS)
 uslot_spmv_kernel(uint64_t n_rows, const uint8_t* __restrict__ pid, const uint32_t* __restrict__ pmask,
                   uint32_t n_pat, const __grid_constant__ USlots us, const double* __restrict__ x,
                   const double* __restrict__ b, double* __restrict__ y, int with_norm,
@@ -786,35 +792,57 @@ uslot_spmv_kernel(uint64_t n_rows, const uint8_t* __restrict__ pid, const uint32
     const int32_t rstep = static_cast<int32_t>(nw * 32);
     const int32_t nr = static_cast<int32_t>(n_rows);
     double acc = 0.0;
-    uint32_t nxt = 0;
-    const uint8_t* pp = pid + r;  // running pointer to the next slice's ids
-    if (iters) nxt = __ldcs(pp);  // ids do not depend on the predecessor
+    // USLOT_U slices per iteration (their gathers in flight together); ids
+    // prefetched one iteration ahead
+    constexpr int U = USLOT_U;
+    uint32_t nxt[U];
+    const uint8_t* pp = pid + r;  // running pointer to the next iteration's ids
+#pragma unroll
+    for (int u = 0; u < U; ++u) nxt[u] = static_cast<uint32_t>(u) < iters ? __ldcs(pp + u * rstep) : 0u;
     __syncthreads();
     pdl_wait();
-    for (uint32_t it = 0; it < iters; ++it, r += rstep) {
-        const uint32_t m = smask[nxt];
-        pp += rstep;
-        if (it + 1 < iters) nxt = __ldcs(pp);
-        const double* xb = x + min(r, nr - 1);
-        asm("" : "+l"(xb));  // one IMAD.WIDE per gather (see ppat_spmv_kernel)
-        double s = 0.0;
+    for (uint32_t it = 0; it < iters; it += U, r += U * rstep) {
+        uint32_t m[U];
+        const double* xb[U];
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+            m[u] = it + u < iters ? smask[nxt[u]] : 0u;
+            xb[u] = x + min(r + u * rstep, nr - 1);
+            asm("" : "+l"(xb[u]));  // one IMAD.WIDE per gather (see ppat_spmv_kernel)
+        }
+        pp += U * rstep;
+#pragma unroll
+        for (int u = 0; u < U; ++u)
+            if (it + U + u < iters) nxt[u] = __ldcs(pp + u * rstep);
+        double sum[U];
+#pragma unroll
+        for (int u = 0; u < U; ++u) sum[u] = 0.0;
 #pragma unroll
         for (int g = 0; g < S; g += 8) {
             constexpr int kMax = 8;
-            double xv[kMax];
+            double xv[U][kMax];
 #pragma unroll
-            for (int k = 0; k < kMax; ++k) {
-                xv[k] = 0.0;
-                if (g + k < S && (m >> (g + k) & 1u)) xv[k] = __ldg(xb + us.off[g + k]);
-            }
+            for (int u = 0; u < U; ++u)
 #pragma unroll
-            for (int k = 0; k < kMax; ++k)
-                if (g + k < S) s = __dadd_rn(s, __dmul_rn(us.val[g + k], xv[k]));
+                for (int k = 0; k < kMax; ++k) {
+                    xv[u][k] = 0.0;
+                    if (g + k < S && (m[u] >> (g + k) & 1u)) xv[u][k] = __ldg(xb[u] + us.off[g + k]);
+                }
+#pragma unroll
+            for (int u = 0; u < U; ++u)
+#pragma unroll
+                for (int k = 0; k < kMax; ++k)
+                    if (g + k < S) sum[u] = __dadd_rn(sum[u], __dmul_rn(us.val[g + k], xv[u][k]));
         }
-        if (r >= nr) continue;
-        if (MODE == 1) s = __dsub_rn(__ldg(b + r), s);
-        y[r] = s;
-        if (with_norm) acc = __dadd_rn(acc, __dmul_rn(s, s));
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+            const int32_t ru = r + u * rstep;
+            if (it + u >= iters || ru >= nr) continue;
+            double sv = sum[u];
+            if (MODE == 1) sv = __dsub_rn(__ldg(b + ru), sv);
+            y[ru] = sv;
+            if (with_norm) acc = __dadd_rn(acc, __dmul_rn(sv, sv));
+        }
     }
     if (!with_norm) return;
     acc = warp_sum(acc);
@@ -1200,15 +1228,19 @@ template <int MODE>
 static uint32_t pell_launch(const cbgx_csr& A, const DictSell& D, const double* x, const double* b, double* y, int fused,
                         double* norm, Workspace* ws, cudaStream_t st, bool pdl, uint64_t s_begin = 0,
                         uint64_t s_end = ~0ull, bool accumulate = false) {
-    static int per_sm = -1;
+    static int per_sm = -1, per_sm_u = -1;  // pair/pattern kernels (PELL_MIN_BLOCKS); uniform slots
     if (per_sm < 0) {
         CBGX_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, pell_spmv_kernel<MODE, 0>, 256, 0));
         per_sm = std::max(per_sm, 1);
+        CBGX_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm_u, uslot_spmv_kernel<MODE, 7>, 256, 0));
+        per_sm_u = std::max(per_sm_u, 1);
     }
+    const bool uslot = D.n_slots && std::max(A.n_rows, A.n_cols) < (1ull << 31);
     s_end = std::min<uint64_t>(s_end, D.nslices);
     if (s_begin >= s_end) return 0;
     const uint64_t want = (s_end - s_begin + 7) / 8;
-    const int grid = static_cast<int>(std::max<uint64_t>(1, std::min<uint64_t>(want, static_cast<uint64_t>(sm_count()) * per_sm)));
+    const int grid = static_cast<int>(std::max<uint64_t>(
+        1, std::min<uint64_t>(want, static_cast<uint64_t>(sm_count()) * (uslot ? per_sm_u : per_sm))));
     // fused == 2: per-CTA omega^2 partials into ws->omega_parts (no ticket)
     double* partials = fused == 2 ? ws->get_omega_parts(grid) : fused ? ws->get_partials(grid) : nullptr;
     unsigned* ticket = fused == 1 ? ws->get_counter() : nullptr;
@@ -1222,7 +1254,7 @@ static uint32_t pell_launch(const cbgx_csr& A, const DictSell& D, const double* 
     lc.attrs = at;
     lc.numAttrs = pdl ? 1 : 0;
     note_launch();
-    if (D.n_slots && std::max(A.n_rows, A.n_cols) < (1ull << 31)) {
+    if (uslot) {
         const uint32_t S = D.n_slots;
         auto k = S == 7 ? uslot_spmv_kernel<MODE, 7> : S == 27 ? uslot_spmv_kernel<MODE, 27>
                : S <= 8 ? uslot_spmv_kernel<MODE, 8> : S <= 16 ? uslot_spmv_kernel<MODE, 16>
