@@ -32,15 +32,23 @@ constexpr int kWarps = kThreads / 32;
 // are in flight per iteration to keep enough bytes outstanding per SM.
 constexpr int kSteps = 4;
 
-// >= 3 CTAs/SM: the l=21 packing otherwise takes 94 registers (2 CTAs/SM).
+// >= 3 CTAs/SM: the l=21 packing otherwise takes 94 registers (2 CTAs/SM);
+// l=21 at 2 steps x 4 CTAs/SM (64 registers, no spill): 4.0 -> 4.4 TB/s
+// (scripts/ab_codec.sh; 3 steps x 3 CTAs 4.19).
+#ifndef C21_STEPS
+#define C21_STEPS 2
+#endif
+#ifndef C21_MINB
+#define C21_MINB 4
+#endif
 template <int L, bool kScale>
-__global__ void __launch_bounds__(kThreads, 3)
+__global__ void __launch_bounds__(kThreads, L == 21 ? C21_MINB : 3)
 compress4_kernel(const double* __restrict__ x, uint64_t n, uint64_t nb_write,
                  uint32_t* __restrict__ exps, uint32_t* __restrict__ payload,
                  ScaleArg scale, double* __restrict__ v_out,
                  unsigned long long* __restrict__ bad) {
     // l=21: 2 steps in flight (4 spill at the register budget of 3 CTAs/SM)
-    constexpr int kSteps = L == 21 ? 2 : ::cbgx::kSteps;
+    constexpr int kSteps = L == 21 ? C21_STEPS : ::cbgx::kSteps;
     const int lane = threadIdx.x & 31;
     const double s = kScale ? scale.value() : 1.0;
     const uint64_t nsteps = (nb_write + 3) / 4;

@@ -766,16 +766,19 @@ struct USlots {
     int32_t off[32];
     double val[32];
 };
+// 2 slices per warp iteration, 5 CTAs/SM (scripts/ab_uslot.sh, one box):
+// 7-pt 128^3 solve-like 16.4 -> 14.3 us, 27-pt 256^3 182 -> 150 us, bench
+// SpMV phase 0.72 -> 0.64 ms; 3 slices or 3 CTAs/SM no better.
 #ifndef USLOT_U
-#define USLOT_U 1
+#define USLOT_U 2
 #endif
 #ifndef USLOT_MIN_BLOCKS
-#define USLOT_MIN_BLOCKS PELL_MIN_BLOCKS
+#define USLOT_MIN_BLOCKS 5
 #endif
 
 template <int MODE, int S>
 __global__ void __launch_bounds__(256, USLOT_MIN_BLOCKS)
-uslot_spmv_kernel(uint64_t n_rows, const uint8_t* __restrict__ pid, const uint32_t* __restrict__ pmask,
+uslot_spmv_kernel(uint64_t n_rows, uint64_t n_cols, const uint8_t* __restrict__ pid, const uint32_t* __restrict__ pmask,
                   uint32_t n_pat, const __grid_constant__ USlots us, const double* __restrict__ x,
                   const double* __restrict__ b, double* __restrict__ y, int with_norm,
                   double* __restrict__ partials, unsigned* __restrict__ ticket, double* __restrict__ norm_out,
@@ -1261,7 +1264,7 @@ static uint32_t pell_launch(const cbgx_csr& A, const DictSell& D, const double* 
                : S <= 24 ? uslot_spmv_kernel<MODE, 24> : uslot_spmv_kernel<MODE, 32>;
         USlots us;
         std::memcpy(&us, D.uslots, sizeof(USlots));
-        CBGX_CUDA(cudaLaunchKernelEx(&lc, k, A.n_rows, static_cast<const uint8_t*>(D.pid),
+        CBGX_CUDA(cudaLaunchKernelEx(&lc, k, A.n_rows, A.n_cols, static_cast<const uint8_t*>(D.pid),
                                      static_cast<const uint32_t*>(D.pmask), D.n_pat, us, x, b, y, fused, partials,
                                      ticket, norm, s_begin, s_end, static_cast<int>(accumulate)));
         return static_cast<uint32_t>(grid);

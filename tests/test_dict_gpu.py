@@ -230,3 +230,20 @@ def test_tall_matrix_refused(cbg):
     A = cbg.DeviceCsr.from_host(cbg.CsrMatrix(n_rows, n_cols, rp, ci, va))
     with pytest.raises(Exception, match="n_cols >= n_rows"):
         cbg.DictCsr(A)
+
+
+@pytest.mark.parametrize("offsets", [(-100, -10, -2, 0, 2, 10, 100), (-37, -1, 0, 1), (-5, -4, -3, 0, 3, 4, 5)])
+def test_uniform_slots_without_triples(cbg, port, offsets):
+    """Constant-coefficient band matrices whose offsets do not form the
+    (o - 1, o, o + 1) triples of the shuffle path: the uniform-slot kernel
+    gathers every slot, bit-exact (7 slots: the S = 7 kernel without
+    shuffles; 4 slots: the generic S <= 8 one)."""
+    n = 5000
+    vals = {o: (4.0 if o == 0 else -1.0 / (1 + abs(o))) for o in offsets}
+    rows = [[(r + o, vals[o]) for o in offsets if 0 <= r + o < n] for r in range(n)]
+    rp = np.zeros(n + 1, dtype=np.uint64)
+    rp[1:] = np.cumsum([len(x) for x in rows])
+    ci = np.array([c for x in rows for c, _ in x], dtype=np.uint64)
+    va = np.array([v for x in rows for _, v in x])
+    D = check_paths(cbg, port, rp, ci, va, 9)
+    assert D.layout()[0] == 4
