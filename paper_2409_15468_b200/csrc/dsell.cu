@@ -1238,7 +1238,8 @@ static uint32_t pell_launch(const cbgx_csr& A, const DictSell& D, const double* 
         CBGX_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm_u, uslot_spmv_kernel<MODE, 7>, 256, 0));
         per_sm_u = std::max(per_sm_u, 1);
     }
-    const bool uslot = D.n_slots && std::max(A.n_rows, A.n_cols) < (1ull << 31);
+    // 32-bit row arithmetic: r + U * rstep stays below 2^31
+    const bool uslot = D.n_slots && std::max(A.n_rows, A.n_cols) < (1ull << 31) - (1ull << 24);
     s_end = std::min<uint64_t>(s_end, D.nslices);
     if (s_begin >= s_end) return 0;
     const uint64_t want = (s_end - s_begin + 7) / 8;
