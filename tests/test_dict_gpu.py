@@ -247,3 +247,34 @@ def test_uniform_slots_without_triples(cbg, port, offsets):
     va = np.array([v for x in rows for _, v in x])
     D = check_paths(cbg, port, rp, ci, va, 9)
     assert D.layout()[0] == 4
+
+
+@pytest.mark.parametrize("seed", [1, 2, 3])
+def test_uniform_slots_random_subsets(cbg, port, seed):
+    """Every row takes a random subset of 8 offsets (one value per offset;
+    dense enough for the ELL4 layout the pair codes need): ~100 row patterns
+    over one slot list -> the uniform-slot kernel with arbitrary slot masks,
+    row counts off the 32-row slices; non-finite x entries propagate exactly
+    as in the reference."""
+    rng = np.random.default_rng(seed)
+    n = 3000 + 17 * seed
+    offsets = np.array([-40, -31, -1, 0, 1, 2, 64, 90])
+    vals = rng.standard_normal(offsets.size)
+    rows = []
+    for r in range(n):
+        pick = rng.random(offsets.size) < 0.9
+        rows.append([(r + o, v) for o, v, p in zip(offsets, vals, pick) if p and 0 <= r + o < n])
+    rp = np.zeros(n + 1, dtype=np.uint64)
+    rp[1:] = np.cumsum([len(x) for x in rows])
+    ci = np.array([c for x in rows for c, _ in x], dtype=np.uint64)
+    va = np.array([v for x in rows for _, v in x])
+    D = check_paths(cbg, port, rp, ci, va, seed)
+    level, _, npat = D.layout()
+    assert level == 4 and npat > 32
+    x = rng.standard_normal(n)
+    x[rng.integers(0, n, 5)] = [np.inf, -np.inf, np.nan, np.inf, np.nan]
+    ref = port.spmv(rp, ci, va, x)
+    y = D.spmv(x).cpu().numpy()
+    np.testing.assert_array_equal(np.isnan(y), np.isnan(ref))
+    fin = ~np.isnan(ref)
+    assert y[fin].tobytes() == ref[fin].tobytes()
