@@ -906,30 +906,6 @@ __global__ void write_plain_kernel(unsigned char* __restrict__ col, const double
     }
 }
 
-// A column's exponent range (cbgx_basis.d_erange, erange_fold) from its
-// block exponents; *out zeroed by the caller, one atomic pair per CTA.
-__global__ void __launch_bounds__(256) erange_kernel(const uint32_t* __restrict__ exps, uint64_t nb,
-                                                     uint32_t* __restrict__ out) {
-    __shared__ uint32_t s_inv[8], s_max[8];
-    uint32_t inv = 0, emax = 0;
-    for (uint64_t b = blockIdx.x * 256ull + threadIdx.x; b < nb; b += gridDim.x * 256ull) erange_fold(exps[b], inv, emax);
-    inv = __reduce_max_sync(0xFFFFFFFFu, inv);
-    emax = __reduce_max_sync(0xFFFFFFFFu, emax);
-    if ((threadIdx.x & 31) == 0) {
-        s_inv[threadIdx.x >> 5] = inv;
-        s_max[threadIdx.x >> 5] = emax;
-    }
-    __syncthreads();
-    if (threadIdx.x == 0) {
-        for (int w = 1; w < 8; ++w) {
-            inv = max(inv, s_inv[w]);
-            emax = max(emax, s_max[w]);
-        }
-        atomicMax(out, inv);
-        atomicMax(out + 1, emax);
-    }
-}
-
 template <int F>
 __global__ void read_kernel(BasisView B, uint64_t col, uint64_t first, uint64_t count,
                             double* __restrict__ out) {
@@ -1268,18 +1244,13 @@ template <int F> struct WriteLaunch {
                     double* v_out, uint64_t* bad, cudaStream_t st) {
         unsigned char* col = static_cast<unsigned char*>(V.d_data) + j * V.col_stride_bytes;
         if constexpr (FmtInfo<F>::frsz) {
+            // the column's exponent range for the vote-free fast decode,
+            // folded by the compress kernel itself
+            uint32_t* er = V.d_erange ? V.d_erange + 2 * j : nullptr;
+            if (er) CBGX_CUDA(cudaMemsetAsync(er, 0, 2 * sizeof(uint32_t), st));
             launch_compress(x, V.n, V.n_pad / 32, 32, FmtInfo<F>::L,
                             V.d_exp + j * V.exp_col_stride, reinterpret_cast<uint32_t*>(col),
-                            scale, v_out, bad, st);
-            if (V.d_erange) {
-                // the column's exponent range for the vote-free fast decode
-                uint32_t* out = V.d_erange + 2 * j;
-                CBGX_CUDA(cudaMemsetAsync(out, 0, 2 * sizeof(uint32_t), st));
-                const uint64_t nb = V.n_pad / 32;
-                const int grid = static_cast<int>(std::max<uint64_t>(
-                    1, std::min<uint64_t>((nb + 1023) / 1024, static_cast<uint64_t>(sm_count()))));
-                CBGX_K(erange_kernel<<<grid, 256, 0, st>>>(V.d_exp + j * V.exp_col_stride, nb, out));
-            }
+                            scale, v_out, bad, st, er);
         } else {
             const uint64_t blocks = std::min<uint64_t>((V.n_pad + 255) / 256, static_cast<uint64_t>(sm_count()) * 16);
             CBGX_K(write_plain_kernel<F><<<static_cast<int>(std::max<uint64_t>(blocks, 1)), 256, 0, st>>>(

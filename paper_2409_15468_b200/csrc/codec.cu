@@ -46,7 +46,10 @@ __global__ void __launch_bounds__(kThreads, L == 21 ? C21_MINB : 3)
 compress4_kernel(const double* __restrict__ x, uint64_t n, uint64_t nb_write,
                  uint32_t* __restrict__ exps, uint32_t* __restrict__ payload,
                  ScaleArg scale, double* __restrict__ v_out,
-                 unsigned long long* __restrict__ bad) {
+                 unsigned long long* __restrict__ bad, uint32_t* __restrict__ erange) {
+    // erange != nullptr: the column's exponent range (erange_fold over the
+    // written blocks, cbgx_basis.d_erange) folded here, one atomic pair per CTA
+    uint32_t e_inv = 0, e_max = 0;
     // l=21: 2 steps in flight (4 spill at the register budget of 3 CTAs/SM)
     constexpr int kSteps = L == 21 ? C21_STEPS : ::cbgx::kSteps;
     const int lane = threadIdx.x & 31;
@@ -96,6 +99,10 @@ compress4_kernel(const double* __restrict__ x, uint64_t n, uint64_t nb_write,
 #pragma unroll
             for (int k = 0; k < 4; ++k) c[k] = encode32<L>(v[u][k], e);
             if (live && (lane & 7) == 0) exps[blk] = e;
+            if (erange && live) {  // erange_fold (basis.cuh)
+                e_max = max(e_max, e);
+                if (e) e_inv = max(e_inv, 2047u - e);
+            }
             if constexpr (L == 32) {
                 if (live) reinterpret_cast<uint4*>(payload)[r / 4] = make_uint4(c[0], c[1], c[2], c[3]);
             } else if constexpr (L == 16) {
@@ -121,6 +128,24 @@ compress4_kernel(const double* __restrict__ x, uint64_t n, uint64_t nb_write,
                 if (i0 + 1 < words) dst[1] = __funnelshift_r(w1, w2, o);
                 if (o < 20u && i0 + 2 < words) dst[2] = __funnelshift_r(w2, w3, o);
             }
+        }
+    }
+    if (erange) {  // kernel-uniform
+        __shared__ uint32_t s_er[2 * kWarps];
+        e_inv = __reduce_max_sync(0xFFFFFFFFu, e_inv);
+        e_max = __reduce_max_sync(0xFFFFFFFFu, e_max);
+        if (lane == 0) {
+            s_er[threadIdx.x >> 5] = e_inv;
+            s_er[kWarps + (threadIdx.x >> 5)] = e_max;
+        }
+        __syncthreads();
+        if (threadIdx.x == 0) {
+            for (int w = 1; w < kWarps; ++w) {
+                e_inv = max(e_inv, s_er[w]);
+                e_max = max(e_max, s_er[kWarps + w]);
+            }
+            atomicMax(erange, e_inv);
+            atomicMax(erange + 1, e_max);
         }
     }
 }
@@ -295,7 +320,7 @@ bool fast_path(uint32_t bs, uint32_t l) { return bs == 32 && (l == 16 || l == 21
 
 void launch_compress(const double* x, uint64_t n, uint64_t nb_write, uint32_t bs, uint32_t l,
                      uint32_t* exps, uint32_t* payload, const ScaleArg& scale, double* v_out, uint64_t* bad,
-                     cudaStream_t st) {
+                     cudaStream_t st, uint32_t* erange) {
     validate(bs, l);
     if (nb_write == 0) return;
     auto* badp = reinterpret_cast<unsigned long long*>(bad);
@@ -304,15 +329,16 @@ void launch_compress(const double* x, uint64_t n, uint64_t nb_write, uint32_t bs
         const bool sc = scale.src != nullptr;
 #define CBGX_LAUNCH_C(LL)                                                                    \
     if (sc) CBGX_K(compress4_kernel<LL, true><<<grid, kThreads, 0, st>>>(x, n, nb_write, exps, payload, \
-                                                                   scale, v_out, badp)); \
+                                                                   scale, v_out, badp, erange)); \
     else CBGX_K(compress4_kernel<LL, false><<<grid, kThreads, 0, st>>>(x, n, nb_write, exps, payload,   \
-                                                                 ScaleArg{}, nullptr, badp))
+                                                                 ScaleArg{}, nullptr, badp, erange))
         if (l == 32) { CBGX_LAUNCH_C(32); }
         else if (l == 16) { CBGX_LAUNCH_C(16); }
         else { CBGX_LAUNCH_C(21); }
 #undef CBGX_LAUNCH_C
     } else {
-        if (scale.src || v_out) throw Error(CBGX_EINVAL, "frsz2: fused scale needs bs=32, l in {16,21,32}");
+        if (scale.src || v_out || erange)
+            throw Error(CBGX_EINVAL, "frsz2: fused scale needs bs=32, l in {16,21,32}");
         const uint64_t nb = (n + bs - 1) / bs;
         if (nb_write != nb) throw Error(CBGX_EINVAL, "frsz2: generic codec writes exactly num_blocks");
         CBGX_K(compress_generic_kernel<<<grid_for(nb, 128), 128, 0, st>>>(x, n, bs, l, (static_cast<uint64_t>(bs) * l + 31) / 32,

@@ -198,3 +198,26 @@ def test_read_benchmark_api(cbg):
     assert [(r.format, r.intensity) for r in res] == [("f64", 1), ("f64", 4), ("frsz2-32", 1), ("frsz2-32", 4)]
     assert res[0].stored_bytes == 8 * 65536 and res[2].stored_bytes == 2048 * 4 * 33
     assert all(r.seconds > 0 and r.logical_gbps > 0 for r in res)
+
+
+@pytest.mark.parametrize("fmt", ["frsz2-16", "frsz2-21", "frsz2-32"])
+def test_column_exponent_ranges(cbg, port, fmt):
+    """Every column write folds the column's exponent range (cbgx_basis.
+    d_erange: max of 2047 - e over nonzero blocks, max e) in the compress
+    kernel; it must equal the range of the oracle's block exponents (the
+    CGS kernels choose their decode path from it)."""
+    rng = np.random.default_rng(7)
+    n = 70_001
+    l = int(fmt.split("-")[1])
+    cols = [rng.standard_normal(n), np.zeros(n), rng.standard_normal(n) * 1e-300,
+            np.where(rng.random(n) < 0.5, 0.0, rng.standard_normal(n) * 10.0 ** rng.integers(-200, 200, n))]
+    B = cbg.KrylovBasis(n, len(cols), cbg.StorageFormat.parse(fmt))
+    for j, c in enumerate(cols):
+        B.write_vector(j, c)
+    er = B._erange.cpu().numpy().astype(np.int64)
+    for j, c in enumerate(cols):
+        e, _ = port.compress(c, l)
+        e = np.asarray(e, dtype=np.int64)
+        nz = e[e != 0]
+        assert er[2 * j] == (int((2047 - nz).max()) if nz.size else 0), j
+        assert er[2 * j + 1] == (int(e.max()) if e.size else 0), j
