@@ -15,6 +15,18 @@
 // so y is bit-identical to spmv() (products and sums in row order, separate
 // roundings). Matrices outside the pattern (more distinct values/offsets,
 // halo-remapped columns) keep the CSR paths.
+//
+// Three further levels, each built from the previous one when it applies
+// (cbgx_csr_dict_create2 caps the level):
+//   pair codes    <= 255 distinct (value, offset) pairs: 1 byte per entry
+//                 (pell_spmv_kernel);
+//   row patterns  <= 255 distinct rows of pair codes: 1 byte per ROW into
+//                 per-pattern {offsets, values} tables (ppat_spmv_kernel);
+//   uniform slots the patterns' offsets embed into one sorted list of <= 32
+//                 slots with one value each (constant coefficients): a slot
+//                 mask per pattern, offsets/values as kernel parameters
+//                 (uslot_spmv_kernel) -- the solver's SpMV on every stencil
+//                 configuration.
 #include <cub/device/device_scan.cuh>
 
 #include <algorithm>
