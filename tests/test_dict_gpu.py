@@ -278,3 +278,11 @@ def test_uniform_slots_random_subsets(cbg, port, seed):
     np.testing.assert_array_equal(np.isnan(y), np.isnan(ref))
     fin = ~np.isnan(ref)
     assert y[fin].tobytes() == ref[fin].tobytes()
+
+
+def test_create2_rejects_unknown_level(cbg, port):
+    rp, ci, va = port.stencil(0, 5, 5, 5)
+    n = rp.size - 1
+    A = cbg.DeviceCsr.from_host(cbg.CsrMatrix(n, n, rp, ci, va))
+    with pytest.raises(Exception, match="max_level"):
+        cbg.DictCsr(A, max_level=4)
